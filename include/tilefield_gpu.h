@@ -1,0 +1,257 @@
+/*
+ * tilefield_gpu.h — C-ABI of the B200-native Snake-NeRF window hot path.
+ *
+ * This is the drop-in boundary the reference's shared C API would have held
+ * (`add_library(tilefield SHARED capi/capi.cpp)`, proj/src/CMakeLists.txt:28-35,
+ * hidden visibility; the capi/ and include/ trees are absent upstream).  Every
+ * entry point is `extern "C"`, takes plain pointers and sizes, returns an int
+ * status (0 = OK) and never lets a C++ exception cross the ABI; the message of
+ * the last failure on the calling thread is available from tfg_last_error().
+ * A header-only C++ wrapper that rethrows `tilefield::Error` in the reference's
+ * style lives in tilefield_gpu.hpp.
+ *
+ * Device memory is owned by the context; host buffers are caller-owned and are
+ * copied (through the context's pinned staging) inside the call.  One context
+ * per GPU; calls on a context are ordered on its stream.  There is no CPU
+ * fallback: creating a context without an sm_100 device fails.
+ *
+ * Reference interfaces replaced (file:line under /root/reference/proj/src/):
+ *   RationalCamera / project / localize / ray_from_pixel   core/camera.hpp:22-67
+ *   crop_for_tile                                          core/camera.hpp:71-72
+ *   Roi / TileGrid::build / candidate_tiles                core/tiler.hpp:10-82
+ *   intersect_ray_aabb / TileBoxSet::segments             core/geometry.hpp:62-70
+ *   FieldConfig                                            core/nn.hpp:14-37
+ *   RaySegmentBatch                                        core/ray_batch.hpp:13-49
+ *   forward_batch / backward_batch                         core/field.hpp:186-197
+ *   adam_step / AdamConfig / LrSchedule                    core/field.hpp:16-48
+ *   OccupancyGrid / TileField::update_occupancy            core/field.hpp:55-102
+ *   TileField::create / GlobalColorNet::create             core/field.hpp:93,118
+ *   save/load_tile_checkpoint (window slide storage tier)  core/field.hpp:206-210
+ *   sample_segments / render / color_loss
+ *   snake_path / advance / accept_rays / memory_report
+ */
+#ifndef TILEFIELD_GPU_H
+#define TILEFIELD_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(_WIN32)
+#define TFG_API
+#else
+#define TFG_API __attribute__((visibility("default")))
+#endif
+
+/* ---- status codes -------------------------------------------------------- */
+enum {
+    TFG_OK = 0,
+    TFG_ERR_INVALID = 1,      /* bad argument / precondition (reference: require) */
+    TFG_ERR_CUDA = 2,         /* CUDA runtime failure                              */
+    TFG_ERR_NONFINITE = 3,    /* non-finite gradient (field.hpp:45-48)            */
+    TFG_ERR_NO_DEVICE = 4,    /* no sm_100 device: there is no CPU fallback        */
+    TFG_ERR_STATE = 5         /* call out of order (e.g. step before set_window)   */
+};
+
+/* ---- plain data mirrors of the reference types --------------------------- */
+
+/* RationalCamera, core/camera.hpp:22-33 (90 doubles + 2 ints). */
+typedef struct tfg_rpc {
+    double line_num[20], line_den[20], samp_num[20], samp_den[20];
+    double line_off, samp_off, lat_off, long_off, height_off;
+    double line_scale, samp_scale, lat_scale, long_scale, height_scale;
+    int32_t image_rows, image_cols;
+} tfg_rpc;
+
+/* Roi, core/tiler.hpp:10-19. */
+typedef struct tfg_roi {
+    double easting_min, easting_max;
+    double northing_min, northing_max;
+    double z_min, z_max;
+} tfg_roi;
+
+/* FieldConfig, core/nn.hpp:14-37 (the GPU kernels are specialised for the
+ * defaults; tfg_create rejects any other shape). */
+typedef struct tfg_field_config {
+    int32_t levels, table_size, features, n_min, n_max;
+    int32_t density_hidden, embedding, color_hidden, color_layers, view_freqs;
+    float density_max;
+    int32_t occupancy_resolution;
+    float occupancy_decay, occupancy_threshold;
+    int32_t occupancy_interval;
+} tfg_field_config;
+
+/* Trainer / sampler knobs: AdamConfig + LrSchedule (field.hpp:16-31), sampler
+ * policy, seeds (rng.hpp:8-10).  See DESIGN.md "pins". */
+typedef struct tfg_train_config {
+    uint64_t seed;               /* run seed: pixel draws, jitter, init, occupancy */
+    double samples_per_meter;    /* per-segment interval density     */
+    int32_t max_samples_per_ray; /* per-ray cap                */
+    double delta_cap;            /* cap of the final delta in meters */
+    float background[3];         /* fixed background RGB             */
+    int32_t margin_px;           /* crop dilation (default 4)         */
+    double lr_field, lr_color;   /* LrSchedule.base per group        */
+    double lr_decay_rate;        /* LrSchedule.decay_rate (1 = constant)           */
+    uint64_t lr_decay_steps;     /* LrSchedule.decay_steps                         */
+    float beta1, beta2, eps;     /* AdamConfig                                     */
+    int32_t batch_rays;          /* global batch size B (loss normaliser)          */
+} tfg_train_config;
+
+/* Ray-ordered batch export, the layout of RaySegmentBatch (ray_batch.hpp:13-49).
+ * Caller allocates: rays: n_rays; offsets: n_rays+1; per-sample arrays: capacity. */
+typedef struct tfg_ray_entry {
+    double origin[3];
+    double direction[3];
+    float target[3];
+    int32_t image_id;
+    int32_t row, col;
+} tfg_ray_entry;
+
+typedef struct tfg_batch_view {
+    tfg_ray_entry* rays;
+    uint32_t* offsets;
+    float* t;
+    float* delta;
+    float* local;      /* 3 per sample */
+    uint8_t* slot;
+    uint8_t* endpoint;
+    uint64_t capacity; /* sample capacity of the per-sample arrays */
+} tfg_batch_view;
+
+/* Per-slot tile state in the reference checkpoint layout (field.hpp:85-109):
+ * enc tables | dnet params; Adam m and v for each; step counts; occupancy EMA. */
+typedef struct tfg_tile_state {
+    float* enc;        /* 434,292 floats (HashGridT::tables)          */
+    float* dnet;       /* 2,128 floats   (MlpT params, flat)          */
+    float* enc_m;
+    float* enc_v;
+    float* dnet_m;
+    float* dnet_v;
+    uint64_t enc_step, dnet_step;
+    float* occupancy;  /* res^3 EMA values, x fastest (field.hpp:59)  */
+} tfg_tile_state;
+
+typedef struct tfg_memory_report {
+    uint64_t tile_params, optimizer_moments, occupancy, crops, accept_list, batch_buffers,
+        color_net, staging, total_device;
+} tfg_memory_report;
+
+typedef struct tfg_ctx tfg_ctx;
+
+/* ---- lifecycle ----------------------------------------------------------- */
+TFG_API const char* tfg_last_error(void);
+TFG_API int tfg_default_field_config(tfg_field_config* out);
+TFG_API int tfg_default_train_config(tfg_train_config* out);
+
+/* Sizes of one tile's parameter groups for a config (HashGridT::param_count,
+ * MlpT::param_count; nn.hpp:57-62,197). */
+TFG_API int tfg_param_counts(const tfg_field_config* cfg, uint64_t* enc, uint64_t* dnet,
+                             uint64_t* color);
+
+/* Creates a context on `device`; `max_rays` bounds the rays of one batch (per
+ * rank).  All device buffers are allocated here (constant HBM footprint). */
+TFG_API int tfg_create(const tfg_field_config* fcfg, const tfg_train_config* tcfg, int device,
+                       int max_rays, tfg_ctx** out);
+TFG_API int tfg_destroy(tfg_ctx* ctx);
+/* Orders all subsequent work of the context on `stream` (a cudaStream_t). */
+TFG_API int tfg_set_stream(tfg_ctx* ctx, void* stream);
+
+/* ---- scene: cameras, images, grid ---------------------------------------- */
+/* Cameras (n_views) and full 8-bit RGB views (rows*cols*3 each, row-major from
+ * the top row, image.hpp:10-18).  Images stay in (pinned) host memory; only the
+ * window's crops are copied to HBM. */
+TFG_API int tfg_set_scene(tfg_ctx* ctx, const tfg_rpc* cams, int n_views,
+                          const uint8_t* const* images, const tfg_roi* roi, int grid_rows,
+                          int grid_cols);
+
+/* ---- window slide (out-of-core) ------------------------- */
+/* Places the 2x2 window with its SW tile at (pos_row, pos_col): evicts the
+ * tiles leaving the window to their host records, loads the entering tiles
+ * (fresh TileField::create when never trained), stages the window crops and
+ * builds the accepted-ray list.  Copies run on a side stream. */
+TFG_API int tfg_set_window(tfg_ctx* ctx, int pos_row, int pos_col);
+/* Loaded tile of each slot (row, col); slot order is the segment tie order. */
+TFG_API int tfg_window_tiles(tfg_ctx* ctx, int32_t* rows4, int32_t* cols4);
+/* Snake path: writes (H-1)(W-1) positions as row,col pairs. */
+TFG_API int tfg_snake_path(int grid_rows, int grid_cols, int32_t* out_pairs, int* n_out);
+/* Prefetch of the next window position's tiles + crops on the side stream. */
+TFG_API int tfg_prefetch_window(tfg_ctx* ctx, int pos_row, int pos_col);
+
+/* Accepted-ray list of the current window: packed
+ * (view << 40) | (row << 20) | col, enumerated view, row, col ascending. */
+TFG_API int tfg_accept_count(tfg_ctx* ctx, uint64_t* n);
+TFG_API int tfg_accept_export(tfg_ctx* ctx, uint64_t* out, uint64_t capacity);
+
+/* ---- one training iteration --------------------------------- */
+/* Draws rays [ray_begin, ray_begin + n_rays) of iteration `iter` from the
+ * global counter-RNG stream, samples, renders, backpropagates.  Gradients are
+ * left in the context's flat gradient buffer (for an allreduce) ... */
+TFG_API int tfg_forward_backward(tfg_ctx* ctx, uint64_t iter, uint64_t ray_begin, int n_rays);
+/* ... then the fused Adam step over the window's 9 groups plus the periodic
+ * occupancy update.  Non-finite gradients raise TFG_ERR_NONFINITE (group named
+ * in tfg_last_error) at the next status read. */
+TFG_API int tfg_optimizer_step(tfg_ctx* ctx, uint64_t iter);
+/* Convenience: forward_backward + optimizer_step + loss readback. */
+TFG_API int tfg_train_step(tfg_ctx* ctx, uint64_t iter, uint64_t ray_begin, int n_rays,
+                           float* loss_out);
+/* Device pointer + float count of the flat gradient buffer (allreduce target). */
+TFG_API int tfg_grad_buffer(tfg_ctx* ctx, void** dptr, uint64_t* count);
+/* Loss of the last forward_backward (sum over this rank's rays, already
+ * divided by 3*B); copies to host and synchronises. */
+TFG_API int tfg_read_loss(tfg_ctx* ctx, float* loss_out);
+
+/* ---- sub-steps exposed for parity (reference-facing operator surface) ---- */
+/* sample_segments over the current window: builds the device batch. */
+TFG_API int tfg_sample(tfg_ctx* ctx, uint64_t iter, uint64_t ray_begin, int n_rays, int jitter,
+                       uint64_t* n_samples);
+/* Builds a batch from caller-given pixels (view,row,col triplets) with jitter
+ * off — the render / evaluation path. */
+TFG_API int tfg_sample_pixels(tfg_ctx* ctx, const int32_t* pixels, int n_rays,
+                              uint64_t* n_samples);
+TFG_API int tfg_batch_export(tfg_ctx* ctx, tfg_batch_view* out);
+/* forward_batch: per-sample sigma and rgb in ray order (n_samples, 3*n_samples). */
+TFG_API int tfg_field_forward(tfg_ctx* ctx, float* sigma, float* rgb);
+/* render + color_loss + render backward: per-ray rgb(3)/depth/opacity, and the
+ * per-sample d_sigma / d_rgb in ray order (any output may be NULL). */
+TFG_API int tfg_composite(tfg_ctx* ctx, float* ray_rgb, float* ray_depth, float* ray_opacity,
+                          float* d_sigma, float* d_rgb, float* loss);
+/* backward_batch into the flat gradient buffer (zeroed first). */
+TFG_API int tfg_field_backward(tfg_ctx* ctx);
+
+/* ---- parameter / state access -------------------------------------------- */
+TFG_API int tfg_get_tile_state(tfg_ctx* ctx, int slot, tfg_tile_state* out);
+TFG_API int tfg_set_tile_state(tfg_ctx* ctx, int slot, const tfg_tile_state* in);
+TFG_API int tfg_get_color(tfg_ctx* ctx, float* params, float* m, float* v, uint64_t* step);
+TFG_API int tfg_set_color(tfg_ctx* ctx, const float* params, const float* m, const float* v,
+                          uint64_t step);
+/* Gradients of the last backward: per slot enc (434,292) + dnet (2,128), colour. */
+TFG_API int tfg_get_grads(tfg_ctx* ctx, int slot, float* enc, float* dnet, float* color);
+TFG_API int tfg_update_occupancy(tfg_ctx* ctx);
+TFG_API int tfg_get_memory_report(tfg_ctx* ctx, tfg_memory_report* out);
+
+/* ---- render path (cmd_render; config 4) --------------------- */
+/* Loads up to `n_tiles` tiles (params only) for forward-only rendering over
+ * an ROI sub-grid; tile_state entries need enc, dnet, occupancy. */
+TFG_API int tfg_render_setup(tfg_ctx* ctx, const int32_t* rows, const int32_t* cols, int n_tiles,
+                             const tfg_tile_state* states, const float* color_params);
+/* Renders caller-given rays of camera `cam` (pixels as row,col pairs):
+ * per-ray rgb(3), depth, opacity to host. */
+TFG_API int tfg_render_pixels(tfg_ctx* ctx, const tfg_rpc* cam, const int32_t* pixels,
+                              int n_rays, float* rgb, float* depth, float* opacity);
+
+/* ---- timing helpers (kernel share inside the timed region) --------------- */
+/* Accumulated device milliseconds and launch counts per kernel family since
+ * the last reset (CUDA events on the context stream; enabled by flag). */
+TFG_API int tfg_profile_enable(tfg_ctx* ctx, int on);
+TFG_API int tfg_profile_read(tfg_ctx* ctx, const char** names, double* ms, uint64_t* launches,
+                             int capacity, int* n_out);
+TFG_API int tfg_kernel_launch_count(tfg_ctx* ctx, uint64_t* launches);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TILEFIELD_GPU_H */

@@ -1,0 +1,133 @@
+"""Synthetic overhead scenes (host-side fixture generator).
+
+The reference's synth module is absent upstream and out of
+scope as a product; this is the minimal stand-in the parity tests and the
+benchmark need: an ROI tiled H x W, N views with rational (RPC00B-style)
+cameras of a given off-nadir angle / azimuth, and 8-bit RGB views.
+
+Camera: a parallel projection along the view direction (off-nadir theta,
+azimuth phi) of the ground point at z = 0, written in RPC normalised
+coordinates (camera.hpp:11-21) with small cubic and denominator terms so the
+rational path of project()/localize() is exercised.  Images: a procedural
+albedo of the z = 0 intersection (flat textured ground) - cheap enough to
+generate 16 x 1536^2 views for the benchmark.
+"""
+from __future__ import annotations
+
+import dataclasses
+import math
+
+import numpy as np
+
+from .abi import Roi, Rpc
+
+
+@dataclasses.dataclass
+class Scene:
+    roi: Roi
+    grid_rows: int
+    grid_cols: int
+    cams: list
+    images: list  # uint8 (rows, cols, 3), row-major from the top row
+    gsd: float
+
+    @property
+    def n_views(self) -> int:
+        return len(self.cams)
+
+
+def make_camera(
+    roi: Roi, gsd: float, off_nadir_deg: float, azimuth_deg: float, nonlinear: float = 2e-4,
+    pad_px: int = 8,
+) -> Rpc:
+    th = math.radians(off_nadir_deg)
+    ph = math.radians(azimuth_deg)
+    tx, ty = math.tan(th) * math.cos(ph), math.tan(th) * math.sin(ph)
+    cam = Rpc()
+    cam.long_off = 0.5 * (roi.easting_min + roi.easting_max)
+    cam.lat_off = 0.5 * (roi.northing_min + roi.northing_max)
+    cam.height_off = 0.5 * (roi.z_min + roi.z_max)
+    cam.long_scale = 0.55 * (roi.easting_max - roi.easting_min)
+    cam.lat_scale = 0.55 * (roi.northing_max - roi.northing_min)
+    cam.height_scale = 0.6 * (roi.z_max - roi.z_min)
+    # ground footprint of the ROI box in the z=0 plane, projected along the view
+    xs, ys = [], []
+    for x in (roi.easting_min, roi.easting_max):
+        for y in (roi.northing_min, roi.northing_max):
+            for z in (roi.z_min, roi.z_max):
+                xs.append(x + z * tx)
+                ys.append(y + z * ty)
+    x0 = min(xs) - pad_px * gsd
+    y0 = max(ys) + pad_px * gsd  # image top = north
+    cols = int(math.ceil((max(xs) - min(xs)) / gsd)) + 2 * pad_px
+    rows = int(math.ceil((max(ys) - min(ys)) / gsd)) + 2 * pad_px
+    cam.samp_scale = cam.long_scale / gsd
+    cam.samp_off = (cam.long_off + cam.height_off * tx - x0) / gsd
+    cam.line_scale = cam.lat_scale / gsd
+    cam.line_off = (y0 - cam.lat_off - cam.height_off * ty) / gsd
+    # col = samp_off + samp_scale * (L + kx H + ...), row = line_off + line_scale * (-P - ky H + ...)
+    cam.samp_num[1] = 1.0
+    cam.samp_num[3] = cam.height_scale * tx / cam.long_scale
+    cam.line_num[2] = -1.0
+    cam.line_num[3] = -cam.height_scale * ty / cam.lat_scale
+    cam.samp_den[0] = 1.0
+    cam.line_den[0] = 1.0
+    if nonlinear:
+        cam.samp_num[4] = nonlinear  # L*P
+        cam.samp_num[11] = 0.5 * nonlinear  # L^3
+        cam.line_num[7] = -nonlinear  # L^2
+        cam.line_num[18] = 0.5 * nonlinear  # P^2 H
+        cam.samp_den[2] = 0.25 * nonlinear  # P
+        cam.line_den[1] = -0.25 * nonlinear  # L
+    cam.image_rows = rows
+    cam.image_cols = cols
+    cam._x0, cam._y0, cam._tx, cam._ty = x0, y0, tx, ty  # analytic model (fixture only)
+    return cam
+
+
+def procedural_image(cam: Rpc, gsd: float, seed: int) -> np.ndarray:
+    rows, cols = cam.image_rows, cam.image_cols
+    r = np.arange(rows, dtype=np.float64)[:, None]
+    c = np.arange(cols, dtype=np.float64)[None, :]
+    x = cam._x0 + c * gsd
+    y = cam._y0 - r * gsd
+    rng = np.random.default_rng(seed)
+    ph = rng.uniform(0, 2 * math.pi, size=6)
+    red = 0.5 + 0.3 * np.sin(x / 9.0 + ph[0]) * np.cos(y / 13.0 + ph[1])
+    grn = 0.5 + 0.3 * np.sin((x + y) / 17.0 + ph[2]) + 0.1 * np.cos(x / 3.1 + ph[3])
+    blu = 0.45 + 0.25 * np.cos(y / 7.0 + ph[4]) * np.sin(x / 23.0 + ph[5])
+    checker = ((np.floor(x / 16.0) + np.floor(y / 16.0)) % 2) * 0.15
+    img = np.stack([red + checker, grn - checker, blu + 0.5 * checker], axis=-1)
+    img = np.broadcast_to(img, (rows, cols, 3))
+    return np.ascontiguousarray(np.clip(img * 255.0 + 0.5, 0, 255).astype(np.uint8))
+
+
+def make_scene(
+    grid_rows: int, grid_cols: int, tile_side: float = 128.0, z_extent: float = 40.0,
+    n_views: int = 8, gsd: float = 0.5, seed: int = 0, max_off_nadir: float = 30.0,
+) -> Scene:
+    roi = Roi(0.0, grid_cols * tile_side, 0.0, grid_rows * tile_side, 0.0, z_extent)
+    rng = np.random.default_rng(seed)
+    cams, images = [], []
+    for v in range(n_views):
+        off = float(rng.uniform(0.0, max_off_nadir))
+        az = float(rng.uniform(0.0, 360.0))
+        cam = make_camera(roi, gsd, off, az)
+        cams.append(cam)
+        images.append(procedural_image(cam, gsd, seed * 1000 + v))
+    return Scene(roi, grid_rows, grid_cols, cams, images, gsd)
+
+
+# Benchmark / parity configurations (BASELINE.json configs).
+CONFIGS = {
+    1: dict(grid=(1, 1), tile_side=128.0, views=4, gsd=0.5, batch=4096),
+    2: dict(grid=(3, 3), tile_side=128.0, views=8, gsd=0.5, batch=16384),
+    3: dict(grid=(8, 8), tile_side=128.0, views=16, gsd=0.5, batch=16384),
+    4: dict(grid=(4, 4), tile_side=128.0, views=1, gsd=0.125, batch=1 << 20),
+    5: dict(grid=(6, 6), tile_side=128.0, views=16, gsd=0.5, batch=65536),
+}
+
+
+def config_scene(cfg: int, seed: int = 0) -> Scene:
+    c = CONFIGS[cfg]
+    return make_scene(c["grid"][0], c["grid"][1], c["tile_side"], 40.0, c["views"], c["gsd"], seed)
