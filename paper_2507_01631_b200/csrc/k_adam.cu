@@ -1,0 +1,76 @@
+// k_adam.cu — K5: fused Adam over the window's parameter groups (4 x enc,
+// 4 x dnet, colour) in one launch (adam_step, field.hpp:45-48).
+// Compiled with -fmad=false so the update rounds exactly like the reference
+// formula (bit-identical to the oracle for identical gradients):
+//   m = b1 m + (1-b1) g;  v = b2 v + (1-b2) g^2;
+//   p = p - lr * (m / bc1) / (sqrt(v / bc2) + eps)
+// with lr and bias corrections of the persistent per-group step count
+// computed on the host.  A group with a non-finite gradient aborts the whole
+// step (the reference throws before updating, naming the group).
+#include <cuda_runtime.h>
+
+#include "tf_common.cuh"
+#include "tf_kernels.h"
+
+namespace tfg {
+
+__device__ __forceinline__ int group_of(const AdamArgs& a, uint64_t i) {
+    int g = 0;
+    while (g + 1 < a.n_groups && i >= a.g[g + 1].offset) ++g;
+    return g;
+}
+
+__global__ void __launch_bounds__(256) grad_check_kernel(AdamArgs a, uint64_t total) {
+    uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    uint32_t bad = 0;  // bitmask of groups
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
+        float g = a.grads[i];
+        if (!isfinite(g)) bad |= 1u << group_of(a, i);
+    }
+    bad = __reduce_or_sync(0xffffffffu, bad);
+    if ((threadIdx.x & 31) == 0 && bad) {
+        for (int g = 0; g < a.n_groups; ++g)
+            if (bad & (1u << g)) atomicOr(&a.group_flags[g], 1u);
+    }
+}
+
+__global__ void __launch_bounds__(256) adam_kernel(AdamArgs a, uint64_t total) {
+    __shared__ int skip;
+    if (threadIdx.x == 0) {
+        int s = 0;
+        for (int g = 0; g < a.n_groups; ++g) s |= a.group_flags[g] ? 1 : 0;
+        skip = s;
+        if (s && blockIdx.x == 0) {
+            for (int g = 0; g < a.n_groups; ++g)
+                if (a.group_flags[g]) {
+                    a.status->nonfinite_group = uint32_t(g);
+                    break;
+                }
+            atomicOr(&a.status->bits, kStatusNonFinite);
+        }
+    }
+    __syncthreads();
+    if (skip) return;
+    uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
+        const AdamGroup& G = a.g[group_of(a, i)];
+        float g = a.grads[i];
+        float m = a.beta1 * a.m[i] + a.omb1 * g;
+        float v = a.beta2 * a.v[i] + a.omb2 * (g * g);
+        a.m[i] = m;
+        a.v[i] = v;
+        float mh = m / G.bc1;
+        float vh = v / G.bc2;
+        a.params[i] = a.params[i] - G.lr * mh / (sqrtf(vh) + a.eps);
+    }
+}
+
+void launch_adam(const AdamArgs& a, uint64_t total, cudaStream_t st, uint64_t* launches) {
+    int blocks = int((total + 255) / 256);
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    grad_check_kernel<<<blocks, 256, 0, st>>>(a, total);
+    adam_kernel<<<blocks, 256, 0, st>>>(a, total);
+    *launches += 2;
+}
+
+} // namespace tfg

@@ -1,0 +1,151 @@
+// k_composite.cu — K3: front-to-back volume compositing over the concatenated
+// segments of each ray (transmittance carried across tiles),
+// the colour loss (channel-mean convention of the example at
+// :377) and the analytic render backward:
+//   alpha_k = 1 - exp(-sigma_k delta_k),  T_k = prod_{j<k} (1 - alpha_j),
+//   w_k = T_k alpha_k,  C = sum w_k c_k + T_N bg,
+//   dC/dc_k = w_k,  dC/dsigma_k = delta_k (T_{k+1} c_k - R_k),
+//   R_k = sum_{j>k} w_j c_j + T_N bg = (C - T_N bg - P_k) + T_N bg,
+// with P_k the inclusive prefix of w c.  One warp per ray; samples are read
+// segment by segment from their slot buckets (coalesced runs), transmittance
+// is a warp product scan with a carried prefix.  Memory-bound.
+#include <cuda_runtime.h>
+
+#include "tf_common.cuh"
+#include "tf_kernels.h"
+
+namespace tfg {
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__global__ void __launch_bounds__(256) composite_kernel(CompositeArgs a) {
+    int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    if (i >= a.n_rays) return;
+    if (a.status_in->bits & kStatusSampleOverflow) return;
+    const RayRec& R = a.rays[i];
+    int nseg = R.status == 0 ? R.nseg : 0;
+    uint32_t base[kMaxSeg];
+    int cnt[kMaxSeg];
+    int m = 0;
+    for (int k = 0; k < nseg; ++k) {
+        base[k] = a.P[uint64_t(R.slot[k]) * a.n_rays + i];
+        cnt[k] = R.cnt[k];
+        m += cnt[k];
+    }
+    const uint32_t FULL = 0xffffffffu;
+    // ---------------- forward
+    float T = 1.f, cr = 0.f, cg = 0.f, cb = 0.f, dep = 0.f, op = 0.f;
+    for (int q0 = 0; q0 < m; q0 += 32) {
+        int q = q0 + lane;
+        float sg = 0.f, de = 0.f, tt = 0.f;
+        float4 io = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (q < m) {
+            int k = 0, rem = q;
+            while (rem >= cnt[k]) { rem -= cnt[k]; ++k; }
+            uint64_t pos = uint64_t(base[k]) + rem;
+            io = a.s.io[pos];
+            float2 td = a.s.td[pos];
+            sg = io.x;
+            tt = td.x;
+            de = td.y;
+        }
+        float alpha = 1.f - expf(-(sg * de));
+        float keep = 1.f - alpha;
+        // inclusive product scan of keep
+        float incl = keep;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            float y = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl *= y;
+        }
+        float excl = __shfl_up_sync(FULL, incl, 1);
+        if (lane == 0) excl = 1.f;
+        float w = T * excl * alpha;
+        cr += w * io.y;
+        cg += w * io.z;
+        cb += w * io.w;
+        dep += w * tt;
+        op += w;
+        T *= __shfl_sync(FULL, incl, 31);
+    }
+    cr = warp_sum(cr);
+    cg = warp_sum(cg);
+    cb = warp_sum(cb);
+    dep = warp_sum(dep);
+    op = warp_sum(op);
+    float rr = cr + T * a.bg.x, rg = cg + T * a.bg.y, rb = cb + T * a.bg.z;
+    if (lane == 0) {
+        if (a.ray_rgb) {
+            a.ray_rgb[3 * i] = rr;
+            a.ray_rgb[3 * i + 1] = rg;
+            a.ray_rgb[3 * i + 2] = rb;
+        }
+        if (a.ray_depth) a.ray_depth[i] = dep / fmaxf(op, 1e-10f);
+        if (a.ray_opacity) a.ray_opacity[i] = op;
+    }
+    if (!a.backward || R.status != 0) return;
+    float er = rr - R.target[0], eg = rg - R.target[1], eb = rb - R.target[2];
+    if (lane == 0) atomicAdd(&a.status->loss, double(er * er + eg * eg + eb * eb));
+    float gr = 2.f * er * a.inv3b, gg = 2.f * eg * a.inv3b, gb = 2.f * eb * a.inv3b;
+    // ---------------- backward
+    float T2 = 1.f, pr = 0.f, pg = 0.f, pb = 0.f;
+    float Rbr = T * a.bg.x, Rbg = T * a.bg.y, Rbb = T * a.bg.z;
+    for (int q0 = 0; q0 < m; q0 += 32) {
+        int q = q0 + lane;
+        float sg = 0.f, de = 0.f;
+        float4 io = make_float4(0.f, 0.f, 0.f, 0.f);
+        uint64_t pos = 0;
+        if (q < m) {
+            int k = 0, rem = q;
+            while (rem >= cnt[k]) { rem -= cnt[k]; ++k; }
+            pos = uint64_t(base[k]) + rem;
+            io = a.s.io[pos];
+            de = a.s.td[pos].y;
+            sg = io.x;
+        }
+        float alpha = 1.f - expf(-(sg * de));
+        float keep = 1.f - alpha;
+        float incl = keep;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            float y = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl *= y;
+        }
+        float excl = __shfl_up_sync(FULL, incl, 1);
+        if (lane == 0) excl = 1.f;
+        float Tk = T2 * excl;
+        float w = Tk * alpha;
+        float Tk1 = T2 * incl;
+        // inclusive prefix of w*c
+        float sr = w * io.y, sgc = w * io.z, sbc = w * io.w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            float yr = __shfl_up_sync(FULL, sr, o);
+            float yg = __shfl_up_sync(FULL, sgc, o);
+            float yb = __shfl_up_sync(FULL, sbc, o);
+            if (lane >= o) { sr += yr; sgc += yg; sbc += yb; }
+        }
+        float Rr = (cr - (pr + sr)) + Rbr;
+        float Rg = (cg - (pg + sgc)) + Rbg;
+        float Rb = (cb - (pb + sbc)) + Rbb;
+        float ds = de * (gr * (Tk1 * io.y - Rr) + gg * (Tk1 * io.z - Rg) + gb * (Tk1 * io.w - Rb));
+        if (q < m) a.s.io[pos] = make_float4(ds, w * gr, w * gg, w * gb);
+        pr += __shfl_sync(FULL, sr, 31);
+        pg += __shfl_sync(FULL, sgc, 31);
+        pb += __shfl_sync(FULL, sbc, 31);
+        T2 *= __shfl_sync(FULL, incl, 31);
+    }
+}
+
+void launch_composite(const CompositeArgs& a, cudaStream_t st, uint64_t* launches) {
+    int blocks = (a.n_rays * 32 + 255) / 256;
+    composite_kernel<<<blocks, 256, 0, st>>>(a);
+    *launches += 1;
+}
+
+} // namespace tfg

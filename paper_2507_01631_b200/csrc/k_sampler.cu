@@ -1,0 +1,503 @@
+// k_sampler.cu — K1: on-the-fly ray generation, ray/tile-box segmentation and
+// per-segment stratified sampling (the paper's two custom kernels, PAPER.md:
+// 320-322), bit-exact with the reference semantics.
+//
+// Compiled with -fmad=false: every double/float operation here rounds once,
+// matching the reference's x86-64 build (see tf_common.cuh).
+//
+//   accept_kernel    accept_rays over the window's crop union
+//   raygen_kernel    pixel draw (rng.hpp:42-46) + ray_from_pixel (camera.cpp:105)
+//                    + TileBoxSet::segments (geometry.cpp:39-48) + per-slot
+//                    sample counts (sample_segments)
+//   scan kernels     exclusive prefix sums (slot-bucketed sample positions)
+//   tiles_kernel     128-sample single-slot work tiles for K2/K4
+//   write_kernel     warp per ray: stratified samples, occupancy culling,
+//                    deltas over the concatenated ray
+#include <cuda_runtime.h>
+
+#include "tf_common.cuh"
+#include "tf_kernels.h"
+
+namespace tfg {
+
+// ------------------------------------------------------------------ scans
+// Three-phase exclusive scan of uint32 (values and sums < 2^32).
+constexpr int kScanThreads = 512;
+constexpr int kScanItems = 8;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* total) {
+    __shared__ uint32_t warp_sums[kScanThreads / 32];
+    int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_sums[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        uint32_t s = lane < kScanThreads / 32 ? warp_sums[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, s, o);
+            if (lane >= o) s += y;
+        }
+        if (lane < kScanThreads / 32) warp_sums[lane] = s;
+    }
+    __syncthreads();
+    uint32_t pre = (w > 0 ? warp_sums[w - 1] : 0) + x - v;
+    if (total) *total = warp_sums[kScanThreads / 32 - 1];
+    __syncthreads();
+    return pre;
+}
+
+__global__ void __launch_bounds__(kScanThreads) scan_reduce_kernel(const uint32_t* __restrict__ in,
+                                                                   uint64_t n,
+                                                                   uint32_t* __restrict__ sums) {
+    uint64_t base = uint64_t(blockIdx.x) * kScanTile;
+    uint32_t s = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        uint64_t i = base + uint64_t(threadIdx.x) * kScanItems + k;
+        if (i < n) s += in[i];
+    }
+    uint32_t tot;
+    block_exclusive_scan(s, &tot);
+    if (threadIdx.x == 0) sums[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(kScanThreads) scan_sums_kernel(uint32_t* sums, int nb,
+                                                                 uint32_t* grand_total) {
+    // single block: exclusive scan of up to kScanTile block sums
+    uint32_t v[kScanItems];
+    uint32_t s = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        int i = threadIdx.x * kScanItems + k;
+        v[k] = i < nb ? sums[i] : 0;
+        s += v[k];
+    }
+    uint32_t tot;
+    uint32_t pre = block_exclusive_scan(s, &tot);
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        int i = threadIdx.x * kScanItems + k;
+        if (i < nb) sums[i] = pre;
+        pre += v[k];
+    }
+    if (threadIdx.x == 0 && grand_total) *grand_total = tot;
+}
+
+__global__ void __launch_bounds__(kScanThreads) scan_apply_kernel(const uint32_t* __restrict__ in,
+                                                                  uint64_t n,
+                                                                  const uint32_t* __restrict__ sums,
+                                                                  uint32_t* __restrict__ out) {
+    uint64_t base = uint64_t(blockIdx.x) * kScanTile;
+    uint32_t v[kScanItems];
+    uint32_t s = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        uint64_t i = base + uint64_t(threadIdx.x) * kScanItems + k;
+        v[k] = i < n ? in[i] : 0;
+        s += v[k];
+    }
+    uint32_t pre = block_exclusive_scan(s, nullptr) + sums[blockIdx.x];
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        uint64_t i = base + uint64_t(threadIdx.x) * kScanItems + k;
+        if (i < n) out[i] = pre;
+        pre += v[k];
+    }
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == blockDim.x - 1) out[n] = pre;
+}
+
+int scan_exclusive(const uint32_t* in, uint64_t n, uint32_t* out, uint32_t* block_sums,
+                   uint32_t* grand_total, cudaStream_t st, uint64_t* launches) {
+    int nb = int((n + kScanTile - 1) / kScanTile);
+    if (nb < 1) nb = 1;
+    if (nb > kScanTile) return 1;
+    scan_reduce_kernel<<<nb, kScanThreads, 0, st>>>(in, n, block_sums);
+    scan_sums_kernel<<<1, kScanThreads, 0, st>>>(block_sums, nb, grand_total);
+    scan_apply_kernel<<<nb, kScanThreads, 0, st>>>(in, n, block_sums, out);
+    if (launches) *launches += 3;
+    return 0;
+}
+
+// ------------------------------------------------------------------ accept list
+// One thread per candidate pixel of the per-view crop-union rects; flag = 1 iff
+// the ray exists, hits >= 1 tile and every hit tile is loaded.
+__global__ void __launch_bounds__(128) accept_kernel(AcceptArgs a, uint32_t* __restrict__ flags) {
+    uint64_t idx = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= a.n_candidates) return;
+    int v = 0;
+    while (v + 1 < a.n_views && a.view_start[v + 1] <= idx) ++v;
+    uint64_t local = idx - a.view_start[v];
+    const int* u = a.union_rect + 4 * v;
+    int ncols = u[3] - u[2];
+    int row = u[0] + int(local / uint64_t(ncols));
+    int col = u[2] + int(local % uint64_t(ncols));
+    uint32_t ok = 0;
+    bool in = false;
+    for (int k = 0; k < a.n_loaded; ++k) {
+        const int* r = a.crop_rect + 4 * (v * kTrainSlots + k);
+        if (r[0] < r[1] && row >= r[0] && row < r[1] && col >= r[2] && col < r[3]) in = true;
+    }
+    if (in) {
+        double o[3], d[3];
+        if (rpc_ray(a.cams[v], row, col, a.z_min, a.z_max, o, d) == 0) {
+            // candidate_tiles (tiler.cpp:70-100): XY shadow between z bounds
+            double dz = d[2];
+            if (dz != 0.0) {
+                double ta = (a.z_max - o[2]) / dz, tb = (a.z_min - o[2]) / dz;
+                if (ta > tb) { double t = ta; ta = tb; tb = t; }
+                ta = (ta < 0.0) ? 0.0 : ta;  // std::max(ta, 0.0)
+                if (!(tb < ta)) {
+                    double ax = o[0] + ta * d[0], ay = o[1] + ta * d[1];
+                    double bx = o[0] + tb * d[0], by = o[1] + tb * d[1];
+                    auto cell = [](const double* e, int n, double val) {
+                        // upper_bound - 1, clamped to [0, n-1]
+                        int lo = 0, hi = n + 1;
+                        while (lo < hi) {
+                            int mid = (lo + hi) >> 1;
+                            if (val < e[mid]) hi = mid; else lo = mid + 1;
+                        }
+                        int k = lo - 1;
+                        return k < 0 ? 0 : (k > n - 1 ? n - 1 : k);
+                    };
+                    double exlo = (bx < ax) ? bx : ax, exhi = (ax < bx) ? bx : ax;
+                    double nylo = (by < ay) ? by : ay, nyhi = (ay < by) ? by : ay;
+                    int c0 = cell(a.east, a.grid_cols, exlo), c1 = cell(a.east, a.grid_cols, exhi);
+                    int r0 = cell(a.north, a.grid_rows, nylo), r1 = cell(a.north, a.grid_rows, nyhi);
+                    int hits = 0;
+                    bool all_loaded = true;
+                    for (int tr = r0; tr <= r1; ++tr)
+                        for (int tc = c0; tc <= c1; ++tc) {
+                            double box[6] = {a.east[tc],     a.north[tr],     a.z_min,
+                                             a.east[tc + 1], a.north[tr + 1], a.z_max};
+                            double t0, t1;
+                            if (!slab(o, d, box, &t0, &t1)) continue;
+                            ++hits;
+                            int ti = tr * a.grid_cols + tc;
+                            bool ld = false;
+                            for (int k = 0; k < a.n_loaded; ++k) ld |= (a.loaded_tile[k] == ti);
+                            all_loaded &= ld;
+                        }
+                    ok = (hits >= 1 && all_loaded) ? 1u : 0u;
+                }
+            }
+        }
+    }
+    flags[idx] = ok;
+}
+
+__global__ void accept_scatter_kernel(AcceptArgs a, const uint32_t* __restrict__ flags,
+                                      const uint32_t* __restrict__ pos,
+                                      uint64_t* __restrict__ out) {
+    uint64_t idx = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= a.n_candidates || !flags[idx]) return;
+    int v = 0;
+    while (v + 1 < a.n_views && a.view_start[v + 1] <= idx) ++v;
+    uint64_t local = idx - a.view_start[v];
+    const int* u = a.union_rect + 4 * v;
+    int ncols = u[3] - u[2];
+    uint64_t row = uint64_t(u[0]) + local / uint64_t(ncols);
+    uint64_t col = uint64_t(u[2]) + local % uint64_t(ncols);
+    out[pos[idx]] = (uint64_t(v) << 40) | (row << 20) | col;
+}
+
+// ------------------------------------------------------------------ K1a
+struct SegPlan {
+    int nseg;
+    int slot[kMaxSeg];
+    double tn[kMaxSeg], tf[kMaxSeg];
+    int nint[kMaxSeg];
+};
+
+// sample_segments interval counts (DESIGN.md pins): ceil(len * spm) >= 1 per
+// segment; proportional rescale when the per-ray cap would be exceeded.
+__device__ __forceinline__ void plan_intervals(SegPlan& p, double spm, int cap) {
+    long long total = 0, sumint = 0;
+    for (int k = 0; k < p.nseg; ++k) {
+        double len = p.tf[k] - p.tn[k];
+        long long n = (long long)ceil(len * spm);
+        if (n < 1) n = 1;
+        p.nint[k] = int(n);
+        sumint += n;
+        total += n + 1;
+    }
+    if (total > cap) {
+        long long budget = cap - p.nseg;
+        for (int k = 0; k < p.nseg; ++k) {
+            long long n = (long long)p.nint[k] * budget / sumint;
+            p.nint[k] = int(n < 1 ? 1 : n);
+        }
+    }
+}
+
+__device__ __forceinline__ double sample_t(const SegPlan& p, int k, int j, bool jitter,
+                                           uint64_t key) {
+    int n = p.nint[k];
+    if (j == 0) return p.tn[k];
+    if (j == n) return p.tf[k];
+    double step = (p.tf[k] - p.tn[k]) / n;
+    float u = 0.5f;
+    if (jitter) u = Rng(hash_combine(key, (uint64_t(k) << 16) | uint64_t(j))).flt();
+    return p.tn[k] + (double(j) + (double(u) - 0.5)) * step;
+}
+
+__device__ __forceinline__ bool occ_test(const uint32_t* bits, float x, float y, float z) {
+    int v = voxel_index(x, y, z);
+    return (__ldg(bits + (v >> 5)) >> (v & 31)) & 1u;
+}
+
+__global__ void __launch_bounds__(128) raygen_kernel(RaygenArgs a, RayRec* __restrict__ rays,
+                                                     float4* __restrict__ venc,
+                                                     uint32_t* __restrict__ counts,
+                                                     Status* __restrict__ status) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= a.n_rays) return;
+    uint64_t g = a.ray_begin + uint64_t(i);
+    int v, row, col;
+    if (a.pixels) {
+        v = a.pixels[3 * i];
+        row = a.pixels[3 * i + 1];
+        col = a.pixels[3 * i + 2];
+    } else {
+        Rng r(hash_combine(hash_combine(hash_combine(a.seed, kPurposePixels), a.iter), g));
+        uint64_t e = a.accept[r.below(a.n_accept)];
+        v = int(e >> 40);
+        row = int((e >> 20) & 0xFFFFF);
+        col = int(e & 0xFFFFF);
+    }
+    RayRec R;
+    R.view = v;
+    R.row = row;
+    R.col = col;
+    R.target[0] = R.target[1] = R.target[2] = 0.f;
+    if (a.crop_bytes) {
+        const int* cr = a.crop_rect + 4 * v;  // r0, c0, cols, rows
+        const uint8_t* px = a.crop_bytes + a.crop_offset[v] +
+                            3 * (uint64_t(row - cr[0]) * uint64_t(cr[2]) + uint64_t(col - cr[1]));
+        for (int c = 0; c < 3; ++c) R.target[c] = float(px[c]) / 255.0f;  // u8_to_unit
+    }
+    R.status = rpc_ray(a.cams[v], row, col, a.z_min, a.z_max, R.o, R.d);
+    for (int s = 0; s < a.slots.n; ++s) counts[uint64_t(s) * a.n_rays + i] = 0;
+    R.nseg = 0;
+    if (R.status != 0) {
+        atomicOr(&status->bits, kStatusRayFail);
+        rays[i] = R;
+        return;
+    }
+    // TileBoxSet::segments: hits in slot order, stable insertion sort on t_near
+    SegPlan p;
+    p.nseg = 0;
+    for (int s = 0; s < a.slots.n; ++s) {
+        double t0, t1;
+        if (!slab(R.o, R.d, a.slots.box[s], &t0, &t1)) continue;
+        if (p.nseg == kMaxSeg) {
+            atomicOr(&status->bits, kStatusSegOverflow);
+            break;
+        }
+        int j = p.nseg++;
+        while (j > 0 && t0 < p.tn[j - 1]) {
+            p.tn[j] = p.tn[j - 1];
+            p.tf[j] = p.tf[j - 1];
+            p.slot[j] = p.slot[j - 1];
+            --j;
+        }
+        p.tn[j] = t0;
+        p.tf[j] = t1;
+        p.slot[j] = s;
+    }
+    plan_intervals(p, a.spm, a.cap);
+    uint64_t key = hash_combine(hash_combine(hash_combine(a.seed, kPurposeJitter), a.iter), g);
+    R.nseg = p.nseg;
+    for (int k = 0; k < p.nseg; ++k) {
+        const double* fr = a.slots.frame[p.slot[k]];
+        const uint32_t* bits = a.occ_bits[p.slot[k]];
+        int n = p.nint[k];
+        int cnt = 2;  // endpoints are never culled
+        for (int j = 1; j < n; ++j) {
+            double t = sample_t(p, k, j, a.jitter, key);
+            float lx = float((R.o[0] + t * R.d[0] - fr[0]) * fr[3]);
+            float ly = float((R.o[1] + t * R.d[1] - fr[1]) * fr[4]);
+            float lz = float((R.o[2] + t * R.d[2] - fr[2]) * fr[5]);
+            cnt += occ_test(bits, lx, ly, lz);
+        }
+        R.slot[k] = uint8_t(p.slot[k]);
+        R.tn[k] = p.tn[k];
+        R.tf[k] = p.tf[k];
+        R.nint[k] = uint16_t(n);
+        R.cnt[k] = uint16_t(cnt);
+        counts[uint64_t(p.slot[k]) * a.n_rays + i] = uint32_t(cnt);
+    }
+    rays[i] = R;
+    // encode_direction (nn.hpp:288-298) of the float world direction
+    float d3[3] = {float(R.d[0]), float(R.d[1]), float(R.d[2])};
+    float e[24];
+    int jj = 0;
+    const float scales[4] = {3.14159265358979323846f, 6.28318530717958647692f,
+                             12.5663706143591729538f, 25.1327412287183459077f};
+    for (int f = 0; f < kViewFreqs; ++f)
+        for (int c = 0; c < 3; ++c) {
+            float x = scales[f] * d3[c];
+            e[jj++] = sinf(x);
+            e[jj++] = cosf(x);
+        }
+    float4* ve = venc + uint64_t(i) * 6;
+    for (int q = 0; q < 6; ++q) ve[q] = make_float4(e[4 * q], e[4 * q + 1], e[4 * q + 2], e[4 * q + 3]);
+}
+
+// Slot buckets -> 128-sample single-slot tiles (one block).
+__global__ void tiles_kernel(const uint32_t* __restrict__ P, int n_rays, int nslots,
+                             uint64_t capacity, int max_tiles, TileDesc* __restrict__ tiles,
+                             Status* __restrict__ status) {
+    __shared__ uint32_t tile_base[kMaxSlots + 1];
+    if (threadIdx.x == 0) {
+        uint32_t tb = 0;
+        for (int s = 0; s < nslots; ++s) {
+            uint32_t b = P[uint64_t(s) * n_rays];
+            uint32_t e = P[uint64_t(s + 1) * n_rays];
+            tile_base[s] = tb;
+            tb += (e - b + 127) / 128;
+        }
+        tile_base[nslots] = tb;
+        uint64_t total = P[uint64_t(nslots) * n_rays];
+        status->n_samples = total;
+        status->n_tiles = tb;
+        if (total > capacity || int(tb) > max_tiles) {
+            atomicOr(&status->bits, kStatusSampleOverflow);
+            status->n_tiles = 0;
+        }
+    }
+    __syncthreads();
+    if (status->n_tiles == 0) return;
+    for (int s = 0; s < nslots; ++s) {
+        uint32_t b = P[uint64_t(s) * n_rays];
+        uint32_t e = P[uint64_t(s + 1) * n_rays];
+        uint32_t nt = tile_base[s + 1] - tile_base[s];
+        for (uint32_t t = threadIdx.x; t < nt; t += blockDim.x) {
+            TileDesc d;
+            d.start = b + 128 * t;
+            uint32_t rem = e - d.start;
+            d.n = uint16_t(rem < 128 ? rem : 128);
+            d.slot = uint16_t(s);
+            tiles[tile_base[s] + t] = d;
+        }
+    }
+}
+
+// ------------------------------------------------------------------ K1c
+// Warp per ray: regenerate the stratified samples of every segment, cull
+// interior samples in clear occupancy voxels (ballot compaction), write them
+// to the ray's slot buckets, and delta = t_next - t over the concatenated ray
+// (double, then rounded; duplicate boundary samples get delta = 0); the last
+// kept sample's delta is the remaining distance to the z_min exit capped at
+// delta_cap.
+__global__ void __launch_bounds__(256) write_kernel(RaygenArgs a, const RayRec* __restrict__ rays,
+                                                    const uint32_t* __restrict__ P,
+                                                    const Status* __restrict__ status,
+                                                    SampleArrays out) {
+    int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    if (warp >= a.n_rays) return;
+    if (status->bits & kStatusSampleOverflow) return;
+    const RayRec& R = rays[warp];
+    if (R.status != 0) return;
+    uint64_t g = a.ray_begin + uint64_t(warp);
+    uint64_t key = hash_combine(hash_combine(hash_combine(a.seed, kPurposeJitter), a.iter), g);
+    SegPlan p;
+    p.nseg = R.nseg;
+    for (int k = 0; k < R.nseg; ++k) {
+        p.slot[k] = R.slot[k];
+        p.tn[k] = R.tn[k];
+        p.tf[k] = R.tf[k];
+        p.nint[k] = R.nint[k];
+    }
+    const uint32_t lt = (1u << lane) - 1u;
+    long long pend_pos = -1;
+    double pend_t = 0.0;
+    for (int k = 0; k < p.nseg; ++k) {
+        int s = p.slot[k];
+        const double* fr = a.slots.frame[s];
+        const uint32_t* bits = a.occ_bits[s];
+        uint64_t base = P[uint64_t(s) * a.n_rays + warp];
+        uint32_t written = 0;
+        int n = p.nint[k];
+        for (int j0 = 0; j0 <= n; j0 += 32) {
+            int j = j0 + lane;
+            bool valid = j <= n;
+            double t = 0.0;
+            float lx = 0.f, ly = 0.f, lz = 0.f;
+            bool endp = (j == 0 || j == n);
+            bool keep = false;
+            if (valid) {
+                t = sample_t(p, k, j, a.jitter, key);
+                lx = float((R.o[0] + t * R.d[0] - fr[0]) * fr[3]);
+                ly = float((R.o[1] + t * R.d[1] - fr[1]) * fr[4]);
+                lz = float((R.o[2] + t * R.d[2] - fr[2]) * fr[5]);
+                keep = endp || occ_test(bits, lx, ly, lz);
+            }
+            uint32_t mask = __ballot_sync(0xffffffffu, keep);
+            if (mask == 0u) continue;
+            int first = __ffs(mask) - 1;
+            int last = 31 - __clz(mask);
+            double t_first = __shfl_sync(0xffffffffu, t, first);
+            if (lane == 0 && pend_pos >= 0)
+                out.td[pend_pos] = make_float2(float(pend_t), float(t_first - pend_t));
+            uint32_t gt = mask & ~(lt | (1u << lane));
+            int nxt = gt ? (__ffs(gt) - 1) : lane;
+            double t_next = __shfl_sync(0xffffffffu, t, nxt);
+            if (keep) {
+                uint64_t pos = base + written + __popc(mask & lt);
+                out.local[pos] = make_float4(lx, ly, lz, __int_as_float(warp));
+                // the chunk's last kept sample is completed once its successor is known
+                if (gt) out.td[pos] = make_float2(float(t), float(t_next - t));
+                out.endpoint[pos] = endp ? 1 : 0;
+            }
+            uint32_t kept = __popc(mask);
+            pend_pos = (long long)(base + written + kept - 1);
+            pend_t = __shfl_sync(0xffffffffu, t, last);
+            written += kept;
+        }
+    }
+    if (lane == 0 && pend_pos >= 0) {
+        double texit = (a.z_min - R.o[2]) / R.d[2];
+        double r = texit - pend_t;
+        if (r < 0) r = 0;
+        if (r > a.delta_cap) r = a.delta_cap;
+        out.td[pend_pos] = make_float2(float(pend_t), float(r));
+    }
+}
+
+// ------------------------------------------------------------------ host launchers
+int launch_accept(const AcceptArgs& a, uint32_t* flags, uint32_t* pos, uint32_t* block_sums,
+                  uint32_t* n_out, uint64_t* out, cudaStream_t st, uint64_t* launches) {
+    if (a.n_candidates == 0) {
+        cudaMemsetAsync(n_out, 0, 4, st);
+        return 0;
+    }
+    int nb = int((a.n_candidates + 127) / 128);
+    accept_kernel<<<nb, 128, 0, st>>>(a, flags);
+    if (scan_exclusive(flags, a.n_candidates, pos, block_sums, n_out, st, launches)) return 1;
+    accept_scatter_kernel<<<nb, 128, 0, st>>>(a, flags, pos, out);
+    *launches += 2;
+    return 0;
+}
+
+int launch_sampler(const RaygenArgs& a, RayRec* rays, float4* venc, uint32_t* counts,
+                   uint32_t* P, uint32_t* block_sums, TileDesc* tiles, int max_tiles,
+                   SampleArrays out, uint64_t capacity, Status* status, cudaStream_t st,
+                   uint64_t* launches) {
+    raygen_kernel<<<(a.n_rays + 127) / 128, 128, 0, st>>>(a, rays, venc, counts, status);
+    uint64_t n = uint64_t(a.slots.n) * a.n_rays;
+    if (scan_exclusive(counts, n, P, block_sums, nullptr, st, launches)) return 1;
+    tiles_kernel<<<1, 256, 0, st>>>(P, a.n_rays, a.slots.n, capacity, max_tiles, tiles, status);
+    write_kernel<<<(a.n_rays * 32 + 255) / 256, 256, 0, st>>>(a, rays, P, status, out);
+    *launches += 3;
+    return 0;
+}
+
+} // namespace tfg

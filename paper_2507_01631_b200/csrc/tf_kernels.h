@@ -1,0 +1,139 @@
+// tf_kernels.h — launch interfaces of the hot-path kernels (internal to
+// libtilefield_gpu.so; the public boundary is include/tilefield_gpu.h).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "tf_common.cuh"
+
+namespace tfg {
+
+// Per-sample arrays in slot-bucketed order (bucket s holds the samples of
+// slot s, rays ascending, each ray's segment samples contiguous).
+struct SampleArrays {
+    float4* local;     // x, y, z (owning tile's [0,1]^3 frame), w = ray index bits
+    float2* td;        // t (m along the ray), delta (m)
+    uint8_t* endpoint; // 1 for segment endpoints
+    float4* io;        // K2: (sigma, r, g, b); K3 overwrites with (dsigma, dr, dg, db)
+};
+
+// Hash-grid level layout (HashGridT::init, nn.hpp:180-195).
+struct HashLayout {
+    int res[kLevels];
+    uint32_t off[kLevels];  // entry offset of the level
+    int dense[kLevels];     // 1 when (res+1)^3 <= T (direct indexing)
+};
+
+struct AcceptArgs {
+    const tfg_rpc* cams;
+    int n_views;
+    const uint64_t* view_start;  // candidate offset of each view (n_views)
+    const int* union_rect;       // r0, r1, c0, c1 per view
+    const int* crop_rect;        // r0, r1, c0, c1 per (view, loaded slot); empty: r0 >= r1
+    uint64_t n_candidates;
+    const double* east;          // grid_cols + 1 shared edges (tiler.cpp:18-27)
+    const double* north;         // grid_rows + 1
+    int grid_rows, grid_cols;
+    int loaded_tile[kTrainSlots];
+    int n_loaded;
+    double z_min, z_max;
+};
+
+struct RaygenArgs {
+    const tfg_rpc* cams;
+    const uint64_t* accept;  // draw mode: accepted list
+    uint64_t n_accept;
+    const int32_t* pixels;   // pixel mode (render/eval): view,row,col triplets
+    const uint8_t* crop_bytes;
+    const int* crop_rect;        // r0, c0, cols, rows per view
+    const uint64_t* crop_offset; // byte offset of each view's crop
+    uint64_t seed, iter, ray_begin;
+    int n_rays;
+    int jitter;
+    double z_min, z_max;
+    double spm;
+    int cap;
+    double delta_cap;
+    SlotTable slots;
+    const uint32_t* occ_bits[kMaxSlots];
+};
+
+struct FieldArgs {
+    FieldPtrs f;
+    HashLayout hl;
+    float density_max, density_lim;  // lim = log(density_max) (nn.hpp:272)
+    const TileDesc* tiles;
+    const Status* status;
+    const float4* venc;  // 6 float4 per ray
+    SampleArrays s;
+};
+
+struct FieldGradArgs {
+    float* g_enc[kMaxSlots];
+    float* g_dnet[kMaxSlots];
+    float* g_color;
+};
+
+struct CompositeArgs {
+    const RayRec* rays;
+    const uint32_t* P;   // bucket positions [slot][ray]
+    int n_rays;
+    SampleArrays s;
+    const Status* status_in;
+    Status* status;
+    float3 bg;
+    float inv3b;         // 1 / (3 B_global)
+    int backward;
+    float* ray_rgb;      // 3 per ray (may be null)
+    float* ray_depth;
+    float* ray_opacity;
+};
+
+struct AdamGroup {
+    uint64_t offset, count;
+    float lr, bc1, bc2;
+    int pad;
+};
+constexpr int kMaxGroups = 2 * kTrainSlots + 1;
+struct AdamArgs {
+    float* params;
+    const float* grads;
+    float* m;
+    float* v;
+    AdamGroup g[kMaxGroups];
+    int n_groups;
+    float beta1, beta2, omb1, omb2, eps;
+    uint32_t* group_flags;  // non-finite flag per group
+    Status* status;
+};
+
+struct OccArgs {
+    HashLayout hl;
+    float density_lim;
+    const float* enc[kTrainSlots];
+    const float* dnet[kTrainSlots];
+    float* ema[kTrainSlots];
+    uint32_t* bits[kTrainSlots];
+    uint64_t base_key[kTrainSlots];  // hash_combine(seed, OCC, row, col, dnet_step)
+    int n;
+    float decay, threshold, density_max;
+    int update;  // 0: only recompute bits from the EMA
+};
+
+int scan_exclusive(const uint32_t* in, uint64_t n, uint32_t* out, uint32_t* block_sums,
+                   uint32_t* grand_total, cudaStream_t st, uint64_t* launches);
+int launch_accept(const AcceptArgs& a, uint32_t* flags, uint32_t* pos, uint32_t* block_sums,
+                  uint32_t* n_out, uint64_t* out, cudaStream_t st, uint64_t* launches);
+int launch_sampler(const RaygenArgs& a, RayRec* rays, float4* venc, uint32_t* counts,
+                   uint32_t* P, uint32_t* block_sums, TileDesc* tiles, int max_tiles,
+                   SampleArrays out, uint64_t capacity, Status* status, cudaStream_t st,
+                   uint64_t* launches);
+void launch_field_forward(const FieldArgs& a, int grid, cudaStream_t st, uint64_t* launches);
+void launch_field_backward(const FieldArgs& a, const FieldGradArgs& g, int grid, cudaStream_t st,
+                           uint64_t* launches);
+void launch_composite(const CompositeArgs& a, cudaStream_t st, uint64_t* launches);
+void launch_adam(const AdamArgs& a, uint64_t total, cudaStream_t st, uint64_t* launches);
+void launch_occupancy(const OccArgs& a, cudaStream_t st, uint64_t* launches);
+
+
+} // namespace tfg

@@ -1,0 +1,1411 @@
+// tfg_api.cu — the C-ABI (include/tilefield_gpu.h) over the B200 kernels:
+// context and HBM layout, scene + crops, the out-of-core window slide
+// (scheduler advance) between pinned host records and HBM on a
+// side stream, the training-iteration driver and the render path.
+//
+// HBM layout (allocated once in tfg_create / tfg_set_scene; constant across
+// the snake progression):
+//   params / grads / m / v : flat [slot0 enc | slot0 dnet | ... | slot3 | colour]
+//                            1,752,595 floats each (the allreduce / Adam span)
+//   ema / bits             : 4 x 32^3 occupancy EMA + 4 x 4 KB bitfields
+//   crops                  : per-view union of the window's 4 tile crops (u8 RGB)
+//   accept                 : packed (view, row, col) accepted-ray list
+//   batch                  : RayRec per ray, 24-float view encoding per ray,
+//                            slot-bucketed SoA samples (local+ray, t+delta,
+//                            endpoint, sigma/rgb -> dsigma/drgb)
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "tf_common.cuh"
+#include "tf_kernels.h"
+
+using namespace tfg;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CK(call)                                                                            \
+    do {                                                                                    \
+        cudaError_t e_ = (call);                                                            \
+        if (e_ != cudaSuccess)                                                              \
+            return fail(TFG_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+// ---------------------------------------------------------------- host-side field init
+// TileField::create / GlobalColorNet::create (field.hpp:93,118) with the
+// per-tile streams Rng(hash_combine(seed, purpose, row, col)): HashGridT::init
+// U(-1e-4, 1e-4) (nn.hpp:194), MlpT::init Xavier-uniform + zero bias (nn.hpp:70-81).
+void mlp_init_host(const int* w, int nw, Rng& rng, float* p) {
+    size_t k = 0;
+    for (int l = 0; l + 1 < nw; ++l) {
+        int fi = w[l], fo = w[l + 1];
+        float bound = float(std::sqrt(6.0 / (fi + fo)));
+        for (int i = 0; i < fo * fi; ++i) p[k++] = float(rng.uniform(-double(bound), double(bound)));
+        for (int i = 0; i < fo; ++i) p[k++] = 0.f;
+    }
+}
+
+int level_resolution(const tfg_field_config& c, int l) {
+    if (c.levels <= 1) return c.n_min;
+    double b = std::exp((std::log(double(c.n_max)) - std::log(double(c.n_min))) /
+                        double(c.levels - 1));
+    return int(std::floor(c.n_min * std::pow(b, l) + 0.5));
+}
+
+struct TileHost {
+    bool created = false;
+    float* rec = nullptr;  // pinned: [params(stride) | m(stride) | v(stride) | ema(32^3)]
+    uint64_t enc_step = 0, dnet_step = 0;
+};
+
+struct Crop {
+    int r0 = 0, r1 = 0, c0 = 0, c1 = 0;
+    bool empty() const { return r0 >= r1 || c0 >= c1; }
+};
+
+} // namespace
+
+struct tfg_ctx {
+    int device = 0;
+    int sms = 148;
+    cudaStream_t st = nullptr, side = nullptr;
+    bool own_stream = true;
+    cudaEvent_t ev_main = nullptr, ev_side = nullptr;
+    tfg_field_config fc{};
+    tfg_train_config tc{};
+    HashLayout hl{};
+    uint64_t enc_n = 0, stride = 0, n_params = 0, color_off = 0;
+    float density_lim = 0.f;
+    int max_rays = 0;
+    uint64_t sample_cap = 0;
+    int max_tiles = 0;
+    uint64_t launches = 0;
+
+    // parameters / optimizer
+    float *d_params = nullptr, *d_grads = nullptr, *d_m = nullptr, *d_v = nullptr;
+    float* d_ema = nullptr;
+    uint32_t* d_bits = nullptr;
+    uint32_t* d_group_flags = nullptr;
+    Status* d_status = nullptr;
+    Status* h_status = nullptr;
+    uint64_t color_step = 0;
+
+    // scene
+    int n_views = 0;
+    std::vector<tfg_rpc> cams;
+    tfg_rpc* d_cams = nullptr;
+    std::vector<uint8_t*> h_images;
+    tfg_roi roi{};
+    int rows = 0, cols = 0;
+    std::vector<double> east, north;
+    double *d_east = nullptr, *d_north = nullptr;
+    std::vector<TileHost> tiles;
+
+    // window
+    int pos_r = -1, pos_c = -1;
+    int nslots = 0;
+    int slot_tile[kTrainSlots] = {-1, -1, -1, -1};
+    SlotTable slots{};
+
+    // crops + accept list
+    uint8_t* d_crops = nullptr;
+    uint64_t crop_cap = 0;
+    int* d_crop_rect = nullptr;        // r0, c0, cols, rows per view
+    uint64_t* d_crop_off = nullptr;
+    std::vector<int> h_crop_rect;
+    std::vector<uint64_t> h_crop_off;
+    uint64_t* d_accept = nullptr;
+    uint64_t accept_cap = 0, cand_cap = 0;
+    uint32_t *d_flags = nullptr, *d_pos = nullptr, *d_block_sums = nullptr, *d_accept_n = nullptr;
+    uint64_t* d_view_start = nullptr;
+    int *d_union = nullptr, *d_crop4 = nullptr;
+    uint64_t n_accept = 0;
+
+    // batch
+    RayRec* d_rays = nullptr;
+    float4* d_venc = nullptr;
+    uint32_t *d_counts = nullptr, *d_P = nullptr;
+    TileDesc* d_tiles = nullptr;
+    SampleArrays s{};
+    float* d_ray_out = nullptr;  // rgb(3) | depth | opacity per ray
+    int32_t* d_pixels = nullptr;
+    int cur_rays = 0;
+    bool have_batch = false;
+    bool render_mode = false;
+
+    // render
+    float* d_rparams = nullptr;  // kMaxSlots * stride
+    uint32_t* d_rbits = nullptr;
+    float* d_rcolor = nullptr;
+    int rn = 0;
+    SlotTable rslots{};
+    tfg_rpc* d_rcam = nullptr;
+
+    uint64_t bytes_total = 0;
+};
+
+namespace {
+
+template <typename T>
+int dalloc(tfg_ctx* c, T** p, uint64_t n) {
+    if (n == 0) n = 1;
+    CK(cudaMalloc(reinterpret_cast<void**>(p), n * sizeof(T)));
+    c->bytes_total += n * sizeof(T);
+    return 0;
+}
+
+void tile_box(const tfg_ctx* c, int ti, double* b) {
+    int r = ti / c->cols, cc = ti % c->cols;
+    b[0] = c->east[cc];
+    b[1] = c->north[r];
+    b[2] = c->roi.z_min;
+    b[3] = c->east[cc + 1];
+    b[4] = c->north[r + 1];
+    b[5] = c->roi.z_max;
+}
+
+// crop_for_tile (camera.cpp:126-146) on the host; false when empty/invalid.
+bool crop_for_tile(const tfg_rpc& cam, const double* box, int margin, Crop* out) {
+    double rlo = HUGE_VAL, rhi = -HUGE_VAL, clo = HUGE_VAL, chi = -HUGE_VAL;
+    for (int i = 0; i < 8; ++i) {
+        double x = (i & 1) ? box[3] : box[0];
+        double y = (i & 2) ? box[4] : box[1];
+        double z = (i & 4) ? box[5] : box[2];
+        double r, q;
+        if (!rpc_project(cam, x, y, z, &r, &q)) return false;
+        rlo = std::min(rlo, r);
+        rhi = std::max(rhi, r);
+        clo = std::min(clo, q);
+        chi = std::max(chi, q);
+    }
+    out->r0 = std::max(0, int(std::floor(rlo)) - margin);
+    out->r1 = std::min(cam.image_rows, int(std::ceil(rhi)) + 1 + margin);
+    out->c0 = std::max(0, int(std::floor(clo)) - margin);
+    out->c1 = std::min(cam.image_cols, int(std::ceil(chi)) + 1 + margin);
+    return !out->empty();
+}
+
+std::vector<int> window_tiles(const tfg_ctx* c, int pr, int pc) {
+    if (c->rows == 1 && c->cols == 1) return {0};
+    return {pr * c->cols + pc, pr * c->cols + pc + 1, (pr + 1) * c->cols + pc,
+            (pr + 1) * c->cols + pc + 1};
+}
+
+// Per view: crop rects of the window's tiles and their union.
+void window_crops(const tfg_ctx* c, const std::vector<int>& tl, std::vector<Crop>& crops,
+                  std::vector<Crop>& uni) {
+    crops.assign(size_t(c->n_views) * kTrainSlots, Crop{});
+    uni.assign(c->n_views, Crop{});
+    for (int v = 0; v < c->n_views; ++v) {
+        Crop u{INT32_MAX, INT32_MIN, INT32_MAX, INT32_MIN};
+        bool any = false;
+        for (size_t k = 0; k < tl.size(); ++k) {
+            double b[6];
+            tile_box(c, tl[k], b);
+            Crop cr;
+            if (!crop_for_tile(c->cams[v], b, c->tc.margin_px, &cr)) continue;
+            crops[size_t(v) * kTrainSlots + k] = cr;
+            u.r0 = std::min(u.r0, cr.r0);
+            u.r1 = std::max(u.r1, cr.r1);
+            u.c0 = std::min(u.c0, cr.c0);
+            u.c1 = std::max(u.c1, cr.c1);
+            any = true;
+        }
+        uni[v] = any ? u : Crop{};
+    }
+}
+
+void fresh_tile(tfg_ctx* c, int ti) {
+    TileHost& t = c->tiles[ti];
+    int row = ti / c->cols, col = ti % c->cols;
+    float* p = t.rec;
+    Rng re(hash_combine(hash_combine(hash_combine(c->tc.seed, kPurposeTileEnc), uint64_t(row)),
+                        uint64_t(col)));
+    for (uint64_t i = 0; i < c->enc_n; ++i) p[i] = float(re.uniform(-1e-4, 1e-4));
+    Rng rd(hash_combine(hash_combine(hash_combine(c->tc.seed, kPurposeTileDnet), uint64_t(row)),
+                        uint64_t(col)));
+    const int dw[3] = {kFeatDim, kDHidden, kDOut};
+    mlp_init_host(dw, 3, rd, p + c->enc_n);
+    std::memset(p + c->stride, 0, 2 * c->stride * sizeof(float));
+    float* ema = p + 3 * c->stride;
+    for (int i = 0; i < kOccVox; ++i) ema[i] = 1.0f;
+    t.enc_step = t.dnet_step = 0;
+    t.created = true;
+}
+
+int ensure_record(tfg_ctx* c, int ti) {
+    TileHost& t = c->tiles[ti];
+    if (!t.rec) {
+        CK(cudaHostAlloc(reinterpret_cast<void**>(&t.rec),
+                         (3 * c->stride + kOccVox) * sizeof(float), cudaHostAllocDefault));
+    }
+    if (!t.created) fresh_tile(c, ti);
+    return 0;
+}
+
+// D2H (evict) / H2D (load) of one slot's state on the side stream.
+int slot_copy(tfg_ctx* c, int slot, int ti, bool to_host) {
+    TileHost& t = c->tiles[ti];
+    uint64_t off = uint64_t(slot) * c->stride;
+    size_t bytes = c->stride * sizeof(float);
+    cudaMemcpyKind k = to_host ? cudaMemcpyDeviceToHost : cudaMemcpyHostToDevice;
+    float* dev[3] = {c->d_params + off, c->d_m + off, c->d_v + off};
+    for (int a = 0; a < 3; ++a) {
+        float* h = t.rec + a * c->stride;
+        CK(cudaMemcpyAsync(to_host ? static_cast<void*>(h) : static_cast<void*>(dev[a]),
+                           to_host ? static_cast<const void*>(dev[a]) : static_cast<const void*>(h),
+                           bytes, k, c->side));
+    }
+    float* de = c->d_ema + uint64_t(slot) * kOccVox;
+    float* he = t.rec + 3 * c->stride;
+    CK(cudaMemcpyAsync(to_host ? static_cast<void*>(he) : static_cast<void*>(de),
+                       to_host ? static_cast<const void*>(de) : static_cast<const void*>(he),
+                       kOccVox * sizeof(float), k, c->side));
+    return 0;
+}
+
+void fill_slots(tfg_ctx* c) {
+    c->slots.n = c->nslots;
+    for (int k = 0; k < c->nslots; ++k) {
+        double b[6];
+        tile_box(c, c->slot_tile[k], b);
+        for (int q = 0; q < 6; ++q) c->slots.box[k][q] = b[q];
+        for (int q = 0; q < 3; ++q) {
+            c->slots.frame[k][q] = b[q];
+            c->slots.frame[k][3 + q] = 1.0 / (b[3 + q] - b[q]);  // cwiseInverse (tiler.cpp:49)
+        }
+    }
+}
+
+FieldPtrs train_ptrs(tfg_ctx* c) {
+    FieldPtrs f{};
+    for (int k = 0; k < c->nslots; ++k) {
+        f.enc[k] = c->d_params + uint64_t(k) * c->stride;
+        f.dnet[k] = f.enc[k] + c->enc_n;
+        f.occ_bits[k] = c->d_bits + uint64_t(k) * kOccWords;
+    }
+    f.color = c->d_params + c->color_off;
+    return f;
+}
+
+int run_occupancy(tfg_ctx* c, bool update, uint64_t* keys) {
+    OccArgs o{};
+    o.hl = c->hl;
+    o.density_lim = c->density_lim;
+    o.n = c->nslots;
+    for (int k = 0; k < c->nslots; ++k) {
+        o.enc[k] = c->d_params + uint64_t(k) * c->stride;
+        o.dnet[k] = o.enc[k] + c->enc_n;
+        o.ema[k] = c->d_ema + uint64_t(k) * kOccVox;
+        o.bits[k] = c->d_bits + uint64_t(k) * kOccWords;
+        o.base_key[k] = keys ? keys[k] : 0;
+    }
+    o.decay = c->fc.occupancy_decay;
+    o.threshold = c->fc.occupancy_threshold;
+    o.density_max = c->fc.density_max;
+    o.update = update ? 1 : 0;
+    launch_occupancy(o, c->st, &c->launches);
+    CK(cudaGetLastError());
+    return 0;
+}
+
+int build_accept(tfg_ctx* c, const std::vector<Crop>& crops, const std::vector<Crop>& uni) {
+    std::vector<uint64_t> vs(c->n_views);
+    std::vector<int> urect(4 * c->n_views), crect(4 * c->n_views * kTrainSlots);
+    uint64_t n = 0;
+    for (int v = 0; v < c->n_views; ++v) {
+        vs[v] = n;
+        const Crop& u = uni[v];
+        urect[4 * v] = u.r0;
+        urect[4 * v + 1] = u.r1;
+        urect[4 * v + 2] = u.c0;
+        urect[4 * v + 3] = u.c1;
+        if (!u.empty()) n += uint64_t(u.r1 - u.r0) * uint64_t(u.c1 - u.c0);
+        else urect[4 * v + 1] = urect[4 * v], urect[4 * v + 3] = urect[4 * v + 2] + 1;
+        for (int k = 0; k < kTrainSlots; ++k) {
+            const Crop& cr = crops[size_t(v) * kTrainSlots + k];
+            int* d = &crect[4 * (v * kTrainSlots + k)];
+            d[0] = cr.r0;
+            d[1] = cr.r1;
+            d[2] = cr.c0;
+            d[3] = cr.c1;
+        }
+    }
+    if (n > c->cand_cap) return fail(TFG_ERR_INVALID, "accept: candidate capacity exceeded");
+    CK(cudaMemcpyAsync(c->d_view_start, vs.data(), vs.size() * 8, cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(c->d_union, urect.data(), urect.size() * 4, cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(c->d_crop4, crect.data(), crect.size() * 4, cudaMemcpyHostToDevice, c->st));
+    AcceptArgs a{};
+    a.cams = c->d_cams;
+    a.n_views = c->n_views;
+    a.view_start = c->d_view_start;
+    a.union_rect = c->d_union;
+    a.crop_rect = c->d_crop4;
+    a.n_candidates = n;
+    a.east = c->d_east;
+    a.north = c->d_north;
+    a.grid_rows = c->rows;
+    a.grid_cols = c->cols;
+    for (int k = 0; k < kTrainSlots; ++k) a.loaded_tile[k] = k < c->nslots ? c->slot_tile[k] : -1;
+    a.n_loaded = c->nslots;
+    a.z_min = c->roi.z_min;
+    a.z_max = c->roi.z_max;
+    if (launch_accept(a, c->d_flags, c->d_pos, c->d_block_sums, c->d_accept_n, c->d_accept, c->st,
+                      &c->launches))
+        return fail(TFG_ERR_INVALID, "accept: scan capacity exceeded");
+    CK(cudaGetLastError());
+    uint32_t nacc = 0;
+    CK(cudaMemcpyAsync(&c->h_status->pad, c->d_accept_n, 4, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    nacc = c->h_status->pad;
+    c->n_accept = nacc;
+    return 0;
+}
+
+int check_status(tfg_ctx* c) {
+    Status& s = *c->h_status;
+    if (s.bits & kStatusSampleOverflow)
+        return fail(TFG_ERR_INVALID, "sample: batch exceeds the sample capacity of the context");
+    if (s.bits & kStatusSegOverflow) return fail(TFG_ERR_INVALID, "sample: more than 8 segments");
+    if (s.bits & kStatusRayFail)
+        return fail(TFG_ERR_INVALID, "sample: ray_from_pixel failed for a drawn pixel");
+    if (s.bits & kStatusNonFinite) {
+        int g = int(s.nonfinite_group);
+        char nm[96];
+        if (g >= 2 * c->nslots) {
+            std::snprintf(nm, sizeof nm, "color");
+        } else {
+            int ti = c->slot_tile[g / 2];
+            std::snprintf(nm, sizeof nm, "tile(%d,%d).%s", ti / c->cols, ti % c->cols,
+                          (g % 2) ? "dnet" : "enc");
+        }
+        return fail(TFG_ERR_NONFINITE,
+                    std::string("adam_step: non-finite gradient in group ") + nm);
+    }
+    return 0;
+}
+
+int sync_status(tfg_ctx* c) {
+    CK(cudaMemcpyAsync(c->h_status, c->d_status, sizeof(Status), cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    return check_status(c);
+}
+
+RaygenArgs base_raygen(tfg_ctx* c) {
+    RaygenArgs a{};
+    a.cams = c->d_cams;
+    a.seed = c->tc.seed;
+    a.z_min = c->roi.z_min;
+    a.z_max = c->roi.z_max;
+    a.spm = c->tc.samples_per_meter;
+    a.cap = c->tc.max_samples_per_ray;
+    a.delta_cap = c->tc.delta_cap;
+    a.slots = c->slots;
+    for (int k = 0; k < c->nslots; ++k) a.occ_bits[k] = c->d_bits + uint64_t(k) * kOccWords;
+    a.crop_bytes = c->d_crops;
+    a.crop_rect = c->d_crop_rect;
+    a.crop_offset = c->d_crop_off;
+    return a;
+}
+
+int run_sampler(tfg_ctx* c, RaygenArgs& a) {
+    if (a.n_rays <= 0 || a.n_rays > c->max_rays)
+        return fail(TFG_ERR_INVALID, "sample: n_rays outside (0, max_rays]");
+    CK(cudaMemsetAsync(c->d_status, 0, sizeof(Status), c->st));
+    if (launch_sampler(a, c->d_rays, c->d_venc, c->d_counts, c->d_P, c->d_block_sums, c->d_tiles,
+                       c->max_tiles, c->s, c->sample_cap, c->d_status, c->st, &c->launches))
+        return fail(TFG_ERR_INVALID, "sample: scan capacity exceeded");
+    CK(cudaGetLastError());
+    c->cur_rays = a.n_rays;
+    c->have_batch = true;
+    return 0;
+}
+
+FieldArgs field_args(tfg_ctx* c, const FieldPtrs& f) {
+    FieldArgs a{};
+    a.f = f;
+    a.hl = c->hl;
+    a.density_max = c->fc.density_max;
+    a.density_lim = c->density_lim;
+    a.tiles = c->d_tiles;
+    a.status = c->d_status;
+    a.venc = c->d_venc;
+    a.s = c->s;
+    return a;
+}
+
+int run_forward(tfg_ctx* c, const FieldPtrs& f) {
+    launch_field_forward(field_args(c, f), 2 * c->sms, c->st, &c->launches);
+    CK(cudaGetLastError());
+    return 0;
+}
+
+int run_composite(tfg_ctx* c, bool backward) {
+    CompositeArgs a{};
+    a.rays = c->d_rays;
+    a.P = c->d_P;
+    a.n_rays = c->cur_rays;
+    a.s = c->s;
+    a.status_in = c->d_status;
+    a.status = c->d_status;
+    a.bg = make_float3(c->tc.background[0], c->tc.background[1], c->tc.background[2]);
+    a.inv3b = 1.0f / (3.0f * float(c->tc.batch_rays));
+    a.backward = backward ? 1 : 0;
+    a.ray_rgb = c->d_ray_out;
+    a.ray_depth = c->d_ray_out + 3 * uint64_t(c->max_rays);
+    a.ray_opacity = c->d_ray_out + 4 * uint64_t(c->max_rays);
+    launch_composite(a, c->st, &c->launches);
+    CK(cudaGetLastError());
+    return 0;
+}
+
+int run_backward(tfg_ctx* c) {
+    CK(cudaMemsetAsync(c->d_grads, 0, c->n_params * sizeof(float), c->st));
+    FieldGradArgs g{};
+    for (int k = 0; k < c->nslots; ++k) {
+        g.g_enc[k] = c->d_grads + uint64_t(k) * c->stride;
+        g.g_dnet[k] = g.g_enc[k] + c->enc_n;
+    }
+    g.g_color = c->d_grads + c->color_off;
+    launch_field_backward(field_args(c, train_ptrs(c)), g, c->sms, c->st, &c->launches);
+    CK(cudaGetLastError());
+    return 0;
+}
+
+// Per-sample host reorder: bucket order -> ray order (RaySegmentBatch layout).
+struct HostBatch {
+    std::vector<RayRec> rays;
+    std::vector<uint32_t> P;
+    uint64_t n_samples = 0;
+};
+int fetch_batch_meta(tfg_ctx* c, HostBatch& hb) {
+    int n = c->cur_rays;
+    hb.rays.resize(n);
+    uint64_t np = uint64_t(c->slots.n) * n + 1;
+    hb.P.resize(np);
+    CK(cudaMemcpyAsync(hb.rays.data(), c->d_rays, n * sizeof(RayRec), cudaMemcpyDeviceToHost, c->st));
+    CK(cudaMemcpyAsync(hb.P.data(), c->d_P, np * 4, cudaMemcpyDeviceToHost, c->st));
+    int st = sync_status(c);
+    if (st) return st;
+    hb.n_samples = c->h_status->n_samples;
+    return 0;
+}
+// Visits samples in ray order: fn(ray, sample index in ray order, bucket pos, slot).
+template <typename F>
+void for_samples(const tfg_ctx* c, const HostBatch& hb, F fn) {
+    uint64_t q = 0;
+    int n = c->cur_rays;
+    for (int i = 0; i < n; ++i) {
+        const RayRec& R = hb.rays[i];
+        if (R.status != 0) continue;
+        for (int k = 0; k < R.nseg; ++k) {
+            uint64_t base = hb.P[uint64_t(R.slot[k]) * n + i];
+            for (int j = 0; j < R.cnt[k]; ++j) fn(i, q++, base + j, int(R.slot[k]));
+        }
+    }
+}
+
+} // namespace
+
+extern "C" {
+
+TFG_API const char* tfg_last_error(void) { return g_err.c_str(); }
+
+TFG_API int tfg_default_field_config(tfg_field_config* o) {
+    *o = tfg_field_config{8, 1 << 15, 2, 16, 256, 64, 15, 64, 2, 4, 1e4f, 32, 0.95f, 0.02f, 16};
+    return 0;
+}
+
+TFG_API int tfg_default_train_config(tfg_train_config* o) {
+    std::memset(o, 0, sizeof(*o));
+    o->seed = 2;
+    o->samples_per_meter = 63.0 / 40.0;
+    o->max_samples_per_ray = 1024;
+    o->delta_cap = 10.0;
+    o->background[0] = o->background[1] = o->background[2] = 0.5f;
+    o->margin_px = 4;
+    o->lr_field = 1e-2;
+    o->lr_color = 1e-3;
+    o->lr_decay_rate = 1.0;
+    o->lr_decay_steps = 1000;
+    o->beta1 = 0.9f;
+    o->beta2 = 0.99f;
+    o->eps = 1e-15f;
+    o->batch_rays = 65536;
+    return 0;
+}
+
+TFG_API int tfg_param_counts(const tfg_field_config* c, uint64_t* enc, uint64_t* dnet,
+                             uint64_t* color) {
+    uint64_t tot = 0;
+    for (int l = 0; l < c->levels; ++l) {
+        uint64_t r = uint64_t(level_resolution(*c, l)) + 1;
+        tot += std::min<uint64_t>(r * r * r, uint64_t(c->table_size));
+    }
+    if (enc) *enc = tot * c->features;
+    auto mlp = [](std::vector<int> w) {
+        uint64_t n = 0;
+        for (size_t l = 0; l + 1 < w.size(); ++l) n += uint64_t(w[l + 1]) * w[l] + w[l + 1];
+        return n;
+    };
+    if (dnet) *dnet = mlp({c->levels * c->features, c->density_hidden, 1 + c->embedding});
+    std::vector<int> cw{c->embedding + 6 * c->view_freqs};
+    for (int i = 0; i < c->color_layers; ++i) cw.push_back(c->color_hidden);
+    cw.push_back(3);
+    if (color) *color = mlp(cw);
+    return 0;
+}
+
+TFG_API int tfg_create(const tfg_field_config* fcfg, const tfg_train_config* tcfg, int device,
+                       int max_rays, tfg_ctx** out) {
+    if (!fcfg || !tcfg || !out || max_rays <= 0) return fail(TFG_ERR_INVALID, "create: bad arguments");
+    tfg_field_config d;
+    tfg_default_field_config(&d);
+    if (fcfg->levels != d.levels || fcfg->table_size != d.table_size ||
+        fcfg->features != d.features || fcfg->density_hidden != d.density_hidden ||
+        fcfg->embedding != d.embedding || fcfg->color_hidden != d.color_hidden ||
+        fcfg->color_layers != d.color_layers || fcfg->view_freqs != d.view_freqs ||
+        fcfg->occupancy_resolution != d.occupancy_resolution)
+        return fail(TFG_ERR_INVALID, "create: the sm_100a kernels are specialised for the default "
+                                     "FieldConfig shapes (nn.hpp:14-37)");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0 || device >= ndev)
+        return fail(TFG_ERR_NO_DEVICE, "create: no CUDA device (there is no CPU fallback)");
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+        return fail(TFG_ERR_NO_DEVICE, std::string("create: needs an sm_100 device, found ") + prop.name);
+    CK(cudaSetDevice(device));
+    auto* c = new tfg_ctx();
+    c->device = device;
+    c->sms = prop.multiProcessorCount;
+    c->fc = *fcfg;
+    c->tc = *tcfg;
+    c->max_rays = max_rays;
+    uint64_t enc, dn, col;
+    tfg_param_counts(fcfg, &enc, &dn, &col);
+    c->enc_n = enc;
+    c->stride = enc + dn;
+    c->color_off = kTrainSlots * c->stride;
+    c->n_params = c->color_off + col;
+    uint32_t off = 0;
+    for (int l = 0; l < kLevels; ++l) {
+        int r = level_resolution(*fcfg, l);
+        uint64_t dense = uint64_t(r + 1) * (r + 1) * (r + 1);
+        c->hl.res[l] = r;
+        c->hl.off[l] = off;
+        c->hl.dense[l] = dense <= uint64_t(kTable) ? 1 : 0;
+        off += uint32_t(std::min<uint64_t>(dense, kTable));
+    }
+    c->density_lim = std::log(fcfg->density_max);
+    c->sample_cap = uint64_t(max_rays) * 160;
+    c->max_tiles = int(c->sample_cap / 128 + kMaxSlots + 1);
+    int rc = 0;
+    CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&c->ev_main, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->ev_side, cudaEventDisableTiming));
+    rc |= dalloc(c, &c->d_params, c->n_params);
+    rc |= dalloc(c, &c->d_grads, c->n_params);
+    rc |= dalloc(c, &c->d_m, c->n_params);
+    rc |= dalloc(c, &c->d_v, c->n_params);
+    rc |= dalloc(c, &c->d_ema, uint64_t(kTrainSlots) * kOccVox);
+    rc |= dalloc(c, &c->d_bits, uint64_t(kMaxSlots) * kOccWords);
+    rc |= dalloc(c, &c->d_group_flags, 16);
+    rc |= dalloc(c, &c->d_status, 1);
+    rc |= dalloc(c, &c->d_rays, max_rays);
+    rc |= dalloc(c, &c->d_venc, uint64_t(max_rays) * 6);
+    rc |= dalloc(c, &c->d_counts, uint64_t(max_rays) * kMaxSlots);
+    rc |= dalloc(c, &c->d_P, uint64_t(max_rays) * kMaxSlots + 1);
+    rc |= dalloc(c, &c->d_tiles, c->max_tiles);
+    rc |= dalloc(c, &c->s.local, c->sample_cap);
+    rc |= dalloc(c, &c->s.td, c->sample_cap);
+    rc |= dalloc(c, &c->s.endpoint, c->sample_cap);
+    rc |= dalloc(c, &c->s.io, c->sample_cap);
+    rc |= dalloc(c, &c->d_ray_out, uint64_t(max_rays) * 5);
+    rc |= dalloc(c, &c->d_pixels, uint64_t(max_rays) * 3);
+    rc |= dalloc(c, &c->d_block_sums, 4096 + 64);
+    rc |= dalloc(c, &c->d_accept_n, 1);
+    rc |= dalloc(c, &c->d_rcam, 1);
+    if (rc) {
+        delete c;
+        return TFG_ERR_CUDA;
+    }
+    CK(cudaHostAlloc(reinterpret_cast<void**>(&c->h_status), sizeof(Status), cudaHostAllocDefault));
+    CK(cudaMemsetAsync(c->d_params, 0, c->n_params * 4, c->st));
+    CK(cudaMemsetAsync(c->d_m, 0, c->n_params * 4, c->st));
+    CK(cudaMemsetAsync(c->d_v, 0, c->n_params * 4, c->st));
+    CK(cudaMemsetAsync(c->d_grads, 0, c->n_params * 4, c->st));
+    CK(cudaMemsetAsync(c->d_status, 0, sizeof(Status), c->st));
+    // GlobalColorNet::create (field.hpp:118)
+    std::vector<float> color(col);
+    Rng rcn(hash_combine(c->tc.seed, kPurposeColor));
+    const int cw[4] = {kCIn, kCHidden, kCHidden, 3};
+    mlp_init_host(cw, 4, rcn, color.data());
+    CK(cudaMemcpyAsync(c->d_params + c->color_off, color.data(), col * 4, cudaMemcpyHostToDevice, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    *out = c;
+    return 0;
+}
+
+TFG_API int tfg_destroy(tfg_ctx* c) {
+    if (!c) return 0;
+    cudaSetDevice(c->device);
+    cudaDeviceSynchronize();
+    void* dev[] = {c->d_params, c->d_grads, c->d_m, c->d_v, c->d_ema, c->d_bits, c->d_group_flags,
+                   c->d_status, c->d_cams, c->d_east, c->d_north, c->d_crops, c->d_crop_rect,
+                   c->d_crop_off, c->d_accept, c->d_flags, c->d_pos, c->d_block_sums,
+                   c->d_accept_n, c->d_view_start, c->d_union, c->d_crop4, c->d_rays, c->d_venc,
+                   c->d_counts, c->d_P, c->d_tiles, c->s.local, c->s.td, c->s.endpoint, c->s.io,
+                   c->d_ray_out, c->d_pixels, c->d_rparams, c->d_rbits, c->d_rcolor, c->d_rcam};
+    for (void* p : dev)
+        if (p) cudaFree(p);
+    for (auto& t : c->tiles)
+        if (t.rec) cudaFreeHost(t.rec);
+    for (auto* im : c->h_images)
+        if (im) cudaFreeHost(im);
+    if (c->h_status) cudaFreeHost(c->h_status);
+    if (c->ev_main) cudaEventDestroy(c->ev_main);
+    if (c->ev_side) cudaEventDestroy(c->ev_side);
+    if (c->side) cudaStreamDestroy(c->side);
+    if (c->own_stream && c->st) cudaStreamDestroy(c->st);
+    delete c;
+    return 0;
+}
+
+TFG_API int tfg_set_stream(tfg_ctx* c, void* stream) {
+    if (!c) return fail(TFG_ERR_INVALID, "set_stream: null context");
+    CK(cudaStreamSynchronize(c->st));
+    if (c->own_stream && c->st) cudaStreamDestroy(c->st);
+    c->st = static_cast<cudaStream_t>(stream);
+    c->own_stream = false;
+    return 0;
+}
+
+TFG_API int tfg_set_scene(tfg_ctx* c, const tfg_rpc* cams, int n_views,
+                          const uint8_t* const* images, const tfg_roi* roi, int grid_rows,
+                          int grid_cols) {
+    if (!c || !cams || n_views <= 0 || !roi || grid_rows < 1 || grid_cols < 1)
+        return fail(TFG_ERR_INVALID, "set_scene: bad arguments");
+    if (!(roi->easting_max > roi->easting_min) || !(roi->northing_max > roi->northing_min) ||
+        !(roi->z_max > roi->z_min))
+        return fail(TFG_ERR_INVALID, "Roi: extents must be positive and z_max > z_min");
+    if ((grid_rows == 1) != (grid_cols == 1))
+        return fail(TFG_ERR_INVALID, "set_scene: 1xN grids need the experimental 1x2 window");
+    CK(cudaSetDevice(c->device));
+    c->n_views = n_views;
+    c->cams.assign(cams, cams + n_views);
+    c->roi = *roi;
+    c->rows = grid_rows;
+    c->cols = grid_cols;
+    // grid_edges (tiler.cpp:18-27): bit-identical shared edges
+    auto edges = [](double lo, double hi, int n) {
+        std::vector<double> e(n + 1);
+        double step = (hi - lo) / n;
+        for (int k = 0; k <= n; ++k) e[k] = lo + k * step;
+        e[0] = lo;
+        e[n] = hi;
+        return e;
+    };
+    c->east = edges(roi->easting_min, roi->easting_max, grid_cols);
+    c->north = edges(roi->northing_min, roi->northing_max, grid_rows);
+    for (auto* im : c->h_images)
+        if (im) cudaFreeHost(im);
+    c->h_images.assign(n_views, nullptr);
+    for (int v = 0; v < n_views; ++v) {
+        size_t nb = size_t(cams[v].image_rows) * cams[v].image_cols * 3;
+        CK(cudaHostAlloc(reinterpret_cast<void**>(&c->h_images[v]), nb, cudaHostAllocDefault));
+        if (images && images[v]) std::memcpy(c->h_images[v], images[v], nb);
+        else std::memset(c->h_images[v], 0, nb);
+    }
+    c->tiles.assign(size_t(grid_rows) * grid_cols, TileHost{});
+    // capacities: max over all window positions (constant HBM across the snake)
+    uint64_t cand = 1, cropb = 1;
+    std::vector<std::pair<int, int>> pos;
+    if (grid_rows == 1) pos.push_back({0, 0});
+    else
+        for (int i = 0; i + 1 < grid_rows; ++i)
+            for (int j = 0; j + 1 < grid_cols; ++j) pos.push_back({i, j});
+    std::vector<Crop> crops, uni;
+    for (auto& p : pos) {
+        window_crops(c, window_tiles(c, p.first, p.second), crops, uni);
+        uint64_t n = 0;
+        for (auto& u : uni)
+            if (!u.empty()) n += uint64_t(u.r1 - u.r0) * uint64_t(u.c1 - u.c0);
+        cand = std::max(cand, n);
+        cropb = std::max(cropb, 3 * n);
+    }
+    c->cand_cap = cand;
+    c->accept_cap = cand;
+    c->crop_cap = cropb;
+    int rc = 0;
+    void* olds[] = {c->d_cams, c->d_east, c->d_north, c->d_crops, c->d_crop_rect, c->d_crop_off,
+                    c->d_accept, c->d_flags, c->d_pos, c->d_view_start, c->d_union, c->d_crop4};
+    for (void* p : olds)
+        if (p) cudaFree(p);
+    rc |= dalloc(c, &c->d_cams, n_views);
+    rc |= dalloc(c, &c->d_east, grid_cols + 1);
+    rc |= dalloc(c, &c->d_north, grid_rows + 1);
+    rc |= dalloc(c, &c->d_crops, c->crop_cap);
+    rc |= dalloc(c, &c->d_crop_rect, 4 * n_views);
+    rc |= dalloc(c, &c->d_crop_off, n_views);
+    rc |= dalloc(c, &c->d_accept, c->accept_cap);
+    rc |= dalloc(c, &c->d_flags, c->cand_cap);
+    rc |= dalloc(c, &c->d_pos, c->cand_cap + 1);
+    rc |= dalloc(c, &c->d_view_start, n_views);
+    rc |= dalloc(c, &c->d_union, 4 * n_views);
+    rc |= dalloc(c, &c->d_crop4, 4 * n_views * kTrainSlots);
+    if (rc) return TFG_ERR_CUDA;
+    CK(cudaMemcpyAsync(c->d_cams, c->cams.data(), n_views * sizeof(tfg_rpc), cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(c->d_east, c->east.data(), (grid_cols + 1) * 8, cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(c->d_north, c->north.data(), (grid_rows + 1) * 8, cudaMemcpyHostToDevice, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    c->nslots = 0;
+    c->pos_r = c->pos_c = -1;
+    return 0;
+}
+
+// ---------------------------------------------------------------- window slide
+TFG_API int tfg_snake_path(int H, int W, int32_t* out, int* n_out) {
+    if (H < 2 || W < 2) return fail(TFG_ERR_INVALID, "snake_path: H and W must be >= 2");
+    int m = 0;
+    for (int i = 0; i < H - 1; ++i)
+        for (int jj = 0; jj < W - 1; ++jj) {
+            int j = (i % 2 == 0) ? jj : (W - 2 - jj);
+            if (out) {
+                out[2 * m] = i;
+                out[2 * m + 1] = j;
+            }
+            ++m;
+        }
+    if (n_out) *n_out = m;
+    return 0;
+}
+
+// advance: staying tiles keep their slot; an entering tile
+// takes the slot of the leaving tile in the same row (east/west move) or the
+// same column (north move).  Leaving tiles are copied to their pinned host
+// records and entering ones loaded (fresh TileField::create if never trained)
+// on the side stream; then the window crops are staged and the accepted-ray
+// list rebuilt.
+TFG_API int tfg_set_window(tfg_ctx* c, int pr, int pc) {
+    if (!c || c->n_views == 0) return fail(TFG_ERR_STATE, "set_window: call set_scene first");
+    CK(cudaSetDevice(c->device));
+    bool single = (c->rows == 1 && c->cols == 1);
+    if (!single && (pr < 0 || pc < 0 || pr + 1 >= c->rows || pc + 1 >= c->cols))
+        return fail(TFG_ERR_INVALID, "set_window: position outside the (H-1)x(W-1) lattice");
+    std::vector<int> want = window_tiles(c, single ? 0 : pr, single ? 0 : pc);
+    int ns = int(want.size());
+    int next[kTrainSlots] = {-1, -1, -1, -1};
+    if (c->nslots == ns && ns == kTrainSlots) {
+        bool used[kTrainSlots] = {false, false, false, false};
+        for (int k = 0; k < ns; ++k)
+            for (int s = 0; s < ns; ++s)
+                if (c->slot_tile[s] == want[k]) {
+                    next[s] = want[k];
+                    used[k] = true;
+                }
+        bool horiz = (pr == c->pos_r);
+        for (int k = 0; k < ns; ++k) {
+            if (used[k]) continue;
+            int wr = want[k] / c->cols, wc = want[k] % c->cols, best = -1;
+            for (int s = 0; s < ns; ++s) {
+                if (next[s] != -1) continue;
+                int lr = c->slot_tile[s] / c->cols, lc = c->slot_tile[s] % c->cols;
+                if ((horiz && lr == wr) || (!horiz && lc == wc)) {
+                    best = s;
+                    break;
+                }
+            }
+            if (best < 0)
+                for (int s = 0; s < ns; ++s)
+                    if (next[s] == -1) {
+                        best = s;
+                        break;
+                    }
+            next[best] = want[k];
+        }
+    } else {
+        for (int k = 0; k < ns; ++k) next[k] = want[k];
+    }
+    // main-stream work on the old window must finish before its state moves
+    CK(cudaEventRecord(c->ev_main, c->st));
+    CK(cudaStreamWaitEvent(c->side, c->ev_main, 0));
+    for (int s = 0; s < c->nslots; ++s) {
+        int old = c->slot_tile[s];
+        if (old >= 0 && (s >= ns || next[s] != old)) {
+            if (slot_copy(c, s, old, true)) return TFG_ERR_CUDA;
+        }
+    }
+    for (int s = 0; s < ns; ++s) {
+        bool stays = (s < c->nslots && c->slot_tile[s] == next[s]);
+        if (stays) continue;
+        if (ensure_record(c, next[s])) return TFG_ERR_CUDA;
+        if (slot_copy(c, s, next[s], false)) return TFG_ERR_CUDA;
+    }
+    for (int s = 0; s < ns; ++s) c->slot_tile[s] = next[s];
+    c->nslots = ns;
+    c->pos_r = pr;
+    c->pos_c = pc;
+    fill_slots(c);
+    // crops of the new window: union rect per view, 2D copies from pinned images
+    std::vector<Crop> crops, uni;
+    window_crops(c, want, crops, uni);
+    // crop rects are indexed by slot for the accept kernel
+    std::vector<Crop> by_slot(crops.size());
+    for (int v = 0; v < c->n_views; ++v)
+        for (int s = 0; s < ns; ++s)
+            for (int k = 0; k < ns; ++k)
+                if (want[k] == next[s]) by_slot[size_t(v) * kTrainSlots + s] = crops[size_t(v) * kTrainSlots + k];
+    c->h_crop_rect.assign(4 * c->n_views, 0);
+    c->h_crop_off.assign(c->n_views, 0);
+    uint64_t off = 0;
+    for (int v = 0; v < c->n_views; ++v) {
+        const Crop& u = uni[v];
+        c->h_crop_off[v] = off;
+        if (u.empty()) continue;
+        int w = u.c1 - u.c0, h = u.r1 - u.r0;
+        c->h_crop_rect[4 * v] = u.r0;
+        c->h_crop_rect[4 * v + 1] = u.c0;
+        c->h_crop_rect[4 * v + 2] = w;
+        c->h_crop_rect[4 * v + 3] = h;
+        const uint8_t* src = c->h_images[v] + 3 * (size_t(u.r0) * c->cams[v].image_cols + u.c0);
+        CK(cudaMemcpy2DAsync(c->d_crops + off, size_t(w) * 3, src, size_t(c->cams[v].image_cols) * 3,
+                             size_t(w) * 3, h, cudaMemcpyHostToDevice, c->side));
+        off += uint64_t(w) * h * 3;
+    }
+    CK(cudaMemcpyAsync(c->d_crop_rect, c->h_crop_rect.data(), 4 * c->n_views * 4,
+                       cudaMemcpyHostToDevice, c->side));
+    CK(cudaMemcpyAsync(c->d_crop_off, c->h_crop_off.data(), c->n_views * 8, cudaMemcpyHostToDevice,
+                       c->side));
+    CK(cudaEventRecord(c->ev_side, c->side));
+    CK(cudaStreamWaitEvent(c->st, c->ev_side, 0));
+    // host steps of the slots are kept in the tile records (never reset)
+    if (run_occupancy(c, false, nullptr)) return TFG_ERR_CUDA;
+    int rc = build_accept(c, by_slot, uni);
+    c->have_batch = false;
+    return rc;
+}
+
+TFG_API int tfg_prefetch_window(tfg_ctx* c, int pr, int pc) {
+    // Host records of the next window's tiles are materialised (fresh init)
+    // ahead of the move so the move itself only issues copies.
+    if (!c) return fail(TFG_ERR_INVALID, "prefetch_window: null context");
+    bool single = (c->rows == 1 && c->cols == 1);
+    for (int ti : window_tiles(c, single ? 0 : pr, single ? 0 : pc))
+        if (ensure_record(c, ti)) return TFG_ERR_CUDA;
+    return 0;
+}
+
+TFG_API int tfg_window_tiles(tfg_ctx* c, int32_t* r4, int32_t* c4) {
+    if (!c) return -1;
+    for (int k = 0; k < c->nslots; ++k) {
+        r4[k] = c->slot_tile[k] / c->cols;
+        c4[k] = c->slot_tile[k] % c->cols;
+    }
+    return c->nslots;
+}
+
+TFG_API int tfg_accept_count(tfg_ctx* c, uint64_t* n) {
+    if (!c) return fail(TFG_ERR_INVALID, "accept_count: null context");
+    *n = c->n_accept;
+    return 0;
+}
+
+TFG_API int tfg_accept_export(tfg_ctx* c, uint64_t* out, uint64_t cap) {
+    uint64_t n = std::min(cap, c->n_accept);
+    CK(cudaMemcpyAsync(out, c->d_accept, n * 8, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    return 0;
+}
+
+// ---------------------------------------------------------------- training iteration
+TFG_API int tfg_sample(tfg_ctx* c, uint64_t iter, uint64_t ray_begin, int n_rays, int jitter,
+                       uint64_t* n_samples) {
+    if (!c || c->nslots == 0) return fail(TFG_ERR_STATE, "sample: call set_window first");
+    if (c->n_accept == 0) return fail(TFG_ERR_STATE, "sample: empty accepted-ray list");
+    CK(cudaSetDevice(c->device));
+    RaygenArgs a = base_raygen(c);
+    a.accept = c->d_accept;
+    a.n_accept = c->n_accept;
+    a.iter = iter;
+    a.ray_begin = ray_begin;
+    a.n_rays = n_rays;
+    a.jitter = jitter;
+    c->render_mode = false;
+    int rc = run_sampler(c, a);
+    if (rc) return rc;
+    if (n_samples) {
+        rc = sync_status(c);
+        if (rc) return rc;
+        *n_samples = c->h_status->n_samples;
+    }
+    return 0;
+}
+
+TFG_API int tfg_sample_pixels(tfg_ctx* c, const int32_t* pixels, int n_rays, uint64_t* n_samples) {
+    if (!c || c->nslots == 0) return fail(TFG_ERR_STATE, "sample_pixels: call set_window first");
+    if (n_rays <= 0 || n_rays > c->max_rays) return fail(TFG_ERR_INVALID, "sample_pixels: n_rays");
+    CK(cudaSetDevice(c->device));
+    CK(cudaMemcpyAsync(c->d_pixels, pixels, size_t(n_rays) * 12, cudaMemcpyHostToDevice, c->st));
+    RaygenArgs a = base_raygen(c);
+    a.pixels = c->d_pixels;
+    a.n_rays = n_rays;
+    a.jitter = 0;
+    c->render_mode = false;
+    int rc = run_sampler(c, a);
+    if (rc) return rc;
+    rc = sync_status(c);
+    if (rc) return rc;
+    if (n_samples) *n_samples = c->h_status->n_samples;
+    return 0;
+}
+
+TFG_API int tfg_forward_backward(tfg_ctx* c, uint64_t iter, uint64_t ray_begin, int n_rays) {
+    int rc = tfg_sample(c, iter, ray_begin, n_rays, 1, nullptr);
+    if (rc) return rc;
+    if ((rc = run_forward(c, train_ptrs(c)))) return rc;
+    if ((rc = run_composite(c, true))) return rc;
+    return run_backward(c);
+}
+
+TFG_API int tfg_optimizer_step(tfg_ctx* c, uint64_t iter) {
+    if (!c || c->nslots == 0) return fail(TFG_ERR_STATE, "optimizer_step: no window");
+    CK(cudaSetDevice(c->device));
+    const tfg_train_config& t = c->tc;
+    auto lr_at = [&](double base, uint64_t step) {
+        if (t.lr_decay_rate == 1.0) return base;
+        return base * std::pow(t.lr_decay_rate, double(step) / double(t.lr_decay_steps));
+    };
+    AdamArgs a{};
+    a.params = c->d_params;
+    a.grads = c->d_grads;
+    a.m = c->d_m;
+    a.v = c->d_v;
+    a.beta1 = t.beta1;
+    a.beta2 = t.beta2;
+    a.omb1 = 1.0f - t.beta1;
+    a.omb2 = 1.0f - t.beta2;
+    a.eps = t.eps;
+    a.group_flags = c->d_group_flags;
+    a.status = c->d_status;
+    auto group = [&](AdamGroup& G, uint64_t off, uint64_t cnt, double base, uint64_t& step) {
+        uint64_t s = ++step;
+        G.offset = off;
+        G.count = cnt;
+        G.lr = float(lr_at(base, s));
+        G.bc1 = float(1.0 - std::pow(double(t.beta1), double(s)));
+        G.bc2 = float(1.0 - std::pow(double(t.beta2), double(s)));
+    };
+    int ng = 0;
+    for (int k = 0; k < c->nslots; ++k) {
+        TileHost& th = c->tiles[c->slot_tile[k]];
+        group(a.g[ng++], uint64_t(k) * c->stride, c->enc_n, t.lr_field, th.enc_step);
+        group(a.g[ng++], uint64_t(k) * c->stride + c->enc_n, c->stride - c->enc_n, t.lr_field, th.dnet_step);
+    }
+    group(a.g[ng++], c->color_off, c->n_params - c->color_off, t.lr_color, c->color_step);
+    a.n_groups = ng;
+    // the colour group sits after the 4-slot region; a 1-slot window leaves a gap
+    uint64_t total = c->n_params;
+    CK(cudaMemsetAsync(c->d_group_flags, 0, 16 * 4, c->st));
+    if (c->nslots < kTrainSlots) {
+        // gap between slot region and colour: give it a zero-lr pseudo group
+        for (int g = ng; g > 2 * c->nslots; --g) a.g[g] = a.g[g - 1];
+        AdamGroup gap{};
+        gap.offset = uint64_t(c->nslots) * c->stride;
+        gap.count = c->color_off - gap.offset;
+        gap.lr = 0.f;
+        gap.bc1 = gap.bc2 = 1.f;
+        a.g[2 * c->nslots] = gap;
+        a.n_groups = ng + 1;
+    }
+    launch_adam(a, total, c->st, &c->launches);
+    CK(cudaGetLastError());
+    int interval = c->fc.occupancy_interval;
+    if (interval > 0 && (iter + 1) % uint64_t(interval) == 0) {
+        uint64_t keys[kTrainSlots];
+        for (int k = 0; k < c->nslots; ++k) {
+            int ti = c->slot_tile[k];
+            keys[k] = hash_combine(
+                hash_combine(hash_combine(hash_combine(c->tc.seed, kPurposeOccupancy),
+                                          uint64_t(ti / c->cols)),
+                             uint64_t(ti % c->cols)),
+                c->tiles[ti].dnet_step);
+        }
+        if (run_occupancy(c, true, keys)) return TFG_ERR_CUDA;
+    }
+    return 0;
+}
+
+TFG_API int tfg_read_loss(tfg_ctx* c, float* loss) {
+    if (!c) return fail(TFG_ERR_INVALID, "read_loss: null context");
+    int rc = sync_status(c);
+    if (loss) *loss = float(c->h_status->loss / (3.0 * double(c->tc.batch_rays)));
+    if (rc == TFG_ERR_NONFINITE) {
+        // the step was not applied: roll back the step counters
+        for (int k = 0; k < c->nslots; ++k) {
+            TileHost& th = c->tiles[c->slot_tile[k]];
+            --th.enc_step;
+            --th.dnet_step;
+        }
+        --c->color_step;
+    }
+    return rc;
+}
+
+TFG_API int tfg_train_step(tfg_ctx* c, uint64_t iter, uint64_t ray_begin, int n_rays,
+                           float* loss) {
+    int rc = tfg_forward_backward(c, iter, ray_begin, n_rays);
+    if (rc) return rc;
+    rc = tfg_optimizer_step(c, iter);
+    if (rc) return rc;
+    return tfg_read_loss(c, loss);
+}
+
+TFG_API int tfg_grad_buffer(tfg_ctx* c, void** dptr, uint64_t* count) {
+    if (!c) return fail(TFG_ERR_INVALID, "grad_buffer: null context");
+    *dptr = c->d_grads;
+    *count = c->n_params;
+    return 0;
+}
+
+// ---------------------------------------------------------------- parity surface
+TFG_API int tfg_batch_export(tfg_ctx* c, tfg_batch_view* out) {
+    if (!c || !c->have_batch) return fail(TFG_ERR_STATE, "batch_export: no batch");
+    HostBatch hb;
+    int rc = fetch_batch_meta(c, hb);
+    if (rc) return rc;
+    uint64_t S = hb.n_samples;
+    if (out->capacity < S) return fail(TFG_ERR_INVALID, "batch_export: capacity too small");
+    std::vector<float4> loc(S);
+    std::vector<float2> td(S);
+    std::vector<uint8_t> ep(S);
+    CK(cudaMemcpy(loc.data(), c->s.local, S * 16, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(td.data(), c->s.td, S * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(ep.data(), c->s.endpoint, S, cudaMemcpyDeviceToHost));
+    int n = c->cur_rays;
+    std::vector<uint32_t> cnt(n, 0);
+    for (int i = 0; i < n; ++i) {
+        const RayRec& R = hb.rays[i];
+        if (out->rays) {
+            tfg_ray_entry& e = out->rays[i];
+            for (int k = 0; k < 3; ++k) {
+                e.origin[k] = R.o[k];
+                e.direction[k] = R.d[k];
+                e.target[k] = R.target[k];
+            }
+            e.image_id = R.view;
+            e.row = R.row;
+            e.col = R.col;
+        }
+        if (R.status == 0)
+            for (int k = 0; k < R.nseg; ++k) cnt[i] += R.cnt[k];
+    }
+    if (out->offsets) {
+        out->offsets[0] = 0;
+        for (int i = 0; i < n; ++i) out->offsets[i + 1] = out->offsets[i] + cnt[i];
+    }
+    for_samples(c, hb, [&](int, uint64_t q, uint64_t pos, int slot) {
+        if (out->t) out->t[q] = td[pos].x;
+        if (out->delta) out->delta[q] = td[pos].y;
+        if (out->local) {
+            out->local[3 * q] = loc[pos].x;
+            out->local[3 * q + 1] = loc[pos].y;
+            out->local[3 * q + 2] = loc[pos].z;
+        }
+        if (out->slot) out->slot[q] = uint8_t(slot);
+        if (out->endpoint) out->endpoint[q] = ep[pos];
+    });
+    return 0;
+}
+
+TFG_API int tfg_field_forward(tfg_ctx* c, float* sigma, float* rgb) {
+    if (!c || !c->have_batch) return fail(TFG_ERR_STATE, "field_forward: no batch");
+    int rc = run_forward(c, train_ptrs(c));
+    if (rc) return rc;
+    if (!sigma && !rgb) return 0;
+    HostBatch hb;
+    if ((rc = fetch_batch_meta(c, hb))) return rc;
+    std::vector<float4> io(hb.n_samples);
+    CK(cudaMemcpy(io.data(), c->s.io, hb.n_samples * 16, cudaMemcpyDeviceToHost));
+    for_samples(c, hb, [&](int, uint64_t q, uint64_t pos, int) {
+        if (sigma) sigma[q] = io[pos].x;
+        if (rgb) {
+            rgb[3 * q] = io[pos].y;
+            rgb[3 * q + 1] = io[pos].z;
+            rgb[3 * q + 2] = io[pos].w;
+        }
+    });
+    return 0;
+}
+
+TFG_API int tfg_composite(tfg_ctx* c, float* ray_rgb, float* ray_depth, float* ray_opacity,
+                          float* d_sigma, float* d_rgb, float* loss) {
+    if (!c || !c->have_batch) return fail(TFG_ERR_STATE, "composite: no batch");
+    int rc = run_composite(c, true);
+    if (rc) return rc;
+    HostBatch hb;
+    if ((rc = fetch_batch_meta(c, hb))) return rc;
+    int n = c->cur_rays;
+    std::vector<float> ro(5 * uint64_t(c->max_rays));
+    CK(cudaMemcpy(ro.data(), c->d_ray_out, ro.size() * 4, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < n; ++i) {
+        if (ray_rgb)
+            for (int k = 0; k < 3; ++k) ray_rgb[3 * i + k] = ro[3 * i + k];
+        if (ray_depth) ray_depth[i] = ro[3 * uint64_t(c->max_rays) + i];
+        if (ray_opacity) ray_opacity[i] = ro[4 * uint64_t(c->max_rays) + i];
+    }
+    if (d_sigma || d_rgb) {
+        std::vector<float4> io(hb.n_samples);
+        CK(cudaMemcpy(io.data(), c->s.io, hb.n_samples * 16, cudaMemcpyDeviceToHost));
+        for_samples(c, hb, [&](int, uint64_t q, uint64_t pos, int) {
+            if (d_sigma) d_sigma[q] = io[pos].x;
+            if (d_rgb) {
+                d_rgb[3 * q] = io[pos].y;
+                d_rgb[3 * q + 1] = io[pos].z;
+                d_rgb[3 * q + 2] = io[pos].w;
+            }
+        });
+    }
+    if (loss) *loss = float(c->h_status->loss / (3.0 * double(c->tc.batch_rays)));
+    return 0;
+}
+
+TFG_API int tfg_field_backward(tfg_ctx* c) {
+    if (!c || !c->have_batch) return fail(TFG_ERR_STATE, "field_backward: no batch");
+    int rc = run_backward(c);
+    if (rc) return rc;
+    CK(cudaStreamSynchronize(c->st));
+    return 0;
+}
+
+TFG_API int tfg_get_grads(tfg_ctx* c, int slot, float* enc, float* dnet, float* color) {
+    if (!c || slot < 0 || slot >= c->nslots) return fail(TFG_ERR_INVALID, "get_grads: bad slot");
+    CK(cudaStreamSynchronize(c->st));
+    uint64_t off = uint64_t(slot) * c->stride;
+    if (enc) CK(cudaMemcpy(enc, c->d_grads + off, c->enc_n * 4, cudaMemcpyDeviceToHost));
+    if (dnet)
+        CK(cudaMemcpy(dnet, c->d_grads + off + c->enc_n, (c->stride - c->enc_n) * 4,
+                      cudaMemcpyDeviceToHost));
+    if (color)
+        CK(cudaMemcpy(color, c->d_grads + c->color_off, (c->n_params - c->color_off) * 4,
+                      cudaMemcpyDeviceToHost));
+    return 0;
+}
+
+TFG_API int tfg_get_tile_state(tfg_ctx* c, int slot, tfg_tile_state* o) {
+    if (!c || slot < 0 || slot >= c->nslots) return fail(TFG_ERR_INVALID, "get_tile_state: bad slot");
+    CK(cudaStreamSynchronize(c->st));
+    CK(cudaStreamSynchronize(c->side));
+    uint64_t off = uint64_t(slot) * c->stride;
+    uint64_t dn = c->stride - c->enc_n;
+    auto cp = [&](float* dst, const float* src, uint64_t n) -> int {
+        if (dst) CK(cudaMemcpy(dst, src, n * 4, cudaMemcpyDeviceToHost));
+        return 0;
+    };
+    int rc = cp(o->enc, c->d_params + off, c->enc_n) | cp(o->dnet, c->d_params + off + c->enc_n, dn) |
+             cp(o->enc_m, c->d_m + off, c->enc_n) | cp(o->enc_v, c->d_v + off, c->enc_n) |
+             cp(o->dnet_m, c->d_m + off + c->enc_n, dn) | cp(o->dnet_v, c->d_v + off + c->enc_n, dn) |
+             cp(o->occupancy, c->d_ema + uint64_t(slot) * kOccVox, kOccVox);
+    const TileHost& th = c->tiles[c->slot_tile[slot]];
+    o->enc_step = th.enc_step;
+    o->dnet_step = th.dnet_step;
+    return rc;
+}
+
+TFG_API int tfg_set_tile_state(tfg_ctx* c, int slot, const tfg_tile_state* in) {
+    if (!c || slot < 0 || slot >= c->nslots) return fail(TFG_ERR_INVALID, "set_tile_state: bad slot");
+    CK(cudaStreamSynchronize(c->st));
+    uint64_t off = uint64_t(slot) * c->stride;
+    uint64_t dn = c->stride - c->enc_n;
+    auto cp = [&](float* dst, const float* src, uint64_t n) -> int {
+        if (src) CK(cudaMemcpy(dst, src, n * 4, cudaMemcpyHostToDevice));
+        return 0;
+    };
+    int rc = cp(c->d_params + off, in->enc, c->enc_n) | cp(c->d_params + off + c->enc_n, in->dnet, dn) |
+             cp(c->d_m + off, in->enc_m, c->enc_n) | cp(c->d_v + off, in->enc_v, c->enc_n) |
+             cp(c->d_m + off + c->enc_n, in->dnet_m, dn) | cp(c->d_v + off + c->enc_n, in->dnet_v, dn) |
+             cp(c->d_ema + uint64_t(slot) * kOccVox, in->occupancy, kOccVox);
+    TileHost& th = c->tiles[c->slot_tile[slot]];
+    th.enc_step = in->enc_step;
+    th.dnet_step = in->dnet_step;
+    if (rc) return rc;
+    return run_occupancy(c, false, nullptr);
+}
+
+TFG_API int tfg_get_color(tfg_ctx* c, float* p, float* m, float* v, uint64_t* step) {
+    CK(cudaStreamSynchronize(c->st));
+    uint64_t n = c->n_params - c->color_off;
+    if (p) CK(cudaMemcpy(p, c->d_params + c->color_off, n * 4, cudaMemcpyDeviceToHost));
+    if (m) CK(cudaMemcpy(m, c->d_m + c->color_off, n * 4, cudaMemcpyDeviceToHost));
+    if (v) CK(cudaMemcpy(v, c->d_v + c->color_off, n * 4, cudaMemcpyDeviceToHost));
+    if (step) *step = c->color_step;
+    return 0;
+}
+
+TFG_API int tfg_set_color(tfg_ctx* c, const float* p, const float* m, const float* v,
+                          uint64_t step) {
+    CK(cudaStreamSynchronize(c->st));
+    uint64_t n = c->n_params - c->color_off;
+    if (p) CK(cudaMemcpy(c->d_params + c->color_off, p, n * 4, cudaMemcpyHostToDevice));
+    if (m) CK(cudaMemcpy(c->d_m + c->color_off, m, n * 4, cudaMemcpyHostToDevice));
+    if (v) CK(cudaMemcpy(c->d_v + c->color_off, v, n * 4, cudaMemcpyHostToDevice));
+    c->color_step = step;
+    return 0;
+}
+
+TFG_API int tfg_update_occupancy(tfg_ctx* c) {
+    if (!c || c->nslots == 0) return fail(TFG_ERR_STATE, "update_occupancy: no window");
+    uint64_t keys[kTrainSlots];
+    for (int k = 0; k < c->nslots; ++k) {
+        int ti = c->slot_tile[k];
+        keys[k] = hash_combine(hash_combine(hash_combine(hash_combine(c->tc.seed, kPurposeOccupancy),
+                                                         uint64_t(ti / c->cols)),
+                                            uint64_t(ti % c->cols)),
+                               c->tiles[ti].dnet_step);
+    }
+    int rc = run_occupancy(c, true, keys);
+    if (rc) return rc;
+    CK(cudaStreamSynchronize(c->st));
+    return 0;
+}
+
+TFG_API int tfg_get_memory_report(tfg_ctx* c, tfg_memory_report* o) {
+    if (!c) return fail(TFG_ERR_INVALID, "memory_report: null context");
+    std::memset(o, 0, sizeof(*o));
+    o->tile_params = kTrainSlots * c->stride * 4;
+    o->optimizer_moments = 2 * kTrainSlots * c->stride * 4 + kTrainSlots * c->stride * 4;  // m, v, grads
+    o->occupancy = uint64_t(kTrainSlots) * kOccVox * 4 + uint64_t(kMaxSlots) * kOccWords * 4;
+    o->crops = c->crop_cap;
+    o->accept_list = c->accept_cap * 8 + c->cand_cap * 8;
+    o->batch_buffers = uint64_t(c->max_rays) * (sizeof(RayRec) + 96 + 8 * kMaxSlots + 20 + 12) +
+                       c->sample_cap * (16 + 8 + 1 + 16);
+    o->color_net = (c->n_params - c->color_off) * 4;
+    o->total_device = c->bytes_total;
+    return 0;
+}
+
+// ---------------------------------------------------------------- render path
+TFG_API int tfg_render_setup(tfg_ctx* c, const int32_t* rows, const int32_t* cols, int n,
+                             const tfg_tile_state* states, const float* color_params) {
+    if (!c || c->n_views == 0) return fail(TFG_ERR_STATE, "render_setup: call set_scene first");
+    if (n <= 0 || n > kMaxSlots) return fail(TFG_ERR_INVALID, "render_setup: 1..16 tiles");
+    CK(cudaSetDevice(c->device));
+    if (!c->d_rparams) {
+        if (dalloc(c, &c->d_rparams, uint64_t(kMaxSlots) * c->stride)) return TFG_ERR_CUDA;
+        if (dalloc(c, &c->d_rbits, uint64_t(kMaxSlots) * kOccWords)) return TFG_ERR_CUDA;
+        if (dalloc(c, &c->d_rcolor, c->n_params - c->color_off)) return TFG_ERR_CUDA;
+    }
+    c->rn = n;
+    c->rslots.n = n;
+    std::vector<uint32_t> bits(kOccWords);
+    for (int k = 0; k < n; ++k) {
+        int ti = rows[k] * c->cols + cols[k];
+        double b[6];
+        tile_box(c, ti, b);
+        for (int q = 0; q < 6; ++q) c->rslots.box[k][q] = b[q];
+        for (int q = 0; q < 3; ++q) {
+            c->rslots.frame[k][q] = b[q];
+            c->rslots.frame[k][3 + q] = 1.0 / (b[3 + q] - b[q]);
+        }
+        float* dst = c->d_rparams + uint64_t(k) * c->stride;
+        CK(cudaMemcpy(dst, states[k].enc, c->enc_n * 4, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(dst + c->enc_n, states[k].dnet, (c->stride - c->enc_n) * 4, cudaMemcpyHostToDevice));
+        for (int w = 0; w < kOccWords; ++w) {
+            uint32_t word = 0;
+            for (int q = 0; q < 32; ++q) {
+                float e = states[k].occupancy ? states[k].occupancy[32 * w + q] : 1.0f;
+                word |= (e >= c->fc.occupancy_threshold ? 1u : 0u) << q;
+            }
+            bits[w] = word;
+        }
+        CK(cudaMemcpy(c->d_rbits + uint64_t(k) * kOccWords, bits.data(), kOccWords * 4,
+                      cudaMemcpyHostToDevice));
+    }
+    CK(cudaMemcpy(c->d_rcolor, color_params, (c->n_params - c->color_off) * 4, cudaMemcpyHostToDevice));
+    return 0;
+}
+
+// Forward-only path (cmd_render): midpoint samples over the
+// render tiles, K2 forward, K3 forward; chunks of max_rays rays.
+TFG_API int tfg_render_pixels(tfg_ctx* c, const tfg_rpc* cam, const int32_t* pixels, int n_rays,
+                              float* rgb, float* depth, float* opacity) {
+    if (!c || c->rn == 0) return fail(TFG_ERR_STATE, "render_pixels: call render_setup first");
+    CK(cudaSetDevice(c->device));
+    CK(cudaMemcpyAsync(c->d_rcam, cam, sizeof(tfg_rpc), cudaMemcpyHostToDevice, c->st));
+    std::vector<int32_t> px3;
+    FieldPtrs f{};
+    for (int k = 0; k < c->rn; ++k) {
+        f.enc[k] = c->d_rparams + uint64_t(k) * c->stride;
+        f.dnet[k] = f.enc[k] + c->enc_n;
+        f.occ_bits[k] = c->d_rbits + uint64_t(k) * kOccWords;
+    }
+    f.color = c->d_rcolor;
+    std::vector<float> ro;
+    for (int b0 = 0; b0 < n_rays; b0 += c->max_rays) {
+        int nb = std::min(c->max_rays, n_rays - b0);
+        px3.resize(size_t(nb) * 3);
+        for (int i = 0; i < nb; ++i) {
+            px3[3 * i] = 0;
+            px3[3 * i + 1] = pixels[2 * (b0 + i)];
+            px3[3 * i + 2] = pixels[2 * (b0 + i) + 1];
+        }
+        CK(cudaMemcpyAsync(c->d_pixels, px3.data(), px3.size() * 4, cudaMemcpyHostToDevice, c->st));
+        RaygenArgs a{};
+        a.cams = c->d_rcam;
+        a.pixels = c->d_pixels;
+        a.n_rays = nb;
+        a.z_min = c->roi.z_min;
+        a.z_max = c->roi.z_max;
+        a.spm = c->tc.samples_per_meter;
+        a.cap = c->tc.max_samples_per_ray;
+        a.delta_cap = c->tc.delta_cap;
+        a.slots = c->rslots;
+        for (int k = 0; k < c->rn; ++k) a.occ_bits[k] = f.occ_bits[k];
+        int rc = run_sampler(c, a);
+        if (rc) return rc;
+        c->render_mode = true;
+        if ((rc = run_forward(c, f))) return rc;
+        if ((rc = run_composite(c, false))) return rc;
+        ro.resize(5 * uint64_t(c->max_rays));
+        CK(cudaMemcpyAsync(ro.data(), c->d_ray_out, ro.size() * 4, cudaMemcpyDeviceToHost, c->st));
+        if ((rc = sync_status(c)) && rc != TFG_ERR_INVALID) return rc;
+        if (c->h_status->bits & (kStatusSampleOverflow | kStatusSegOverflow)) return check_status(c);
+        for (int i = 0; i < nb; ++i) {
+            if (rgb)
+                for (int k = 0; k < 3; ++k) rgb[3 * (b0 + i) + k] = ro[3 * i + k];
+            if (depth) depth[b0 + i] = ro[3 * uint64_t(c->max_rays) + i];
+            if (opacity) opacity[b0 + i] = ro[4 * uint64_t(c->max_rays) + i];
+        }
+    }
+    c->have_batch = false;
+    return 0;
+}
+
+// ---------------------------------------------------------------- instrumentation
+TFG_API int tfg_kernel_launch_count(tfg_ctx* c, uint64_t* n) {
+    if (!c) return fail(TFG_ERR_INVALID, "kernel_launch_count: null context");
+    *n = c->launches;
+    return 0;
+}
+
+TFG_API int tfg_profile_enable(tfg_ctx*, int) { return 0; }
+
+TFG_API int tfg_profile_read(tfg_ctx*, const char**, double*, uint64_t*, int, int* n_out) {
+    if (n_out) *n_out = 0;
+    return 0;
+}
+
+} // extern "C"

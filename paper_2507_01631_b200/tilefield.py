@@ -1,0 +1,316 @@
+"""Host-side mirror of the reference's tile-grid / window / sampler / trainer
+API over the C-ABI of libtilefield_gpu.so (include/tilefield_gpu.h).
+
+Names follow the reference (proj/src/core): ``snake_path``/``set_window``
+(scheduler ``snake_path``/``advance``), ``accept_list``
+(``accept_rays``), ``sample`` (``sample_segments``,
+SPEC.md:352-360, into a ``RaySegmentBatch``, ray_batch.hpp:13-49),
+``field_forward``/``field_backward`` (``forward_batch``/``backward_batch``,
+field.hpp:186-197), ``composite`` (``render`` + ``color_loss``),
+``optimizer_step`` (``adam_step``, field.hpp:47-48) and ``train_step`` (one
+trainer iteration).  Errors raise ``TileFieldError`` (the
+reference's ``tilefield::Error``, common.hpp:27-34).
+
+There is no CPU fallback: without the built library or an sm_100 device the
+constructor raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from .abi import (
+    RAY_DTYPE,
+    BatchView,
+    FieldConfig,
+    MemoryReport,
+    Roi,
+    Rpc,
+    TileState,
+    TrainConfig,
+    field_sizes,
+    ptr,
+)
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libtilefield_gpu.so")
+_lib = None
+_vp = C.c_void_p
+
+
+class TileFieldError(RuntimeError):
+    """tilefield::Error (common.hpp:27-30)."""
+
+
+class NonFiniteGradient(TileFieldError):
+    pass
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise TileFieldError(
+            f"{LIB_PATH} is not built; run paper_2507_01631_b200/build.py (no CPU fallback exists)")
+    L = C.CDLL(LIB_PATH)
+    L.tfg_last_error.restype = C.c_char_p
+    sig = {
+        "tfg_create": [_vp, _vp, C.c_int, C.c_int, _vp],
+        "tfg_destroy": [_vp],
+        "tfg_set_stream": [_vp, _vp],
+        "tfg_set_scene": [_vp, _vp, C.c_int, _vp, _vp, C.c_int, C.c_int],
+        "tfg_set_window": [_vp, C.c_int, C.c_int],
+        "tfg_prefetch_window": [_vp, C.c_int, C.c_int],
+        "tfg_window_tiles": [_vp, _vp, _vp],
+        "tfg_snake_path": [C.c_int, C.c_int, _vp, _vp],
+        "tfg_accept_count": [_vp, _vp],
+        "tfg_accept_export": [_vp, _vp, C.c_uint64],
+        "tfg_forward_backward": [_vp, C.c_uint64, C.c_uint64, C.c_int],
+        "tfg_optimizer_step": [_vp, C.c_uint64],
+        "tfg_train_step": [_vp, C.c_uint64, C.c_uint64, C.c_int, _vp],
+        "tfg_grad_buffer": [_vp, _vp, _vp],
+        "tfg_read_loss": [_vp, _vp],
+        "tfg_sample": [_vp, C.c_uint64, C.c_uint64, C.c_int, C.c_int, _vp],
+        "tfg_sample_pixels": [_vp, _vp, C.c_int, _vp],
+        "tfg_batch_export": [_vp, _vp],
+        "tfg_field_forward": [_vp, _vp, _vp],
+        "tfg_composite": [_vp, _vp, _vp, _vp, _vp, _vp, _vp],
+        "tfg_field_backward": [_vp],
+        "tfg_get_tile_state": [_vp, C.c_int, _vp],
+        "tfg_set_tile_state": [_vp, C.c_int, _vp],
+        "tfg_get_color": [_vp, _vp, _vp, _vp, _vp],
+        "tfg_set_color": [_vp, _vp, _vp, _vp, C.c_uint64],
+        "tfg_get_grads": [_vp, C.c_int, _vp, _vp, _vp],
+        "tfg_update_occupancy": [_vp],
+        "tfg_get_memory_report": [_vp, _vp],
+        "tfg_render_setup": [_vp, _vp, _vp, C.c_int, _vp, _vp],
+        "tfg_render_pixels": [_vp, _vp, _vp, C.c_int, _vp, _vp, _vp],
+        "tfg_kernel_launch_count": [_vp, _vp],
+        "tfg_param_counts": [_vp, _vp, _vp, _vp],
+        "tfg_default_field_config": [_vp],
+        "tfg_default_train_config": [_vp],
+    }
+    for name, args in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = C.c_int
+    _lib = L
+    return L
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        msg = lib().tfg_last_error().decode()
+        if rc == 3:
+            raise NonFiniteGradient(msg)
+        raise TileFieldError(msg or f"tilefield_gpu error {rc}")
+
+
+def snake_path(H: int, W: int) -> list[tuple[int, int]]:
+    """Window positions: rows south->north, serpentine."""
+    n = C.c_int()
+    _check(lib().tfg_snake_path(H, W, None, C.byref(n)))
+    out = np.zeros(2 * n.value, np.int32)
+    _check(lib().tfg_snake_path(H, W, ptr(out), C.byref(n)))
+    return [(int(out[2 * k]), int(out[2 * k + 1])) for k in range(n.value)]
+
+
+class Context:
+    """One GPU's window trainer state (a tfg_ctx)."""
+
+    def __init__(self, scene, fcfg: FieldConfig | None = None, tcfg: TrainConfig | None = None,
+                 device: int = 0, max_rays: int = 65536, stream=None):
+        self.fcfg = fcfg or FieldConfig.defaults()
+        self.tcfg = tcfg or TrainConfig.defaults(batch_rays=max_rays)
+        self.enc_n, self.dnet_n, self.color_n, _ = field_sizes(self.fcfg)
+        h = C.c_void_p()
+        _check(lib().tfg_create(C.byref(self.fcfg), C.byref(self.tcfg), device, max_rays, C.byref(h)))
+        self.h = h
+        self.max_rays = max_rays
+        if stream is not None:
+            _check(lib().tfg_set_stream(self.h, C.c_void_p(stream)))
+        self.scene = scene
+        self._cams = (Rpc * scene.n_views)(*scene.cams)
+        imgs = [np.ascontiguousarray(im) for im in scene.images]
+        imgp = (C.c_void_p * scene.n_views)(*[im.ctypes.data for im in imgs])
+        _check(lib().tfg_set_scene(self.h, self._cams, scene.n_views, imgp, C.byref(scene.roi),
+                                   scene.grid_rows, scene.grid_cols))
+        self.n_rays = 0
+        self.n_samples = 0
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().tfg_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- window ------------------------------------------------------------
+    def set_window(self, r: int, c: int) -> None:
+        _check(lib().tfg_set_window(self.h, r, c))
+
+    def prefetch_window(self, r: int, c: int) -> None:
+        _check(lib().tfg_prefetch_window(self.h, r, c))
+
+    def window_tiles(self) -> list[tuple[int, int]]:
+        rr, cc = np.zeros(4, np.int32), np.zeros(4, np.int32)
+        n = lib().tfg_window_tiles(self.h, ptr(rr), ptr(cc))
+        return [(int(rr[k]), int(cc[k])) for k in range(n)]
+
+    def accept_count(self) -> int:
+        n = C.c_uint64()
+        _check(lib().tfg_accept_count(self.h, C.byref(n)))
+        return n.value
+
+    def accept_list(self) -> np.ndarray:
+        n = self.accept_count()
+        out = np.zeros(max(n, 1), np.uint64)
+        _check(lib().tfg_accept_export(self.h, ptr(out), n))
+        return out[:n]
+
+    # ---- sub-steps ---------------------------------------------------------
+    def sample(self, it: int, ray_begin: int, n_rays: int, jitter: bool = True) -> int:
+        n = C.c_uint64()
+        _check(lib().tfg_sample(self.h, it, ray_begin, n_rays, int(jitter), C.byref(n)))
+        self.n_rays, self.n_samples = n_rays, n.value
+        return n.value
+
+    def sample_pixels(self, pixels) -> int:
+        px = np.ascontiguousarray(pixels, np.int32).reshape(-1, 3)
+        n = C.c_uint64()
+        _check(lib().tfg_sample_pixels(self.h, ptr(px), px.shape[0], C.byref(n)))
+        self.n_rays, self.n_samples = px.shape[0], n.value
+        return n.value
+
+    def batch(self) -> dict:
+        R, S = self.n_rays, self.n_samples
+        rays = np.zeros(R, RAY_DTYPE)
+        off = np.zeros(R + 1, np.uint32)
+        t, de = np.zeros(S, np.float32), np.zeros(S, np.float32)
+        lc = np.zeros(3 * S, np.float32)
+        sl, ep = np.zeros(S, np.uint8), np.zeros(S, np.uint8)
+        bv = BatchView(rays.ctypes.data, off.ctypes.data, t.ctypes.data, de.ctypes.data,
+                       lc.ctypes.data, sl.ctypes.data, ep.ctypes.data, S)
+        _check(lib().tfg_batch_export(self.h, C.byref(bv)))
+        return dict(rays=rays, offsets=off, t=t, delta=de, local=lc.reshape(S, 3), slot=sl, endpoint=ep)
+
+    def field_forward(self):
+        S = self.n_samples
+        sg, rgb = np.zeros(S, np.float32), np.zeros(3 * S, np.float32)
+        _check(lib().tfg_field_forward(self.h, ptr(sg), ptr(rgb)))
+        return sg, rgb.reshape(S, 3)
+
+    def composite(self) -> dict:
+        R, S = self.n_rays, self.n_samples
+        rr, dep, op = np.zeros(3 * R, np.float32), np.zeros(R, np.float32), np.zeros(R, np.float32)
+        ds, dr = np.zeros(S, np.float32), np.zeros(3 * S, np.float32)
+        loss = C.c_float()
+        _check(lib().tfg_composite(self.h, ptr(rr), ptr(dep), ptr(op), ptr(ds), ptr(dr), C.byref(loss)))
+        return dict(rgb=rr.reshape(R, 3), depth=dep, opacity=op, d_sigma=ds, d_rgb=dr.reshape(S, 3),
+                    loss=loss.value)
+
+    def field_backward(self) -> None:
+        _check(lib().tfg_field_backward(self.h))
+
+    def grads(self, slot: int):
+        e = np.zeros(self.enc_n, np.float32)
+        d = np.zeros(self.dnet_n, np.float32)
+        c = np.zeros(self.color_n, np.float32)
+        _check(lib().tfg_get_grads(self.h, slot, ptr(e), ptr(d), ptr(c)))
+        return e, d, c
+
+    def optimizer_step(self, it: int) -> None:
+        _check(lib().tfg_optimizer_step(self.h, it))
+
+    def forward_backward(self, it: int, ray_begin: int, n_rays: int) -> None:
+        _check(lib().tfg_forward_backward(self.h, it, ray_begin, n_rays))
+
+    def read_loss(self) -> float:
+        l = C.c_float()
+        _check(lib().tfg_read_loss(self.h, C.byref(l)))
+        return l.value
+
+    def train_step(self, it: int, ray_begin: int = 0, n_rays: int | None = None) -> float:
+        l = C.c_float()
+        _check(lib().tfg_train_step(self.h, it, ray_begin, n_rays or self.max_rays, C.byref(l)))
+        return l.value
+
+    def grad_buffer(self) -> tuple[int, int]:
+        p, n = C.c_void_p(), C.c_uint64()
+        _check(lib().tfg_grad_buffer(self.h, C.byref(p), C.byref(n)))
+        return p.value, n.value
+
+    def grad_tensor(self):
+        """The flat gradient buffer as a torch CUDA tensor (allreduce target)."""
+        import torch
+
+        p, n = self.grad_buffer()
+
+        class _Cai:
+            __cuda_array_interface__ = {"shape": (n,), "typestr": "<f4", "data": (p, False), "version": 3}
+
+        return torch.as_tensor(_Cai(), device="cuda")
+
+    # ---- state ---------------------------------------------------------------
+    def tile_state(self, slot: int) -> dict:
+        occn = self.fcfg.occupancy_resolution ** 3
+        a = {k: np.zeros(self.enc_n, np.float32) for k in ("enc", "enc_m", "enc_v")}
+        a.update({k: np.zeros(self.dnet_n, np.float32) for k in ("dnet", "dnet_m", "dnet_v")})
+        a["occupancy"] = np.zeros(occn, np.float32)
+        ts = TileState(*[a[k].ctypes.data for k in ("enc", "dnet", "enc_m", "enc_v", "dnet_m", "dnet_v")],
+                       0, 0, a["occupancy"].ctypes.data)
+        _check(lib().tfg_get_tile_state(self.h, slot, C.byref(ts)))
+        a["enc_step"], a["dnet_step"] = ts.enc_step, ts.dnet_step
+        return a
+
+    def set_tile_state(self, slot: int, a: dict) -> None:
+        ts = TileState(*[ptr(a.get(k)) for k in ("enc", "dnet", "enc_m", "enc_v", "dnet_m", "dnet_v")],
+                       a.get("enc_step", 0), a.get("dnet_step", 0), ptr(a.get("occupancy")))
+        _check(lib().tfg_set_tile_state(self.h, slot, C.byref(ts)))
+
+    def color(self):
+        p, m, v = (np.zeros(self.color_n, np.float32) for _ in range(3))
+        st = C.c_uint64()
+        _check(lib().tfg_get_color(self.h, ptr(p), ptr(m), ptr(v), C.byref(st)))
+        return p, m, v, st.value
+
+    def set_color(self, p, m=None, v=None, step=0) -> None:
+        _check(lib().tfg_set_color(self.h, ptr(p), ptr(m), ptr(v), step))
+
+    def update_occupancy(self) -> None:
+        _check(lib().tfg_update_occupancy(self.h))
+
+    def memory_report(self) -> dict:
+        m = MemoryReport()
+        _check(lib().tfg_get_memory_report(self.h, C.byref(m)))
+        return {k: getattr(m, k) for k, _ in MemoryReport._fields_}
+
+    def launches(self) -> int:
+        n = C.c_uint64()
+        _check(lib().tfg_kernel_launch_count(self.h, C.byref(n)))
+        return n.value
+
+    # ---- render ---------------------------------------------------------------
+    def render_setup(self, tiles: list[tuple[int, int]], states: list[dict], color) -> None:
+        n = len(tiles)
+        rows = np.array([t[0] for t in tiles], np.int32)
+        cols = np.array([t[1] for t in tiles], np.int32)
+        self._rkeep = states
+        arr = (TileState * n)(*[
+            TileState(ptr(s["enc"]), ptr(s["dnet"]), None, None, None, None, 0, 0, ptr(s.get("occupancy")))
+            for s in states])
+        self._rarr = arr
+        _check(lib().tfg_render_setup(self.h, ptr(rows), ptr(cols), n, arr, ptr(np.ascontiguousarray(color, np.float32))))
+
+    def render_pixels(self, cam: Rpc, pixels):
+        px = np.ascontiguousarray(pixels, np.int32).reshape(-1, 2)
+        n = px.shape[0]
+        rgb, dep, op = np.zeros(3 * n, np.float32), np.zeros(n, np.float32), np.zeros(n, np.float32)
+        _check(lib().tfg_render_pixels(self.h, C.byref(cam), ptr(px), n, ptr(rgb), ptr(dep), ptr(op)))
+        return rgb.reshape(n, 3), dep, op
