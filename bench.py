@@ -1,0 +1,366 @@
+#!/usr/bin/env python
+"""Benchmark of the Snake-NeRF 2x2-window training hot path on B200.
+
+Metric (BASELINE.json): training rays/s of the 2x2 window (ray generation +
+segmentation + sampling, field fwd/bwd, compositing + loss + backward, fused
+Adam, periodic occupancy update), whole job over N GPUs; plus render rays/s.
+
+Workload: config 5 (6x6 grid of 128 m tiles, 16 synthetic views ~1650^2 px at
+0.5 m, 65,536 rays per batch per GPU, window at position (2,2)).  Ray-sharded
+data parallelism (weak scaling): rank r trains rays [r*B, (r+1)*B) of the
+global counter-RNG stream with an NCCL allreduce of the 7.01 MB gradient.
+
+`python bench.py [--gpus N --steps K --warmup W]`           (our arm)
+`python bench.py --impl reference [...]`                     (CPU reference arm)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "training rays/sec (2x2 window, fwd+bwd+Adam)"
+UNIT = "rays/s"
+B_PER_GPU = 65536
+WINDOW = (2, 2)
+FLOP_FWD = 17664          # per sample (density 4,096 + colour 13,568), SURVEY.md §8
+FLOP_FWD_BWD = 52992      # per sample
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p["hbm_gbs"], p["bf16_tflops"], p.get("bf16_tflops_sustained", p["bf16_tflops"]), "measured"
+    except Exception:
+        return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        if self.p:
+            self.p.terminate()
+            try:
+                self.p.wait(timeout=5)
+            except Exception:
+                self.p.kill()
+
+    def summary(self):
+        self.f.flush()
+        try:
+            rows = [l.strip().split(", ") for l in open(self.f.name) if l.strip()]
+        except Exception:
+            rows = []
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                s, m = float(r[1]), float(r[2])
+            except Exception:
+                continue
+            mx = max(mx, m)
+            sm.append(s)
+            for k, n in enumerate(names):
+                if len(r) > 5 + k and "Active" in r[5 + k] and "Not" not in r[5 + k]:
+                    reasons.add(n)
+        load = [s for s in sm if s > 0.3 * mx] or sm
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def cpu_baseline(scene, n_rays: int, steps: int, warmup: int):
+    """The CPU oracle trainer (oracle/, the reference's algorithm restated; the
+    absent trainer/field bodies have no other CPU implementation) on the host
+    cores, on a bounded sample of the same workload."""
+    from oracle.pyoracle import Oracle, Session
+    from paper_2507_01631_b200.abi import FieldConfig, TrainConfig
+
+    cores = os.cpu_count() or 1
+    ses = Session(Oracle(), scene, FieldConfig.defaults(), TrainConfig.defaults(batch_rays=n_rays, seed=2),
+                  workers=cores)
+    ses.set_window(*WINDOW)
+    t0 = time.perf_counter()
+    n_acc = ses.build_accept().size
+    t_accept = time.perf_counter() - t0
+    for i in range(warmup):
+        ses.train_step(i, 0, n_rays)
+    t0 = time.perf_counter()
+    for i in range(steps):
+        ses.train_step(warmup + i, 0, n_rays)
+    dt = time.perf_counter() - t0
+    return {"value": n_rays * steps / dt, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"oracle trainer on cfg5 window {WINDOW}: {steps} timed iterations x {n_rays} rays "
+                      f"(after {warmup} warm-up; accepted-ray list of {n_acc} built once in {t_accept:.1f} s, untimed)"}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_2507_01631_b200 import synth
+
+    scene = synth.config_scene(5, seed=0)
+    n = 2048
+    cb = cpu_baseline(scene, n, max(args.steps // 4, 2), 1)
+    line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus,
+            "steps": max(args.steps // 4, 2), "warmup": 1, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "cfg5 6x6 grid, 2x2 window at (2,2), 16 views ~1650^2 px, bounded ray sample",
+                       "rays_per_step": n},
+            "cpu_baseline": cb,
+            "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+KERNEL_UNITS = {
+    # phase: (bound, per-sample, per-ray, unit) algorithmic work
+    "field_bwd": ("tensor", FLOP_FWD_BWD, 0, "flop"),
+    "field_fwd": ("tensor", FLOP_FWD, 0, "flop"),
+    "composite": ("hbm", 40, 36, "byte"),
+    "sampler": ("hbm", 22, 79, "byte"),
+    "adam": ("hbm", 0, 0, "byte"),
+}
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2507_01631_b200 import synth
+    from paper_2507_01631_b200.abi import FieldConfig, TrainConfig
+    from paper_2507_01631_b200.tilefield import Context, snake_path, tile_init
+
+    rank, world, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    B = B_PER_GPU
+    scene = synth.config_scene(5, seed=0)
+    fc = FieldConfig.defaults()
+    tc = TrainConfig.defaults(batch_rays=B * world, seed=2)
+    stream = torch.cuda.current_stream(dev)
+    ctx = Context(scene, fc, tc, device=local, max_rays=B, stream=stream.cuda_stream)
+    ctx.set_window(*WINDOW)
+    grads = ctx.grad_tensor()
+    l2 = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    def step(it):
+        ctx.forward_backward(it, rank * B, B)
+        if world > 1:
+            dist.all_reduce(grads)
+        ctx.optimizer_step(it)
+        l2.zero_()  # flush L2 between timed iterations
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    _, n_samples = ctx.last_batch()
+    ctx.profile_enable(True)
+    l0 = ctx.launches()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with Clocks(local) as clk:
+        ev0.record(stream)
+        for i in range(args.steps):
+            step(args.warmup + i)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    prof = ctx.profile_read()
+    launches = ctx.launches() - l0
+    ctx.profile_enable(False)
+    t = torch.tensor([ms], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = world * B * args.steps / (ms_max / 1e3)
+
+    hbm, tf_burst, tf_sust, peak_src = peaks()
+    K = args.steps
+    kern = {}
+    for ph, (ph_ms, nl) in prof.items():
+        if ph_ms <= 0:
+            continue
+        kern[ph] = {"ms_per_step": ph_ms / K, "share": ph_ms / ms, "launches": nl}
+        if ph in KERNEL_UNITS:
+            bound, ps, pr, u = KERNEL_UNITS[ph]
+            if ph == "adam":
+                work = 28 * 1752595 * K
+            else:
+                work = (ps * n_samples + pr * B) * K
+            sec = ph_ms / 1e3
+            if bound == "tensor":
+                kern[ph].update(bound="tensor", achieved=work / sec / 1e12, unit="TFLOP/s")
+            else:
+                kern[ph].update(bound="hbm", achieved=work / sec / 1e9, unit="GB/s")
+    dom = max((p for p in kern if p in KERNEL_UNITS), key=lambda p: kern[p]["ms_per_step"])
+    d = kern[dom]
+    peak = (tf_sust if d["bound"] == "tensor" else hbm)
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get(dom)
+        except Exception:
+            traffic = None
+    roofline = {"kernel": dom, "bound": d["bound"], "achieved": d["achieved"], "peak": peak,
+                "unit": d["unit"], "frac": d["achieved"] / peak, "traffic": traffic,
+                "peak_source": f"{peak_src} ({'bf16 sustained' if d['bound'] == 'tensor' else 'HBM copy'})",
+                "per_launch_work": (FLOP_FWD_BWD if dom == "field_bwd" else KERNEL_UNITS[dom][1]) * n_samples}
+
+    # ---- end to end through the public API with host buffers: window slides
+    # (pinned host <-> HBM tile state + crops), accepted-list rebuilds, loss
+    # readback every step; the window moves every 4 iterations along the snake.
+    path = snake_path(scene.grid_rows, scene.grid_cols)
+    h0, d0 = ctx.copy_bytes()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e2e_steps = args.steps
+    for i in range(e2e_steps):
+        if i % 4 == 0:
+            ctx.set_window(*path[(i // 4) % len(path)])
+        ctx.forward_backward(10_000 + i, rank * B, B)
+        if world > 1:
+            dist.all_reduce(grads)
+        ctx.optimizer_step(10_000 + i)
+        ctx.read_loss()
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    h1, d1 = ctx.copy_bytes()
+    te = torch.tensor([e2e_s], device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e = {"value": world * B * e2e_steps / float(te.item()), "unit": UNIT,
+           "h2d_bytes_per_step": (h1 - h0) // e2e_steps, "d2h_bytes_per_step": (d1 - d0) // e2e_steps,
+           "window_move_every": 4}
+
+    # ---- render (config 4: 4x4-tile ROI, random-init weights, occupancy all on)
+    render = None
+    if rank == 0 and not args.no_render:
+        render = bench_render(args)
+
+    out = None
+    if rank == 0:
+        cb = None
+        if world == 1 and not args.no_cpu:
+            cb = cpu_baseline(scene, 2048, 2, 1)
+        out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+               "warmup": args.warmup, "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak",
+               "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+               "config": {"workload": "cfg5: 6x6 grid of 128 m tiles, 2x2 window at (2,2), 16 synthetic views "
+                                      "~1650^2 px at 0.5 m, random-init fields",
+                          "rays_per_gpu_per_step": B, "global_batch": B * world,
+                          "samples_per_step_per_gpu": n_samples,
+                          "samples_per_ray": n_samples / B, "parallelism": f"ray-sharded dp{world}",
+                          "l2": "flushed between timed iterations (256 MB write)"},
+               "roofline": roofline, "kernels": kern, "cpu_baseline": cb, "e2e": e2e,
+               "gpu_launches": launches, "clocks": clk.summary(), "render": render}
+        print(json.dumps(out), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def bench_render(args):
+    import numpy as np
+    import torch
+
+    from paper_2507_01631_b200 import synth
+    from paper_2507_01631_b200.abi import FieldConfig, Roi, TrainConfig
+    from paper_2507_01631_b200.synth import Scene, make_camera
+    from paper_2507_01631_b200.tilefield import Context, tile_init
+
+    roi = Roi(0.0, 512.0, 0.0, 512.0, 0.0, 40.0)
+    cam = make_camera(roi, 0.125, 12.0, 40.0)
+    img = np.zeros((cam.image_rows, cam.image_cols, 3), np.uint8)
+    scene = Scene(roi, 4, 4, [cam], [img], 0.125)
+    fc = FieldConfig.defaults()
+    chunk = 1 << 20
+    ctx = Context(scene, fc, TrainConfig.defaults(batch_rays=chunk), max_rays=chunk)
+    tiles = [(r, c) for r in range(4) for c in range(4)]
+    states = [tile_init(fc, 1, r, c) for r, c in tiles]
+    color = ctx.color()[0]
+    ctx.render_setup(tiles, states, color)
+    # a 1024 x 1024 block of the 4096^2-class novel view
+    r0, c0 = cam.image_rows // 2 - 512, cam.image_cols // 2 - 512
+    rr, cc = np.meshgrid(np.arange(r0, r0 + 1024), np.arange(c0, c0 + 1024), indexing="ij")
+    px = np.stack([rr.ravel(), cc.ravel()], axis=1).astype(np.int32)
+    ctx.render_pixels(cam, px)  # warm-up
+    ctx.profile_enable(True)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    reps = 3
+    for _ in range(reps):
+        rgb, dep, op = ctx.render_pixels(cam, px)
+    wall = time.perf_counter() - t0
+    prof = ctx.profile_read()
+    dev_ms = sum(prof[p][0] for p in ("sampler", "field_fwd", "composite"))
+    _, ns = ctx.last_batch()
+    ctx.close()
+    return {"value": reps * chunk / (dev_ms / 1e3), "unit": "rays/s",
+            "e2e": {"value": reps * chunk / wall, "unit": "rays/s", "h2d_bytes_per_step": chunk * 12,
+                    "d2h_bytes_per_step": chunk * 20},
+            "config": "cfg4: 4x4-tile ROI (512 m), novel view at 0.125 m, 1024^2-ray block, random-init "
+                      "weights, occupancy all on, midpoint samples",
+            "samples_per_ray": ns / chunk,
+            "phases_ms": {p: prof[p][0] / reps for p in ("sampler", "field_fwd", "composite")}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-render", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -249,6 +249,13 @@ TFG_API int tfg_profile_enable(tfg_ctx* ctx, int on);
 TFG_API int tfg_profile_read(tfg_ctx* ctx, const char** names, double* ms, uint64_t* launches,
                              int capacity, int* n_out);
 TFG_API int tfg_kernel_launch_count(tfg_ctx* ctx, uint64_t* launches);
+/* Rays and samples of the last batch (synchronises). */
+TFG_API int tfg_last_batch(tfg_ctx* ctx, int* n_rays, uint64_t* n_samples);
+/* TileField::create (field.hpp:93) on the host into caller buffers. */
+TFG_API int tfg_tile_init(const tfg_field_config* cfg, uint64_t seed, int row, int col,
+                          tfg_tile_state* out);
+/* Host<->device bytes copied by the context (window slides, crops, status). */
+TFG_API int tfg_copy_bytes(tfg_ctx* ctx, uint64_t* h2d, uint64_t* d2h);
 
 #ifdef __cplusplus
 }

@@ -70,6 +70,11 @@ struct TileHost {
     uint64_t enc_step = 0, dnet_step = 0;
 };
 
+enum Phase { kPhSampler, kPhFieldFwd, kPhComposite, kPhFieldBwd, kPhAdam, kPhOccupancy,
+             kPhAccept, kNumPhases };
+const char* kPhaseNames[kNumPhases] = {"sampler", "field_fwd", "composite", "field_bwd",
+                                       "adam", "occupancy", "accept"};
+
 struct Crop {
     int r0 = 0, r1 = 0, c0 = 0, c1 = 0;
     bool empty() const { return r0 >= r1 || c0 >= c1; }
@@ -154,6 +159,15 @@ struct tfg_ctx {
     tfg_rpc* d_rcam = nullptr;
 
     uint64_t bytes_total = 0;
+    uint64_t h2d_bytes = 0, d2h_bytes = 0;
+
+    // per-phase device timing (CUDA events on the context stream)
+    bool prof = false;
+    std::vector<cudaEvent_t> ev_pool;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_open;
+    double prof_ms[kNumPhases] = {};
+    uint64_t prof_n[kNumPhases] = {};
+    uint64_t prof_launch[kNumPhases] = {};
 };
 
 namespace {
@@ -164,6 +178,49 @@ int dalloc(tfg_ctx* c, T** p, uint64_t n) {
     CK(cudaMalloc(reinterpret_cast<void**>(p), n * sizeof(T)));
     c->bytes_total += n * sizeof(T);
     return 0;
+}
+
+cudaEvent_t pool_event(tfg_ctx* c) {
+    if (!c->ev_pool.empty()) {
+        cudaEvent_t e = c->ev_pool.back();
+        c->ev_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+struct PhaseScope {
+    tfg_ctx* c;
+    int ph;
+    cudaEvent_t a = nullptr;
+    uint64_t l0;
+    PhaseScope(tfg_ctx* c_, int ph_) : c(c_), ph(ph_), l0(c_->launches) {
+        if (c->prof) {
+            a = pool_event(c);
+            cudaEventRecord(a, c->st);
+        }
+    }
+    ~PhaseScope() {
+        if (c->prof) {
+            cudaEvent_t b = pool_event(c);
+            cudaEventRecord(b, c->st);
+            c->ev_open.push_back({ph, {a, b}});
+        }
+        c->prof_launch[ph] += c->launches - l0;
+    }
+};
+void prof_collect(tfg_ctx* c) {
+    for (auto& e : c->ev_open) {
+        cudaEventSynchronize(e.second.second);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e.second.first, e.second.second);
+        c->prof_ms[e.first] += ms;
+        c->prof_n[e.first] += 1;
+        c->ev_pool.push_back(e.second.first);
+        c->ev_pool.push_back(e.second.second);
+    }
+    c->ev_open.clear();
 }
 
 void tile_box(const tfg_ctx* c, int ti, double* b) {
@@ -262,6 +319,7 @@ int slot_copy(tfg_ctx* c, int slot, int ti, bool to_host) {
     size_t bytes = c->stride * sizeof(float);
     cudaMemcpyKind k = to_host ? cudaMemcpyDeviceToHost : cudaMemcpyHostToDevice;
     float* dev[3] = {c->d_params + off, c->d_m + off, c->d_v + off};
+    (to_host ? c->d2h_bytes : c->h2d_bytes) += 3 * bytes + kOccVox * sizeof(float);
     for (int a = 0; a < 3; ++a) {
         float* h = t.rec + a * c->stride;
         CK(cudaMemcpyAsync(to_host ? static_cast<void*>(h) : static_cast<void*>(dev[a]),
@@ -301,6 +359,7 @@ FieldPtrs train_ptrs(tfg_ctx* c) {
 }
 
 int run_occupancy(tfg_ctx* c, bool update, uint64_t* keys) {
+    PhaseScope ps(c, kPhOccupancy);
     OccArgs o{};
     o.hl = c->hl;
     o.density_lim = c->density_lim;
@@ -362,6 +421,7 @@ int build_accept(tfg_ctx* c, const std::vector<Crop>& crops, const std::vector<C
     a.n_loaded = c->nslots;
     a.z_min = c->roi.z_min;
     a.z_max = c->roi.z_max;
+    PhaseScope ps(c, kPhAccept);
     if (launch_accept(a, c->d_flags, c->d_pos, c->d_block_sums, c->d_accept_n, c->d_accept, c->st,
                       &c->launches))
         return fail(TFG_ERR_INVALID, "accept: scan capacity exceeded");
@@ -398,6 +458,7 @@ int check_status(tfg_ctx* c) {
 }
 
 int sync_status(tfg_ctx* c) {
+    c->d2h_bytes += sizeof(Status);
     CK(cudaMemcpyAsync(c->h_status, c->d_status, sizeof(Status), cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
     return check_status(c);
@@ -423,6 +484,7 @@ RaygenArgs base_raygen(tfg_ctx* c) {
 int run_sampler(tfg_ctx* c, RaygenArgs& a) {
     if (a.n_rays <= 0 || a.n_rays > c->max_rays)
         return fail(TFG_ERR_INVALID, "sample: n_rays outside (0, max_rays]");
+    PhaseScope ps(c, kPhSampler);
     CK(cudaMemsetAsync(c->d_status, 0, sizeof(Status), c->st));
     if (launch_sampler(a, c->d_rays, c->d_venc, c->d_counts, c->d_P, c->d_block_sums, c->d_tiles,
                        c->max_tiles, c->s, c->sample_cap, c->d_status, c->st, &c->launches))
@@ -447,12 +509,14 @@ FieldArgs field_args(tfg_ctx* c, const FieldPtrs& f) {
 }
 
 int run_forward(tfg_ctx* c, const FieldPtrs& f) {
+    PhaseScope ps(c, kPhFieldFwd);
     launch_field_forward(field_args(c, f), 2 * c->sms, c->st, &c->launches);
     CK(cudaGetLastError());
     return 0;
 }
 
 int run_composite(tfg_ctx* c, bool backward) {
+    PhaseScope ps(c, kPhComposite);
     CompositeArgs a{};
     a.rays = c->d_rays;
     a.P = c->d_P;
@@ -472,6 +536,7 @@ int run_composite(tfg_ctx* c, bool backward) {
 }
 
 int run_backward(tfg_ctx* c) {
+    PhaseScope ps(c, kPhFieldBwd);
     CK(cudaMemsetAsync(c->d_grads, 0, c->n_params * sizeof(float), c->st));
     FieldGradArgs g{};
     for (int k = 0; k < c->nslots; ++k) {
@@ -882,6 +947,7 @@ TFG_API int tfg_set_window(tfg_ctx* c, int pr, int pc) {
         c->h_crop_rect[4 * v + 2] = w;
         c->h_crop_rect[4 * v + 3] = h;
         const uint8_t* src = c->h_images[v] + 3 * (size_t(u.r0) * c->cams[v].image_cols + u.c0);
+        c->h2d_bytes += uint64_t(w) * 3 * h;
         CK(cudaMemcpy2DAsync(c->d_crops + off, size_t(w) * 3, src, size_t(c->cams[v].image_cols) * 3,
                              size_t(w) * 3, h, cudaMemcpyHostToDevice, c->side));
         off += uint64_t(w) * h * 3;
@@ -1031,7 +1097,10 @@ TFG_API int tfg_optimizer_step(tfg_ctx* c, uint64_t iter) {
         a.g[2 * c->nslots] = gap;
         a.n_groups = ng + 1;
     }
-    launch_adam(a, total, c->st, &c->launches);
+    {
+        PhaseScope ps(c, kPhAdam);
+        launch_adam(a, total, c->st, &c->launches);
+    }
     CK(cudaGetLastError());
     int interval = c->fc.occupancy_interval;
     if (interval > 0 && (iter + 1) % uint64_t(interval) == 0) {
@@ -1401,10 +1470,69 @@ TFG_API int tfg_kernel_launch_count(tfg_ctx* c, uint64_t* n) {
     return 0;
 }
 
-TFG_API int tfg_profile_enable(tfg_ctx*, int) { return 0; }
+TFG_API int tfg_profile_enable(tfg_ctx* c, int on) {
+    if (!c) return fail(TFG_ERR_INVALID, "profile_enable: null context");
+    prof_collect(c);
+    c->prof = on != 0;
+    for (int p = 0; p < kNumPhases; ++p) {
+        c->prof_ms[p] = 0;
+        c->prof_n[p] = 0;
+        c->prof_launch[p] = 0;
+    }
+    return 0;
+}
 
-TFG_API int tfg_profile_read(tfg_ctx*, const char**, double*, uint64_t*, int, int* n_out) {
-    if (n_out) *n_out = 0;
+// Accumulated device ms, bracket counts and kernel launches per phase since
+// the last tfg_profile_enable (synchronises on the recorded events).
+TFG_API int tfg_profile_read(tfg_ctx* c, const char** names, double* ms, uint64_t* launches,
+                             int capacity, int* n_out) {
+    if (!c) return fail(TFG_ERR_INVALID, "profile_read: null context");
+    prof_collect(c);
+    int n = std::min(capacity, int(kNumPhases));
+    for (int p = 0; p < n; ++p) {
+        if (names) names[p] = kPhaseNames[p];
+        if (ms) ms[p] = c->prof_ms[p];
+        if (launches) launches[p] = c->prof_launch[p];
+    }
+    if (n_out) *n_out = n;
+    return 0;
+}
+
+TFG_API int tfg_last_batch(tfg_ctx* c, int* n_rays, uint64_t* n_samples) {
+    if (!c) return fail(TFG_ERR_INVALID, "last_batch: null context");
+    int rc = sync_status(c);
+    if (n_rays) *n_rays = c->cur_rays;
+    if (n_samples) *n_samples = c->h_status->n_samples;
+    return rc;
+}
+
+// TileField::create (field.hpp:93) on the host into caller buffers (enc, dnet,
+// occupancy all 1.0; moments zero when given).
+TFG_API int tfg_tile_init(const tfg_field_config* fc, uint64_t seed, int row, int col,
+                          tfg_tile_state* o) {
+    uint64_t enc, dn;
+    tfg_param_counts(fc, &enc, &dn, nullptr);
+    Rng re(hash_combine(hash_combine(hash_combine(seed, kPurposeTileEnc), uint64_t(row)), uint64_t(col)));
+    if (o->enc)
+        for (uint64_t i = 0; i < enc; ++i) o->enc[i] = float(re.uniform(-1e-4, 1e-4));
+    Rng rd(hash_combine(hash_combine(hash_combine(seed, kPurposeTileDnet), uint64_t(row)), uint64_t(col)));
+    const int dw[3] = {fc->levels * fc->features, fc->density_hidden, 1 + fc->embedding};
+    if (o->dnet) mlp_init_host(dw, 3, rd, o->dnet);
+    for (float* z : {o->enc_m, o->enc_v})
+        if (z) std::memset(z, 0, enc * 4);
+    for (float* z : {o->dnet_m, o->dnet_v})
+        if (z) std::memset(z, 0, dn * 4);
+    uint64_t nv = uint64_t(fc->occupancy_resolution) * fc->occupancy_resolution * fc->occupancy_resolution;
+    if (o->occupancy)
+        for (uint64_t i = 0; i < nv; ++i) o->occupancy[i] = 1.0f;
+    o->enc_step = o->dnet_step = 0;
+    return 0;
+}
+
+TFG_API int tfg_copy_bytes(tfg_ctx* c, uint64_t* h2d, uint64_t* d2h) {
+    if (!c) return fail(TFG_ERR_INVALID, "copy_bytes: null context");
+    if (h2d) *h2d = c->h2d_bytes;
+    if (d2h) *d2h = c->d2h_bytes;
     return 0;
 }
 

@@ -88,6 +88,11 @@ def lib() -> C.CDLL:
         "tfg_render_setup": [_vp, _vp, _vp, C.c_int, _vp, _vp],
         "tfg_render_pixels": [_vp, _vp, _vp, C.c_int, _vp, _vp, _vp],
         "tfg_kernel_launch_count": [_vp, _vp],
+        "tfg_copy_bytes": [_vp, _vp, _vp],
+        "tfg_last_batch": [_vp, _vp, _vp],
+        "tfg_tile_init": [_vp, C.c_uint64, C.c_int, C.c_int, _vp],
+        "tfg_profile_enable": [_vp, C.c_int],
+        "tfg_profile_read": [_vp, _vp, _vp, _vp, C.c_int, _vp],
         "tfg_param_counts": [_vp, _vp, _vp, _vp],
         "tfg_default_field_config": [_vp],
         "tfg_default_train_config": [_vp],
@@ -106,6 +111,19 @@ def _check(rc: int) -> None:
         if rc == 3:
             raise NonFiniteGradient(msg)
         raise TileFieldError(msg or f"tilefield_gpu error {rc}")
+
+
+def tile_init(fcfg: FieldConfig, seed: int, row: int, col: int) -> dict:
+    """TileField::create (field.hpp:93): fresh params, zero moments, occupancy 1."""
+    enc_n, dnet_n, _, _ = field_sizes(fcfg)
+    a = {k: np.zeros(enc_n, np.float32) for k in ("enc", "enc_m", "enc_v")}
+    a.update({k: np.zeros(dnet_n, np.float32) for k in ("dnet", "dnet_m", "dnet_v")})
+    a["occupancy"] = np.zeros(fcfg.occupancy_resolution ** 3, np.float32)
+    ts = TileState(*[a[k].ctypes.data for k in ("enc", "dnet", "enc_m", "enc_v", "dnet_m", "dnet_v")],
+                   0, 0, a["occupancy"].ctypes.data)
+    _check(lib().tfg_tile_init(C.byref(fcfg), seed, row, col, C.byref(ts)))
+    a["enc_step"], a["dnet_step"] = 0, 0
+    return a
 
 
 def snake_path(H: int, W: int) -> list[tuple[int, int]]:
@@ -295,6 +313,28 @@ class Context:
         n = C.c_uint64()
         _check(lib().tfg_kernel_launch_count(self.h, C.byref(n)))
         return n.value
+
+    def last_batch(self) -> tuple[int, int]:
+        r, n = C.c_int(), C.c_uint64()
+        _check(lib().tfg_last_batch(self.h, C.byref(r), C.byref(n)))
+        return r.value, n.value
+
+    def copy_bytes(self) -> tuple[int, int]:
+        a, b = C.c_uint64(), C.c_uint64()
+        _check(lib().tfg_copy_bytes(self.h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+    def profile_enable(self, on: bool = True) -> None:
+        _check(lib().tfg_profile_enable(self.h, int(on)))
+
+    def profile_read(self) -> dict:
+        """{phase: (device ms, kernel launches)} since profile_enable."""
+        names = (C.c_char_p * 16)()
+        ms = np.zeros(16, np.float64)
+        ln = np.zeros(16, np.uint64)
+        n = C.c_int()
+        _check(lib().tfg_profile_read(self.h, names, ptr(ms), ptr(ln), 16, C.byref(n)))
+        return {names[i].decode(): (float(ms[i]), int(ln[i])) for i in range(n.value)}
 
     # ---- render ---------------------------------------------------------------
     def render_setup(self, tiles: list[tuple[int, int]], states: list[dict], color) -> None:
