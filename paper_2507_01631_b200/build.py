@@ -27,6 +27,7 @@ UNITS = [
     ("k_adam.cu", ["-fmad=false"]),
     ("tfg_api.cu", ["-fmad=false"]),
     ("k_field.cu", []),
+    ("k_field_tc.cu", []),
     ("k_composite.cu", []),
 ]
 

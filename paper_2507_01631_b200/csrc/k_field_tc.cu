@@ -1,0 +1,795 @@
+// k_field_tc.cu — K2/K4 on the 5th-generation tensor cores (tcgen05 + TMEM).
+//
+// The per-tile NeRF field (forward_batch / backward_batch, field.hpp:185-197;
+// MlpT nn.hpp:90-157; HashGridT nn.hpp:213-245) split by bound:
+//   K2a hash_fwd_kernel   hash-grid gather (L2-latency bound): 16 features per
+//                         sample -> bf16 tile in UMMA operand layout (4 KB/tile)
+//   K2b mlp_fwd_kernel    density MLP 16->64->16 + colour MLP 39->64->64->3 as
+//                         tcgen05.mma (bf16 x bf16 -> fp32 in TMEM), operands
+//                         staged by the bulk-copy engine, epilogues
+//                         (bias, ReLU, exp/sigmoid) from tcgen05.ld
+//   K4b mlp_bwd_kernel    recomputed forward + data-gradient GEMMs + weight-
+//                         gradient GEMMs (K = 128 samples, MN-major operands
+//                         read from the same smem tiles) accumulated in TMEM
+//                         across all tiles of a persistent CTA, flushed with
+//                         one fp32 atomic per weight per CTA
+//   K4a hash_bwd_kernel   hash-table scatter-add (red.global.add.v2.f32)
+// A tile is <= 128 samples of one slot bucket (K1), so the density weights of
+// a tile are one tile's.  Precision: bf16 operands, fp32 accumulation (tests
+// state the tolerance against the fp32 oracle).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "tf_common.cuh"
+#include "tf_hash.cuh"
+#include "tf_kernels.h"
+#include "umma.cuh"
+
+namespace tfg {
+
+namespace {
+
+constexpr int kT = 128;
+constexpr uint32_t kChunk = kT * 16;  // bytes of one 8-column chunk of a 128-row tile
+constexpr uint32_t kFeatTile = 2 * kChunk;
+
+// smem weight tiles (bf16, chunk-major interleave; rows = out features)
+constexpr uint32_t kW1dRows = 64, kW2dRows = 16, kWc1Rows = 64, kWc2Rows = 64, kWc3Rows = 16;
+constexpr uint32_t kW1dBytes = kW1dRows * 16 * 2;   // [64 x 16]
+constexpr uint32_t kW2dBytes = kW2dRows * 64 * 2;   // [16 x 64]
+constexpr uint32_t kWc1Bytes = kWc1Rows * 48 * 2;   // [64 x 48] (39 real)
+constexpr uint32_t kWc2Bytes = kWc2Rows * 64 * 2;   // [64 x 64]
+constexpr uint32_t kWc3Bytes = kWc3Rows * 64 * 2;   // [16 x 64] (3 real)
+constexpr uint32_t kBiasFloats = 64 + 16 + 64 + 64 + 16;
+
+struct Weights {
+    uint8_t* w1d;
+    uint8_t* w2d;
+    uint8_t* wc1;
+    uint8_t* wc2;
+    uint8_t* wc3;
+    float* b1d;
+    float* b2d;
+    float* bc1;
+    float* bc2;
+    float* bc3;
+};
+
+__device__ __forceinline__ uint8_t* carve(uint8_t*& p, uint32_t bytes) {
+    uint8_t* r = p;
+    p += (bytes + 127) & ~127u;
+    return r;
+}
+
+__device__ __forceinline__ Weights carve_weights(uint8_t*& p) {
+    Weights w;
+    w.w1d = carve(p, kW1dBytes);
+    w.w2d = carve(p, kW2dBytes);
+    w.wc1 = carve(p, kWc1Bytes);
+    w.wc2 = carve(p, kWc2Bytes);
+    w.wc3 = carve(p, kWc3Bytes);
+    float* b = reinterpret_cast<float*>(carve(p, kBiasFloats * 4));
+    w.b1d = b;
+    w.b2d = b + 64;
+    w.bc1 = b + 80;
+    w.bc2 = b + 144;
+    w.bc3 = b + 208;
+    return w;
+}
+constexpr uint32_t kWeightsBytes = ((kW1dBytes + 127) & ~127u) + ((kW2dBytes + 127) & ~127u) +
+                                   ((kWc1Bytes + 127) & ~127u) + ((kWc2Bytes + 127) & ~127u) +
+                                   ((kWc3Bytes + 127) & ~127u) + ((kBiasFloats * 4 + 127) & ~127u);
+
+// fp32 row-major W [rows_src x cols_src] (out x in) -> bf16 [rows x cols]
+// chunk-major tile, zero padded.
+__device__ __forceinline__ void stage_matrix(uint8_t* dst, const float* __restrict__ W, int rows_src,
+                                             int cols_src, int rows, int cols) {
+    for (int i = threadIdx.x; i < rows * cols; i += blockDim.x) {
+        int r = i / cols, c = i - r * cols;
+        float v = (r < rows_src && c < cols_src) ? W[r * cols_src + c] : 0.f;
+        *reinterpret_cast<__nv_bfloat16*>(dst + umma::off(rows, r, c)) = __float2bfloat16_rn(v);
+    }
+}
+__device__ __forceinline__ void stage_density(const Weights& w, const float* __restrict__ p) {
+    stage_matrix(w.w1d, p + kDW1, kDHidden, kFeatDim, 64, 16);
+    stage_matrix(w.w2d, p + kDW2, kDOut, kDHidden, 16, 64);
+    for (int i = threadIdx.x; i < 64; i += blockDim.x) w.b1d[i] = p[kDB1 + i];
+    for (int i = threadIdx.x; i < 16; i += blockDim.x) w.b2d[i] = p[kDB2 + i];
+}
+__device__ __forceinline__ void stage_color(const Weights& w, const float* __restrict__ p) {
+    stage_matrix(w.wc1, p + kCW1, kCHidden, kCIn, 64, 48);
+    stage_matrix(w.wc2, p + kCW2, kCHidden, kCHidden, 64, 64);
+    stage_matrix(w.wc3, p + kCW3, 3, kCHidden, 16, 64);
+    for (int i = threadIdx.x; i < 64; i += blockDim.x) {
+        w.bc1[i] = p[kCB1 + i];
+        w.bc2[i] = p[kCB2 + i];
+    }
+    for (int i = threadIdx.x; i < 16; i += blockDim.x) w.bc3[i] = i < 3 ? p[kCB3 + i] : 0.f;
+}
+
+__device__ __forceinline__ uint32_t pack2(float a, float b) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+}
+// Writes 8 consecutive columns [8c, 8c+8) of row r of a 128-row tile.
+__device__ __forceinline__ void st_chunk(uint8_t* buf, int r, int c, const float* v) {
+    uint4 q = make_uint4(pack2(v[0], v[1]), pack2(v[2], v[3]), pack2(v[4], v[5]), pack2(v[6], v[7]));
+    *reinterpret_cast<uint4*>(buf + c * kChunk + (r >> 3) * 128 + (r & 7) * 16) = q;
+}
+
+// Descriptors for the chunk-major tiles (see umma.cuh).
+__device__ __forceinline__ uint64_t kmaj(const uint8_t* base, uint32_t rows, int kstep) {
+    // rows x K tile read K-major; kstep-th group of 16 K columns
+    return umma::desc(umma::smem_u32(base) + kstep * 2 * rows * 16, rows * 16, 128);
+}
+__device__ __forceinline__ uint64_t mnmaj(const uint8_t* base, uint32_t rows, int kstep) {
+    // rows = K x cols = MN tile read MN-major; kstep-th group of 16 K rows
+    return umma::desc(umma::smem_u32(base) + kstep * 256, 128, rows * 16);
+}
+
+// Barrier before a single thread issues MMAs that read smem written by all
+// threads (generic -> async proxy) and overwrite TMEM other threads read.
+__device__ __forceinline__ void sync_for_mma() {
+    umma::fence_async_smem();
+    umma::fence_before_sync();
+    __syncthreads();
+    umma::fence_after_sync();
+}
+__device__ __forceinline__ void wait_mma(uint64_t* bar, uint32_t& phase) {
+    umma::mbar_wait(bar, phase);
+    phase ^= 1u;
+    umma::fence_after_sync();
+}
+
+// 16 TMEM columns starting at col of this thread's lane row.
+__device__ __forceinline__ void tld16(uint32_t tmem, int col, float* v) {
+    uint32_t w = threadIdx.x >> 5;
+    umma::ld16(tmem + ((32u * w) << 16) + uint32_t(col), v);
+}
+
+__device__ __forceinline__ float sigm(float x) { return 1.f / (1.f + __expf(-x)); }
+
+} // namespace
+
+// ------------------------------------------------------------------ K2a
+// Thread per tile row: 8-level hash gather -> 16 bf16 features in the tile's
+// chunk-major layout (the A operand of the first density layer) + ray id.
+__global__ void __launch_bounds__(128) hash_fwd_kernel(FieldArgs a, uint8_t* __restrict__ feat,
+                                                       int32_t* __restrict__ rays) {
+    uint32_t n_tiles = a.status->n_tiles;
+    int r = threadIdx.x;
+    for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        TileDesc td = a.tiles[t];
+        float f[kFeatDim];
+        int ray = -1;
+        if (r < td.n) {
+            float4 L = a.s.local[uint64_t(td.start) + r];
+            ray = __float_as_int(L.w);
+            hash_encode(a.hl, a.f.enc[td.slot], L.x, L.y, L.z, f);
+        } else {
+#pragma unroll
+            for (int i = 0; i < kFeatDim; ++i) f[i] = 0.f;
+        }
+        uint8_t* base = feat + uint64_t(t) * kFeatTile;
+        st_chunk(base, r, 0, f);
+        st_chunk(base, r, 1, f + 8);
+        rays[uint64_t(t) * kT + r] = ray;
+    }
+}
+
+// ------------------------------------------------------------------ K4a
+__global__ void __launch_bounds__(128) hash_bwd_kernel(FieldArgs a, FieldGradArgs g,
+                                                       const float4* __restrict__ dfeat) {
+    uint32_t n_tiles = a.status->n_tiles;
+    int r = threadIdx.x;
+    for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        TileDesc td = a.tiles[t];
+        if (r >= td.n) continue;
+        float4 L = a.s.local[uint64_t(td.start) + r];
+        const float4* d4 = dfeat + (uint64_t(t) * kT + r) * 4;
+        float d[kFeatDim];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            float4 v = d4[q];
+            d[4 * q] = v.x;
+            d[4 * q + 1] = v.y;
+            d[4 * q + 2] = v.z;
+            d[4 * q + 3] = v.w;
+        }
+        hash_scatter(a.hl, g.g_enc[td.slot], L.x, L.y, L.z, d);
+    }
+}
+
+// ------------------------------------------------------------------ K2b
+// smem: weights | X0 [128x16] | CIN [128x48] | A [128x64] (H1, then C2) | C1 [128x64]
+constexpr uint32_t kFwdSmem = kWeightsBytes + 4096 + 12288 + 16384 + 16384 + 128;
+constexpr uint32_t kFwdTmemCols = 64;
+
+__global__ void __launch_bounds__(128) mlp_fwd_kernel(FieldArgs a, const uint8_t* __restrict__ feat,
+                                                      const int32_t* __restrict__ rays) {
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    __shared__ uint64_t bar_mma, bar_ld;
+    __shared__ uint32_t tmem_slot;
+    uint8_t* p = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+    Weights W = carve_weights(p);
+    uint8_t* X0 = carve(p, 4096);
+    uint8_t* CIN = carve(p, 12288);
+    uint8_t* HA = carve(p, 16384);
+    uint8_t* C1 = carve(p, 16384);
+    const int r = threadIdx.x;
+    if (r == 0) {
+        umma::mbar_init(&bar_mma, 1);
+        umma::mbar_init(&bar_ld, 1);
+        umma::fence_mbar_init();
+    }
+    if (r < 32) umma::tmem_alloc<kFwdTmemCols>(&tmem_slot);
+    stage_color(W, a.f.color);
+    uint32_t ph_mma = 0, ph_ld = 0;
+    int cur = -1;
+    uint32_t n_tiles = a.status->n_tiles;
+    sync_for_mma();
+    const uint32_t tmem = tmem_slot;
+    const uint32_t id64 = umma::idesc_bf16(128, 64, 0, 0);
+    const uint32_t id16 = umma::idesc_bf16(128, 16, 0, 0);
+    for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        TileDesc td = a.tiles[t];
+        if (td.slot != cur) {
+            stage_density(W, a.f.dnet[td.slot]);
+            cur = td.slot;
+        }
+        if (r == 0) {
+            umma::mbar_expect_tx(&bar_ld, kFeatTile);
+            umma::bulk_g2s(X0, feat + uint64_t(t) * kFeatTile, kFeatTile, &bar_ld);
+        }
+        int ray = rays[uint64_t(t) * kT + r];
+        float ve[kViewDim];
+        {
+            const float4* v4 = a.venc + uint64_t(ray < 0 ? 0 : ray) * 6;
+#pragma unroll
+            for (int q = 0; q < 6; ++q) {
+                float4 v = __ldg(v4 + q);
+                ve[4 * q] = v.x;
+                ve[4 * q + 1] = v.y;
+                ve[4 * q + 2] = v.z;
+                ve[4 * q + 3] = v.w;
+            }
+        }
+        sync_for_mma();  // density weights staged, previous tile's TMEM reads done
+        umma::mbar_wait(&bar_ld, ph_ld);
+        ph_ld ^= 1u;
+        // ---- density layer 1: [128x16] x W1d^T -> 64
+        if (r == 0) {
+            umma::mma(tmem, kmaj(X0, kT, 0), kmaj(W.w1d, kW1dRows, 0), id64, 0);
+            umma::commit(&bar_mma);
+        }
+        wait_mma(&bar_mma, ph_mma);
+        {
+            float v[64];
+            tld16(tmem, 0, v);
+            tld16(tmem, 16, v + 16);
+            tld16(tmem, 32, v + 32);
+            tld16(tmem, 48, v + 48);
+            umma::ld_wait();
+#pragma unroll
+            for (int i = 0; i < 64; ++i) v[i] = fmaxf(v[i] + W.b1d[i], 0.f);
+#pragma unroll
+            for (int c = 0; c < 8; ++c) st_chunk(HA, r, c, v + 8 * c);
+        }
+        sync_for_mma();
+        // ---- density layer 2: [128x64] x W2d^T -> 16 (raw sigma | embedding)
+        if (r == 0) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                umma::mma(tmem, kmaj(HA, kT, k), kmaj(W.w2d, kW2dRows, k), id16, k > 0);
+            umma::commit(&bar_mma);
+        }
+        wait_mma(&bar_mma, ph_mma);
+        float sigma;
+        {
+            float v[16];
+            tld16(tmem, 0, v);
+            umma::ld_wait();
+            float raw = v[0] + W.b2d[0];
+            sigma = raw >= a.density_lim ? a.density_max : __expf(raw);
+            float cin[48];
+#pragma unroll
+            for (int i = 0; i < kEmb; ++i) cin[i] = v[1 + i] + W.b2d[1 + i];
+#pragma unroll
+            for (int i = 0; i < kViewDim; ++i) cin[kEmb + i] = ve[i];
+            cin[kCIn] = 1.f;  // ones column (bias gradient of colour layer 1 in K4)
+#pragma unroll
+            for (int i = kCIn + 1; i < 48; ++i) cin[i] = 0.f;
+#pragma unroll
+            for (int c = 0; c < 6; ++c) st_chunk(CIN, r, c, cin + 8 * c);
+        }
+        sync_for_mma();
+        // ---- colour layer 1: [128x48] x Wc1^T -> 64
+        if (r == 0) {
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+                umma::mma(tmem, kmaj(CIN, kT, k), kmaj(W.wc1, kWc1Rows, k), id64, k > 0);
+            umma::commit(&bar_mma);
+        }
+        wait_mma(&bar_mma, ph_mma);
+        {
+            float v[64];
+            tld16(tmem, 0, v);
+            tld16(tmem, 16, v + 16);
+            tld16(tmem, 32, v + 32);
+            tld16(tmem, 48, v + 48);
+            umma::ld_wait();
+#pragma unroll
+            for (int i = 0; i < 64; ++i) v[i] = fmaxf(v[i] + W.bc1[i], 0.f);
+#pragma unroll
+            for (int c = 0; c < 8; ++c) st_chunk(C1, r, c, v + 8 * c);
+        }
+        sync_for_mma();
+        // ---- colour layer 2: [128x64] x Wc2^T -> 64
+        if (r == 0) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                umma::mma(tmem, kmaj(C1, kT, k), kmaj(W.wc2, kWc2Rows, k), id64, k > 0);
+            umma::commit(&bar_mma);
+        }
+        wait_mma(&bar_mma, ph_mma);
+        {
+            float v[64];
+            tld16(tmem, 0, v);
+            tld16(tmem, 16, v + 16);
+            tld16(tmem, 32, v + 32);
+            tld16(tmem, 48, v + 48);
+            umma::ld_wait();
+#pragma unroll
+            for (int i = 0; i < 64; ++i) v[i] = fmaxf(v[i] + W.bc2[i], 0.f);
+#pragma unroll
+            for (int c = 0; c < 8; ++c) st_chunk(HA, r, c, v + 8 * c);
+        }
+        sync_for_mma();
+        // ---- colour layer 3: [128x64] x Wc3^T -> 16 (3 real) -> sigmoid
+        if (r == 0) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                umma::mma(tmem, kmaj(HA, kT, k), kmaj(W.wc3, kWc3Rows, k), id16, k > 0);
+            umma::commit(&bar_mma);
+        }
+        wait_mma(&bar_mma, ph_mma);
+        {
+            float v[16];
+            tld16(tmem, 0, v);
+            umma::ld_wait();
+            if (r < td.n)
+                a.s.io[uint64_t(td.start) + r] =
+                    make_float4(sigma, sigm(v[0] + W.bc3[0]), sigm(v[1] + W.bc3[1]), sigm(v[2] + W.bc3[2]));
+        }
+    }
+    umma::fence_before_sync();
+    __syncthreads();
+    if (r < 32) umma::tmem_free<kFwdTmemCols>(tmem);
+}
+
+// ------------------------------------------------------------------ K4b
+// smem (order matters: tiles read as M-padded MN-major operands (H1, C1, C2)
+// may over-read up to 16 chunks = 32 KB from their start, which stays inside
+// the allocation):
+//   H1 [128 x 72] | C1 [128 x 72] | C2 [128 x 72]   (chunk 8 = ones row)
+//   X0 [128 x 32] (chunk 2 = ones column, chunk 3 = 0) | CIN [128 x 48]
+//   D3 [128 x 16] | DO [128 x 16] | weights
+// TMEM (256 columns): working accumulator [0,64); weight-gradient
+// accumulators persistent across the CTA's tiles:
+//   dWc2^T [64,128)  dWc1 [128,176)  dW1d [176,208)  dWc3^T [208,224)  dW2d^T [224,240)
+constexpr uint32_t kBufA = 9 * kChunk;  // 18432
+constexpr uint32_t kBwdSmem = 3 * kBufA + 4 * kChunk + 6 * kChunk + 2 * kChunk + 2 * kChunk + kWeightsBytes + 128;
+constexpr uint32_t kBwdTmemCols = 256;
+constexpr int kColWc2 = 64, kColWc1 = 128, kColW1d = 176, kColWc3 = 208, kColW2d = 224;
+
+__device__ __forceinline__ void set_ones_chunk(uint8_t* buf, int chunk, int r) {
+    float v[8] = {1.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    st_chunk(buf, r, chunk, v);
+}
+
+// Adds the CTA's TMEM weight-gradient accumulators into the global gradients.
+__device__ __forceinline__ void flush_density(uint32_t tmem, float* __restrict__ gd) {
+    int m = threadIdx.x;  // TMEM lane row
+    float v[32];
+    // dW1d [o=m][i] (cols 0..15), bias at col 16
+    tld16(tmem, kColW1d, v);
+    tld16(tmem, kColW1d + 16, v + 16);
+    umma::ld_wait();
+    if (m < kDHidden) {
+        for (int i = 0; i < kFeatDim; ++i) atomicAdd(gd + kDW1 + m * kFeatDim + i, v[i]);
+        atomicAdd(gd + kDB1 + m, v[16]);
+    }
+    // dW2d^T [i=m][o], bias row m = 64
+    tld16(tmem, kColW2d, v);
+    umma::ld_wait();
+    if (m < kDHidden)
+        for (int o = 0; o < kDOut; ++o) atomicAdd(gd + kDW2 + o * kDHidden + m, v[o]);
+    else if (m == kDHidden)
+        for (int o = 0; o < kDOut; ++o) atomicAdd(gd + kDB2 + o, v[o]);
+}
+__device__ __forceinline__ void flush_color(uint32_t tmem, float* __restrict__ gc) {
+    int m = threadIdx.x;
+    float v[64];
+    // dWc2^T [i=m][o], bias row 64
+    tld16(tmem, kColWc2, v);
+    tld16(tmem, kColWc2 + 16, v + 16);
+    tld16(tmem, kColWc2 + 32, v + 32);
+    tld16(tmem, kColWc2 + 48, v + 48);
+    umma::ld_wait();
+    if (m < kCHidden)
+        for (int o = 0; o < kCHidden; ++o) atomicAdd(gc + kCW2 + o * kCHidden + m, v[o]);
+    else if (m == kCHidden)
+        for (int o = 0; o < kCHidden; ++o) atomicAdd(gc + kCB2 + o, v[o]);
+    // dWc1 [o=m][i], i < 39, bias at col 39
+    tld16(tmem, kColWc1, v);
+    tld16(tmem, kColWc1 + 16, v + 16);
+    tld16(tmem, kColWc1 + 32, v + 32);
+    umma::ld_wait();
+    if (m < kCHidden) {
+        for (int i = 0; i < kCIn; ++i) atomicAdd(gc + kCW1 + m * kCIn + i, v[i]);
+        atomicAdd(gc + kCB1 + m, v[kCIn]);
+    }
+    // dWc3^T [i=m][o], bias row 64
+    tld16(tmem, kColWc3, v);
+    umma::ld_wait();
+    if (m < kCHidden)
+        for (int o = 0; o < 3; ++o) atomicAdd(gc + kCW3 + o * kCHidden + m, v[o]);
+    else if (m == kCHidden)
+        for (int o = 0; o < 3; ++o) atomicAdd(gc + kCB3 + o, v[o]);
+}
+
+__global__ void __launch_bounds__(128) mlp_bwd_kernel(FieldArgs a, FieldGradArgs g,
+                                                      const uint8_t* __restrict__ feat,
+                                                      const int32_t* __restrict__ rays,
+                                                      float4* __restrict__ dfeat) {
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    __shared__ uint64_t bar_mma, bar_ld;
+    __shared__ uint32_t tmem_slot;
+    uint8_t* p = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+    uint8_t* H1 = carve(p, kBufA);
+    uint8_t* C1 = carve(p, kBufA);
+    uint8_t* C2 = carve(p, kBufA);
+    uint8_t* X0 = carve(p, 4 * kChunk);
+    uint8_t* CIN = carve(p, 6 * kChunk);
+    uint8_t* D3 = carve(p, 2 * kChunk);
+    uint8_t* DO = carve(p, 2 * kChunk);
+    Weights W = carve_weights(p);
+    const int r = threadIdx.x;
+    if (r == 0) {
+        umma::mbar_init(&bar_mma, 1);
+        umma::mbar_init(&bar_ld, 1);
+        umma::fence_mbar_init();
+    }
+    if (r < 32) umma::tmem_alloc<kBwdTmemCols>(&tmem_slot);
+    stage_color(W, a.f.color);
+    // constant ones chunks
+    set_ones_chunk(H1, 8, r);
+    set_ones_chunk(C1, 8, r);
+    set_ones_chunk(C2, 8, r);
+    set_ones_chunk(X0, 2, r);
+    {
+        float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        st_chunk(X0, r, 3, z);
+    }
+    uint32_t ph_mma = 0, ph_ld = 0;
+    int cur = -1;
+    bool first_d = true, first_c = true;
+    uint32_t n_tiles = a.status->n_tiles;
+    sync_for_mma();
+    const uint32_t tmem = tmem_slot;
+    const uint32_t id64 = umma::idesc_bf16(128, 64, 0, 0);
+    const uint32_t id16 = umma::idesc_bf16(128, 16, 0, 0);
+    const uint32_t id64_kmn = umma::idesc_bf16(128, 64, 0, 1);  // A K-major, B MN-major
+    const uint32_t id16_kmn = umma::idesc_bf16(128, 16, 0, 1);
+    const uint32_t idw64 = umma::idesc_bf16(128, 64, 1, 1);     // weight grads: both MN-major
+    const uint32_t idw48 = umma::idesc_bf16(128, 48, 1, 1);
+    const uint32_t idw32 = umma::idesc_bf16(128, 32, 1, 1);
+    const uint32_t idw16 = umma::idesc_bf16(128, 16, 1, 1);
+    for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        TileDesc td = a.tiles[t];
+        if (td.slot != cur) {
+            if (cur >= 0) flush_density(tmem, g.g_dnet[cur]);
+            stage_density(W, a.f.dnet[td.slot]);
+            cur = td.slot;
+            first_d = true;
+        }
+        if (r == 0) {
+            umma::mbar_expect_tx(&bar_ld, kFeatTile);
+            umma::bulk_g2s(X0, feat + uint64_t(t) * kFeatTile, kFeatTile, &bar_ld);
+        }
+        bool live = r < td.n;
+        int ray = rays[uint64_t(t) * kT + r];
+        float4 dio = live ? a.s.io[uint64_t(td.start) + r] : make_float4(0.f, 0.f, 0.f, 0.f);
+        float ve[kViewDim];
+        {
+            const float4* v4 = a.venc + uint64_t(ray < 0 ? 0 : ray) * 6;
+#pragma unroll
+            for (int q = 0; q < 6; ++q) {
+                float4 v = __ldg(v4 + q);
+                ve[4 * q] = v.x;
+                ve[4 * q + 1] = v.y;
+                ve[4 * q + 2] = v.z;
+                ve[4 * q + 3] = v.w;
+            }
+        }
+        sync_for_mma();
+        umma::mbar_wait(&bar_ld, ph_ld);
+        ph_ld ^= 1u;
+        uint32_t mh[2], mc1[2], mc2[2];  // ReLU masks of H1, C1, C2
+        float draw;
+        // ================= forward recompute
+        if (r == 0) {
+            umma::mma(tmem, kmaj(X0, kT, 0), kmaj(W.w1d, kW1dRows, 0), id64, 0);
+            umma::commit(&bar_mma);
+        }
+        wait_mma(&bar_mma, ph_mma);
+        {
+            float v[64];
+            tld16(tmem, 0, v);
+            tld16(tmem, 16, v + 16);
+            tld16(tmem, 32, v + 32);
+            tld16(tmem, 48, v + 48);
+            umma::ld_wait();
+            mh[0] = mh[1] = 0;
+#pragma unroll
+            for (int i = 0; i < 64; ++i) {
+                float x = v[i] + W.b1d[i];
+                if (x > 0.f) mh[i >> 5] |= 1u << (i & 31);
+                v[i] = fmaxf(x, 0.f);
+            }
+#pragma unroll
+            for (int c = 0; c < 8; ++c) st_chunk(H1, r, c, v + 8 * c);
+        }
+        sync_for_mma();
+        if (r == 0) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                umma::mma(tmem, kmaj(H1, kT, k), kmaj(W.w2d, kW2dRows, k), id16, k > 0);
+            umma::commit(&bar_mma);
+        }
+        wait_mma(&bar_mma, ph_mma);
+        {
+            float v[16];
+            tld16(tmem, 0, v);
+            umma::ld_wait();
+            float raw = v[0] + W.b2d[0];
+            draw = raw >= a.density_lim ? 0.f : __expf(raw);
+            float cin[48];
+#pragma unroll
+            for (int i = 0; i < kEmb; ++i) cin[i] = v[1 + i] + W.b2d[1 + i];
+#pragma unroll
+            for (int i = 0; i < kViewDim; ++i) cin[kEmb + i] = ve[i];
+            cin[kCIn] = 1.f;
+#pragma unroll
+            for (int i = kCIn + 1; i < 48; ++i) cin[i] = 0.f;
+#pragma unroll
+            for (int c = 0; c < 6; ++c) st_chunk(CIN, r, c, cin + 8 * c);
+        }
+        sync_for_mma();
+        if (r == 0) {
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+                umma::mma(tmem, kmaj(CIN, kT, k), kmaj(W.wc1, kWc1Rows, k), id64, k > 0);
+            umma::commit(&bar_mma);
+        }
+        wait_mma(&bar_mma, ph_mma);
+        {
+            float v[64];
+            tld16(tmem, 0, v);
+            tld16(tmem, 16, v + 16);
+            tld16(tmem, 32, v + 32);
+            tld16(tmem, 48, v + 48);
+            umma::ld_wait();
+            mc1[0] = mc1[1] = 0;
+#pragma unroll
+            for (int i = 0; i < 64; ++i) {
+                float x = v[i] + W.bc1[i];
+                if (x > 0.f) mc1[i >> 5] |= 1u << (i & 31);
+                v[i] = fmaxf(x, 0.f);
+            }
+#pragma unroll
+            for (int c = 0; c < 8; ++c) st_chunk(C1, r, c, v + 8 * c);
+        }
+        sync_for_mma();
+        if (r == 0) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                umma::mma(tmem, kmaj(C1, kT, k), kmaj(W.wc2, kWc2Rows, k), id64, k > 0);
+            umma::commit(&bar_mma);
+        }
+        wait_mma(&bar_mma, ph_mma);
+        {
+            float v[64];
+            tld16(tmem, 0, v);
+            tld16(tmem, 16, v + 16);
+            tld16(tmem, 32, v + 32);
+            tld16(tmem, 48, v + 48);
+            umma::ld_wait();
+            mc2[0] = mc2[1] = 0;
+#pragma unroll
+            for (int i = 0; i < 64; ++i) {
+                float x = v[i] + W.bc2[i];
+                if (x > 0.f) mc2[i >> 5] |= 1u << (i & 31);
+                v[i] = fmaxf(x, 0.f);
+            }
+#pragma unroll
+            for (int c = 0; c < 8; ++c) st_chunk(C2, r, c, v + 8 * c);
+        }
+        sync_for_mma();
+        if (r == 0) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                umma::mma(tmem, kmaj(C2, kT, k), kmaj(W.wc3, kWc3Rows, k), id16, k > 0);
+            umma::commit(&bar_mma);
+        }
+        wait_mma(&bar_mma, ph_mma);
+        {
+            float v[16];
+            tld16(tmem, 0, v);
+            umma::ld_wait();
+            float d3[16];
+            float gin[3] = {dio.y, dio.z, dio.w};
+#pragma unroll
+            for (int o = 0; o < 3; ++o) {
+                float s = sigm(v[o] + W.bc3[o]);
+                d3[o] = live ? gin[o] * s * (1.f - s) : 0.f;
+            }
+#pragma unroll
+            for (int o = 3; o < 16; ++o) d3[o] = 0.f;
+            st_chunk(D3, r, 0, d3);
+            st_chunk(D3, r, 1, d3 + 8);
+        }
+        sync_for_mma();
+        // ================= backward
+        // (A) dC2pre = D3 . Wc3 ; dWc3^T += [C2|1]^T . D3
+        if (r == 0) {
+            umma::mma(tmem, kmaj(D3, kT, 0), mnmaj(W.wc3, kWc3Rows, 0), id64_kmn, 0);
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                umma::mma(tmem + kColWc3, mnmaj(C2, kT, k), mnmaj(D3, kT, k), idw16, (first_c && k == 0) ? 0 : 1);
+            umma::commit(&bar_mma);
+        }
+        wait_mma(&bar_mma, ph_mma);
+        {
+            float v[64];
+            tld16(tmem, 0, v);
+            tld16(tmem, 16, v + 16);
+            tld16(tmem, 32, v + 32);
+            tld16(tmem, 48, v + 48);
+            umma::ld_wait();
+#pragma unroll
+            for (int i = 0; i < 64; ++i) v[i] = ((mc2[i >> 5] >> (i & 31)) & 1u) ? v[i] : 0.f;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) st_chunk(C2, r, c, v + 8 * c);  // DC2 over C2
+        }
+        sync_for_mma();
+        // (B) dC1pre = DC2 . Wc2 ; dWc2^T += [C1|1]^T . DC2
+        if (r == 0) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                umma::mma(tmem, kmaj(C2, kT, k), mnmaj(W.wc2, kWc2Rows, k), id64_kmn, k > 0);
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                umma::mma(tmem + kColWc2, mnmaj(C1, kT, k), mnmaj(C2, kT, k), idw64, (first_c && k == 0) ? 0 : 1);
+            umma::commit(&bar_mma);
+        }
+        wait_mma(&bar_mma, ph_mma);
+        {
+            float v[64];
+            tld16(tmem, 0, v);
+            tld16(tmem, 16, v + 16);
+            tld16(tmem, 32, v + 32);
+            tld16(tmem, 48, v + 48);
+            umma::ld_wait();
+#pragma unroll
+            for (int i = 0; i < 64; ++i) v[i] = ((mc1[i >> 5] >> (i & 31)) & 1u) ? v[i] : 0.f;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) st_chunk(C1, r, c, v + 8 * c);  // DC1 over C1
+        }
+        sync_for_mma();
+        // (C) dCIN[0:16] = DC1 . Wc1[:, 0:16] ; dWc1 += DC1^T . CIN
+        if (r == 0) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                umma::mma(tmem, kmaj(C1, kT, k), mnmaj(W.wc1, kWc1Rows, k), id16_kmn, k > 0);
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                umma::mma(tmem + kColWc1, mnmaj(C1, kT, k), mnmaj(CIN, kT, k), idw48, (first_c && k == 0) ? 0 : 1);
+            umma::commit(&bar_mma);
+        }
+        wait_mma(&bar_mma, ph_mma);
+        first_c = false;
+        {
+            float v[16];
+            tld16(tmem, 0, v);
+            umma::ld_wait();
+            float d[16];
+            d[0] = live ? dio.x * draw : 0.f;
+#pragma unroll
+            for (int i = 0; i < kEmb; ++i) d[1 + i] = v[i];
+            st_chunk(DO, r, 0, d);
+            st_chunk(DO, r, 1, d + 8);
+        }
+        sync_for_mma();
+        // (D) dH1pre = DO . W2d ; dW2d^T += [H1|1]^T . DO
+        if (r == 0) {
+            umma::mma(tmem, kmaj(DO, kT, 0), mnmaj(W.w2d, kW2dRows, 0), id64_kmn, 0);
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                umma::mma(tmem + kColW2d, mnmaj(H1, kT, k), mnmaj(DO, kT, k), idw16, (first_d && k == 0) ? 0 : 1);
+            umma::commit(&bar_mma);
+        }
+        wait_mma(&bar_mma, ph_mma);
+        {
+            float v[64];
+            tld16(tmem, 0, v);
+            tld16(tmem, 16, v + 16);
+            tld16(tmem, 32, v + 32);
+            tld16(tmem, 48, v + 48);
+            umma::ld_wait();
+#pragma unroll
+            for (int i = 0; i < 64; ++i) v[i] = ((mh[i >> 5] >> (i & 31)) & 1u) ? v[i] : 0.f;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) st_chunk(H1, r, c, v + 8 * c);  // DH1 over H1
+        }
+        sync_for_mma();
+        // (E) dX0 = DH1 . W1d ; dW1d += DH1^T . [X0|1|0]
+        if (r == 0) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                umma::mma(tmem, kmaj(H1, kT, k), mnmaj(W.w1d, kW1dRows, k), id16_kmn, k > 0);
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                umma::mma(tmem + kColW1d, mnmaj(H1, kT, k), mnmaj(X0, kT, k), idw32, (first_d && k == 0) ? 0 : 1);
+            umma::commit(&bar_mma);
+        }
+        wait_mma(&bar_mma, ph_mma);
+        first_d = false;
+        {
+            float v[16];
+            tld16(tmem, 0, v);
+            umma::ld_wait();
+            float4* d4 = dfeat + (uint64_t(t) * kT + r) * 4;
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                d4[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        }
+    }
+    umma::fence_before_sync();
+    __syncthreads();
+    umma::fence_after_sync();
+    if (cur >= 0) flush_density(tmem, g.g_dnet[cur]);
+    if (!first_c) flush_color(tmem, g.g_color);
+    umma::fence_before_sync();
+    __syncthreads();
+    if (r < 32) umma::tmem_free<kBwdTmemCols>(tmem);
+}
+
+// ------------------------------------------------------------------ launchers
+void launch_field_forward_tc(const FieldArgs& a, uint8_t* feat, int32_t* rays, int sms,
+                             cudaStream_t st, uint64_t* launches) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(mlp_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kFwdSmem));
+        attr = true;
+    }
+    hash_fwd_kernel<<<sms * 8, 128, 0, st>>>(a, feat, rays);
+    mlp_fwd_kernel<<<sms * 3, 128, kFwdSmem, st>>>(a, feat, rays);
+    *launches += 2;
+}
+
+void launch_field_backward_tc(const FieldArgs& a, const FieldGradArgs& g, uint8_t* feat,
+                              int32_t* rays, float4* dfeat, int sms, cudaStream_t st,
+                              uint64_t* launches) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(mlp_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kBwdSmem));
+        attr = true;
+    }
+    hash_fwd_kernel<<<sms * 8, 128, 0, st>>>(a, feat, rays);
+    mlp_bwd_kernel<<<sms * 2, 128, kBwdSmem, st>>>(a, g, feat, rays, dfeat);
+    hash_bwd_kernel<<<sms * 8, 128, 0, st>>>(a, g, dfeat);
+    *launches += 3;
+}
+
+} // namespace tfg

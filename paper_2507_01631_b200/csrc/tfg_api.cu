@@ -18,6 +18,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -146,6 +147,10 @@ struct tfg_ctx {
     SampleArrays s{};
     float* d_ray_out = nullptr;  // rgb(3) | depth | opacity per ray
     int32_t* d_pixels = nullptr;
+    uint8_t* d_feat = nullptr;    // bf16 feature tiles (4 KB per 128-sample tile)
+    int32_t* d_tile_rays = nullptr;
+    float4* d_dfeat = nullptr;    // fp32 d(features) per tile row (training only)
+    bool simt = false;            // bring-up switch: CUDA-core field kernels
     int cur_rays = 0;
     bool have_batch = false;
     bool render_mode = false;
@@ -510,7 +515,11 @@ FieldArgs field_args(tfg_ctx* c, const FieldPtrs& f) {
 
 int run_forward(tfg_ctx* c, const FieldPtrs& f) {
     PhaseScope ps(c, kPhFieldFwd);
-    launch_field_forward(field_args(c, f), 2 * c->sms, c->st, &c->launches);
+    if (c->simt)
+        launch_field_forward(field_args(c, f), 2 * c->sms, c->st, &c->launches);
+    else
+        launch_field_forward_tc(field_args(c, f), c->d_feat, c->d_tile_rays, c->sms, c->st,
+                                &c->launches);
     CK(cudaGetLastError());
     return 0;
 }
@@ -544,7 +553,14 @@ int run_backward(tfg_ctx* c) {
         g.g_dnet[k] = g.g_enc[k] + c->enc_n;
     }
     g.g_color = c->d_grads + c->color_off;
-    launch_field_backward(field_args(c, train_ptrs(c)), g, c->sms, c->st, &c->launches);
+    if (c->simt) {
+        launch_field_backward(field_args(c, train_ptrs(c)), g, c->sms, c->st, &c->launches);
+    } else {
+        if (!c->d_dfeat && dalloc(c, &c->d_dfeat, uint64_t(c->max_tiles) * 128 * 4))
+            return TFG_ERR_CUDA;
+        launch_field_backward_tc(field_args(c, train_ptrs(c)), g, c->d_feat, c->d_tile_rays,
+                                 c->d_dfeat, c->sms, c->st, &c->launches);
+    }
     CK(cudaGetLastError());
     return 0;
 }
@@ -675,7 +691,8 @@ TFG_API int tfg_create(const tfg_field_config* fcfg, const tfg_train_config* tcf
         off += uint32_t(std::min<uint64_t>(dense, kTable));
     }
     c->density_lim = std::log(fcfg->density_max);
-    c->sample_cap = uint64_t(max_rays) * 160;
+    c->sample_cap = uint64_t(max_rays) * 128;
+    c->simt = getenv("TFG_FIELD_SIMT") != nullptr;
     c->max_tiles = int(c->sample_cap / 128 + kMaxSlots + 1);
     int rc = 0;
     CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
@@ -701,6 +718,8 @@ TFG_API int tfg_create(const tfg_field_config* fcfg, const tfg_train_config* tcf
     rc |= dalloc(c, &c->s.io, c->sample_cap);
     rc |= dalloc(c, &c->d_ray_out, uint64_t(max_rays) * 5);
     rc |= dalloc(c, &c->d_pixels, uint64_t(max_rays) * 3);
+    rc |= dalloc(c, &c->d_feat, uint64_t(c->max_tiles) * 4096);
+    rc |= dalloc(c, &c->d_tile_rays, uint64_t(c->max_tiles) * 128);
     rc |= dalloc(c, &c->d_block_sums, 4096 + 64);
     rc |= dalloc(c, &c->d_accept_n, 1);
     rc |= dalloc(c, &c->d_rcam, 1);
@@ -734,7 +753,8 @@ TFG_API int tfg_destroy(tfg_ctx* c) {
                    c->d_crop_off, c->d_accept, c->d_flags, c->d_pos, c->d_block_sums,
                    c->d_accept_n, c->d_view_start, c->d_union, c->d_crop4, c->d_rays, c->d_venc,
                    c->d_counts, c->d_P, c->d_tiles, c->s.local, c->s.td, c->s.endpoint, c->s.io,
-                   c->d_ray_out, c->d_pixels, c->d_rparams, c->d_rbits, c->d_rcolor, c->d_rcam};
+                   c->d_ray_out, c->d_pixels, c->d_rparams, c->d_rbits, c->d_rcolor, c->d_rcam,
+                   c->d_feat, c->d_tile_rays, c->d_dfeat};
     for (void* p : dev)
         if (p) cudaFree(p);
     for (auto& t : c->tiles)
