@@ -1,0 +1,120 @@
+// tilefield_gpu.hpp — header-only C++ mirror of the reference's tile-grid /
+// window / sampler / trainer API over the C-ABI (tilefield_gpu.h).
+//
+// Errors surface as tilefield::Error (core/common.hpp:27-30 of the reference)
+// with the library's message, so reference-side callers keep their error
+// handling.  The reference types RationalCamera (camera.hpp:22-33), Roi
+// (tiler.hpp:10-19) and FieldConfig (nn.hpp:14-37) map 1:1 onto tfg_rpc,
+// tfg_roi and tfg_field_config; see INTEGRATION.md for the adapter that
+// implements forward_batch / backward_batch / adam_step on top of this.
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "tilefield_gpu.h"
+
+namespace tilefield {
+
+#ifndef TILEFIELD_ERROR_DEFINED
+#define TILEFIELD_ERROR_DEFINED
+class Error : public std::runtime_error {
+public:
+    explicit Error(const std::string& msg) : std::runtime_error(msg) {}
+};
+#endif
+
+namespace gpu {
+
+inline void check(int rc) {
+    if (rc != TFG_OK) throw Error(tfg_last_error());
+}
+
+// One GPU's window trainer (a tfg_ctx): owns HBM state of the 2x2 window.
+class Context {
+public:
+    Context(const tfg_field_config& f, const tfg_train_config& t, int device, int max_rays) {
+        check(tfg_create(&f, &t, device, max_rays, &c_));
+    }
+    ~Context() { tfg_destroy(c_); }
+    Context(const Context&) = delete;
+    Context& operator=(const Context&) = delete;
+
+    void set_stream(void* stream) { check(tfg_set_stream(c_, stream)); }
+    void set_scene(const std::vector<tfg_rpc>& cams, const std::vector<const uint8_t*>& images,
+                   const tfg_roi& roi, int rows, int cols) {
+        check(tfg_set_scene(c_, cams.data(), int(cams.size()), images.data(), &roi, rows, cols));
+    }
+
+    // scheduler: snake_path / advance
+    static std::vector<std::pair<int, int>> snake_path(int H, int W) {
+        int n = 0;
+        check(tfg_snake_path(H, W, nullptr, &n));
+        std::vector<int32_t> p(2 * n);
+        check(tfg_snake_path(H, W, p.data(), &n));
+        std::vector<std::pair<int, int>> out;
+        for (int k = 0; k < n; ++k) out.push_back({p[2 * k], p[2 * k + 1]});
+        return out;
+    }
+    void advance(int pos_row, int pos_col) { check(tfg_set_window(c_, pos_row, pos_col)); }
+    uint64_t accepted_rays() const {
+        uint64_t n = 0;
+        check(tfg_accept_count(c_, &n));
+        return n;
+    }
+
+    // one trainer iteration; loss = color_loss
+    float train_step(uint64_t iter, uint64_t ray_begin, int n_rays) {
+        float loss = 0.f;
+        check(tfg_train_step(c_, iter, ray_begin, n_rays, &loss));
+        return loss;
+    }
+    // split form for data parallelism: fwd/bwd, allreduce(grad_buffer()), step
+    void forward_backward(uint64_t iter, uint64_t ray_begin, int n_rays) {
+        check(tfg_forward_backward(c_, iter, ray_begin, n_rays));
+    }
+    std::pair<float*, uint64_t> grad_buffer() {
+        void* p = nullptr;
+        uint64_t n = 0;
+        check(tfg_grad_buffer(c_, &p, &n));
+        return {static_cast<float*>(p), n};
+    }
+    void optimizer_step(uint64_t iter) { check(tfg_optimizer_step(c_, iter)); }
+    float read_loss() {
+        float l = 0.f;
+        check(tfg_read_loss(c_, &l));
+        return l;
+    }
+
+    // reference-facing operator surface (RaySegmentBatch, forward_batch, render)
+    uint64_t sample_segments(uint64_t iter, uint64_t ray_begin, int n_rays, bool jitter) {
+        uint64_t n = 0;
+        check(tfg_sample(c_, iter, ray_begin, n_rays, jitter ? 1 : 0, &n));
+        return n;
+    }
+    void export_batch(tfg_batch_view* out) { check(tfg_batch_export(c_, out)); }
+    void forward_batch(float* sigma, float* rgb) { check(tfg_field_forward(c_, sigma, rgb)); }
+    float render_and_loss(float* rgb, float* depth, float* opacity, float* d_sigma, float* d_rgb) {
+        float loss = 0.f;
+        check(tfg_composite(c_, rgb, depth, opacity, d_sigma, d_rgb, &loss));
+        return loss;
+    }
+    void backward_batch() { check(tfg_field_backward(c_)); }
+    void tile_state(int slot, tfg_tile_state* out) { check(tfg_get_tile_state(c_, slot, out)); }
+    void set_tile_state(int slot, const tfg_tile_state& in) { check(tfg_set_tile_state(c_, slot, &in)); }
+    tfg_memory_report memory_report() {
+        tfg_memory_report r{};
+        check(tfg_get_memory_report(c_, &r));
+        return r;
+    }
+    tfg_ctx* raw() { return c_; }
+
+private:
+    tfg_ctx* c_ = nullptr;
+};
+
+} // namespace gpu
+} // namespace tilefield

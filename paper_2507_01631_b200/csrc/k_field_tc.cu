@@ -178,25 +178,69 @@ __global__ void __launch_bounds__(128) hash_fwd_kernel(FieldArgs a, uint8_t* __r
 }
 
 // ------------------------------------------------------------------ K4a
+// Hash-table scatter-add (HashGridT::backward, nn.hpp:231-245).  Lanes of a
+// warp hold consecutive samples of a slot bucket, i.e. consecutive samples
+// along a ray, so on the coarse levels the same corner entry repeats in runs
+// of lanes: a warp-segmented sum over equal-entry runs leaves one
+// red.global.add.v2.f32 per run instead of one per sample.
+constexpr int kAggLevels = 5;  // levels 0..4 (cells >= 1.6% of the tile)
+
+__device__ __forceinline__ void seg_red(float2* g2, uint32_t idx, float v0, float v1, bool live) {
+    const uint32_t FULL = 0xffffffffu;
+    int lane = threadIdx.x & 31;
+    uint32_t key = live ? idx : 0xffffffffu;
+    uint32_t prev = __shfl_up_sync(FULL, key, 1);
+    bool head = lane == 0 || prev != key;
+    uint32_t heads = __ballot_sync(FULL, head);
+    int hidx = 31 - __clz(heads & (0xffffffffu >> (31 - lane)));  // head of my run
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        float y0 = __shfl_up_sync(FULL, v0, d);
+        float y1 = __shfl_up_sync(FULL, v1, d);
+        if (lane - d >= hidx) {
+            v0 += y0;
+            v1 += y1;
+        }
+    }
+    uint32_t next = __shfl_down_sync(FULL, key, 1);
+    bool tail = lane == 31 || next != key;
+    if (tail && live) atomicAdd(g2 + idx, make_float2(v0, v1));
+}
+
 __global__ void __launch_bounds__(128) hash_bwd_kernel(FieldArgs a, FieldGradArgs g,
                                                        const float4* __restrict__ dfeat) {
     uint32_t n_tiles = a.status->n_tiles;
     int r = threadIdx.x;
     for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
         TileDesc td = a.tiles[t];
-        if (r >= td.n) continue;
-        float4 L = a.s.local[uint64_t(td.start) + r];
+        bool live = r < td.n;
+        float4 L = live ? a.s.local[uint64_t(td.start) + r] : make_float4(0.f, 0.f, 0.f, 0.f);
         const float4* d4 = dfeat + (uint64_t(t) * kT + r) * 4;
         float d[kFeatDim];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            float4 v = d4[q];
+            float4 v = live ? d4[q] : make_float4(0.f, 0.f, 0.f, 0.f);
             d[4 * q] = v.x;
             d[4 * q + 1] = v.y;
             d[4 * q + 2] = v.z;
             d[4 * q + 3] = v.w;
         }
-        hash_scatter(a.hl, g.g_enc[td.slot], L.x, L.y, L.z, d);
+        float2* g2 = reinterpret_cast<float2*>(g.g_enc[td.slot]);
+#pragma unroll
+        for (int l = 0; l < kLevels; ++l) {
+            Corner c;
+            hash_level(a.hl, l, L.x, L.y, L.z, c);
+            if (l < kAggLevels) {
+                // warp-uniform control flow: every lane takes part in the shuffles
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    seg_red(g2, c.idx[k], c.w[k] * d[2 * l], c.w[k] * d[2 * l + 1], live);
+            } else if (live) {
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    atomicAdd(g2 + c.idx[k], make_float2(c.w[k] * d[2 * l], c.w[k] * d[2 * l + 1]));
+            }
+        }
     }
 }
 
@@ -786,10 +830,10 @@ void launch_field_backward_tc(const FieldArgs& a, const FieldGradArgs& g, uint8_
         cudaFuncSetAttribute(mlp_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kBwdSmem));
         attr = true;
     }
-    hash_fwd_kernel<<<sms * 8, 128, 0, st>>>(a, feat, rays);
+    // the feature tiles of the forward pass (same batch) are still resident
     mlp_bwd_kernel<<<sms * 2, 128, kBwdSmem, st>>>(a, g, feat, rays, dfeat);
     hash_bwd_kernel<<<sms * 8, 128, 0, st>>>(a, g, dfeat);
-    *launches += 3;
+    *launches += 2;
 }
 
 } // namespace tfg

@@ -153,6 +153,7 @@ struct tfg_ctx {
     bool simt = false;            // bring-up switch: CUDA-core field kernels
     int cur_rays = 0;
     bool have_batch = false;
+    bool fwd_done = false;  // feature tiles of the current batch are resident
     bool render_mode = false;
 
     // render
@@ -497,6 +498,7 @@ int run_sampler(tfg_ctx* c, RaygenArgs& a) {
     CK(cudaGetLastError());
     c->cur_rays = a.n_rays;
     c->have_batch = true;
+    c->fwd_done = false;
     return 0;
 }
 
@@ -515,6 +517,7 @@ FieldArgs field_args(tfg_ctx* c, const FieldPtrs& f) {
 
 int run_forward(tfg_ctx* c, const FieldPtrs& f) {
     PhaseScope ps(c, kPhFieldFwd);
+    c->fwd_done = true;
     if (c->simt)
         launch_field_forward(field_args(c, f), 2 * c->sms, c->st, &c->launches);
     else
@@ -545,6 +548,10 @@ int run_composite(tfg_ctx* c, bool backward) {
 }
 
 int run_backward(tfg_ctx* c) {
+    if (!c->fwd_done) {
+        int rc = run_forward(c, train_ptrs(c));
+        if (rc) return rc;
+    }
     PhaseScope ps(c, kPhFieldBwd);
     CK(cudaMemsetAsync(c->d_grads, 0, c->n_params * sizeof(float), c->st));
     FieldGradArgs g{};
@@ -1467,6 +1474,7 @@ TFG_API int tfg_render_pixels(tfg_ctx* c, const tfg_rpc* cam, const int32_t* pix
         if (rc) return rc;
         c->render_mode = true;
         if ((rc = run_forward(c, f))) return rc;
+        c->fwd_done = false;
         if ((rc = run_composite(c, false))) return rc;
         ro.resize(5 * uint64_t(c->max_rays));
         CK(cudaMemcpyAsync(ro.data(), c->d_ray_out, ro.size() * 4, cudaMemcpyDeviceToHost, c->st));
