@@ -207,6 +207,25 @@ __device__ __forceinline__ void seg_red(float2* g2, uint32_t idx, float v0, floa
     if (tail && live) atomicAdd(g2 + idx, make_float2(v0, v1));
 }
 
+__device__ __forceinline__ void scatter_row(const HashLayout& hl, float* genc, float x, float y, float z,
+                                            const float* d, bool live) {
+    float2* g2 = reinterpret_cast<float2*>(genc);
+#pragma unroll
+    for (int l = 0; l < kLevels; ++l) {
+        Corner c;
+        hash_level(hl, l, x, y, z, c);
+        if (l < kAggLevels) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                seg_red(g2, c.idx[k], c.w[k] * d[2 * l], c.w[k] * d[2 * l + 1], live);
+        } else if (live) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                atomicAdd(g2 + c.idx[k], make_float2(c.w[k] * d[2 * l], c.w[k] * d[2 * l + 1]));
+        }
+    }
+}
+
 __global__ void __launch_bounds__(128) hash_bwd_kernel(FieldArgs a, FieldGradArgs g,
                                                        const float4* __restrict__ dfeat) {
     uint32_t n_tiles = a.status->n_tiles;
@@ -544,6 +563,7 @@ __global__ void __launch_bounds__(128) mlp_bwd_kernel(FieldArgs a, FieldGradArgs
         bool live = r < td.n;
         int ray = rays[uint64_t(t) * kT + r];
         float4 dio = live ? a.s.io[uint64_t(td.start) + r] : make_float4(0.f, 0.f, 0.f, 0.f);
+        float4 L = live ? a.s.local[uint64_t(td.start) + r] : make_float4(0.f, 0.f, 0.f, 0.f);
         float ve[kViewDim];
         {
             const float4* v4 = a.venc + uint64_t(ray < 0 ? 0 : ray) * 6;
@@ -790,13 +810,12 @@ __global__ void __launch_bounds__(128) mlp_bwd_kernel(FieldArgs a, FieldGradArgs
         wait_mma(&bar_mma, ph_mma);
         first_d = false;
         {
+            // d(features) -> hash-table scatter straight from the epilogue
+            // (fire-and-forget red atomics overlap the other CTA's MMAs)
             float v[16];
             tld16(tmem, 0, v);
             umma::ld_wait();
-            float4* d4 = dfeat + (uint64_t(t) * kT + r) * 4;
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-                d4[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            scatter_row(a.hl, g.g_enc[td.slot], L.x, L.y, L.z, v, live);
         }
     }
     umma::fence_before_sync();
@@ -830,10 +849,10 @@ void launch_field_backward_tc(const FieldArgs& a, const FieldGradArgs& g, uint8_
         cudaFuncSetAttribute(mlp_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kBwdSmem));
         attr = true;
     }
-    // the feature tiles of the forward pass (same batch) are still resident
+    // the feature tiles of the forward pass (same batch) are still resident;
+    // the hash-table scatter is fused into the backward's last epilogue
     mlp_bwd_kernel<<<sms * 2, 128, kBwdSmem, st>>>(a, g, feat, rays, dfeat);
-    hash_bwd_kernel<<<sms * 8, 128, 0, st>>>(a, g, dfeat);
-    *launches += 2;
+    *launches += 1;
 }
 
 } // namespace tfg
