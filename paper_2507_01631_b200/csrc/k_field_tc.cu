@@ -143,7 +143,7 @@ __device__ __forceinline__ void wait_mma(uint64_t* bar, uint32_t& phase) {
 
 // 16 TMEM columns starting at col of this thread's lane row.
 __device__ __forceinline__ void tld16(uint32_t tmem, int col, float* v) {
-    uint32_t w = (threadIdx.x >> 5) & 3u;  // warp w may access TMEM lanes [32(w%4), +32)
+    uint32_t w = threadIdx.x >> 5;
     umma::ld16(tmem + ((32u * w) << 16) + uint32_t(col), v);
 }
 
@@ -207,24 +207,21 @@ __device__ __forceinline__ void seg_red(float2* g2, uint32_t idx, float v0, floa
     if (tail && live) atomicAdd(g2 + idx, make_float2(v0, v1));
 }
 
-// d holds the 8 feature gradients of levels [L0, L0 + 4).
-template <int L0>
-__device__ __forceinline__ void scatter_levels(const HashLayout& hl, float* genc, float x, float y,
-                                               float z, const float* d, bool live) {
+__device__ __forceinline__ void scatter_row(const HashLayout& hl, float* genc, float x, float y, float z,
+                                            const float* d, bool live) {
     float2* g2 = reinterpret_cast<float2*>(genc);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        const int l = L0 + q;
+    for (int l = 0; l < kLevels; ++l) {
         Corner c;
         hash_level(hl, l, x, y, z, c);
         if (l < kAggLevels) {
 #pragma unroll
             for (int k = 0; k < 8; ++k)
-                seg_red(g2, c.idx[k], c.w[k] * d[2 * q], c.w[k] * d[2 * q + 1], live);
+                seg_red(g2, c.idx[k], c.w[k] * d[2 * l], c.w[k] * d[2 * l + 1], live);
         } else if (live) {
 #pragma unroll
             for (int k = 0; k < 8; ++k)
-                atomicAdd(g2 + c.idx[k], make_float2(c.w[k] * d[2 * q], c.w[k] * d[2 * q + 1]));
+                atomicAdd(g2 + c.idx[k], make_float2(c.w[k] * d[2 * l], c.w[k] * d[2 * l + 1]));
         }
     }
 }
@@ -266,103 +263,13 @@ __global__ void __launch_bounds__(128) hash_bwd_kernel(FieldArgs a, FieldGradArg
     }
 }
 
-// ------------------------------------------------------------------ K2b / K4b
-// 256 threads per CTA: two threads per tile row.  Warps 4-7 access the same
-// TMEM lanes as warps 0-3 (lane group = warp % 4), so thread (row r, half h)
-// runs the epilogue of columns [32h, 32h + 32) of every 64-wide layer; the
-// 16-wide layers are split by meaning (embedding / view encoding, levels 0-3
-// / 4-7 of the hash scatter).  This halves the latency of every MMA ->
-// epilogue round trip of the serial per-tile chain.
-constexpr int kThreads = 256;
-
-// Epilogue of a 64-wide layer: bias + ReLU (mask bits out) -> bf16 chunks.
-__device__ __forceinline__ uint32_t epi_relu(uint32_t tmem, int h, const float* bias, uint8_t* dst, int r) {
-    float v[32];
-    tld16(tmem, 32 * h, v);
-    tld16(tmem, 32 * h + 16, v + 16);
-    umma::ld_wait();
-    uint32_t m = 0;
-#pragma unroll
-    for (int i = 0; i < 32; ++i) {
-        float x = v[i] + bias[32 * h + i];
-        m |= (x > 0.f ? 1u : 0u) << i;
-        v[i] = fmaxf(x, 0.f);
-    }
-#pragma unroll
-    for (int c = 0; c < 4; ++c) st_chunk(dst, r, 4 * h + c, v + 8 * c);
-    return m;
-}
-// Epilogue of a 64-wide data gradient: ReLU mask -> bf16 chunks.
-__device__ __forceinline__ void epi_mask(uint32_t tmem, int h, uint32_t mask, uint8_t* dst, int r) {
-    float v[32];
-    tld16(tmem, 32 * h, v);
-    tld16(tmem, 32 * h + 16, v + 16);
-    umma::ld_wait();
-#pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] = ((mask >> i) & 1u) ? v[i] : 0.f;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) st_chunk(dst, r, 4 * h + c, v + 8 * c);
-}
-
-// View encoding of the row's ray into CIN: half 0 keeps venc[0..8] for chunk
-// 1..2 (written with the embedding), half 1 writes chunks 3..5 now.
-__device__ __forceinline__ void load_venc(const float4* __restrict__ venc, int ray, int h, float* ve,
-                                          uint8_t* CIN, int r) {
-    const float4* v4 = venc + uint64_t(ray < 0 ? 0 : ray) * 6;
-    if (h == 0) {
-#pragma unroll
-        for (int q = 0; q < 3; ++q) {
-            float4 v = __ldg(v4 + q);
-            ve[4 * q] = v.x;
-            ve[4 * q + 1] = v.y;
-            ve[4 * q + 2] = v.z;
-            ve[4 * q + 3] = v.w;
-        }
-    } else {
-        float e[16];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            float4 v = __ldg(v4 + 2 + q);
-            e[4 * q] = v.x;
-            e[4 * q + 1] = v.y;
-            e[4 * q + 2] = v.z;
-            e[4 * q + 3] = v.w;
-        }
-        // e[i] = venc[8 + i]; CIN col 15 + j = venc[j]
-        float c[24];
-#pragma unroll
-        for (int i = 0; i < 15; ++i) c[i] = e[1 + i];  // cols 24..38 = venc[9..23]
-        c[15] = 1.f;                                   // col 39: ones (colour-layer-1 bias grad)
-#pragma unroll
-        for (int i = 16; i < 24; ++i) c[i] = 0.f;      // cols 40..47
-        st_chunk(CIN, r, 3, c);
-        st_chunk(CIN, r, 4, c + 8);
-        st_chunk(CIN, r, 5, c + 16);
-    }
-}
-// Half 0: raw sigma + embedding (d2 output) + venc[0..8] -> CIN chunks 0..2.
-__device__ __forceinline__ float emb_chunks(uint32_t tmem, const float* b2d, const float* ve, uint8_t* CIN,
-                                            int r) {
-    float v[16];
-    tld16(tmem, 0, v);
-    umma::ld_wait();
-    float c[24];
-#pragma unroll
-    for (int i = 0; i < kEmb; ++i) c[i] = v[1 + i] + b2d[1 + i];
-#pragma unroll
-    for (int i = 0; i < 9; ++i) c[kEmb + i] = ve[i];
-    st_chunk(CIN, r, 0, c);
-    st_chunk(CIN, r, 1, c + 8);
-    st_chunk(CIN, r, 2, c + 16);
-    return v[0] + b2d[0];  // raw sigma
-}
-
+// ------------------------------------------------------------------ K2b
 // smem: weights | X0 [128x16] | CIN [128x48] | A [128x64] (H1, then C2) | C1 [128x64]
 constexpr uint32_t kFwdSmem = kWeightsBytes + 4096 + 12288 + 16384 + 16384 + 128;
 constexpr uint32_t kFwdTmemCols = 64;
 
-__global__ void __launch_bounds__(kThreads, 2) mlp_fwd_kernel(FieldArgs a, const uint8_t* __restrict__ feat,
-                                                              const int32_t* __restrict__ rays) {
+__global__ void __launch_bounds__(128) mlp_fwd_kernel(FieldArgs a, const uint8_t* __restrict__ feat,
+                                                      const int32_t* __restrict__ rays) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
     __shared__ uint64_t bar_mma, bar_ld;
     __shared__ uint32_t tmem_slot;
@@ -372,13 +279,13 @@ __global__ void __launch_bounds__(kThreads, 2) mlp_fwd_kernel(FieldArgs a, const
     uint8_t* CIN = carve(p, 12288);
     uint8_t* HA = carve(p, 16384);
     uint8_t* C1 = carve(p, 16384);
-    const int tid = threadIdx.x, r = tid & 127, h = tid >> 7;
-    if (tid == 0) {
+    const int r = threadIdx.x;
+    if (r == 0) {
         umma::mbar_init(&bar_mma, 1);
         umma::mbar_init(&bar_ld, 1);
         umma::fence_mbar_init();
     }
-    if (tid < 32) umma::tmem_alloc<kFwdTmemCols>(&tmem_slot);
+    if (r < 32) umma::tmem_alloc<kFwdTmemCols>(&tmem_slot);
     stage_color(W, a.f.color);
     uint32_t ph_mma = 0, ph_ld = 0;
     int cur = -1;
@@ -393,66 +300,123 @@ __global__ void __launch_bounds__(kThreads, 2) mlp_fwd_kernel(FieldArgs a, const
             stage_density(W, a.f.dnet[td.slot]);
             cur = td.slot;
         }
-        if (tid == 0) {
+        if (r == 0) {
             umma::mbar_expect_tx(&bar_ld, kFeatTile);
             umma::bulk_g2s(X0, feat + uint64_t(t) * kFeatTile, kFeatTile, &bar_ld);
         }
-        float ve[12];
-        load_venc(a.venc, rays[uint64_t(t) * kT + r], h, ve, CIN, r);
-        sync_for_mma();
+        int ray = rays[uint64_t(t) * kT + r];
+        float ve[kViewDim];
+        {
+            const float4* v4 = a.venc + uint64_t(ray < 0 ? 0 : ray) * 6;
+#pragma unroll
+            for (int q = 0; q < 6; ++q) {
+                float4 v = __ldg(v4 + q);
+                ve[4 * q] = v.x;
+                ve[4 * q + 1] = v.y;
+                ve[4 * q + 2] = v.z;
+                ve[4 * q + 3] = v.w;
+            }
+        }
+        sync_for_mma();  // density weights staged, previous tile's TMEM reads done
         umma::mbar_wait(&bar_ld, ph_ld);
         ph_ld ^= 1u;
-        // density layer 1: [128x16] x W1d^T -> 64
-        if (tid == 0) {
+        // ---- density layer 1: [128x16] x W1d^T -> 64
+        if (r == 0) {
             umma::mma(tmem, kmaj(X0, kT, 0), kmaj(W.w1d, kW1dRows, 0), id64, 0);
             umma::commit(&bar_mma);
         }
         wait_mma(&bar_mma, ph_mma);
-        epi_relu(tmem, h, W.b1d, HA, r);
+        {
+            float v[64];
+            tld16(tmem, 0, v);
+            tld16(tmem, 16, v + 16);
+            tld16(tmem, 32, v + 32);
+            tld16(tmem, 48, v + 48);
+            umma::ld_wait();
+#pragma unroll
+            for (int i = 0; i < 64; ++i) v[i] = fmaxf(v[i] + W.b1d[i], 0.f);
+#pragma unroll
+            for (int c = 0; c < 8; ++c) st_chunk(HA, r, c, v + 8 * c);
+        }
         sync_for_mma();
-        // density layer 2: [128x64] x W2d^T -> 16 (raw sigma | embedding)
-        if (tid == 0) {
+        // ---- density layer 2: [128x64] x W2d^T -> 16 (raw sigma | embedding)
+        if (r == 0) {
 #pragma unroll
             for (int k = 0; k < 4; ++k)
                 umma::mma(tmem, kmaj(HA, kT, k), kmaj(W.w2d, kW2dRows, k), id16, k > 0);
             umma::commit(&bar_mma);
         }
         wait_mma(&bar_mma, ph_mma);
-        float sigma = 0.f;
-        if (h == 0) {
-            float raw = emb_chunks(tmem, W.b2d, ve, CIN, r);
+        float sigma;
+        {
+            float v[16];
+            tld16(tmem, 0, v);
+            umma::ld_wait();
+            float raw = v[0] + W.b2d[0];
             sigma = raw >= a.density_lim ? a.density_max : __expf(raw);
+            float cin[48];
+#pragma unroll
+            for (int i = 0; i < kEmb; ++i) cin[i] = v[1 + i] + W.b2d[1 + i];
+#pragma unroll
+            for (int i = 0; i < kViewDim; ++i) cin[kEmb + i] = ve[i];
+            cin[kCIn] = 1.f;  // ones column (bias gradient of colour layer 1 in K4)
+#pragma unroll
+            for (int i = kCIn + 1; i < 48; ++i) cin[i] = 0.f;
+#pragma unroll
+            for (int c = 0; c < 6; ++c) st_chunk(CIN, r, c, cin + 8 * c);
         }
         sync_for_mma();
-        // colour layer 1: [128x48] x Wc1^T -> 64
-        if (tid == 0) {
+        // ---- colour layer 1: [128x48] x Wc1^T -> 64
+        if (r == 0) {
 #pragma unroll
             for (int k = 0; k < 3; ++k)
                 umma::mma(tmem, kmaj(CIN, kT, k), kmaj(W.wc1, kWc1Rows, k), id64, k > 0);
             umma::commit(&bar_mma);
         }
         wait_mma(&bar_mma, ph_mma);
-        epi_relu(tmem, h, W.bc1, C1, r);
+        {
+            float v[64];
+            tld16(tmem, 0, v);
+            tld16(tmem, 16, v + 16);
+            tld16(tmem, 32, v + 32);
+            tld16(tmem, 48, v + 48);
+            umma::ld_wait();
+#pragma unroll
+            for (int i = 0; i < 64; ++i) v[i] = fmaxf(v[i] + W.bc1[i], 0.f);
+#pragma unroll
+            for (int c = 0; c < 8; ++c) st_chunk(C1, r, c, v + 8 * c);
+        }
         sync_for_mma();
-        // colour layer 2: [128x64] x Wc2^T -> 64
-        if (tid == 0) {
+        // ---- colour layer 2: [128x64] x Wc2^T -> 64
+        if (r == 0) {
 #pragma unroll
             for (int k = 0; k < 4; ++k)
                 umma::mma(tmem, kmaj(C1, kT, k), kmaj(W.wc2, kWc2Rows, k), id64, k > 0);
             umma::commit(&bar_mma);
         }
         wait_mma(&bar_mma, ph_mma);
-        epi_relu(tmem, h, W.bc2, HA, r);
+        {
+            float v[64];
+            tld16(tmem, 0, v);
+            tld16(tmem, 16, v + 16);
+            tld16(tmem, 32, v + 32);
+            tld16(tmem, 48, v + 48);
+            umma::ld_wait();
+#pragma unroll
+            for (int i = 0; i < 64; ++i) v[i] = fmaxf(v[i] + W.bc2[i], 0.f);
+#pragma unroll
+            for (int c = 0; c < 8; ++c) st_chunk(HA, r, c, v + 8 * c);
+        }
         sync_for_mma();
-        // colour layer 3: [128x64] x Wc3^T -> 16 (3 real) -> sigmoid
-        if (tid == 0) {
+        // ---- colour layer 3: [128x64] x Wc3^T -> 16 (3 real) -> sigmoid
+        if (r == 0) {
 #pragma unroll
             for (int k = 0; k < 4; ++k)
                 umma::mma(tmem, kmaj(HA, kT, k), kmaj(W.wc3, kWc3Rows, k), id16, k > 0);
             umma::commit(&bar_mma);
         }
         wait_mma(&bar_mma, ph_mma);
-        if (h == 0) {
+        {
             float v[16];
             tld16(tmem, 0, v);
             umma::ld_wait();
@@ -463,7 +427,7 @@ __global__ void __launch_bounds__(kThreads, 2) mlp_fwd_kernel(FieldArgs a, const
     }
     umma::fence_before_sync();
     __syncthreads();
-    if (tid < 32) umma::tmem_free<kFwdTmemCols>(tmem);
+    if (r < 32) umma::tmem_free<kFwdTmemCols>(tmem);
 }
 
 // ------------------------------------------------------------------ K4b
@@ -486,10 +450,9 @@ __device__ __forceinline__ void set_ones_chunk(uint8_t* buf, int chunk, int r) {
     st_chunk(buf, r, chunk, v);
 }
 
-// Adds the CTA's TMEM weight-gradient accumulators into the global gradients
-// (warps 0-3; one thread per TMEM lane row).
+// Adds the CTA's TMEM weight-gradient accumulators into the global gradients.
 __device__ __forceinline__ void flush_density(uint32_t tmem, float* __restrict__ gd) {
-    int m = threadIdx.x;
+    int m = threadIdx.x;  // TMEM lane row
     float v[32];
     // dW1d [o=m][i] (cols 0..15), bias at col 16
     tld16(tmem, kColW1d, v);
@@ -538,9 +501,10 @@ __device__ __forceinline__ void flush_color(uint32_t tmem, float* __restrict__ g
         for (int o = 0; o < 3; ++o) atomicAdd(gc + kCB3 + o, v[o]);
 }
 
-__global__ void __launch_bounds__(kThreads, 2) mlp_bwd_kernel(FieldArgs a, FieldGradArgs g,
-                                                              const uint8_t* __restrict__ feat,
-                                                              const int32_t* __restrict__ rays) {
+__global__ void __launch_bounds__(128) mlp_bwd_kernel(FieldArgs a, FieldGradArgs g,
+                                                      const uint8_t* __restrict__ feat,
+                                                      const int32_t* __restrict__ rays,
+                                                      float4* __restrict__ dfeat) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
     __shared__ uint64_t bar_mma, bar_ld;
     __shared__ uint32_t tmem_slot;
@@ -553,21 +517,20 @@ __global__ void __launch_bounds__(kThreads, 2) mlp_bwd_kernel(FieldArgs a, Field
     uint8_t* D3 = carve(p, 2 * kChunk);
     uint8_t* DO = carve(p, 2 * kChunk);
     Weights W = carve_weights(p);
-    const int tid = threadIdx.x, r = tid & 127, h = tid >> 7;
-    if (tid == 0) {
+    const int r = threadIdx.x;
+    if (r == 0) {
         umma::mbar_init(&bar_mma, 1);
         umma::mbar_init(&bar_ld, 1);
         umma::fence_mbar_init();
     }
-    if (tid < 32) umma::tmem_alloc<kBwdTmemCols>(&tmem_slot);
+    if (r < 32) umma::tmem_alloc<kBwdTmemCols>(&tmem_slot);
     stage_color(W, a.f.color);
     // constant ones chunks
-    if (h == 0) {
-        set_ones_chunk(H1, 8, r);
-        set_ones_chunk(C1, 8, r);
-        set_ones_chunk(C2, 8, r);
-    } else {
-        set_ones_chunk(X0, 2, r);
+    set_ones_chunk(H1, 8, r);
+    set_ones_chunk(C1, 8, r);
+    set_ones_chunk(C2, 8, r);
+    set_ones_chunk(X0, 2, r);
+    {
         float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         st_chunk(X0, r, 3, z);
     }
@@ -588,76 +551,148 @@ __global__ void __launch_bounds__(kThreads, 2) mlp_bwd_kernel(FieldArgs a, Field
     for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
         TileDesc td = a.tiles[t];
         if (td.slot != cur) {
-            if (cur >= 0 && h == 0) flush_density(tmem, g.g_dnet[cur]);
+            if (cur >= 0) flush_density(tmem, g.g_dnet[cur]);
             stage_density(W, a.f.dnet[td.slot]);
             cur = td.slot;
             first_d = true;
         }
-        if (tid == 0) {
+        if (r == 0) {
             umma::mbar_expect_tx(&bar_ld, kFeatTile);
             umma::bulk_g2s(X0, feat + uint64_t(t) * kFeatTile, kFeatTile, &bar_ld);
         }
-        const bool live = r < td.n;
-        const uint64_t pos = uint64_t(td.start) + r;
-        float4 dio = (live && h == 0) ? a.s.io[pos] : make_float4(0.f, 0.f, 0.f, 0.f);
-        float4 L = live ? a.s.local[pos] : make_float4(0.f, 0.f, 0.f, 0.f);
-        float ve[12];
-        load_venc(a.venc, rays[uint64_t(t) * kT + r], h, ve, CIN, r);
+        bool live = r < td.n;
+        int ray = rays[uint64_t(t) * kT + r];
+        float4 dio = live ? a.s.io[uint64_t(td.start) + r] : make_float4(0.f, 0.f, 0.f, 0.f);
+        float4 L = live ? a.s.local[uint64_t(td.start) + r] : make_float4(0.f, 0.f, 0.f, 0.f);
+        float ve[kViewDim];
+        {
+            const float4* v4 = a.venc + uint64_t(ray < 0 ? 0 : ray) * 6;
+#pragma unroll
+            for (int q = 0; q < 6; ++q) {
+                float4 v = __ldg(v4 + q);
+                ve[4 * q] = v.x;
+                ve[4 * q + 1] = v.y;
+                ve[4 * q + 2] = v.z;
+                ve[4 * q + 3] = v.w;
+            }
+        }
         sync_for_mma();
         umma::mbar_wait(&bar_ld, ph_ld);
         ph_ld ^= 1u;
+        uint32_t mh[2], mc1[2], mc2[2];  // ReLU masks of H1, C1, C2
+        float draw;
         // ================= forward recompute
-        if (tid == 0) {
+        if (r == 0) {
             umma::mma(tmem, kmaj(X0, kT, 0), kmaj(W.w1d, kW1dRows, 0), id64, 0);
             umma::commit(&bar_mma);
         }
         wait_mma(&bar_mma, ph_mma);
-        const uint32_t mh = epi_relu(tmem, h, W.b1d, H1, r);
+        {
+            float v[64];
+            tld16(tmem, 0, v);
+            tld16(tmem, 16, v + 16);
+            tld16(tmem, 32, v + 32);
+            tld16(tmem, 48, v + 48);
+            umma::ld_wait();
+            mh[0] = mh[1] = 0;
+#pragma unroll
+            for (int i = 0; i < 64; ++i) {
+                float x = v[i] + W.b1d[i];
+                if (x > 0.f) mh[i >> 5] |= 1u << (i & 31);
+                v[i] = fmaxf(x, 0.f);
+            }
+#pragma unroll
+            for (int c = 0; c < 8; ++c) st_chunk(H1, r, c, v + 8 * c);
+        }
         sync_for_mma();
-        if (tid == 0) {
+        if (r == 0) {
 #pragma unroll
             for (int k = 0; k < 4; ++k)
                 umma::mma(tmem, kmaj(H1, kT, k), kmaj(W.w2d, kW2dRows, k), id16, k > 0);
             umma::commit(&bar_mma);
         }
         wait_mma(&bar_mma, ph_mma);
-        float draw = 0.f;
-        if (h == 0) {
-            float raw = emb_chunks(tmem, W.b2d, ve, CIN, r);
+        {
+            float v[16];
+            tld16(tmem, 0, v);
+            umma::ld_wait();
+            float raw = v[0] + W.b2d[0];
             draw = raw >= a.density_lim ? 0.f : __expf(raw);
+            float cin[48];
+#pragma unroll
+            for (int i = 0; i < kEmb; ++i) cin[i] = v[1 + i] + W.b2d[1 + i];
+#pragma unroll
+            for (int i = 0; i < kViewDim; ++i) cin[kEmb + i] = ve[i];
+            cin[kCIn] = 1.f;
+#pragma unroll
+            for (int i = kCIn + 1; i < 48; ++i) cin[i] = 0.f;
+#pragma unroll
+            for (int c = 0; c < 6; ++c) st_chunk(CIN, r, c, cin + 8 * c);
         }
         sync_for_mma();
-        if (tid == 0) {
+        if (r == 0) {
 #pragma unroll
             for (int k = 0; k < 3; ++k)
                 umma::mma(tmem, kmaj(CIN, kT, k), kmaj(W.wc1, kWc1Rows, k), id64, k > 0);
             umma::commit(&bar_mma);
         }
         wait_mma(&bar_mma, ph_mma);
-        const uint32_t mc1 = epi_relu(tmem, h, W.bc1, C1, r);
+        {
+            float v[64];
+            tld16(tmem, 0, v);
+            tld16(tmem, 16, v + 16);
+            tld16(tmem, 32, v + 32);
+            tld16(tmem, 48, v + 48);
+            umma::ld_wait();
+            mc1[0] = mc1[1] = 0;
+#pragma unroll
+            for (int i = 0; i < 64; ++i) {
+                float x = v[i] + W.bc1[i];
+                if (x > 0.f) mc1[i >> 5] |= 1u << (i & 31);
+                v[i] = fmaxf(x, 0.f);
+            }
+#pragma unroll
+            for (int c = 0; c < 8; ++c) st_chunk(C1, r, c, v + 8 * c);
+        }
         sync_for_mma();
-        if (tid == 0) {
+        if (r == 0) {
 #pragma unroll
             for (int k = 0; k < 4; ++k)
                 umma::mma(tmem, kmaj(C1, kT, k), kmaj(W.wc2, kWc2Rows, k), id64, k > 0);
             umma::commit(&bar_mma);
         }
         wait_mma(&bar_mma, ph_mma);
-        const uint32_t mc2 = epi_relu(tmem, h, W.bc2, C2, r);
+        {
+            float v[64];
+            tld16(tmem, 0, v);
+            tld16(tmem, 16, v + 16);
+            tld16(tmem, 32, v + 32);
+            tld16(tmem, 48, v + 48);
+            umma::ld_wait();
+            mc2[0] = mc2[1] = 0;
+#pragma unroll
+            for (int i = 0; i < 64; ++i) {
+                float x = v[i] + W.bc2[i];
+                if (x > 0.f) mc2[i >> 5] |= 1u << (i & 31);
+                v[i] = fmaxf(x, 0.f);
+            }
+#pragma unroll
+            for (int c = 0; c < 8; ++c) st_chunk(C2, r, c, v + 8 * c);
+        }
         sync_for_mma();
-        if (tid == 0) {
+        if (r == 0) {
 #pragma unroll
             for (int k = 0; k < 4; ++k)
                 umma::mma(tmem, kmaj(C2, kT, k), kmaj(W.wc3, kWc3Rows, k), id16, k > 0);
             umma::commit(&bar_mma);
         }
         wait_mma(&bar_mma, ph_mma);
-        if (h == 0) {
+        {
             float v[16];
             tld16(tmem, 0, v);
             umma::ld_wait();
             float d3[16];
-            const float gin[3] = {dio.y, dio.z, dio.w};
+            float gin[3] = {dio.y, dio.z, dio.w};
 #pragma unroll
             for (int o = 0; o < 3; ++o) {
                 float s = sigm(v[o] + W.bc3[o]);
@@ -671,7 +706,7 @@ __global__ void __launch_bounds__(kThreads, 2) mlp_bwd_kernel(FieldArgs a, Field
         sync_for_mma();
         // ================= backward
         // (A) dC2pre = D3 . Wc3 ; dWc3^T += [C2|1]^T . D3
-        if (tid == 0) {
+        if (r == 0) {
             umma::mma(tmem, kmaj(D3, kT, 0), mnmaj(W.wc3, kWc3Rows, 0), id64_kmn, 0);
 #pragma unroll
             for (int k = 0; k < 8; ++k)
@@ -679,10 +714,21 @@ __global__ void __launch_bounds__(kThreads, 2) mlp_bwd_kernel(FieldArgs a, Field
             umma::commit(&bar_mma);
         }
         wait_mma(&bar_mma, ph_mma);
-        epi_mask(tmem, h, mc2, C2, r);  // DC2 over C2
+        {
+            float v[64];
+            tld16(tmem, 0, v);
+            tld16(tmem, 16, v + 16);
+            tld16(tmem, 32, v + 32);
+            tld16(tmem, 48, v + 48);
+            umma::ld_wait();
+#pragma unroll
+            for (int i = 0; i < 64; ++i) v[i] = ((mc2[i >> 5] >> (i & 31)) & 1u) ? v[i] : 0.f;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) st_chunk(C2, r, c, v + 8 * c);  // DC2 over C2
+        }
         sync_for_mma();
         // (B) dC1pre = DC2 . Wc2 ; dWc2^T += [C1|1]^T . DC2
-        if (tid == 0) {
+        if (r == 0) {
 #pragma unroll
             for (int k = 0; k < 4; ++k)
                 umma::mma(tmem, kmaj(C2, kT, k), mnmaj(W.wc2, kWc2Rows, k), id64_kmn, k > 0);
@@ -692,10 +738,21 @@ __global__ void __launch_bounds__(kThreads, 2) mlp_bwd_kernel(FieldArgs a, Field
             umma::commit(&bar_mma);
         }
         wait_mma(&bar_mma, ph_mma);
-        epi_mask(tmem, h, mc1, C1, r);  // DC1 over C1
+        {
+            float v[64];
+            tld16(tmem, 0, v);
+            tld16(tmem, 16, v + 16);
+            tld16(tmem, 32, v + 32);
+            tld16(tmem, 48, v + 48);
+            umma::ld_wait();
+#pragma unroll
+            for (int i = 0; i < 64; ++i) v[i] = ((mc1[i >> 5] >> (i & 31)) & 1u) ? v[i] : 0.f;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) st_chunk(C1, r, c, v + 8 * c);  // DC1 over C1
+        }
         sync_for_mma();
         // (C) dCIN[0:16] = DC1 . Wc1[:, 0:16] ; dWc1 += DC1^T . CIN
-        if (tid == 0) {
+        if (r == 0) {
 #pragma unroll
             for (int k = 0; k < 4; ++k)
                 umma::mma(tmem, kmaj(C1, kT, k), mnmaj(W.wc1, kWc1Rows, k), id16_kmn, k > 0);
@@ -706,7 +763,7 @@ __global__ void __launch_bounds__(kThreads, 2) mlp_bwd_kernel(FieldArgs a, Field
         }
         wait_mma(&bar_mma, ph_mma);
         first_c = false;
-        if (h == 0) {
+        {
             float v[16];
             tld16(tmem, 0, v);
             umma::ld_wait();
@@ -719,7 +776,7 @@ __global__ void __launch_bounds__(kThreads, 2) mlp_bwd_kernel(FieldArgs a, Field
         }
         sync_for_mma();
         // (D) dH1pre = DO . W2d ; dW2d^T += [H1|1]^T . DO
-        if (tid == 0) {
+        if (r == 0) {
             umma::mma(tmem, kmaj(DO, kT, 0), mnmaj(W.w2d, kW2dRows, 0), id64_kmn, 0);
 #pragma unroll
             for (int k = 0; k < 8; ++k)
@@ -727,10 +784,21 @@ __global__ void __launch_bounds__(kThreads, 2) mlp_bwd_kernel(FieldArgs a, Field
             umma::commit(&bar_mma);
         }
         wait_mma(&bar_mma, ph_mma);
-        epi_mask(tmem, h, mh, H1, r);  // DH1 over H1
+        {
+            float v[64];
+            tld16(tmem, 0, v);
+            tld16(tmem, 16, v + 16);
+            tld16(tmem, 32, v + 32);
+            tld16(tmem, 48, v + 48);
+            umma::ld_wait();
+#pragma unroll
+            for (int i = 0; i < 64; ++i) v[i] = ((mh[i >> 5] >> (i & 31)) & 1u) ? v[i] : 0.f;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) st_chunk(H1, r, c, v + 8 * c);  // DH1 over H1
+        }
         sync_for_mma();
         // (E) dX0 = DH1 . W1d ; dW1d += DH1^T . [X0|1|0]
-        if (tid == 0) {
+        if (r == 0) {
 #pragma unroll
             for (int k = 0; k < 4; ++k)
                 umma::mma(tmem, kmaj(H1, kT, k), mnmaj(W.w1d, kW1dRows, k), id16_kmn, k > 0);
@@ -742,26 +810,22 @@ __global__ void __launch_bounds__(kThreads, 2) mlp_bwd_kernel(FieldArgs a, Field
         wait_mma(&bar_mma, ph_mma);
         first_d = false;
         {
-            // d(features) -> hash-table scatter from the epilogue: half 0 takes
-            // levels 0-3, half 1 levels 4-7
+            // d(features) -> hash-table scatter straight from the epilogue
+            // (fire-and-forget red atomics overlap the other CTA's MMAs)
             float v[16];
             tld16(tmem, 0, v);
             umma::ld_wait();
-            float* genc = g.g_enc[td.slot];
-            if (h == 0) scatter_levels<0>(a.hl, genc, L.x, L.y, L.z, v, live);
-            else scatter_levels<4>(a.hl, genc, L.x, L.y, L.z, v + 8, live);
+            scatter_row(a.hl, g.g_enc[td.slot], L.x, L.y, L.z, v, live);
         }
     }
     umma::fence_before_sync();
     __syncthreads();
     umma::fence_after_sync();
-    if (h == 0) {
-        if (cur >= 0) flush_density(tmem, g.g_dnet[cur]);
-        if (!first_c) flush_color(tmem, g.g_color);
-    }
+    if (cur >= 0) flush_density(tmem, g.g_dnet[cur]);
+    if (!first_c) flush_color(tmem, g.g_color);
     umma::fence_before_sync();
     __syncthreads();
-    if (tid < 32) umma::tmem_free<kBwdTmemCols>(tmem);
+    if (r < 32) umma::tmem_free<kBwdTmemCols>(tmem);
 }
 
 // ------------------------------------------------------------------ launchers
@@ -773,14 +837,13 @@ void launch_field_forward_tc(const FieldArgs& a, uint8_t* feat, int32_t* rays, i
         attr = true;
     }
     hash_fwd_kernel<<<sms * 8, 128, 0, st>>>(a, feat, rays);
-    mlp_fwd_kernel<<<sms * 2, kThreads, kFwdSmem, st>>>(a, feat, rays);  // 2 resident per SM
+    mlp_fwd_kernel<<<sms * 3, 128, kFwdSmem, st>>>(a, feat, rays);
     *launches += 2;
 }
 
 void launch_field_backward_tc(const FieldArgs& a, const FieldGradArgs& g, uint8_t* feat,
                               int32_t* rays, float4* dfeat, int sms, cudaStream_t st,
                               uint64_t* launches) {
-    (void)dfeat;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(mlp_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kBwdSmem));
@@ -788,7 +851,7 @@ void launch_field_backward_tc(const FieldArgs& a, const FieldGradArgs& g, uint8_
     }
     // the feature tiles of the forward pass (same batch) are still resident;
     // the hash-table scatter is fused into the backward's last epilogue
-    mlp_bwd_kernel<<<sms * 2, kThreads, kBwdSmem, st>>>(a, g, feat, rays);
+    mlp_bwd_kernel<<<sms * 2, 128, kBwdSmem, st>>>(a, g, feat, rays, dfeat);
     *launches += 1;
 }
 
