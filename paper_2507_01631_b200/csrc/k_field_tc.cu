@@ -183,7 +183,29 @@ __global__ void __launch_bounds__(128) hash_fwd_kernel(FieldArgs a, uint8_t* __r
 // along a ray, so on the coarse levels the same corner entry repeats in runs
 // of lanes: a warp-segmented sum over equal-entry runs leaves one
 // red.global.add.v2.f32 per run instead of one per sample.
-constexpr int kAggLevels = 5;  // levels 0..4 (cells >= 1.6% of the tile)
+constexpr int kAggLevels = 3;  // levels 0..2 (cells >= 2.8% of the tile)
+
+// Pair-vectorised scatter of one level's 8 corners (see hash_encode): one
+// red.global.add.v4.f32 for an aligned x-neighbour pair, else two v2.
+__device__ __forceinline__ void scatter_pairs(float* __restrict__ genc, const Corner& c, float d0,
+                                              float d1) {
+    float2* g2 = reinterpret_cast<float2*>(genc);
+    float4* g4 = reinterpret_cast<float4*>(genc);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        uint32_t i0 = c.idx[2 * q], i1 = c.idx[2 * q + 1];
+        float w0 = c.w[2 * q], w1 = c.w[2 * q + 1];
+        if (i1 == (i0 ^ 1u)) {
+            bool odd = i0 & 1u;
+            float4 v = odd ? make_float4(w1 * d0, w1 * d1, w0 * d0, w0 * d1)
+                           : make_float4(w0 * d0, w0 * d1, w1 * d0, w1 * d1);
+            atomicAdd(g4 + (i0 >> 1), v);
+        } else {
+            atomicAdd(g2 + i0, make_float2(w0 * d0, w0 * d1));
+            atomicAdd(g2 + i1, make_float2(w1 * d0, w1 * d1));
+        }
+    }
+}
 
 __device__ __forceinline__ void seg_red(float2* g2, uint32_t idx, float v0, float v1, bool live) {
     const uint32_t FULL = 0xffffffffu;
@@ -219,46 +241,7 @@ __device__ __forceinline__ void scatter_row(const HashLayout& hl, float* genc, f
             for (int k = 0; k < 8; ++k)
                 seg_red(g2, c.idx[k], c.w[k] * d[2 * l], c.w[k] * d[2 * l + 1], live);
         } else if (live) {
-#pragma unroll
-            for (int k = 0; k < 8; ++k)
-                atomicAdd(g2 + c.idx[k], make_float2(c.w[k] * d[2 * l], c.w[k] * d[2 * l + 1]));
-        }
-    }
-}
-
-__global__ void __launch_bounds__(128) hash_bwd_kernel(FieldArgs a, FieldGradArgs g,
-                                                       const float4* __restrict__ dfeat) {
-    uint32_t n_tiles = a.status->n_tiles;
-    int r = threadIdx.x;
-    for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-        TileDesc td = a.tiles[t];
-        bool live = r < td.n;
-        float4 L = live ? a.s.local[uint64_t(td.start) + r] : make_float4(0.f, 0.f, 0.f, 0.f);
-        const float4* d4 = dfeat + (uint64_t(t) * kT + r) * 4;
-        float d[kFeatDim];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            float4 v = live ? d4[q] : make_float4(0.f, 0.f, 0.f, 0.f);
-            d[4 * q] = v.x;
-            d[4 * q + 1] = v.y;
-            d[4 * q + 2] = v.z;
-            d[4 * q + 3] = v.w;
-        }
-        float2* g2 = reinterpret_cast<float2*>(g.g_enc[td.slot]);
-#pragma unroll
-        for (int l = 0; l < kLevels; ++l) {
-            Corner c;
-            hash_level(a.hl, l, L.x, L.y, L.z, c);
-            if (l < kAggLevels) {
-                // warp-uniform control flow: every lane takes part in the shuffles
-#pragma unroll
-                for (int k = 0; k < 8; ++k)
-                    seg_red(g2, c.idx[k], c.w[k] * d[2 * l], c.w[k] * d[2 * l + 1], live);
-            } else if (live) {
-#pragma unroll
-                for (int k = 0; k < 8; ++k)
-                    atomicAdd(g2 + c.idx[k], make_float2(c.w[k] * d[2 * l], c.w[k] * d[2 * l + 1]));
-            }
+            scatter_pairs(genc, c, d[2 * l], d[2 * l + 1]);
         }
     }
 }

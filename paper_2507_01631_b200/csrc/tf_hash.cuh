@@ -44,16 +44,32 @@ __device__ __forceinline__ void hash_level(const HashLayout& hl, int l, float x,
     }
 }
 
+// The two x-neighbour corners (dx = 0, 1) of a cell hit the same aligned
+// 16-byte entry pair whenever idx1 == idx0 ^ 1 (dense levels: even index;
+// hashed levels: even cell x, since (x + 1) ^ h = (x ^ h) ^ 1).  Such pairs
+// are fetched with one 16-byte load (fewer L1 wavefronts).
 __device__ __forceinline__ void hash_encode(const HashLayout& hl, const float* __restrict__ tab,
                                             float x, float y, float z, float* feat) {
     const float2* t2 = reinterpret_cast<const float2*>(tab);
+    const float4* t4 = reinterpret_cast<const float4*>(tab);
 #pragma unroll
     for (int l = 0; l < kLevels; ++l) {
         Corner c;
         hash_level(hl, l, x, y, z, c);
         float2 e[8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) e[k] = __ldg(t2 + c.idx[k]);
+        for (int q = 0; q < 4; ++q) {
+            uint32_t i0 = c.idx[2 * q], i1 = c.idx[2 * q + 1];
+            if (i1 == (i0 ^ 1u)) {
+                float4 v = __ldg(t4 + (i0 >> 1));
+                bool odd = i0 & 1u;
+                e[2 * q] = odd ? make_float2(v.z, v.w) : make_float2(v.x, v.y);
+                e[2 * q + 1] = odd ? make_float2(v.x, v.y) : make_float2(v.z, v.w);
+            } else {
+                e[2 * q] = __ldg(t2 + i0);
+                e[2 * q + 1] = __ldg(t2 + i1);
+            }
+        }
         float a0 = 0.f, a1 = 0.f;
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
