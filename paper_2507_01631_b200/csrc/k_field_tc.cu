@@ -183,7 +183,10 @@ __global__ void __launch_bounds__(128) hash_fwd_kernel(FieldArgs a, uint8_t* __r
 // along a ray, so on the coarse levels the same corner entry repeats in runs
 // of lanes: a warp-segmented sum over equal-entry runs leaves one
 // red.global.add.v2.f32 per run instead of one per sample.
-constexpr int kAggLevels = 3;  // levels 0..2 (cells >= 2.8% of the tile)
+#ifndef TFG_AGG_LEVELS
+#define TFG_AGG_LEVELS 0
+#endif
+constexpr int kAggLevels = TFG_AGG_LEVELS;  // 0: measured fastest on B200 (pairing alone wins)
 
 // Pair-vectorised scatter of one level's 8 corners (see hash_encode): one
 // red.global.add.v4.f32 for an aligned x-neighbour pair, else two v2.

@@ -129,8 +129,12 @@ int scan_exclusive(const uint32_t* in, uint64_t n, uint32_t* out, uint32_t* bloc
 // One thread per candidate pixel of the per-view crop-union rects; flag = 1 iff
 // the ray exists, hits >= 1 tile and every hit tile is loaded.
 __global__ void __launch_bounds__(128) accept_kernel(AcceptArgs a, uint32_t* __restrict__ flags) {
-    uint64_t idx = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (idx >= a.n_candidates) return;
+    // two threads per candidate: one Newton localisation each (z_max / z_min)
+    const uint64_t gt = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint64_t idx = gt >> 1;
+    const int hi = int(gt & 1);
+    const uint32_t pair = 3u << ((threadIdx.x & 31) & ~1);
+    if (idx >= a.n_candidates) return;  // both lanes of a pair leave together
     int v = 0;
     while (v + 1 < a.n_views && a.view_start[v + 1] <= idx) ++v;
     uint64_t local = idx - a.view_start[v];
@@ -145,8 +149,13 @@ __global__ void __launch_bounds__(128) accept_kernel(AcceptArgs a, uint32_t* __r
         if (r[0] < r[1] && row >= r[0] && row < r[1] && col >= r[2] && col < r[3]) in = true;
     }
     if (in) {
+        double gx = 0.0, gy = 0.0;
+        int st = rpc_localize(a.cams[v], double(row), double(col), hi ? a.z_min : a.z_max, &gx, &gy);
+        double ox = __shfl_xor_sync(pair, gx, 1), oy = __shfl_xor_sync(pair, gy, 1);
+        int ost = __shfl_xor_sync(pair, st, 1);
         double o[3], d[3];
-        if (rpc_ray(a.cams[v], row, col, a.z_min, a.z_max, o, d) == 0) {
+        if (hi == 0 && st == 0 && ost == 0 &&
+            rpc_ray_finish(gx, gy, ox, oy, a.z_min, a.z_max, o, d) == 0) {
             // candidate_tiles (tiler.cpp:70-100): XY shadow between z bounds
             double dz = d[2];
             if (dz != 0.0) {
@@ -158,10 +167,10 @@ __global__ void __launch_bounds__(128) accept_kernel(AcceptArgs a, uint32_t* __r
                     double bx = o[0] + tb * d[0], by = o[1] + tb * d[1];
                     auto cell = [](const double* e, int n, double val) {
                         // upper_bound - 1, clamped to [0, n-1]
-                        int lo = 0, hi = n + 1;
-                        while (lo < hi) {
-                            int mid = (lo + hi) >> 1;
-                            if (val < e[mid]) hi = mid; else lo = mid + 1;
+                        int lo = 0, hi2 = n + 1;
+                        while (lo < hi2) {
+                            int mid = (lo + hi2) >> 1;
+                            if (val < e[mid]) hi2 = mid; else lo = mid + 1;
                         }
                         int k = lo - 1;
                         return k < 0 ? 0 : (k > n - 1 ? n - 1 : k);
@@ -189,7 +198,7 @@ __global__ void __launch_bounds__(128) accept_kernel(AcceptArgs a, uint32_t* __r
             }
         }
     }
-    flags[idx] = ok;
+    if (hi == 0) flags[idx] = ok;
 }
 
 __global__ void accept_scatter_kernel(AcceptArgs a, const uint32_t* __restrict__ flags,
@@ -252,18 +261,26 @@ __device__ __forceinline__ bool occ_test(const uint32_t* bits, float x, float y,
     return (__ldg(bits + (v >> 5)) >> (v & 31)) & 1u;
 }
 
+// Two threads per ray: the even lane localises at z_max, the odd lane at
+// z_min (the two Newton solves of ray_from_pixel are independent), the
+// results are exchanged by shuffle and both lanes finish the ray with the
+// same arithmetic (same bits); the interior-sample counting is split by
+// sample parity; the odd lane also writes the view encoding.
 __global__ void __launch_bounds__(128) raygen_kernel(RaygenArgs a, RayRec* __restrict__ rays,
                                                      float4* __restrict__ venc,
                                                      uint32_t* __restrict__ counts,
                                                      Status* __restrict__ status) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= a.n_rays) return;
-    uint64_t g = a.ray_begin + uint64_t(i);
+    const int gt = blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = gt >> 1, hi = gt & 1;
+    const uint32_t pair = 3u << ((threadIdx.x & 31) & ~1);
+    const bool valid = i < a.n_rays;
+    const int ii = valid ? i : 0;
+    uint64_t g = a.ray_begin + uint64_t(ii);
     int v, row, col;
     if (a.pixels) {
-        v = a.pixels[3 * i];
-        row = a.pixels[3 * i + 1];
-        col = a.pixels[3 * i + 2];
+        v = a.pixels[3 * ii];
+        row = a.pixels[3 * ii + 1];
+        col = a.pixels[3 * ii + 2];
     } else {
         Rng r(hash_combine(hash_combine(hash_combine(a.seed, kPurposePixels), a.iter), g));
         uint64_t e = a.accept[r.below(a.n_accept)];
@@ -271,33 +288,47 @@ __global__ void __launch_bounds__(128) raygen_kernel(RaygenArgs a, RayRec* __res
         row = int((e >> 20) & 0xFFFFF);
         col = int(e & 0xFFFFF);
     }
+    double gx = 0.0, gy = 0.0;
+    int st = rpc_localize(a.cams[v], double(row), double(col), hi ? a.z_min : a.z_max, &gx, &gy);
+    double ox = __shfl_xor_sync(pair, gx, 1), oy = __shfl_xor_sync(pair, gy, 1);
+    int ost = __shfl_xor_sync(pair, st, 1);
     RayRec R;
     R.view = v;
     R.row = row;
     R.col = col;
     R.target[0] = R.target[1] = R.target[2] = 0.f;
-    if (a.crop_bytes) {
+    // status of the top (z_max) localisation first, as ray_from_pixel throws
+    int st_top = hi ? ost : st, st_bot = hi ? st : ost;
+    R.status = st_top ? st_top : st_bot;
+    if (R.status == 0) {
+        double tx = hi ? ox : gx, ty = hi ? oy : gy, bx = hi ? gx : ox, by = hi ? gy : oy;
+        R.status = rpc_ray_finish(tx, ty, bx, by, a.z_min, a.z_max, R.o, R.d);
+    }
+    if (valid && hi == 0)
+        for (int s = 0; s < a.slots.n; ++s) counts[uint64_t(s) * a.n_rays + i] = 0;
+    R.nseg = 0;
+    if (R.status != 0) {
+        if (valid && hi == 0) {
+            atomicOr(&status->bits, kStatusRayFail);
+            rays[i] = R;
+        }
+        return;
+    }
+    if (a.crop_bytes && hi == 0) {
         const int* cr = a.crop_rect + 4 * v;  // r0, c0, cols, rows
         const uint8_t* px = a.crop_bytes + a.crop_offset[v] +
                             3 * (uint64_t(row - cr[0]) * uint64_t(cr[2]) + uint64_t(col - cr[1]));
         for (int c = 0; c < 3; ++c) R.target[c] = float(px[c]) / 255.0f;  // u8_to_unit
     }
-    R.status = rpc_ray(a.cams[v], row, col, a.z_min, a.z_max, R.o, R.d);
-    for (int s = 0; s < a.slots.n; ++s) counts[uint64_t(s) * a.n_rays + i] = 0;
-    R.nseg = 0;
-    if (R.status != 0) {
-        atomicOr(&status->bits, kStatusRayFail);
-        rays[i] = R;
-        return;
-    }
     // TileBoxSet::segments: hits in slot order, stable insertion sort on t_near
     SegPlan p;
     p.nseg = 0;
+    bool overflow = false;
     for (int s = 0; s < a.slots.n; ++s) {
         double t0, t1;
         if (!slab(R.o, R.d, a.slots.box[s], &t0, &t1)) continue;
         if (p.nseg == kMaxSeg) {
-            atomicOr(&status->bits, kStatusSegOverflow);
+            overflow = true;
             break;
         }
         int j = p.nseg++;
@@ -311,6 +342,7 @@ __global__ void __launch_bounds__(128) raygen_kernel(RaygenArgs a, RayRec* __res
         p.tf[j] = t1;
         p.slot[j] = s;
     }
+    if (overflow && valid && hi == 0) atomicOr(&status->bits, kStatusSegOverflow);
     plan_intervals(p, a.spm, a.cap);
     uint64_t key = hash_combine(hash_combine(hash_combine(a.seed, kPurposeJitter), a.iter), g);
     R.nseg = p.nseg;
@@ -318,22 +350,28 @@ __global__ void __launch_bounds__(128) raygen_kernel(RaygenArgs a, RayRec* __res
         const double* fr = a.slots.frame[p.slot[k]];
         const uint32_t* bits = a.occ_bits[p.slot[k]];
         int n = p.nint[k];
-        int cnt = 2;  // endpoints are never culled
-        for (int j = 1; j < n; ++j) {
+        int cnt = 0;
+        for (int j = 1 + hi; j < n; j += 2) {
             double t = sample_t(p, k, j, a.jitter, key);
             float lx = float((R.o[0] + t * R.d[0] - fr[0]) * fr[3]);
             float ly = float((R.o[1] + t * R.d[1] - fr[1]) * fr[4]);
             float lz = float((R.o[2] + t * R.d[2] - fr[2]) * fr[5]);
             cnt += occ_test(bits, lx, ly, lz);
         }
+        cnt += __shfl_xor_sync(pair, cnt, 1);
+        cnt += 2;  // endpoints are never culled
         R.slot[k] = uint8_t(p.slot[k]);
         R.tn[k] = p.tn[k];
         R.tf[k] = p.tf[k];
         R.nint[k] = uint16_t(n);
         R.cnt[k] = uint16_t(cnt);
-        counts[uint64_t(p.slot[k]) * a.n_rays + i] = uint32_t(cnt);
+        if (valid && hi == 0) counts[uint64_t(p.slot[k]) * a.n_rays + i] = uint32_t(cnt);
     }
-    rays[i] = R;
+    if (!valid) return;
+    if (hi == 0) {
+        rays[i] = R;
+        return;
+    }
     // encode_direction (nn.hpp:288-298) of the float world direction
     float d3[3] = {float(R.d[0]), float(R.d[1]), float(R.d[2])};
     float e[24];
@@ -480,7 +518,7 @@ int launch_accept(const AcceptArgs& a, uint32_t* flags, uint32_t* pos, uint32_t*
         return 0;
     }
     int nb = int((a.n_candidates + 127) / 128);
-    accept_kernel<<<nb, 128, 0, st>>>(a, flags);
+    accept_kernel<<<int((2 * a.n_candidates + 127) / 128), 128, 0, st>>>(a, flags);
     if (scan_exclusive(flags, a.n_candidates, pos, block_sums, n_out, st, launches)) return 1;
     accept_scatter_kernel<<<nb, 128, 0, st>>>(a, flags, pos, out);
     *launches += 2;
@@ -491,7 +529,7 @@ int launch_sampler(const RaygenArgs& a, RayRec* rays, float4* venc, uint32_t* co
                    uint32_t* P, uint32_t* block_sums, TileDesc* tiles, int max_tiles,
                    SampleArrays out, uint64_t capacity, Status* status, cudaStream_t st,
                    uint64_t* launches) {
-    raygen_kernel<<<(a.n_rays + 127) / 128, 128, 0, st>>>(a, rays, venc, counts, status);
+    raygen_kernel<<<(2 * a.n_rays + 127) / 128, 128, 0, st>>>(a, rays, venc, counts, status);
     uint64_t n = uint64_t(a.slots.n) * a.n_rays;
     if (scan_exclusive(counts, n, P, block_sums, nullptr, st, launches)) return 1;
     tiles_kernel<<<1, 256, 0, st>>>(P, a.n_rays, a.slots.n, capacity, max_tiles, tiles, status);

@@ -223,7 +223,22 @@ TF_HD int rpc_localize(const tfg_rpc& c, double pr, double pc, double h, double*
     return 2;
 }
 
-// ray_from_pixel (camera.cpp:105-124); |delta| summed as (x²+y²)+z².
+// ray_from_pixel (camera.cpp:105-124) from the two localisations (top at
+// z_max, bottom at z_min); |delta| summed as (x²+y²)+z².
+TF_HD int rpc_ray_finish(double tx, double ty, double bx, double by, double zmin, double zmax,
+                         double* o, double* d) {
+    double dx = bx - tx, dy = by - ty, dz = zmin - zmax;
+    double len = sqrt(dx * dx + dy * dy + dz * dz);
+    if (!(len > 1e-12 && zmax > zmin)) return 3;
+    o[0] = tx;
+    o[1] = ty;
+    o[2] = zmax;
+    d[0] = dx / len;
+    d[1] = dy / len;
+    d[2] = dz / len;
+    return 0;
+}
+
 TF_HD int rpc_ray(const tfg_rpc& c, int row, int col, double zmin, double zmax, double* o,
                   double* d) {
     double tx, ty, bx, by;

@@ -34,7 +34,8 @@ from .abi import (
     ptr,
 )
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libtilefield_gpu.so")
+LIB_PATH = os.environ.get(
+    "TFG_LIB", os.path.join(os.path.dirname(os.path.abspath(__file__)), "libtilefield_gpu.so"))
 _lib = None
 _vp = C.c_void_p
 
