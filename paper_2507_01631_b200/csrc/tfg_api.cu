@@ -16,6 +16,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <memory>
+#include <thread>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -69,6 +72,18 @@ struct TileHost {
     bool created = false;
     float* rec = nullptr;  // pinned: [params(stride) | m(stride) | v(stride) | ema(32^3)]
     uint64_t enc_step = 0, dnet_step = 0;
+};
+
+// Background TileField::create of the host records (the Rng stream of a tile
+// is inherently sequential: 434k draws whose state is the previous output).
+// Workers initialise tiles in snake first-visit order; ensure_record waits
+// for a tile that is not ready yet.
+struct InitPool {
+    std::vector<std::thread> workers;
+    std::vector<int> order;
+    std::atomic<size_t> next{0};
+    std::unique_ptr<std::atomic<int>[]> ready;
+    std::atomic<bool> stop{false};
 };
 
 enum Phase { kPhSampler, kPhFieldFwd, kPhComposite, kPhFieldBwd, kPhAdam, kPhOccupancy,
@@ -166,6 +181,8 @@ struct tfg_ctx {
 
     uint64_t bytes_total = 0;
     uint64_t h2d_bytes = 0, d2h_bytes = 0;
+    float* h_records = nullptr;  // one pinned block for every tile record
+    InitPool init;
 
     // per-phase device timing (CUDA events on the context stream)
     bool prof = false;
@@ -309,13 +326,54 @@ void fresh_tile(tfg_ctx* c, int ti) {
 }
 
 int ensure_record(tfg_ctx* c, int ti) {
-    TileHost& t = c->tiles[ti];
-    if (!t.rec) {
-        CK(cudaHostAlloc(reinterpret_cast<void**>(&t.rec),
-                         (3 * c->stride + kOccVox) * sizeof(float), cudaHostAllocDefault));
-    }
-    if (!t.created) fresh_tile(c, ti);
+    // the record was created by the init pool (or is being created now)
+    while (!c->init.ready[ti].load(std::memory_order_acquire)) std::this_thread::yield();
     return 0;
+}
+
+void stop_init_pool(tfg_ctx* c) {
+    c->init.stop = true;
+    for (auto& w : c->init.workers) w.join();
+    c->init.workers.clear();
+    c->init.stop = false;
+}
+
+void start_init_pool(tfg_ctx* c) {
+    int n = c->rows * c->cols;
+    c->init.ready.reset(new std::atomic<int>[n]);
+    for (int i = 0; i < n; ++i) c->init.ready[i] = 0;
+    // first-visit order along the snake path
+    std::vector<int> order;
+    std::vector<char> seen(n, 0);
+    auto visit = [&](int ti) {
+        if (!seen[ti]) {
+            seen[ti] = 1;
+            order.push_back(ti);
+        }
+    };
+    if (c->rows == 1 && c->cols == 1) {
+        visit(0);
+    } else {
+        for (int i = 0; i < c->rows - 1; ++i)
+            for (int jj = 0; jj < c->cols - 1; ++jj) {
+                int j = (i % 2 == 0) ? jj : (c->cols - 2 - jj);
+                for (int ti : window_tiles(c, i, j)) visit(ti);
+            }
+    }
+    for (int ti = 0; ti < n; ++ti) visit(ti);
+    c->init.order = order;
+    c->init.next = 0;
+    int nw = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+    for (int w = 0; w < nw; ++w)
+        c->init.workers.emplace_back([c] {
+            for (;;) {
+                size_t k = c->init.next.fetch_add(1);
+                if (k >= c->init.order.size() || c->init.stop) return;
+                int ti = c->init.order[k];
+                fresh_tile(c, ti);
+                c->init.ready[ti].store(1, std::memory_order_release);
+            }
+        });
 }
 
 // D2H (evict) / H2D (load) of one slot's state on the side stream.
@@ -764,8 +822,8 @@ TFG_API int tfg_destroy(tfg_ctx* c) {
                    c->d_feat, c->d_tile_rays, c->d_dfeat};
     for (void* p : dev)
         if (p) cudaFree(p);
-    for (auto& t : c->tiles)
-        if (t.rec) cudaFreeHost(t.rec);
+    stop_init_pool(c);
+    if (c->h_records) cudaFreeHost(c->h_records);
     for (auto* im : c->h_images)
         if (im) cudaFreeHost(im);
     if (c->h_status) cudaFreeHost(c->h_status);
@@ -822,7 +880,16 @@ TFG_API int tfg_set_scene(tfg_ctx* c, const tfg_rpc* cams, int n_views,
         if (images && images[v]) std::memcpy(c->h_images[v], images[v], nb);
         else std::memset(c->h_images[v], 0, nb);
     }
+    stop_init_pool(c);
+    if (c->h_records) cudaFreeHost(c->h_records);
+    c->h_records = nullptr;
     c->tiles.assign(size_t(grid_rows) * grid_cols, TileHost{});
+    {
+        uint64_t rec = 3 * c->stride + kOccVox;
+        CK(cudaHostAlloc(reinterpret_cast<void**>(&c->h_records),
+                         c->tiles.size() * rec * sizeof(float), cudaHostAllocDefault));
+        for (size_t ti = 0; ti < c->tiles.size(); ++ti) c->tiles[ti].rec = c->h_records + ti * rec;
+    }
     // capacities: max over all window positions (constant HBM across the snake)
     uint64_t cand = 1, cropb = 1;
     std::vector<std::pair<int, int>> pos;
@@ -866,6 +933,7 @@ TFG_API int tfg_set_scene(tfg_ctx* c, const tfg_rpc* cams, int n_views,
     CK(cudaStreamSynchronize(c->st));
     c->nslots = 0;
     c->pos_r = c->pos_c = -1;
+    start_init_pool(c);
     return 0;
 }
 
