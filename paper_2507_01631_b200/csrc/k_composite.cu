@@ -134,7 +134,16 @@ __global__ void __launch_bounds__(256) composite_kernel(CompositeArgs a) {
         float Rg = (cg - (pg + sgc)) + Rbg;
         float Rb = (cb - (pb + sbc)) + Rbb;
         float ds = de * (gr * (Tk1 * io.y - Rr) + gg * (Tk1 * io.z - Rg) + gb * (Tk1 * io.w - Rb));
-        if (q < m) a.s.io[pos] = make_float4(ds, w * gr, w * gg, w * gb);
+        if (q < m) {
+            // pre-activation gradients for K4: d raw = dsigma * exp'(raw)
+            // (= sigma, or 0 where the activation is clamped, nn.hpp:270-280),
+            // d pre-sigmoid = dc * s (1 - s) (nn.hpp:283-285)
+            float dr = w * gr, dg = w * gg, db = w * gb;
+            float draw = sg >= a.density_max ? 0.f : ds * sg;
+            a.s.io[pos] = make_float4(draw, dr * io.y * (1.f - io.y), dg * io.z * (1.f - io.z),
+                                      db * io.w * (1.f - io.w));
+            if (a.export_io) a.export_io[pos] = make_float4(ds, dr, dg, db);
+        }
         pr += __shfl_sync(FULL, sr, 31);
         pg += __shfl_sync(FULL, sgc, 31);
         pb += __shfl_sync(FULL, sbc, 31);

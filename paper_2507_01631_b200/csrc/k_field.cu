@@ -264,9 +264,9 @@ __global__ void __launch_bounds__(kTile) field_bwd_kernel(FieldArgs a, FieldGrad
             float acc = Wc[kCB3 + o];
 #pragma unroll 16
             for (int i = 0; i < kCHidden; ++i) acc += Wc[kCW3 + o * kCHidden + i] * c2[i];
-            float s = sigmoidf_(acc);
+            (void)acc;  // K3 hands over the pre-sigmoid gradient
             float gin = o == 0 ? dio.y : (o == 1 ? dio.z : dio.w);
-            d3[o] = live ? gin * s * (1.f - s) : 0.f;
+            d3[o] = live ? gin : 0.f;
         }
         d3[3] = 0.f;
         __syncthreads();
@@ -308,7 +308,8 @@ __global__ void __launch_bounds__(kTile) field_bwd_kernel(FieldArgs a, FieldGrad
 #pragma unroll
                 for (int i = 0; i < kEmb; ++i) acc[i] += Wc[kCW1 + o * kCIn + i] * d;
             }
-            o16[0] = live ? dio.x * draw : 0.f;
+            o16[0] = live ? dio.x : 0.f;  // d raw sigma (K3)
+            (void)draw;
 #pragma unroll
             for (int i = 0; i < kEmb; ++i) o16[1 + i] = acc[i];
         }

@@ -183,6 +183,9 @@ __global__ void __launch_bounds__(128) hash_fwd_kernel(FieldArgs a, uint8_t* __r
 // along a ray, so on the coarse levels the same corner entry repeats in runs
 // of lanes: a warp-segmented sum over equal-entry runs leaves one
 // red.global.add.v2.f32 per run instead of one per sample.
+#ifndef TFG_FUSED_GATHER
+#define TFG_FUSED_GATHER 0
+#endif
 #ifndef TFG_AGG_LEVELS
 #define TFG_AGG_LEVELS 0
 #endif
@@ -286,11 +289,34 @@ __global__ void __launch_bounds__(128) mlp_fwd_kernel(FieldArgs a, const uint8_t
             stage_density(W, a.f.dnet[td.slot]);
             cur = td.slot;
         }
+#if TFG_FUSED_GATHER
+        // hash gather of this row straight into the X0 operand tile; the tile
+        // (and the ray id) also goes to global memory for the backward pass
+        int ray = -1;
+        {
+            float f[kFeatDim];
+            if (r < td.n) {
+                float4 L = a.s.local[uint64_t(td.start) + r];
+                ray = __float_as_int(L.w);
+                hash_encode(a.hl, a.f.enc[td.slot], L.x, L.y, L.z, f);
+            } else {
+#pragma unroll
+                for (int i = 0; i < kFeatDim; ++i) f[i] = 0.f;
+            }
+            st_chunk(X0, r, 0, f);
+            st_chunk(X0, r, 1, f + 8);
+            uint8_t* gbase = const_cast<uint8_t*>(feat) + uint64_t(t) * kFeatTile;
+            st_chunk(gbase, r, 0, f);
+            st_chunk(gbase, r, 1, f + 8);
+            const_cast<int32_t*>(rays)[uint64_t(t) * kT + r] = ray;
+        }
+#else
         if (r == 0) {
             umma::mbar_expect_tx(&bar_ld, kFeatTile);
             umma::bulk_g2s(X0, feat + uint64_t(t) * kFeatTile, kFeatTile, &bar_ld);
         }
         int ray = rays[uint64_t(t) * kT + r];
+#endif
         float ve[kViewDim];
         {
             const float4* v4 = a.venc + uint64_t(ray < 0 ? 0 : ray) * 6;
@@ -304,8 +330,10 @@ __global__ void __launch_bounds__(128) mlp_fwd_kernel(FieldArgs a, const uint8_t
             }
         }
         sync_for_mma();  // density weights staged, previous tile's TMEM reads done
+#if !TFG_FUSED_GATHER
         umma::mbar_wait(&bar_ld, ph_ld);
         ph_ld ^= 1u;
+#endif
         // ---- density layer 1: [128x16] x W1d^T -> 64
         if (r == 0) {
             umma::mma(tmem, kmaj(X0, kT, 0), kmaj(W.w1d, kW1dRows, 0), id64, 0);
@@ -492,7 +520,7 @@ __global__ void __launch_bounds__(128) mlp_bwd_kernel(FieldArgs a, FieldGradArgs
                                                       const int32_t* __restrict__ rays,
                                                       float4* __restrict__ dfeat) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
-    __shared__ uint64_t bar_mma, bar_ld;
+    __shared__ uint64_t bar_mma, bar_ld, bar_w;
     __shared__ uint32_t tmem_slot;
     uint8_t* p = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
     uint8_t* H1 = carve(p, kBufA);
@@ -507,6 +535,7 @@ __global__ void __launch_bounds__(128) mlp_bwd_kernel(FieldArgs a, FieldGradArgs
     if (r == 0) {
         umma::mbar_init(&bar_mma, 1);
         umma::mbar_init(&bar_ld, 1);
+        umma::mbar_init(&bar_w, 1);
         umma::fence_mbar_init();
     }
     if (r < 32) umma::tmem_alloc<kBwdTmemCols>(&tmem_slot);
@@ -520,7 +549,7 @@ __global__ void __launch_bounds__(128) mlp_bwd_kernel(FieldArgs a, FieldGradArgs
         float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         st_chunk(X0, r, 3, z);
     }
-    uint32_t ph_mma = 0, ph_ld = 0;
+    uint32_t ph_mma = 0, ph_ld = 0, ph_w = 0;
     int cur = -1;
     bool first_d = true, first_c = true;
     uint32_t n_tiles = a.status->n_tiles;
@@ -566,7 +595,6 @@ __global__ void __launch_bounds__(128) mlp_bwd_kernel(FieldArgs a, FieldGradArgs
         umma::mbar_wait(&bar_ld, ph_ld);
         ph_ld ^= 1u;
         uint32_t mh[2], mc1[2], mc2[2];  // ReLU masks of H1, C1, C2
-        float draw;
         // ================= forward recompute
         if (r == 0) {
             umma::mma(tmem, kmaj(X0, kT, 0), kmaj(W.w1d, kW1dRows, 0), id64, 0);
@@ -602,8 +630,6 @@ __global__ void __launch_bounds__(128) mlp_bwd_kernel(FieldArgs a, FieldGradArgs
             float v[16];
             tld16(tmem, 0, v);
             umma::ld_wait();
-            float raw = v[0] + W.b2d[0];
-            draw = raw >= a.density_lim ? 0.f : __expf(raw);
             float cin[48];
 #pragma unroll
             for (int i = 0; i < kEmb; ++i) cin[i] = v[1 + i] + W.b2d[1 + i];
@@ -666,24 +692,13 @@ __global__ void __launch_bounds__(128) mlp_bwd_kernel(FieldArgs a, FieldGradArgs
             for (int c = 0; c < 8; ++c) st_chunk(C2, r, c, v + 8 * c);
         }
         sync_for_mma();
-        if (r == 0) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-                umma::mma(tmem, kmaj(C2, kT, k), kmaj(W.wc3, kWc3Rows, k), id16, k > 0);
-            umma::commit(&bar_mma);
-        }
-        wait_mma(&bar_mma, ph_mma);
         {
-            float v[16];
-            tld16(tmem, 0, v);
-            umma::ld_wait();
+            // K3 already applied the sigmoid derivative: io = (d raw sigma,
+            // d pre-sigmoid r, g, b), so the colour output layer is not recomputed
             float d3[16];
-            float gin[3] = {dio.y, dio.z, dio.w};
-#pragma unroll
-            for (int o = 0; o < 3; ++o) {
-                float s = sigm(v[o] + W.bc3[o]);
-                d3[o] = live ? gin[o] * s * (1.f - s) : 0.f;
-            }
+            d3[0] = dio.y;
+            d3[1] = dio.z;
+            d3[2] = dio.w;
 #pragma unroll
             for (int o = 3; o < 16; ++o) d3[o] = 0.f;
             st_chunk(D3, r, 0, d3);
@@ -694,10 +709,11 @@ __global__ void __launch_bounds__(128) mlp_bwd_kernel(FieldArgs a, FieldGradArgs
         // (A) dC2pre = D3 . Wc3 ; dWc3^T += [C2|1]^T . D3
         if (r == 0) {
             umma::mma(tmem, kmaj(D3, kT, 0), mnmaj(W.wc3, kWc3Rows, 0), id64_kmn, 0);
+            umma::commit(&bar_mma);
 #pragma unroll
             for (int k = 0; k < 8; ++k)
                 umma::mma(tmem + kColWc3, mnmaj(C2, kT, k), mnmaj(D3, kT, k), idw16, (first_c && k == 0) ? 0 : 1);
-            umma::commit(&bar_mma);
+            umma::commit(&bar_w);
         }
         wait_mma(&bar_mma, ph_mma);
         {
@@ -709,6 +725,7 @@ __global__ void __launch_bounds__(128) mlp_bwd_kernel(FieldArgs a, FieldGradArgs
             umma::ld_wait();
 #pragma unroll
             for (int i = 0; i < 64; ++i) v[i] = ((mc2[i >> 5] >> (i & 31)) & 1u) ? v[i] : 0.f;
+            wait_mma(&bar_w, ph_w);  // dWc3^T has read C2
 #pragma unroll
             for (int c = 0; c < 8; ++c) st_chunk(C2, r, c, v + 8 * c);  // DC2 over C2
         }
@@ -718,10 +735,11 @@ __global__ void __launch_bounds__(128) mlp_bwd_kernel(FieldArgs a, FieldGradArgs
 #pragma unroll
             for (int k = 0; k < 4; ++k)
                 umma::mma(tmem, kmaj(C2, kT, k), mnmaj(W.wc2, kWc2Rows, k), id64_kmn, k > 0);
+            umma::commit(&bar_mma);
 #pragma unroll
             for (int k = 0; k < 8; ++k)
                 umma::mma(tmem + kColWc2, mnmaj(C1, kT, k), mnmaj(C2, kT, k), idw64, (first_c && k == 0) ? 0 : 1);
-            umma::commit(&bar_mma);
+            umma::commit(&bar_w);
         }
         wait_mma(&bar_mma, ph_mma);
         {
@@ -733,6 +751,7 @@ __global__ void __launch_bounds__(128) mlp_bwd_kernel(FieldArgs a, FieldGradArgs
             umma::ld_wait();
 #pragma unroll
             for (int i = 0; i < 64; ++i) v[i] = ((mc1[i >> 5] >> (i & 31)) & 1u) ? v[i] : 0.f;
+            wait_mma(&bar_w, ph_w);  // dWc2^T has read C1
 #pragma unroll
             for (int c = 0; c < 8; ++c) st_chunk(C1, r, c, v + 8 * c);  // DC1 over C1
         }
@@ -742,10 +761,11 @@ __global__ void __launch_bounds__(128) mlp_bwd_kernel(FieldArgs a, FieldGradArgs
 #pragma unroll
             for (int k = 0; k < 4; ++k)
                 umma::mma(tmem, kmaj(C1, kT, k), mnmaj(W.wc1, kWc1Rows, k), id16_kmn, k > 0);
+            umma::commit(&bar_mma);
 #pragma unroll
             for (int k = 0; k < 8; ++k)
                 umma::mma(tmem + kColWc1, mnmaj(C1, kT, k), mnmaj(CIN, kT, k), idw48, (first_c && k == 0) ? 0 : 1);
-            umma::commit(&bar_mma);
+            umma::commit(&bar_w);
         }
         wait_mma(&bar_mma, ph_mma);
         first_c = false;
@@ -754,9 +774,10 @@ __global__ void __launch_bounds__(128) mlp_bwd_kernel(FieldArgs a, FieldGradArgs
             tld16(tmem, 0, v);
             umma::ld_wait();
             float d[16];
-            d[0] = live ? dio.x * draw : 0.f;
+            d[0] = dio.x;  // d raw sigma (K3)
 #pragma unroll
             for (int i = 0; i < kEmb; ++i) d[1 + i] = v[i];
+            wait_mma(&bar_w, ph_w);  // (in-order retire; keeps the phases paired)
             st_chunk(DO, r, 0, d);
             st_chunk(DO, r, 1, d + 8);
         }
@@ -764,10 +785,11 @@ __global__ void __launch_bounds__(128) mlp_bwd_kernel(FieldArgs a, FieldGradArgs
         // (D) dH1pre = DO . W2d ; dW2d^T += [H1|1]^T . DO
         if (r == 0) {
             umma::mma(tmem, kmaj(DO, kT, 0), mnmaj(W.w2d, kW2dRows, 0), id64_kmn, 0);
+            umma::commit(&bar_mma);
 #pragma unroll
             for (int k = 0; k < 8; ++k)
                 umma::mma(tmem + kColW2d, mnmaj(H1, kT, k), mnmaj(DO, kT, k), idw16, (first_d && k == 0) ? 0 : 1);
-            umma::commit(&bar_mma);
+            umma::commit(&bar_w);
         }
         wait_mma(&bar_mma, ph_mma);
         {
@@ -779,6 +801,7 @@ __global__ void __launch_bounds__(128) mlp_bwd_kernel(FieldArgs a, FieldGradArgs
             umma::ld_wait();
 #pragma unroll
             for (int i = 0; i < 64; ++i) v[i] = ((mh[i >> 5] >> (i & 31)) & 1u) ? v[i] : 0.f;
+            wait_mma(&bar_w, ph_w);  // dW2d^T has read H1
 #pragma unroll
             for (int c = 0; c < 8; ++c) st_chunk(H1, r, c, v + 8 * c);  // DH1 over H1
         }
@@ -788,10 +811,11 @@ __global__ void __launch_bounds__(128) mlp_bwd_kernel(FieldArgs a, FieldGradArgs
 #pragma unroll
             for (int k = 0; k < 4; ++k)
                 umma::mma(tmem, kmaj(H1, kT, k), mnmaj(W.w1d, kW1dRows, k), id16_kmn, k > 0);
+            umma::commit(&bar_mma);
 #pragma unroll
             for (int k = 0; k < 8; ++k)
                 umma::mma(tmem + kColW1d, mnmaj(H1, kT, k), mnmaj(X0, kT, k), idw32, (first_d && k == 0) ? 0 : 1);
-            umma::commit(&bar_mma);
+            umma::commit(&bar_w);
         }
         wait_mma(&bar_mma, ph_mma);
         first_d = false;
@@ -801,8 +825,13 @@ __global__ void __launch_bounds__(128) mlp_bwd_kernel(FieldArgs a, FieldGradArgs
             float v[16];
             tld16(tmem, 0, v);
             umma::ld_wait();
+#if !TFG_NO_SCATTER  // timing experiments only
             scatter_row(a.hl, g.g_enc[td.slot], L.x, L.y, L.z, v, live);
+#else
+            if (live && v[0] == 12345.f) g.g_enc[td.slot][0] = L.x;
+#endif
         }
+        wait_mma(&bar_w, ph_w);  // dW1d has read H1 / X0 before the next tile
     }
     umma::fence_before_sync();
     __syncthreads();
@@ -822,9 +851,14 @@ void launch_field_forward_tc(const FieldArgs& a, uint8_t* feat, int32_t* rays, i
         cudaFuncSetAttribute(mlp_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kFwdSmem));
         attr = true;
     }
+#if TFG_FUSED_GATHER
+    mlp_fwd_kernel<<<sms * 3, 128, kFwdSmem, st>>>(a, feat, rays);
+    *launches += 1;
+#else
     hash_fwd_kernel<<<sms * 8, 128, 0, st>>>(a, feat, rays);
     mlp_fwd_kernel<<<sms * 3, 128, kFwdSmem, st>>>(a, feat, rays);
     *launches += 2;
+#endif
 }
 
 void launch_field_backward_tc(const FieldArgs& a, const FieldGradArgs& g, uint8_t* feat,

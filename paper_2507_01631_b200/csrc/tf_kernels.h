@@ -14,7 +14,8 @@ struct SampleArrays {
     float4* local;     // x, y, z (owning tile's [0,1]^3 frame), w = ray index bits
     float2* td;        // t (m along the ray), delta (m)
     uint8_t* endpoint; // 1 for segment endpoints
-    float4* io;        // K2: (sigma, r, g, b); K3 overwrites with (dsigma, dr, dg, db)
+    float4* io;        // K2: (sigma, r, g, b); K3 overwrites with the pre-activation
+                       // gradients (d raw sigma, d pre-sigmoid r, g, b) for K4
 };
 
 // Hash-grid level layout (HashGridT::init, nn.hpp:180-195).
@@ -87,6 +88,8 @@ struct CompositeArgs {
     float* ray_rgb;      // 3 per ray (may be null)
     float* ray_depth;
     float* ray_opacity;
+    float density_max;   // sigma == density_max <=> clamped activation (zero grad)
+    float4* export_io;   // optional: (d_sigma, d_rgb) per sample in reference semantics
 };
 
 struct AdamGroup {

@@ -165,6 +165,7 @@ struct tfg_ctx {
     uint8_t* d_feat = nullptr;    // bf16 feature tiles (4 KB per 128-sample tile)
     int32_t* d_tile_rays = nullptr;
     float4* d_dfeat = nullptr;    // fp32 d(features) per tile row (training only)
+    float4* d_export = nullptr;   // parity export of (d_sigma, d_rgb) in ray semantics
     bool simt = false;            // bring-up switch: CUDA-core field kernels
     int cur_rays = 0;
     bool have_batch = false;
@@ -585,7 +586,7 @@ int run_forward(tfg_ctx* c, const FieldPtrs& f) {
     return 0;
 }
 
-int run_composite(tfg_ctx* c, bool backward) {
+int run_composite(tfg_ctx* c, bool backward, float4* export_io = nullptr) {
     PhaseScope ps(c, kPhComposite);
     CompositeArgs a{};
     a.rays = c->d_rays;
@@ -600,6 +601,8 @@ int run_composite(tfg_ctx* c, bool backward) {
     a.ray_rgb = c->d_ray_out;
     a.ray_depth = c->d_ray_out + 3 * uint64_t(c->max_rays);
     a.ray_opacity = c->d_ray_out + 4 * uint64_t(c->max_rays);
+    a.density_max = c->fc.density_max;
+    a.export_io = export_io;
     launch_composite(a, c->st, &c->launches);
     CK(cudaGetLastError());
     return 0;
@@ -819,7 +822,7 @@ TFG_API int tfg_destroy(tfg_ctx* c) {
                    c->d_accept_n, c->d_view_start, c->d_union, c->d_crop4, c->d_rays, c->d_venc,
                    c->d_counts, c->d_P, c->d_tiles, c->s.local, c->s.td, c->s.endpoint, c->s.io,
                    c->d_ray_out, c->d_pixels, c->d_rparams, c->d_rbits, c->d_rcolor, c->d_rcam,
-                   c->d_feat, c->d_tile_rays, c->d_dfeat};
+                   c->d_feat, c->d_tile_rays, c->d_dfeat, c->d_export};
     for (void* p : dev)
         if (p) cudaFree(p);
     stop_init_pool(c);
@@ -1318,7 +1321,8 @@ TFG_API int tfg_field_forward(tfg_ctx* c, float* sigma, float* rgb) {
 TFG_API int tfg_composite(tfg_ctx* c, float* ray_rgb, float* ray_depth, float* ray_opacity,
                           float* d_sigma, float* d_rgb, float* loss) {
     if (!c || !c->have_batch) return fail(TFG_ERR_STATE, "composite: no batch");
-    int rc = run_composite(c, true);
+    if (!c->d_export && dalloc(c, &c->d_export, c->sample_cap)) return TFG_ERR_CUDA;
+    int rc = run_composite(c, true, c->d_export);
     if (rc) return rc;
     HostBatch hb;
     if ((rc = fetch_batch_meta(c, hb))) return rc;
@@ -1333,7 +1337,7 @@ TFG_API int tfg_composite(tfg_ctx* c, float* ray_rgb, float* ray_depth, float* r
     }
     if (d_sigma || d_rgb) {
         std::vector<float4> io(hb.n_samples);
-        CK(cudaMemcpy(io.data(), c->s.io, hb.n_samples * 16, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(io.data(), c->d_export, hb.n_samples * 16, cudaMemcpyDeviceToHost));
         for_samples(c, hb, [&](int, uint64_t q, uint64_t pos, int) {
             if (d_sigma) d_sigma[q] = io[pos].x;
             if (d_rgb) {
