@@ -13,7 +13,8 @@
 //                         read from the same smem tiles) accumulated in TMEM
 //                         across all tiles of a persistent CTA, flushed with
 //                         one fp32 atomic per weight per CTA
-//   K4a hash_bwd_kernel   hash-table scatter-add (red.global.add.v2.f32)
+//   (K4a)                 hash-table scatter-add fused into K4b's last epilogue
+//                         (red.global.add.v4/v2.f32, aligned x-neighbour pairs)
 // A tile is <= 128 samples of one slot bucket (K1), so the density weights of
 // a tile are one tile's.  Precision: bf16 operands, fp32 accumulation (tests
 // state the tolerance against the fp32 oracle).
@@ -517,8 +518,7 @@ __device__ __forceinline__ void flush_color(uint32_t tmem, float* __restrict__ g
 
 __global__ void __launch_bounds__(128) mlp_bwd_kernel(FieldArgs a, FieldGradArgs g,
                                                       const uint8_t* __restrict__ feat,
-                                                      const int32_t* __restrict__ rays,
-                                                      float4* __restrict__ dfeat) {
+                                                      const int32_t* __restrict__ rays) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
     __shared__ uint64_t bar_mma, bar_ld, bar_w;
     __shared__ uint32_t tmem_slot;
@@ -825,11 +825,7 @@ __global__ void __launch_bounds__(128) mlp_bwd_kernel(FieldArgs a, FieldGradArgs
             float v[16];
             tld16(tmem, 0, v);
             umma::ld_wait();
-#if !TFG_NO_SCATTER  // timing experiments only
             scatter_row(a.hl, g.g_enc[td.slot], L.x, L.y, L.z, v, live);
-#else
-            if (live && v[0] == 12345.f) g.g_enc[td.slot][0] = L.x;
-#endif
         }
         wait_mma(&bar_w, ph_w);  // dW1d has read H1 / X0 before the next tile
     }
@@ -862,8 +858,7 @@ void launch_field_forward_tc(const FieldArgs& a, uint8_t* feat, int32_t* rays, i
 }
 
 void launch_field_backward_tc(const FieldArgs& a, const FieldGradArgs& g, uint8_t* feat,
-                              int32_t* rays, float4* dfeat, int sms, cudaStream_t st,
-                              uint64_t* launches) {
+                              int32_t* rays, int sms, cudaStream_t st, uint64_t* launches) {
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(mlp_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kBwdSmem));
@@ -871,7 +866,7 @@ void launch_field_backward_tc(const FieldArgs& a, const FieldGradArgs& g, uint8_
     }
     // the feature tiles of the forward pass (same batch) are still resident;
     // the hash-table scatter is fused into the backward's last epilogue
-    mlp_bwd_kernel<<<sms * 2, 128, kBwdSmem, st>>>(a, g, feat, rays, dfeat);
+    mlp_bwd_kernel<<<sms * 2, 128, kBwdSmem, st>>>(a, g, feat, rays);
     *launches += 1;
 }
 

@@ -131,14 +131,10 @@ int launch_sampler(const RaygenArgs& a, RayRec* rays, float4* venc, uint32_t* co
                    uint32_t* P, uint32_t* block_sums, TileDesc* tiles, int max_tiles,
                    SampleArrays out, uint64_t capacity, Status* status, cudaStream_t st,
                    uint64_t* launches);
-void launch_field_forward(const FieldArgs& a, int grid, cudaStream_t st, uint64_t* launches);
-void launch_field_backward(const FieldArgs& a, const FieldGradArgs& g, int grid, cudaStream_t st,
-                           uint64_t* launches);
 void launch_field_forward_tc(const FieldArgs& a, uint8_t* feat, int32_t* rays, int sms,
                              cudaStream_t st, uint64_t* launches);
 void launch_field_backward_tc(const FieldArgs& a, const FieldGradArgs& g, uint8_t* feat,
-                              int32_t* rays, float4* dfeat, int sms, cudaStream_t st,
-                              uint64_t* launches);
+                              int32_t* rays, int sms, cudaStream_t st, uint64_t* launches);
 void launch_composite(const CompositeArgs& a, cudaStream_t st, uint64_t* launches);
 void launch_adam(const AdamArgs& a, uint64_t total, cudaStream_t st, uint64_t* launches);
 void launch_occupancy(const OccArgs& a, cudaStream_t st, uint64_t* launches);

@@ -164,9 +164,7 @@ struct tfg_ctx {
     int32_t* d_pixels = nullptr;
     uint8_t* d_feat = nullptr;    // bf16 feature tiles (4 KB per 128-sample tile)
     int32_t* d_tile_rays = nullptr;
-    float4* d_dfeat = nullptr;    // fp32 d(features) per tile row (training only)
     float4* d_export = nullptr;   // parity export of (d_sigma, d_rgb) in ray semantics
-    bool simt = false;            // bring-up switch: CUDA-core field kernels
     int cur_rays = 0;
     bool have_batch = false;
     bool fwd_done = false;  // feature tiles of the current batch are resident
@@ -577,11 +575,8 @@ FieldArgs field_args(tfg_ctx* c, const FieldPtrs& f) {
 int run_forward(tfg_ctx* c, const FieldPtrs& f) {
     PhaseScope ps(c, kPhFieldFwd);
     c->fwd_done = true;
-    if (c->simt)
-        launch_field_forward(field_args(c, f), 2 * c->sms, c->st, &c->launches);
-    else
-        launch_field_forward_tc(field_args(c, f), c->d_feat, c->d_tile_rays, c->sms, c->st,
-                                &c->launches);
+    launch_field_forward_tc(field_args(c, f), c->d_feat, c->d_tile_rays, c->sms, c->st,
+                            &c->launches);
     CK(cudaGetLastError());
     return 0;
 }
@@ -621,14 +616,8 @@ int run_backward(tfg_ctx* c) {
         g.g_dnet[k] = g.g_enc[k] + c->enc_n;
     }
     g.g_color = c->d_grads + c->color_off;
-    if (c->simt) {
-        launch_field_backward(field_args(c, train_ptrs(c)), g, c->sms, c->st, &c->launches);
-    } else {
-        if (!c->d_dfeat && dalloc(c, &c->d_dfeat, uint64_t(c->max_tiles) * 128 * 4))
-            return TFG_ERR_CUDA;
-        launch_field_backward_tc(field_args(c, train_ptrs(c)), g, c->d_feat, c->d_tile_rays,
-                                 c->d_dfeat, c->sms, c->st, &c->launches);
-    }
+    launch_field_backward_tc(field_args(c, train_ptrs(c)), g, c->d_feat, c->d_tile_rays,
+                             c->sms, c->st, &c->launches);
     CK(cudaGetLastError());
     return 0;
 }
@@ -760,7 +749,6 @@ TFG_API int tfg_create(const tfg_field_config* fcfg, const tfg_train_config* tcf
     }
     c->density_lim = std::log(fcfg->density_max);
     c->sample_cap = uint64_t(max_rays) * 128;
-    c->simt = getenv("TFG_FIELD_SIMT") != nullptr;
     c->max_tiles = int(c->sample_cap / 128 + kMaxSlots + 1);
     int rc = 0;
     CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
@@ -822,7 +810,7 @@ TFG_API int tfg_destroy(tfg_ctx* c) {
                    c->d_accept_n, c->d_view_start, c->d_union, c->d_crop4, c->d_rays, c->d_venc,
                    c->d_counts, c->d_P, c->d_tiles, c->s.local, c->s.td, c->s.endpoint, c->s.io,
                    c->d_ray_out, c->d_pixels, c->d_rparams, c->d_rbits, c->d_rcolor, c->d_rcam,
-                   c->d_feat, c->d_tile_rays, c->d_dfeat, c->d_export};
+                   c->d_feat, c->d_tile_rays, c->d_export};
     for (void* p : dev)
         if (p) cudaFree(p);
     stop_init_pool(c);
