@@ -1,0 +1,140 @@
+"""Summarises ncu outputs into profiles/ (launch-list shares, per-kernel key
+metrics, and profiles/traffic.json = measured DRAM bytes per launch of each
+bench kernel family, read by bench.py's roofline 'traffic' field).
+
+usage: python tools/summarize_profiles.py <launches.csv> <prof.ncu-rep> <tag>
+"""
+import collections
+import csv
+import io
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+FAMILY = {
+    "mlp_bwd_kernel": "field_bwd",
+    "mlp_fwd_kernel": "field_fwd",
+    "hash_fwd_kernel": "field_fwd",
+    "raygen_kernel": "sampler",
+    "write_kernel": "sampler",
+    "tiles_kernel": "sampler",
+    "scan_reduce_kernel": "sampler",
+    "scan_sums_kernel": "sampler",
+    "scan_apply_kernel": "sampler",
+    "composite_kernel": "composite",
+    "adam_kernel": "adam",
+    "grad_check_kernel": "adam",
+    "occupancy_kernel": "occupancy",
+    "accept_kernel": "accept",
+    "accept_scatter_kernel": "accept",
+}
+METRICS = [
+    "gpu__time_duration.sum",
+    "dram__bytes_read.sum",
+    "dram__bytes_write.sum",
+    "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+    "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+    "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+    "l1tex__throughput.avg.pct_of_peak_sustained_elapsed",
+    "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__warps_active.avg.pct_of_peak_sustained_active",
+    "smsp__issue_active.avg.pct_of_peak_sustained_active",
+    "launch__registers_per_thread",
+    "launch__occupancy_limit_shared_mem",
+]
+
+
+def short(name):
+    n = name.split("(")[0]
+    return n.split("::")[-1]
+
+
+def launches(path):
+    rows = list(csv.reader(open(path)))
+    hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
+    h = rows[hi]
+    ki, vi = h.index("Kernel Name"), h.index("Metric Value")
+    agg = collections.defaultdict(lambda: [0, 0.0])
+    for r in rows[hi + 1:]:
+        if len(r) <= vi:
+            continue
+        agg[short(r[ki])][0] += 1
+        agg[short(r[ki])][1] += float(r[vi].replace(",", ""))
+    return agg
+
+
+def raw(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    h, units = rows[0], rows[1]
+    res = collections.defaultdict(list)
+    for r in rows[2:]:
+        k = short(r[h.index("Kernel Name")])
+        d = {}
+        for m in METRICS:
+            if m in h:
+                v = r[h.index(m)]
+                u = units[h.index(m)]
+                try:
+                    x = float(v.replace(",", ""))
+                except ValueError:
+                    continue
+                if u == "Mbyte":
+                    x *= 1e6
+                elif u == "Kbyte":
+                    x *= 1e3
+                elif u == "Gbyte":
+                    x *= 1e9
+                elif u in ("msecond", "ms"):
+                    x *= 1e-3
+                elif u in ("usecond", "us"):
+                    x *= 1e-6
+                elif u in ("nsecond", "ns"):
+                    x *= 1e-9
+                d[m] = x
+        res[k].append(d)
+    return res
+
+
+def main():
+    lpath, rep, tag = sys.argv[1], sys.argv[2], sys.argv[3]
+    agg = launches(lpath)
+    tot = sum(v[1] for v in agg.values())
+    lines = [f"# ncu summary {tag}", "", "Launch list (`ncu --metrics gpu__time_duration.sum --clock-control none`,",
+             "`python bench.py --steps 2 --warmup 3 --no-render --no-cpu`; cold-cache, serialised:",
+             "compare shares, not absolute times).", "",
+             "| kernel | family | launches | ms/launch | share |", "|---|---|---|---|---|"]
+    for k, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
+        lines.append(f"| {k} | {FAMILY.get(k, '-')} | {n} | {t / 1e6 / n:.3f} | {100 * t / tot:.1f}% |")
+    r = raw(rep)
+    lines += ["", "Full captures (`ncu --set full --clock-control none`), one launch each:", "",
+              "| kernel | time ms | DRAM read MB | DRAM write MB | SM % | DRAM % | L2 % | L1 % | tensor % | warps % | issue % | regs |",
+              "|---|---|---|---|---|---|---|---|---|---|---|---|"]
+    traffic = collections.defaultdict(float)
+    for k, ds in r.items():
+        d = ds[0]
+        g = lambda m: d.get(m, float("nan"))
+        lines.append(f"| {k} | {g('gpu__time_duration.sum') * 1e3:.3f} | {g('dram__bytes_read.sum') / 1e6:.1f} | "
+                     f"{g('dram__bytes_write.sum') / 1e6:.1f} | {g('sm__throughput.avg.pct_of_peak_sustained_elapsed'):.1f} | "
+                     f"{g('gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed'):.1f} | "
+                     f"{g('lts__throughput.avg.pct_of_peak_sustained_elapsed'):.1f} | "
+                     f"{g('l1tex__throughput.avg.pct_of_peak_sustained_elapsed'):.1f} | "
+                     f"{g('sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active'):.1f} | "
+                     f"{g('sm__warps_active.avg.pct_of_peak_sustained_active'):.1f} | "
+                     f"{g('smsp__issue_active.avg.pct_of_peak_sustained_active'):.1f} | "
+                     f"{g('launch__registers_per_thread'):.0f} |")
+        fam = FAMILY.get(k)
+        if fam:
+            traffic[fam] += g("dram__bytes_read.sum") + g("dram__bytes_write.sum")
+    os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
+    with open(os.path.join(ROOT, "profiles", f"{tag}_summary.md"), "w") as f:
+        f.write("\n".join(lines) + "\n")
+    with open(os.path.join(ROOT, "profiles", "traffic.json"), "w") as f:
+        json.dump({k: v for k, v in traffic.items()}, f, indent=1)
+    print("\n".join(lines))
+
+
+if __name__ == "__main__":
+    main()
