@@ -38,26 +38,31 @@ __global__ void __launch_bounds__(256) composite_kernel(CompositeArgs a) {
         m += cnt[k];
     }
     const uint32_t FULL = 0xffffffffu;
-    // ---------------- forward
-    float T = 1.f, cr = 0.f, cg = 0.f, cb = 0.f, dep = 0.f, op = 0.f;
-    for (int q0 = 0; q0 < m; q0 += 32) {
-        int q = q0 + lane;
-        float sg = 0.f, de = 0.f, tt = 0.f;
-        float4 io = make_float4(0.f, 0.f, 0.f, 0.f);
+    // The first kCache chunks of 32 samples stay in registers between the
+    // forward and the backward sweep (rays have ~70 samples), longer rays
+    // re-read their tail.
+    constexpr int kCache = 4;
+    float4 cio[kCache];
+    float2 ctd[kCache];
+    uint64_t cpos[kCache];
+    auto fetch = [&](int q, float4& io, float2& td, uint64_t& pos) {
+        io = make_float4(0.f, 0.f, 0.f, 0.f);
+        td = make_float2(0.f, 0.f);
+        pos = 0;
         if (q < m) {
             int k = 0, rem = q;
             while (rem >= cnt[k]) { rem -= cnt[k]; ++k; }
-            uint64_t pos = uint64_t(base[k]) + rem;
+            pos = uint64_t(base[k]) + rem;
             io = a.s.io[pos];
-            float2 td = a.s.td[pos];
-            sg = io.x;
-            tt = td.x;
-            de = td.y;
+            td = a.s.td[pos];
         }
-        float alpha = 1.f - expf(-(sg * de));
+    };
+    // ---------------- forward
+    float T = 1.f, cr = 0.f, cg = 0.f, cb = 0.f, dep = 0.f, op = 0.f;
+    auto fwd_chunk = [&](const float4& io, const float2& td) {
+        float alpha = 1.f - expf(-(io.x * td.y));
         float keep = 1.f - alpha;
-        // inclusive product scan of keep
-        float incl = keep;
+        float incl = keep;  // inclusive product scan of (1 - alpha)
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             float y = __shfl_up_sync(FULL, incl, o);
@@ -69,9 +74,23 @@ __global__ void __launch_bounds__(256) composite_kernel(CompositeArgs a) {
         cr += w * io.y;
         cg += w * io.z;
         cb += w * io.w;
-        dep += w * tt;
+        dep += w * td.x;
         op += w;
         T *= __shfl_sync(FULL, incl, 31);
+    };
+#pragma unroll
+    for (int ci = 0; ci < kCache; ++ci) {
+        if (ci * 32 < m) {
+            fetch(ci * 32 + lane, cio[ci], ctd[ci], cpos[ci]);
+            fwd_chunk(cio[ci], ctd[ci]);
+        }
+    }
+    for (int q0 = kCache * 32; q0 < m; q0 += 32) {
+        float4 io;
+        float2 td;
+        uint64_t pos;
+        fetch(q0 + lane, io, td, pos);
+        fwd_chunk(io, td);
     }
     cr = warp_sum(cr);
     cg = warp_sum(cg);
@@ -95,19 +114,8 @@ __global__ void __launch_bounds__(256) composite_kernel(CompositeArgs a) {
     // ---------------- backward
     float T2 = 1.f, pr = 0.f, pg = 0.f, pb = 0.f;
     float Rbr = T * a.bg.x, Rbg = T * a.bg.y, Rbb = T * a.bg.z;
-    for (int q0 = 0; q0 < m; q0 += 32) {
-        int q = q0 + lane;
-        float sg = 0.f, de = 0.f;
-        float4 io = make_float4(0.f, 0.f, 0.f, 0.f);
-        uint64_t pos = 0;
-        if (q < m) {
-            int k = 0, rem = q;
-            while (rem >= cnt[k]) { rem -= cnt[k]; ++k; }
-            pos = uint64_t(base[k]) + rem;
-            io = a.s.io[pos];
-            de = a.s.td[pos].y;
-            sg = io.x;
-        }
+    auto bwd_chunk = [&](int q, const float4& io, const float2& td, uint64_t pos) {
+        float sg = io.x, de = td.y;
         float alpha = 1.f - expf(-(sg * de));
         float keep = 1.f - alpha;
         float incl = keep;
@@ -148,6 +156,16 @@ __global__ void __launch_bounds__(256) composite_kernel(CompositeArgs a) {
         pg += __shfl_sync(FULL, sgc, 31);
         pb += __shfl_sync(FULL, sbc, 31);
         T2 *= __shfl_sync(FULL, incl, 31);
+    };
+#pragma unroll
+    for (int ci = 0; ci < kCache; ++ci)
+        if (ci * 32 < m) bwd_chunk(ci * 32 + lane, cio[ci], ctd[ci], cpos[ci]);
+    for (int q0 = kCache * 32; q0 < m; q0 += 32) {
+        float4 io;
+        float2 td;
+        uint64_t pos;
+        fetch(q0 + lane, io, td, pos);
+        bwd_chunk(q0 + lane, io, td, pos);
     }
 }
 

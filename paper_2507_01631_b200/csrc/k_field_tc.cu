@@ -254,21 +254,27 @@ __device__ __forceinline__ void scatter_row(const HashLayout& hl, float* genc, f
 }
 
 // ------------------------------------------------------------------ K2b
-// smem: weights | X0 [128x16] | CIN [128x48] | A [128x64] (H1, then C2) | C1 [128x64]
-constexpr uint32_t kFwdSmem = kWeightsBytes + 4096 + 12288 + 16384 + 16384 + 128;
+// smem: weights | A [128x64] | B [128x64]; the five layers ping-pong:
+//   X0 (in B) -> H1 (A) -> CIN (B) -> C1 (A) -> C2 (B) -> rgb
+// (each buffer is overwritten only after the MMA reading it has completed),
+// 53 KB per CTA -> 4 resident CTAs per SM.
+constexpr uint32_t kFwdSmem = kWeightsBytes + 16384 + 16384 + 128;
 constexpr uint32_t kFwdTmemCols = 64;
 
-__global__ void __launch_bounds__(128) mlp_fwd_kernel(FieldArgs a, const uint8_t* __restrict__ feat,
+__global__ void __launch_bounds__(128, 4) mlp_fwd_kernel(FieldArgs a, const uint8_t* __restrict__ feat,
                                                       const int32_t* __restrict__ rays) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
     __shared__ uint64_t bar_mma, bar_ld;
     __shared__ uint32_t tmem_slot;
     uint8_t* p = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
     Weights W = carve_weights(p);
-    uint8_t* X0 = carve(p, 4096);
-    uint8_t* CIN = carve(p, 12288);
-    uint8_t* HA = carve(p, 16384);
-    uint8_t* C1 = carve(p, 16384);
+    uint8_t* BA = carve(p, 16384);
+    uint8_t* BB = carve(p, 16384);
+    uint8_t* X0 = BB;   // [128 x 16]
+    uint8_t* HA = BA;   // H1
+    uint8_t* CIN = BB;  // [128 x 48]
+    uint8_t* C1 = BA;
+    uint8_t* C2 = BB;
     const int r = threadIdx.x;
     if (r == 0) {
         umma::mbar_init(&bar_mma, 1);
@@ -420,14 +426,14 @@ __global__ void __launch_bounds__(128) mlp_fwd_kernel(FieldArgs a, const uint8_t
 #pragma unroll
             for (int i = 0; i < 64; ++i) v[i] = fmaxf(v[i] + W.bc2[i], 0.f);
 #pragma unroll
-            for (int c = 0; c < 8; ++c) st_chunk(HA, r, c, v + 8 * c);
+            for (int c = 0; c < 8; ++c) st_chunk(C2, r, c, v + 8 * c);
         }
         sync_for_mma();
         // ---- colour layer 3: [128x64] x Wc3^T -> 16 (3 real) -> sigmoid
         if (r == 0) {
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-                umma::mma(tmem, kmaj(HA, kT, k), kmaj(W.wc3, kWc3Rows, k), id16, k > 0);
+                umma::mma(tmem, kmaj(C2, kT, k), kmaj(W.wc3, kWc3Rows, k), id16, k > 0);
             umma::commit(&bar_mma);
         }
         wait_mma(&bar_mma, ph_mma);
@@ -848,11 +854,11 @@ void launch_field_forward_tc(const FieldArgs& a, uint8_t* feat, int32_t* rays, i
         attr = true;
     }
 #if TFG_FUSED_GATHER
-    mlp_fwd_kernel<<<sms * 3, 128, kFwdSmem, st>>>(a, feat, rays);
+    mlp_fwd_kernel<<<sms * 4, 128, kFwdSmem, st>>>(a, feat, rays);
     *launches += 1;
 #else
     hash_fwd_kernel<<<sms * 8, 128, 0, st>>>(a, feat, rays);
-    mlp_fwd_kernel<<<sms * 3, 128, kFwdSmem, st>>>(a, feat, rays);
+    mlp_fwd_kernel<<<sms * 4, 128, kFwdSmem, st>>>(a, feat, rays);  // 4 resident per SM
     *launches += 2;
 #endif
 }
