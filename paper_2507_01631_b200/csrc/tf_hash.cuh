@@ -15,32 +15,66 @@ struct Corner {
     uint32_t idx[8];
     float w[8];
 };
-__device__ __forceinline__ void hash_level(const HashLayout& hl, int l, float x, float y, float z,
-                                           Corner& c) {
-    int n = hl.res[l];
+
+// Level layout of the default FieldConfig (nn.hpp:14-45: N_min 16, N_max 256,
+// 8 levels, T = 2^15): resolutions, entry offsets; levels 0-1 are dense.
+// tfg_create checks the runtime HashLayout against these constants.
+constexpr int kRes[kLevels] = {16, 24, 35, 53, 78, 116, 172, 256};
+constexpr uint32_t kOff[kLevels] = {0, 4913, 20538, 53306, 86074, 118842, 151610, 184378};
+
+// HashGridT::cell_of + corner_entry (nn.hpp:248-266) for level L, with the
+// level constants folded: clamp to [0,1], scale, cell + fraction, 8 trilinear
+// weights ((wx*wy)*wz, the reference's product order) and entry indices
+// (dense x + n(y + n z), or the spatial hash x ^ y*2654435761 ^ z*805459861).
+template <int L>
+__device__ __forceinline__ void hash_level_c(float x, float y, float z, Corner& c) {
+    constexpr int n = kRes[L];
+    constexpr uint32_t n1 = uint32_t(n + 1);
+    constexpr bool dense = uint64_t(n1) * n1 * n1 <= uint64_t(kTable);
     float p[3] = {x, y, z};
-    int ci[3];
+    int q[3];
     float f[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-        float v = p[k];
-        v = v < 0.f ? 0.f : v;
-        v = v > 1.f ? 1.f : v;
+        float v = fminf(fmaxf(p[k], 0.f), 1.f);
         float sc = v * float(n);
-        int q = int(sc);
-        q = q > n - 1 ? n - 1 : q;
-        ci[k] = q;
-        f[k] = sc - float(q);
+        int ci = int(sc);
+        ci = ci > n - 1 ? n - 1 : ci;
+        q[k] = ci;
+        f[k] = sc - float(ci);
     }
-    uint32_t np1 = uint32_t(n + 1);
+    float wx[2] = {1.f - f[0], f[0]}, wy[2] = {1.f - f[1], f[1]}, wz[2] = {1.f - f[2], f[2]};
+    float wxy[4] = {wx[0] * wy[0], wx[1] * wy[0], wx[0] * wy[1], wx[1] * wy[1]};
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        int dx = k & 1, dy = (k >> 1) & 1, dz = (k >> 2) & 1;
-        c.w[k] = (dx ? f[0] : 1.f - f[0]) * (dy ? f[1] : 1.f - f[1]) * (dz ? f[2] : 1.f - f[2]);
-        uint32_t X = uint32_t(ci[0] + dx), Y = uint32_t(ci[1] + dy), Z = uint32_t(ci[2] + dz);
-        uint32_t e = hl.dense[l] ? X + np1 * (Y + np1 * Z)
-                                 : ((X ^ (Y * 2654435761u) ^ (Z * 805459861u)) & uint32_t(kTable - 1));
-        c.idx[k] = hl.off[l] + e;
+    for (int k = 0; k < 8; ++k) c.w[k] = wxy[k & 3] * wz[k >> 2];
+    if constexpr (dense) {
+        uint32_t base = kOff[L] + uint32_t(q[0]) + n1 * (uint32_t(q[1]) + n1 * uint32_t(q[2]));
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            c.idx[k] = base + uint32_t(k & 1) + n1 * uint32_t((k >> 1) & 1) + n1 * n1 * uint32_t(k >> 2);
+    } else {
+        uint32_t X = uint32_t(q[0]);
+        uint32_t hy0 = uint32_t(q[1]) * 2654435761u, hy1 = hy0 + 2654435761u;
+        uint32_t hz0 = uint32_t(q[2]) * 805459861u, hz1 = hz0 + 805459861u;
+        uint32_t hyz[4] = {hy0 ^ hz0, hy1 ^ hz0, hy0 ^ hz1, hy1 ^ hz1};
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            c.idx[k] = kOff[L] + (((X + uint32_t(k & 1)) ^ hyz[k >> 1]) & uint32_t(kTable - 1));
+    }
+}
+
+// Runtime-level form (the layout is the constant one above).
+__device__ __forceinline__ void hash_level(const HashLayout&, int l, float x, float y, float z,
+                                           Corner& c) {
+    switch (l) {
+    case 0: hash_level_c<0>(x, y, z, c); break;
+    case 1: hash_level_c<1>(x, y, z, c); break;
+    case 2: hash_level_c<2>(x, y, z, c); break;
+    case 3: hash_level_c<3>(x, y, z, c); break;
+    case 4: hash_level_c<4>(x, y, z, c); break;
+    case 5: hash_level_c<5>(x, y, z, c); break;
+    case 6: hash_level_c<6>(x, y, z, c); break;
+    default: hash_level_c<7>(x, y, z, c); break;
     }
 }
 

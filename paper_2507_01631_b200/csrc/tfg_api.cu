@@ -747,6 +747,17 @@ TFG_API int tfg_create(const tfg_field_config* fcfg, const tfg_train_config* tcf
         c->hl.dense[l] = dense <= uint64_t(kTable) ? 1 : 0;
         off += uint32_t(std::min<uint64_t>(dense, kTable));
     }
+    {
+        // the hash kernels fold the default level layout in as constants
+        const int res[kLevels] = {16, 24, 35, 53, 78, 116, 172, 256};
+        const uint32_t off[kLevels] = {0, 4913, 20538, 53306, 86074, 118842, 151610, 184378};
+        for (int l = 0; l < kLevels; ++l)
+            if (c->hl.res[l] != res[l] || c->hl.off[l] != off[l]) {
+                delete c;
+                return fail(TFG_ERR_INVALID, "create: hash-grid level layout differs from the "
+                                             "default FieldConfig the kernels are built for");
+            }
+    }
     c->density_lim = std::log(fcfg->density_max);
     c->sample_cap = uint64_t(max_rays) * 128;
     c->max_tiles = int(c->sample_cap / 128 + kMaxSlots + 1);
