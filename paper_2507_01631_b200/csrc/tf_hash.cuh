@@ -19,8 +19,13 @@ struct Corner {
 // Level layout of the default FieldConfig (nn.hpp:14-45: N_min 16, N_max 256,
 // 8 levels, T = 2^15): resolutions, entry offsets; levels 0-1 are dense.
 // tfg_create checks the runtime HashLayout against these constants.
-constexpr int kRes[kLevels] = {16, 24, 35, 53, 78, 116, 172, 256};
-constexpr uint32_t kOff[kLevels] = {0, 4913, 20538, 53306, 86074, 118842, 151610, 184378};
+__host__ __device__ constexpr int level_res_c(int l) {
+    return l == 0 ? 16 : l == 1 ? 24 : l == 2 ? 35 : l == 3 ? 53 : l == 4 ? 78 : l == 5 ? 116 : l == 6 ? 172 : 256;
+}
+__host__ __device__ constexpr uint32_t level_off_c(int l) {
+    return l == 0 ? 0u : l == 1 ? 4913u : l == 2 ? 20538u : l == 3 ? 53306u : l == 4 ? 86074u
+         : l == 5 ? 118842u : l == 6 ? 151610u : 184378u;
+}
 
 // HashGridT::cell_of + corner_entry (nn.hpp:248-266) for level L, with the
 // level constants folded: clamp to [0,1], scale, cell + fraction, 8 trilinear
@@ -28,7 +33,7 @@ constexpr uint32_t kOff[kLevels] = {0, 4913, 20538, 53306, 86074, 118842, 151610
 // (dense x + n(y + n z), or the spatial hash x ^ y*2654435761 ^ z*805459861).
 template <int L>
 __device__ __forceinline__ void hash_level_c(float x, float y, float z, Corner& c) {
-    constexpr int n = kRes[L];
+    constexpr int n = level_res_c(L);
     constexpr uint32_t n1 = uint32_t(n + 1);
     constexpr bool dense = uint64_t(n1) * n1 * n1 <= uint64_t(kTable);
     float p[3] = {x, y, z};
@@ -48,7 +53,7 @@ __device__ __forceinline__ void hash_level_c(float x, float y, float z, Corner& 
 #pragma unroll
     for (int k = 0; k < 8; ++k) c.w[k] = wxy[k & 3] * wz[k >> 2];
     if constexpr (dense) {
-        uint32_t base = kOff[L] + uint32_t(q[0]) + n1 * (uint32_t(q[1]) + n1 * uint32_t(q[2]));
+        uint32_t base = level_off_c(L) + uint32_t(q[0]) + n1 * (uint32_t(q[1]) + n1 * uint32_t(q[2]));
 #pragma unroll
         for (int k = 0; k < 8; ++k)
             c.idx[k] = base + uint32_t(k & 1) + n1 * uint32_t((k >> 1) & 1) + n1 * n1 * uint32_t(k >> 2);
@@ -59,7 +64,7 @@ __device__ __forceinline__ void hash_level_c(float x, float y, float z, Corner& 
         uint32_t hyz[4] = {hy0 ^ hz0, hy1 ^ hz0, hy0 ^ hz1, hy1 ^ hz1};
 #pragma unroll
         for (int k = 0; k < 8; ++k)
-            c.idx[k] = kOff[L] + (((X + uint32_t(k & 1)) ^ hyz[k >> 1]) & uint32_t(kTable - 1));
+            c.idx[k] = level_off_c(L) + (((X + uint32_t(k & 1)) ^ hyz[k >> 1]) & uint32_t(kTable - 1));
     }
 }
 
