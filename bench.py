@@ -257,6 +257,7 @@ def run_ours(args):
     for i in range(e2e_steps):
         if i % 4 == 0:
             ctx.set_window(*path[(i // 4) % len(path)])
+            ctx.prefetch_window(*path[(i // 4 + 1) % len(path)])  # staged on the side stream
         ctx.forward_backward(10_000 + i, rank * B, B)
         if world > 1:
             dist.all_reduce(grads)

@@ -282,11 +282,13 @@ __global__ void __launch_bounds__(128) raygen_kernel(RaygenArgs a, RayRec* __res
         row = a.pixels[3 * ii + 1];
         col = a.pixels[3 * ii + 2];
     } else {
+        uint64_t na = *a.n_accept_dev;
         Rng r(hash_combine(hash_combine(hash_combine(a.seed, kPurposePixels), a.iter), g));
-        uint64_t e = a.accept[r.below(a.n_accept)];
+        uint64_t e = na ? a.accept[r.below(na)] : 0;
         v = int(e >> 40);
         row = int((e >> 20) & 0xFFFFF);
         col = int(e & 0xFFFFF);
+        if (na == 0 && valid && hi == 0) atomicOr(&status->bits, kStatusRayFail);
     }
     double gx = 0.0, gy = 0.0;
     int st = rpc_localize(a.cams[v], double(row), double(col), hi ? a.z_min : a.z_max, &gx, &gy);

@@ -43,7 +43,7 @@ struct AcceptArgs {
 struct RaygenArgs {
     const tfg_rpc* cams;
     const uint64_t* accept;  // draw mode: accepted list
-    uint64_t n_accept;
+    const uint32_t* n_accept_dev;  // its length, read on device (no host sync per move)
     const int32_t* pixels;   // pixel mode (render/eval): view,row,col triplets
     const uint8_t* crop_bytes;
     const int* crop_rect;        // r0, c0, cols, rows per view

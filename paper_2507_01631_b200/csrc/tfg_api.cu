@@ -91,6 +91,18 @@ enum Phase { kPhSampler, kPhFieldFwd, kPhComposite, kPhFieldBwd, kPhAdam, kPhOcc
 const char* kPhaseNames[kNumPhases] = {"sampler", "field_fwd", "composite", "field_bwd",
                                        "adam", "occupancy", "accept"};
 
+struct WinBuf {
+    uint8_t* d_crops = nullptr;      // per-view union crop, u8 RGB
+    int* d_crop_rect = nullptr;      // r0, c0, cols, rows per view
+    uint64_t* d_crop_off = nullptr;  // byte offset of each view's crop
+    uint64_t* d_accept = nullptr;    // packed (view, row, col)
+    uint32_t* d_n = nullptr;         // accepted count (read by the ray draw on device)
+    std::vector<int> h_crop_rect;
+    std::vector<uint64_t> h_crop_off;
+    int pos_r = -1, pos_c = -1;
+    cudaEvent_t ready = nullptr;
+};
+
 struct Crop {
     int r0 = 0, r1 = 0, c0 = 0, c1 = 0;
     bool empty() const { return r0 >= r1 || c0 >= c1; }
@@ -140,19 +152,16 @@ struct tfg_ctx {
     int slot_tile[kTrainSlots] = {-1, -1, -1, -1};
     SlotTable slots{};
 
-    // crops + accept list
-    uint8_t* d_crops = nullptr;
-    uint64_t crop_cap = 0;
-    int* d_crop_rect = nullptr;        // r0, c0, cols, rows per view
-    uint64_t* d_crop_off = nullptr;
-    std::vector<int> h_crop_rect;
-    std::vector<uint64_t> h_crop_off;
-    uint64_t* d_accept = nullptr;
-    uint64_t accept_cap = 0, cand_cap = 0;
-    uint32_t *d_flags = nullptr, *d_pos = nullptr, *d_block_sums = nullptr, *d_accept_n = nullptr;
+    // per-window staging (crops + accepted-ray list), double buffered so the
+    // next position can be staged on the side stream while this one trains
+    WinBuf win[2];
+    int front = 0;
+    cudaEvent_t ev_swap = nullptr;  // main-stream point after which the back buffer is free
+    uint64_t crop_cap = 0, accept_cap = 0, cand_cap = 0;
+    // accepted-list build scratch (one build at a time)
+    uint32_t *d_flags = nullptr, *d_pos = nullptr, *d_block_sums = nullptr, *d_acc_sums = nullptr;
     uint64_t* d_view_start = nullptr;
     int *d_union = nullptr, *d_crop4 = nullptr;
-    uint64_t n_accept = 0;
 
     // batch
     RayRec* d_rays = nullptr;
@@ -443,9 +452,36 @@ int run_occupancy(tfg_ctx* c, bool update, uint64_t* keys) {
     return 0;
 }
 
-int build_accept(tfg_ctx* c, const std::vector<Crop>& crops, const std::vector<Crop>& uni) {
+// Stages window position (pr, pc) into w on `st`: the union crop of each
+// view (2D copies from the pinned images) and the accepted-ray list
+// (SPEC.md:437-445).  Independent of the slot assignment.
+int stage_window(tfg_ctx* c, WinBuf& w, int pr, int pc, cudaStream_t st) {
+    std::vector<int> want = window_tiles(c, pr, pc);
+    std::vector<Crop> crops, uni;
+    window_crops(c, want, crops, uni);
+    w.h_crop_rect.assign(4 * c->n_views, 0);
+    w.h_crop_off.assign(c->n_views, 0);
+    uint64_t off = 0;
+    for (int v = 0; v < c->n_views; ++v) {
+        const Crop& u = uni[v];
+        w.h_crop_off[v] = off;
+        if (u.empty()) continue;
+        int cw = u.c1 - u.c0, ch = u.r1 - u.r0;
+        w.h_crop_rect[4 * v] = u.r0;
+        w.h_crop_rect[4 * v + 1] = u.c0;
+        w.h_crop_rect[4 * v + 2] = cw;
+        w.h_crop_rect[4 * v + 3] = ch;
+        const uint8_t* src = c->h_images[v] + 3 * (size_t(u.r0) * c->cams[v].image_cols + u.c0);
+        c->h2d_bytes += uint64_t(cw) * 3 * ch;
+        CK(cudaMemcpy2DAsync(w.d_crops + off, size_t(cw) * 3, src, size_t(c->cams[v].image_cols) * 3,
+                             size_t(cw) * 3, ch, cudaMemcpyHostToDevice, st));
+        off += uint64_t(cw) * ch * 3;
+    }
+    CK(cudaMemcpyAsync(w.d_crop_rect, w.h_crop_rect.data(), 4 * c->n_views * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(w.d_crop_off, w.h_crop_off.data(), c->n_views * 8, cudaMemcpyHostToDevice, st));
+    // accepted-ray list
     std::vector<uint64_t> vs(c->n_views);
-    std::vector<int> urect(4 * c->n_views), crect(4 * c->n_views * kTrainSlots);
+    std::vector<int> urect(4 * c->n_views), crect(4 * c->n_views * kTrainSlots, 0);
     uint64_t n = 0;
     for (int v = 0; v < c->n_views; ++v) {
         vs[v] = n;
@@ -466,9 +502,10 @@ int build_accept(tfg_ctx* c, const std::vector<Crop>& crops, const std::vector<C
         }
     }
     if (n > c->cand_cap) return fail(TFG_ERR_INVALID, "accept: candidate capacity exceeded");
-    CK(cudaMemcpyAsync(c->d_view_start, vs.data(), vs.size() * 8, cudaMemcpyHostToDevice, c->st));
-    CK(cudaMemcpyAsync(c->d_union, urect.data(), urect.size() * 4, cudaMemcpyHostToDevice, c->st));
-    CK(cudaMemcpyAsync(c->d_crop4, crect.data(), crect.size() * 4, cudaMemcpyHostToDevice, c->st));
+    // synchronous pageable copies: the host vectors may go out of scope
+    CK(cudaMemcpyAsync(c->d_view_start, vs.data(), vs.size() * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(c->d_union, urect.data(), urect.size() * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(c->d_crop4, crect.data(), crect.size() * 4, cudaMemcpyHostToDevice, st));
     AcceptArgs a{};
     a.cams = c->d_cams;
     a.n_views = c->n_views;
@@ -480,21 +517,27 @@ int build_accept(tfg_ctx* c, const std::vector<Crop>& crops, const std::vector<C
     a.north = c->d_north;
     a.grid_rows = c->rows;
     a.grid_cols = c->cols;
-    for (int k = 0; k < kTrainSlots; ++k) a.loaded_tile[k] = k < c->nslots ? c->slot_tile[k] : -1;
-    a.n_loaded = c->nslots;
+    for (int k = 0; k < kTrainSlots; ++k) a.loaded_tile[k] = k < int(want.size()) ? want[k] : -1;
+    a.n_loaded = int(want.size());
     a.z_min = c->roi.z_min;
     a.z_max = c->roi.z_max;
-    PhaseScope ps(c, kPhAccept);
-    if (launch_accept(a, c->d_flags, c->d_pos, c->d_block_sums, c->d_accept_n, c->d_accept, c->st,
-                      &c->launches))
+    if (launch_accept(a, c->d_flags, c->d_pos, c->d_acc_sums, w.d_n, w.d_accept, st, &c->launches))
         return fail(TFG_ERR_INVALID, "accept: scan capacity exceeded");
     CK(cudaGetLastError());
-    uint32_t nacc = 0;
-    CK(cudaMemcpyAsync(&c->h_status->pad, c->d_accept_n, 4, cudaMemcpyDeviceToHost, c->st));
-    CK(cudaStreamSynchronize(c->st));
-    nacc = c->h_status->pad;
-    c->n_accept = nacc;
+    CK(cudaEventRecord(w.ready, st));
+    w.pos_r = pr;
+    w.pos_c = pc;
     return 0;
+}
+
+uint64_t read_accept_count(tfg_ctx* c) {
+    uint32_t n = 0;
+    if (cudaMemcpyAsync(&c->h_status->pad, c->win[c->front].d_n, 4, cudaMemcpyDeviceToHost, c->st) !=
+            cudaSuccess ||
+        cudaStreamSynchronize(c->st) != cudaSuccess)
+        return 0;
+    n = c->h_status->pad;
+    return n;
 }
 
 int check_status(tfg_ctx* c) {
@@ -503,7 +546,9 @@ int check_status(tfg_ctx* c) {
         return fail(TFG_ERR_INVALID, "sample: batch exceeds the sample capacity of the context");
     if (s.bits & kStatusSegOverflow) return fail(TFG_ERR_INVALID, "sample: more than 8 segments");
     if (s.bits & kStatusRayFail)
-        return fail(TFG_ERR_INVALID, "sample: ray_from_pixel failed for a drawn pixel");
+        return fail(TFG_ERR_INVALID,
+                    "sample: ray generation failed (ray_from_pixel threw for a drawn pixel, or the "
+                    "window's accepted-ray list is empty)");
     if (s.bits & kStatusNonFinite) {
         int g = int(s.nonfinite_group);
         char nm[96];
@@ -538,9 +583,10 @@ RaygenArgs base_raygen(tfg_ctx* c) {
     a.delta_cap = c->tc.delta_cap;
     a.slots = c->slots;
     for (int k = 0; k < c->nslots; ++k) a.occ_bits[k] = c->d_bits + uint64_t(k) * kOccWords;
-    a.crop_bytes = c->d_crops;
-    a.crop_rect = c->d_crop_rect;
-    a.crop_offset = c->d_crop_off;
+    const WinBuf& w = c->win[c->front];
+    a.crop_bytes = w.d_crops;
+    a.crop_rect = w.d_crop_rect;
+    a.crop_offset = w.d_crop_off;
     return a;
 }
 
@@ -766,6 +812,8 @@ TFG_API int tfg_create(const tfg_field_config* fcfg, const tfg_train_config* tcf
     CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&c->ev_main, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->ev_side, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->ev_swap, cudaEventDisableTiming));
+    CK(cudaEventRecord(c->ev_swap, c->st));
     rc |= dalloc(c, &c->d_params, c->n_params);
     rc |= dalloc(c, &c->d_grads, c->n_params);
     rc |= dalloc(c, &c->d_m, c->n_params);
@@ -788,7 +836,7 @@ TFG_API int tfg_create(const tfg_field_config* fcfg, const tfg_train_config* tcf
     rc |= dalloc(c, &c->d_feat, uint64_t(c->max_tiles) * 4096);
     rc |= dalloc(c, &c->d_tile_rays, uint64_t(c->max_tiles) * 128);
     rc |= dalloc(c, &c->d_block_sums, 4096 + 64);
-    rc |= dalloc(c, &c->d_accept_n, 1);
+    rc |= dalloc(c, &c->d_acc_sums, 4096 + 64);
     rc |= dalloc(c, &c->d_rcam, 1);
     if (rc) {
         delete c;
@@ -816,9 +864,9 @@ TFG_API int tfg_destroy(tfg_ctx* c) {
     cudaSetDevice(c->device);
     cudaDeviceSynchronize();
     void* dev[] = {c->d_params, c->d_grads, c->d_m, c->d_v, c->d_ema, c->d_bits, c->d_group_flags,
-                   c->d_status, c->d_cams, c->d_east, c->d_north, c->d_crops, c->d_crop_rect,
-                   c->d_crop_off, c->d_accept, c->d_flags, c->d_pos, c->d_block_sums,
-                   c->d_accept_n, c->d_view_start, c->d_union, c->d_crop4, c->d_rays, c->d_venc,
+                   c->d_status, c->d_cams, c->d_east, c->d_north, c->d_flags, c->d_pos,
+                   c->d_block_sums, c->d_acc_sums, c->d_view_start, c->d_union, c->d_crop4,
+                   c->d_rays, c->d_venc,
                    c->d_counts, c->d_P, c->d_tiles, c->s.local, c->s.td, c->s.endpoint, c->s.io,
                    c->d_ray_out, c->d_pixels, c->d_rparams, c->d_rbits, c->d_rcolor, c->d_rcam,
                    c->d_feat, c->d_tile_rays, c->d_export};
@@ -829,6 +877,13 @@ TFG_API int tfg_destroy(tfg_ctx* c) {
     for (auto* im : c->h_images)
         if (im) cudaFreeHost(im);
     if (c->h_status) cudaFreeHost(c->h_status);
+    for (WinBuf& w : c->win) {
+        void* wo[] = {w.d_crops, w.d_crop_rect, w.d_crop_off, w.d_accept, w.d_n};
+        for (void* p : wo)
+            if (p) cudaFree(p);
+        if (w.ready) cudaEventDestroy(w.ready);
+    }
+    if (c->ev_swap) cudaEventDestroy(c->ev_swap);
     if (c->ev_main) cudaEventDestroy(c->ev_main);
     if (c->ev_side) cudaEventDestroy(c->ev_side);
     if (c->side) cudaStreamDestroy(c->side);
@@ -912,17 +967,25 @@ TFG_API int tfg_set_scene(tfg_ctx* c, const tfg_rpc* cams, int n_views,
     c->accept_cap = cand;
     c->crop_cap = cropb;
     int rc = 0;
-    void* olds[] = {c->d_cams, c->d_east, c->d_north, c->d_crops, c->d_crop_rect, c->d_crop_off,
-                    c->d_accept, c->d_flags, c->d_pos, c->d_view_start, c->d_union, c->d_crop4};
+    void* olds[] = {c->d_cams, c->d_east, c->d_north, c->d_flags, c->d_pos, c->d_view_start,
+                    c->d_union, c->d_crop4};
     for (void* p : olds)
         if (p) cudaFree(p);
     rc |= dalloc(c, &c->d_cams, n_views);
     rc |= dalloc(c, &c->d_east, grid_cols + 1);
     rc |= dalloc(c, &c->d_north, grid_rows + 1);
-    rc |= dalloc(c, &c->d_crops, c->crop_cap);
-    rc |= dalloc(c, &c->d_crop_rect, 4 * n_views);
-    rc |= dalloc(c, &c->d_crop_off, n_views);
-    rc |= dalloc(c, &c->d_accept, c->accept_cap);
+    for (WinBuf& w : c->win) {
+        void* wo[] = {w.d_crops, w.d_crop_rect, w.d_crop_off, w.d_accept, w.d_n};
+        for (void* p : wo)
+            if (p) cudaFree(p);
+        rc |= dalloc(c, &w.d_crops, c->crop_cap);
+        rc |= dalloc(c, &w.d_crop_rect, 4 * n_views);
+        rc |= dalloc(c, &w.d_crop_off, n_views);
+        rc |= dalloc(c, &w.d_accept, c->accept_cap);
+        rc |= dalloc(c, &w.d_n, 1);
+        if (!w.ready) CK(cudaEventCreateWithFlags(&w.ready, cudaEventDisableTiming));
+        w.pos_r = w.pos_c = -1;
+    }
     rc |= dalloc(c, &c->d_flags, c->cand_cap);
     rc |= dalloc(c, &c->d_pos, c->cand_cap + 1);
     rc |= dalloc(c, &c->d_view_start, n_views);
@@ -1022,54 +1085,40 @@ TFG_API int tfg_set_window(tfg_ctx* c, int pr, int pc) {
     c->pos_r = pr;
     c->pos_c = pc;
     fill_slots(c);
-    // crops of the new window: union rect per view, 2D copies from pinned images
-    std::vector<Crop> crops, uni;
-    window_crops(c, want, crops, uni);
-    // crop rects are indexed by slot for the accept kernel
-    std::vector<Crop> by_slot(crops.size());
-    for (int v = 0; v < c->n_views; ++v)
-        for (int s = 0; s < ns; ++s)
-            for (int k = 0; k < ns; ++k)
-                if (want[k] == next[s]) by_slot[size_t(v) * kTrainSlots + s] = crops[size_t(v) * kTrainSlots + k];
-    c->h_crop_rect.assign(4 * c->n_views, 0);
-    c->h_crop_off.assign(c->n_views, 0);
-    uint64_t off = 0;
-    for (int v = 0; v < c->n_views; ++v) {
-        const Crop& u = uni[v];
-        c->h_crop_off[v] = off;
-        if (u.empty()) continue;
-        int w = u.c1 - u.c0, h = u.r1 - u.r0;
-        c->h_crop_rect[4 * v] = u.r0;
-        c->h_crop_rect[4 * v + 1] = u.c0;
-        c->h_crop_rect[4 * v + 2] = w;
-        c->h_crop_rect[4 * v + 3] = h;
-        const uint8_t* src = c->h_images[v] + 3 * (size_t(u.r0) * c->cams[v].image_cols + u.c0);
-        c->h2d_bytes += uint64_t(w) * 3 * h;
-        CK(cudaMemcpy2DAsync(c->d_crops + off, size_t(w) * 3, src, size_t(c->cams[v].image_cols) * 3,
-                             size_t(w) * 3, h, cudaMemcpyHostToDevice, c->side));
-        off += uint64_t(w) * h * 3;
+    // window crops + accepted-ray list: use the prefetched back buffer when it
+    // holds this position, else stage it now
+    WinBuf& back = c->win[c->front ^ 1];
+    if (back.pos_r != pr || back.pos_c != pc) {
+        CK(cudaStreamWaitEvent(c->side, c->ev_swap, 0));
+        int rc = stage_window(c, back, pr, pc, c->side);
+        if (rc) return rc;
     }
-    CK(cudaMemcpyAsync(c->d_crop_rect, c->h_crop_rect.data(), 4 * c->n_views * 4,
-                       cudaMemcpyHostToDevice, c->side));
-    CK(cudaMemcpyAsync(c->d_crop_off, c->h_crop_off.data(), c->n_views * 8, cudaMemcpyHostToDevice,
-                       c->side));
     CK(cudaEventRecord(c->ev_side, c->side));
     CK(cudaStreamWaitEvent(c->st, c->ev_side, 0));
+    CK(cudaStreamWaitEvent(c->st, back.ready, 0));
+    c->front ^= 1;
+    // kernels issued from here on use the new front; the old one may be restaged
+    CK(cudaEventRecord(c->ev_swap, c->st));
     // host steps of the slots are kept in the tile records (never reset)
     if (run_occupancy(c, false, nullptr)) return TFG_ERR_CUDA;
-    int rc = build_accept(c, by_slot, uni);
     c->have_batch = false;
-    return rc;
+    return 0;
 }
 
+// Stages the next window position (crops + accepted-ray list) into the back
+// buffer on the side stream while the current position trains; the entering
+// tiles' host records are materialised by the init pool.
 TFG_API int tfg_prefetch_window(tfg_ctx* c, int pr, int pc) {
-    // Host records of the next window's tiles are materialised (fresh init)
-    // ahead of the move so the move itself only issues copies.
-    if (!c) return fail(TFG_ERR_INVALID, "prefetch_window: null context");
+    if (!c || c->n_views == 0) return fail(TFG_ERR_STATE, "prefetch_window: call set_scene first");
+    CK(cudaSetDevice(c->device));
     bool single = (c->rows == 1 && c->cols == 1);
-    for (int ti : window_tiles(c, single ? 0 : pr, single ? 0 : pc))
-        if (ensure_record(c, ti)) return TFG_ERR_CUDA;
-    return 0;
+    if (!single && (pr < 0 || pc < 0 || pr + 1 >= c->rows || pc + 1 >= c->cols))
+        return fail(TFG_ERR_INVALID, "prefetch_window: position outside the (H-1)x(W-1) lattice");
+    WinBuf& back = c->win[c->front ^ 1];
+    if (back.pos_r == pr && back.pos_c == pc) return 0;
+    back.pos_r = back.pos_c = -1;
+    CK(cudaStreamWaitEvent(c->side, c->ev_swap, 0));
+    return stage_window(c, back, pr, pc, c->side);
 }
 
 TFG_API int tfg_window_tiles(tfg_ctx* c, int32_t* r4, int32_t* c4) {
@@ -1083,13 +1132,13 @@ TFG_API int tfg_window_tiles(tfg_ctx* c, int32_t* r4, int32_t* c4) {
 
 TFG_API int tfg_accept_count(tfg_ctx* c, uint64_t* n) {
     if (!c) return fail(TFG_ERR_INVALID, "accept_count: null context");
-    *n = c->n_accept;
+    *n = c->nslots ? read_accept_count(c) : 0;
     return 0;
 }
 
 TFG_API int tfg_accept_export(tfg_ctx* c, uint64_t* out, uint64_t cap) {
-    uint64_t n = std::min(cap, c->n_accept);
-    CK(cudaMemcpyAsync(out, c->d_accept, n * 8, cudaMemcpyDeviceToHost, c->st));
+    uint64_t n = std::min(cap, read_accept_count(c));
+    CK(cudaMemcpyAsync(out, c->win[c->front].d_accept, n * 8, cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
     return 0;
 }
@@ -1098,11 +1147,11 @@ TFG_API int tfg_accept_export(tfg_ctx* c, uint64_t* out, uint64_t cap) {
 TFG_API int tfg_sample(tfg_ctx* c, uint64_t iter, uint64_t ray_begin, int n_rays, int jitter,
                        uint64_t* n_samples) {
     if (!c || c->nslots == 0) return fail(TFG_ERR_STATE, "sample: call set_window first");
-    if (c->n_accept == 0) return fail(TFG_ERR_STATE, "sample: empty accepted-ray list");
+
     CK(cudaSetDevice(c->device));
     RaygenArgs a = base_raygen(c);
-    a.accept = c->d_accept;
-    a.n_accept = c->n_accept;
+    a.accept = c->win[c->front].d_accept;
+    a.n_accept_dev = c->win[c->front].d_n;
     a.iter = iter;
     a.ray_begin = ray_begin;
     a.n_rays = n_rays;
@@ -1455,8 +1504,8 @@ TFG_API int tfg_get_memory_report(tfg_ctx* c, tfg_memory_report* o) {
     o->tile_params = kTrainSlots * c->stride * 4;
     o->optimizer_moments = 2 * kTrainSlots * c->stride * 4 + kTrainSlots * c->stride * 4;  // m, v, grads
     o->occupancy = uint64_t(kTrainSlots) * kOccVox * 4 + uint64_t(kMaxSlots) * kOccWords * 4;
-    o->crops = c->crop_cap;
-    o->accept_list = c->accept_cap * 8 + c->cand_cap * 8;
+    o->crops = 2 * c->crop_cap;
+    o->accept_list = 2 * c->accept_cap * 8 + c->cand_cap * 8;
     o->batch_buffers = uint64_t(c->max_rays) * (sizeof(RayRec) + 96 + 8 * kMaxSlots + 20 + 12) +
                        c->sample_cap * (16 + 8 + 1 + 16);
     o->color_net = (c->n_params - c->color_off) * 4;

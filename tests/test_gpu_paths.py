@@ -89,9 +89,12 @@ def test_snake_progression_bit_exact_and_constant_memory():
     ses = Session(Oracle(), scene, fc, tc, workers=8)
     mem = None
     visits = {}
-    for it, pos in enumerate(snake_path(4, 4)):
+    path = snake_path(4, 4)
+    for it, pos in enumerate(path):
         ctx.set_window(*pos)
         ses.set_window(*pos)
+        if it % 2 == 0 and it + 1 < len(path):
+            ctx.prefetch_window(*path[it + 1])  # every other move uses the staged buffer
         assert ctx.window_tiles() == ses.window_tiles()
         np.testing.assert_array_equal(ctx.accept_list(), ses.build_accept())
         assert ctx.sample(it, 0, 1024, True) == ses.sample(it, 0, 1024, True)
