@@ -246,7 +246,9 @@ def run_ours(args):
 
     # ---- end to end through the public API with host buffers: window slides
     # (pinned host <-> HBM tile state + crops), accepted-list rebuilds, loss
-    # readback every step; the window moves every 4 iterations along the snake.
+    # readback every step; the window moves every `move_every` iterations
+    # along the snake (default 16 = the occupancy interval; the paper trains
+    # hundreds of iterations per position, so this over-weights the slide).
     path = snake_path(scene.grid_rows, scene.grid_cols)
     h0, d0 = ctx.copy_bytes()
     if world > 1:
@@ -255,9 +257,10 @@ def run_ours(args):
     t0 = time.perf_counter()
     e2e_steps = args.steps
     for i in range(e2e_steps):
-        if i % 4 == 0:
-            ctx.set_window(*path[(i // 4) % len(path)])
-            ctx.prefetch_window(*path[(i // 4 + 1) % len(path)])  # staged on the side stream
+        if i % args.move_every == 0:
+            k = i // args.move_every
+            ctx.set_window(*path[k % len(path)])
+            ctx.prefetch_window(*path[(k + 1) % len(path)])  # staged on the side stream
         ctx.forward_backward(10_000 + i, rank * B, B)
         if world > 1:
             dist.all_reduce(grads)
@@ -271,7 +274,7 @@ def run_ours(args):
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e = {"value": world * B * e2e_steps / float(te.item()), "unit": UNIT,
            "h2d_bytes_per_step": (h1 - h0) // e2e_steps, "d2h_bytes_per_step": (d1 - d0) // e2e_steps,
-           "window_move_every": 4}
+           "window_move_every": args.move_every, "window_moves": (e2e_steps + args.move_every - 1) // args.move_every}
 
     # ---- render (config 4: 4x4-tile ROI, random-init weights, occupancy all on)
     render = None
@@ -353,6 +356,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-render", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--move-every", type=int, default=16, help="e2e: iterations per window position")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
