@@ -125,6 +125,10 @@ def cpu_baseline(scene, n_rays: int, steps: int, warmup: int):
 
 
 def run_reference(args):
+    """The reference arm: the CPU oracle trainer (restated reference algorithm,
+    primitives pinned bit-for-bit to the reference sources) on all host cores,
+    exactly --steps timed iterations after --warmup, each a bounded 2048-ray
+    sample of the same workload.  Under torchrun only rank 0 runs."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
@@ -132,9 +136,9 @@ def run_reference(args):
 
     scene = synth.config_scene(5, seed=0)
     n = 2048
-    cb = cpu_baseline(scene, n, max(args.steps // 4, 2), 1)
+    cb = cpu_baseline(scene, n, args.steps, args.warmup)
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus,
-            "steps": max(args.steps // 4, 2), "warmup": 1, "higher_is_better": True, "scaling": "weak",
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": "cfg5 6x6 grid, 2x2 window at (2,2), 16 views ~1650^2 px, bounded ray sample",
                        "rays_per_step": n},
