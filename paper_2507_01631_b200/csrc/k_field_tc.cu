@@ -118,34 +118,6 @@ __device__ __forceinline__ void st_chunk(uint8_t* buf, int r, int c, const float
     *reinterpret_cast<uint4*>(buf + c * kChunk + (r >> 3) * 128 + (r & 7) * 16) = q;
 }
 
-// Same chunk to the smem tile and (training) to its copy in global memory.
-__device__ __forceinline__ void st_chunk2(uint8_t* buf, uint8_t* gbuf, int r, int c, const float* v) {
-    uint4 q = make_uint4(pack2(v[0], v[1]), pack2(v[2], v[3]), pack2(v[4], v[5]), pack2(v[6], v[7]));
-    uint32_t o = c * kChunk + (r >> 3) * 128 + (r & 7) * 16;
-    *reinterpret_cast<uint4*>(buf + o) = q;
-    if (gbuf) *reinterpret_cast<uint4*>(gbuf + o) = q;
-}
-// ReLU mask of a row of a 64-wide bf16 tile (value > 0).
-__device__ __forceinline__ void row_mask(const uint8_t* buf, int r, uint32_t* m) {
-    m[0] = m[1] = 0;
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-        uint4 q = *reinterpret_cast<const uint4*>(buf + c * kChunk + (r >> 3) * 128 + (r & 7) * 16);
-        uint32_t w[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            // bf16 pair: positive iff sign clear and not +0
-            uint32_t lo = w[j] & 0xFFFFu, hi = w[j] >> 16;
-            int i = 8 * c + 2 * j;
-            m[i >> 5] |= ((lo != 0 && !(lo & 0x8000u)) ? 1u : 0u) << (i & 31);
-            m[(i + 1) >> 5] |= ((hi != 0 && !(hi & 0x8000u)) ? 1u : 0u) << ((i + 1) & 31);
-        }
-    }
-}
-
-// Forward activations kept for the backward: per tile [H1 16K | CIN 12K | C1 16K | C2 16K].
-constexpr uint32_t kActH1 = 0, kActCIN = 16384, kActC1 = 28672, kActC2 = 45056, kActsTile = 61440;
-
 // Descriptors for the chunk-major tiles (see umma.cuh).
 __device__ __forceinline__ uint64_t kmaj(const uint8_t* base, uint32_t rows, int kstep) {
     // rows x K tile read K-major; kstep-th group of 16 K columns
@@ -320,7 +292,6 @@ __global__ void __launch_bounds__(128, 4) mlp_fwd_kernel(FieldArgs a, const uint
     const uint32_t id16 = umma::idesc_bf16(128, 16, 0, 0);
     for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
         TileDesc td = a.tiles[t];
-        uint8_t* gact = a.acts ? a.acts + uint64_t(t) * kActsTile : nullptr;
         if (td.slot != cur) {
             stage_density(W, a.f.dnet[td.slot]);
             cur = td.slot;
@@ -386,7 +357,7 @@ __global__ void __launch_bounds__(128, 4) mlp_fwd_kernel(FieldArgs a, const uint
 #pragma unroll
             for (int i = 0; i < 64; ++i) v[i] = fmaxf(v[i] + W.b1d[i], 0.f);
 #pragma unroll
-            for (int c = 0; c < 8; ++c) st_chunk2(HA, gact ? gact + kActH1 : nullptr, r, c, v + 8 * c);
+            for (int c = 0; c < 8; ++c) st_chunk(HA, r, c, v + 8 * c);
         }
         sync_for_mma();
         // ---- density layer 2: [128x64] x W2d^T -> 16 (raw sigma | embedding)
@@ -413,7 +384,7 @@ __global__ void __launch_bounds__(128, 4) mlp_fwd_kernel(FieldArgs a, const uint
 #pragma unroll
             for (int i = kCIn + 1; i < 48; ++i) cin[i] = 0.f;
 #pragma unroll
-            for (int c = 0; c < 6; ++c) st_chunk2(CIN, gact ? gact + kActCIN : nullptr, r, c, cin + 8 * c);
+            for (int c = 0; c < 6; ++c) st_chunk(CIN, r, c, cin + 8 * c);
         }
         sync_for_mma();
         // ---- colour layer 1: [128x48] x Wc1^T -> 64
@@ -434,7 +405,7 @@ __global__ void __launch_bounds__(128, 4) mlp_fwd_kernel(FieldArgs a, const uint
 #pragma unroll
             for (int i = 0; i < 64; ++i) v[i] = fmaxf(v[i] + W.bc1[i], 0.f);
 #pragma unroll
-            for (int c = 0; c < 8; ++c) st_chunk2(C1, gact ? gact + kActC1 : nullptr, r, c, v + 8 * c);
+            for (int c = 0; c < 8; ++c) st_chunk(C1, r, c, v + 8 * c);
         }
         sync_for_mma();
         // ---- colour layer 2: [128x64] x Wc2^T -> 64
@@ -455,7 +426,7 @@ __global__ void __launch_bounds__(128, 4) mlp_fwd_kernel(FieldArgs a, const uint
 #pragma unroll
             for (int i = 0; i < 64; ++i) v[i] = fmaxf(v[i] + W.bc2[i], 0.f);
 #pragma unroll
-            for (int c = 0; c < 8; ++c) st_chunk2(C2, gact ? gact + kActC2 : nullptr, r, c, v + 8 * c);
+            for (int c = 0; c < 8; ++c) st_chunk(C2, r, c, v + 8 * c);
         }
         sync_for_mma();
         // ---- colour layer 3: [128x64] x Wc3^T -> 16 (3 real) -> sigmoid
@@ -607,21 +578,129 @@ __global__ void __launch_bounds__(128) mlp_bwd_kernel(FieldArgs a, FieldGradArgs
             first_d = true;
         }
         if (r == 0) {
-            // the forward's feature tile and activation tiles of this tile
-            const uint8_t* ga = a.acts + uint64_t(t) * kActsTile;
-            umma::mbar_expect_tx(&bar_ld, kFeatTile + kActsTile);
+            umma::mbar_expect_tx(&bar_ld, kFeatTile);
             umma::bulk_g2s(X0, feat + uint64_t(t) * kFeatTile, kFeatTile, &bar_ld);
-            umma::bulk_g2s(H1, ga + kActH1, 16384, &bar_ld);
-            umma::bulk_g2s(CIN, ga + kActCIN, 12288, &bar_ld);
-            umma::bulk_g2s(C1, ga + kActC1, 16384, &bar_ld);
-            umma::bulk_g2s(C2, ga + kActC2, 16384, &bar_ld);
         }
         bool live = r < td.n;
+        int ray = rays[uint64_t(t) * kT + r];
         float4 dio = live ? a.s.io[uint64_t(td.start) + r] : make_float4(0.f, 0.f, 0.f, 0.f);
         float4 L = live ? a.s.local[uint64_t(td.start) + r] : make_float4(0.f, 0.f, 0.f, 0.f);
+        float ve[kViewDim];
         {
-            // K3 already applied the activation derivatives: io = (d raw sigma,
-            // d pre-sigmoid r, g, b)
+            const float4* v4 = a.venc + uint64_t(ray < 0 ? 0 : ray) * 6;
+#pragma unroll
+            for (int q = 0; q < 6; ++q) {
+                float4 v = __ldg(v4 + q);
+                ve[4 * q] = v.x;
+                ve[4 * q + 1] = v.y;
+                ve[4 * q + 2] = v.z;
+                ve[4 * q + 3] = v.w;
+            }
+        }
+        sync_for_mma();
+        umma::mbar_wait(&bar_ld, ph_ld);
+        ph_ld ^= 1u;
+        uint32_t mh[2], mc1[2], mc2[2];  // ReLU masks of H1, C1, C2
+        // ================= forward recompute
+        if (r == 0) {
+            umma::mma(tmem, kmaj(X0, kT, 0), kmaj(W.w1d, kW1dRows, 0), id64, 0);
+            umma::commit(&bar_mma);
+        }
+        wait_mma(&bar_mma, ph_mma);
+        {
+            float v[64];
+            tld16(tmem, 0, v);
+            tld16(tmem, 16, v + 16);
+            tld16(tmem, 32, v + 32);
+            tld16(tmem, 48, v + 48);
+            umma::ld_wait();
+            mh[0] = mh[1] = 0;
+#pragma unroll
+            for (int i = 0; i < 64; ++i) {
+                float x = v[i] + W.b1d[i];
+                if (x > 0.f) mh[i >> 5] |= 1u << (i & 31);
+                v[i] = fmaxf(x, 0.f);
+            }
+#pragma unroll
+            for (int c = 0; c < 8; ++c) st_chunk(H1, r, c, v + 8 * c);
+        }
+        sync_for_mma();
+        if (r == 0) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                umma::mma(tmem, kmaj(H1, kT, k), kmaj(W.w2d, kW2dRows, k), id16, k > 0);
+            umma::commit(&bar_mma);
+        }
+        wait_mma(&bar_mma, ph_mma);
+        {
+            float v[16];
+            tld16(tmem, 0, v);
+            umma::ld_wait();
+            float cin[48];
+#pragma unroll
+            for (int i = 0; i < kEmb; ++i) cin[i] = v[1 + i] + W.b2d[1 + i];
+#pragma unroll
+            for (int i = 0; i < kViewDim; ++i) cin[kEmb + i] = ve[i];
+            cin[kCIn] = 1.f;
+#pragma unroll
+            for (int i = kCIn + 1; i < 48; ++i) cin[i] = 0.f;
+#pragma unroll
+            for (int c = 0; c < 6; ++c) st_chunk(CIN, r, c, cin + 8 * c);
+        }
+        sync_for_mma();
+        if (r == 0) {
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+                umma::mma(tmem, kmaj(CIN, kT, k), kmaj(W.wc1, kWc1Rows, k), id64, k > 0);
+            umma::commit(&bar_mma);
+        }
+        wait_mma(&bar_mma, ph_mma);
+        {
+            float v[64];
+            tld16(tmem, 0, v);
+            tld16(tmem, 16, v + 16);
+            tld16(tmem, 32, v + 32);
+            tld16(tmem, 48, v + 48);
+            umma::ld_wait();
+            mc1[0] = mc1[1] = 0;
+#pragma unroll
+            for (int i = 0; i < 64; ++i) {
+                float x = v[i] + W.bc1[i];
+                if (x > 0.f) mc1[i >> 5] |= 1u << (i & 31);
+                v[i] = fmaxf(x, 0.f);
+            }
+#pragma unroll
+            for (int c = 0; c < 8; ++c) st_chunk(C1, r, c, v + 8 * c);
+        }
+        sync_for_mma();
+        if (r == 0) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                umma::mma(tmem, kmaj(C1, kT, k), kmaj(W.wc2, kWc2Rows, k), id64, k > 0);
+            umma::commit(&bar_mma);
+        }
+        wait_mma(&bar_mma, ph_mma);
+        {
+            float v[64];
+            tld16(tmem, 0, v);
+            tld16(tmem, 16, v + 16);
+            tld16(tmem, 32, v + 32);
+            tld16(tmem, 48, v + 48);
+            umma::ld_wait();
+            mc2[0] = mc2[1] = 0;
+#pragma unroll
+            for (int i = 0; i < 64; ++i) {
+                float x = v[i] + W.bc2[i];
+                if (x > 0.f) mc2[i >> 5] |= 1u << (i & 31);
+                v[i] = fmaxf(x, 0.f);
+            }
+#pragma unroll
+            for (int c = 0; c < 8; ++c) st_chunk(C2, r, c, v + 8 * c);
+        }
+        sync_for_mma();
+        {
+            // K3 already applied the sigmoid derivative: io = (d raw sigma,
+            // d pre-sigmoid r, g, b), so the colour output layer is not recomputed
             float d3[16];
             d3[0] = dio.y;
             d3[1] = dio.z;
@@ -631,12 +710,6 @@ __global__ void __launch_bounds__(128) mlp_bwd_kernel(FieldArgs a, FieldGradArgs
             st_chunk(D3, r, 0, d3);
             st_chunk(D3, r, 1, d3 + 8);
         }
-        umma::mbar_wait(&bar_ld, ph_ld);
-        ph_ld ^= 1u;
-        uint32_t mh[2], mc1[2], mc2[2];  // ReLU masks of H1, C1, C2 (from the stored values)
-        row_mask(H1, r, mh);
-        row_mask(C1, r, mc1);
-        row_mask(C2, r, mc2);
         sync_for_mma();
         // ================= backward
         // (A) dC2pre = D3 . Wc3 ; dWc3^T += [C2|1]^T . D3

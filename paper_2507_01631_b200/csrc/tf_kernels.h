@@ -67,7 +67,6 @@ struct FieldArgs {
     const Status* status;
     const float4* venc;  // 6 float4 per ray
     SampleArrays s;
-    uint8_t* acts;       // training: per-tile forward activations for the backward (60 KB/tile)
 };
 
 struct FieldGradArgs {

@@ -172,7 +172,6 @@ struct tfg_ctx {
     float* d_ray_out = nullptr;  // rgb(3) | depth | opacity per ray
     int32_t* d_pixels = nullptr;
     uint8_t* d_feat = nullptr;    // bf16 feature tiles (4 KB per 128-sample tile)
-    uint8_t* d_acts = nullptr;    // bf16 forward activation tiles kept for the backward
     int32_t* d_tile_rays = nullptr;
     float4* d_export = nullptr;   // parity export of (d_sigma, d_rgb) in ray semantics
     int cur_rays = 0;
@@ -606,9 +605,8 @@ int run_sampler(tfg_ctx* c, RaygenArgs& a) {
     return 0;
 }
 
-FieldArgs field_args(tfg_ctx* c, const FieldPtrs& f, uint8_t* acts = nullptr) {
+FieldArgs field_args(tfg_ctx* c, const FieldPtrs& f) {
     FieldArgs a{};
-    a.acts = acts;
     a.f = f;
     a.hl = c->hl;
     a.density_max = c->fc.density_max;
@@ -620,15 +618,11 @@ FieldArgs field_args(tfg_ctx* c, const FieldPtrs& f, uint8_t* acts = nullptr) {
     return a;
 }
 
-// Training forwards keep their activation tiles for the backward (60 KB per
-// 128-sample tile, allocated on first use); the render path does not.
-int run_forward(tfg_ctx* c, const FieldPtrs& f, bool training = true) {
+int run_forward(tfg_ctx* c, const FieldPtrs& f) {
     PhaseScope ps(c, kPhFieldFwd);
-    if (training && !c->d_acts && dalloc(c, &c->d_acts, uint64_t(c->max_tiles) * 61440))
-        return TFG_ERR_CUDA;
-    c->fwd_done = training;
-    launch_field_forward_tc(field_args(c, f, training ? c->d_acts : nullptr), c->d_feat,
-                            c->d_tile_rays, c->sms, c->st, &c->launches);
+    c->fwd_done = true;
+    launch_field_forward_tc(field_args(c, f), c->d_feat, c->d_tile_rays, c->sms, c->st,
+                            &c->launches);
     CK(cudaGetLastError());
     return 0;
 }
@@ -668,8 +662,8 @@ int run_backward(tfg_ctx* c) {
         g.g_dnet[k] = g.g_enc[k] + c->enc_n;
     }
     g.g_color = c->d_grads + c->color_off;
-    launch_field_backward_tc(field_args(c, train_ptrs(c), c->d_acts), g, c->d_feat,
-                             c->d_tile_rays, c->sms, c->st, &c->launches);
+    launch_field_backward_tc(field_args(c, train_ptrs(c)), g, c->d_feat, c->d_tile_rays,
+                             c->sms, c->st, &c->launches);
     CK(cudaGetLastError());
     return 0;
 }
@@ -875,7 +869,7 @@ TFG_API int tfg_destroy(tfg_ctx* c) {
                    c->d_rays, c->d_venc,
                    c->d_counts, c->d_P, c->d_tiles, c->s.local, c->s.td, c->s.endpoint, c->s.io,
                    c->d_ray_out, c->d_pixels, c->d_rparams, c->d_rbits, c->d_rcolor, c->d_rcam,
-                   c->d_feat, c->d_tile_rays, c->d_export, c->d_acts};
+                   c->d_feat, c->d_tile_rays, c->d_export};
     for (void* p : dev)
         if (p) cudaFree(p);
     stop_init_pool(c);
@@ -1599,7 +1593,8 @@ TFG_API int tfg_render_pixels(tfg_ctx* c, const tfg_rpc* cam, const int32_t* pix
         int rc = run_sampler(c, a);
         if (rc) return rc;
         c->render_mode = true;
-        if ((rc = run_forward(c, f, false))) return rc;
+        if ((rc = run_forward(c, f))) return rc;
+        c->fwd_done = false;
         if ((rc = run_composite(c, false))) return rc;
         ro.resize(5 * uint64_t(c->max_rays));
         CK(cudaMemcpyAsync(ro.data(), c->d_ray_out, ro.size() * 4, cudaMemcpyDeviceToHost, c->st));
