@@ -68,6 +68,20 @@ def build(verbose: bool = False, force: bool = False) -> str:
     return OUT
 
 
+def build_examples() -> str:
+    """The C++ host example (examples/train_window.cpp) against the C-ABI."""
+    lib = build()
+    out_dir = os.path.join(HERE, "bin")
+    os.makedirs(out_dir, exist_ok=True)
+    exe = os.path.join(out_dir, "train_window")
+    src = os.path.join(HERE, "..", "examples", "train_window.cpp")
+    if _newer([src, lib], exe):
+        subprocess.check_call(["g++", "-std=c++17", "-O2", "-o", exe, src, "-L", HERE, "-ltilefield_gpu",
+                               "-Wl,-rpath,$ORIGIN/.."])
+    return exe
+
+
 if __name__ == "__main__":
     build(verbose="-v" in sys.argv, force="-f" in sys.argv)
+    build_examples()
     print(OUT)
