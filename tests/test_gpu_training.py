@@ -39,7 +39,7 @@ def test_training_psnr_and_depth_match_oracle():
     B, iters = 1024, 160
     tc = TrainConfig.defaults(batch_rays=B, seed=11)
     tc.samples_per_meter = 3.2  # ~32 samples over the 10 m extent
-    ctx = Context(scene, fc, tc, max_rays=B)
+    ctx = Context(scene, fc, tc, max_rays=2048)
     ses = Session(Oracle(), scene, fc, tc, workers=os.cpu_count() or 8)
     ctx.set_window(0, 0)
     ses.set_window(0, 0)
