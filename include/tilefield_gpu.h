@@ -232,6 +232,27 @@ TFG_API int tfg_get_grads(tfg_ctx* ctx, int slot, float* enc, float* dnet, float
 TFG_API int tfg_update_occupancy(tfg_ctx* ctx);
 TFG_API int tfg_get_memory_report(tfg_ctx* ctx, tfg_memory_report* out);
 
+/* ---- checkpoints (save/load_tile_checkpoint, save/load_color_checkpoint,
+ * field.hpp:202-210) ---------------------------------------
+ * Versioned little-endian binary: "TFCKPT01" | u32 version (1) | u32 kind
+ * (1 tile, 2 colour net) | tfg_field_config | i32 row, col | u64 n_params,
+ * n_occupancy | u64 step(s) | f32 params | f32 m | f32 v | f32 occupancy.
+ * Round trips are bit-exact; a mismatching FieldConfig is rejected. */
+TFG_API int tfg_save_tile_checkpoint(const char* path, const tfg_field_config* cfg, int row, int col,
+                                     const tfg_tile_state* st);
+TFG_API int tfg_load_tile_checkpoint(const char* path, const tfg_field_config* cfg, int* row, int* col,
+                                     tfg_tile_state* st);
+TFG_API int tfg_save_color_checkpoint(const char* path, const tfg_field_config* cfg, const float* params,
+                                      const float* m, const float* v, uint64_t step);
+TFG_API int tfg_load_color_checkpoint(const char* path, const tfg_field_config* cfg, float* params,
+                                      float* m, float* v, uint64_t* step);
+/* Whole run state: every tile ever loaded (tiles/r{R}_c{C}.ckpt, from the
+ * window slots or the host records) + color_net.ckpt under `dir` (which must
+ * exist, with a tiles/ subdirectory); load restores it into a context after
+ * set_scene (before set_window). */
+TFG_API int tfg_save_run(tfg_ctx* ctx, const char* dir);
+TFG_API int tfg_load_run(tfg_ctx* ctx, const char* dir);
+
 /* ---- render path (cmd_render; config 4) --------------------- */
 /* Loads up to `n_tiles` tiles (params only) for forward-only rendering over
  * an ROI sub-grid; tile_state entries need enc, dnet, occupancy. */

@@ -21,6 +21,7 @@
 #include <thread>
 #include <cmath>
 #include <cstdio>
+#include <fstream>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -1682,6 +1683,215 @@ TFG_API int tfg_copy_bytes(tfg_ctx* c, uint64_t* h2d, uint64_t* d2h) {
     if (h2d) *h2d = c->h2d_bytes;
     if (d2h) *d2h = c->d2h_bytes;
     return 0;
+}
+
+} // extern "C"
+
+// ---------------------------------------------------------------- checkpoints
+namespace {
+constexpr char kCkptMagic[8] = {'T', 'F', 'C', 'K', 'P', 'T', '0', '1'};
+constexpr uint32_t kCkptVersion = 1;
+
+bool same_cfg(const tfg_field_config& a, const tfg_field_config& b) {
+    return std::memcmp(&a, &b, sizeof(a)) == 0;
+}
+
+int write_ckpt(const char* path, uint32_t kind, const tfg_field_config& cfg, int row, int col,
+               uint64_t n_params, uint64_t n_occ, uint64_t step0, uint64_t step1,
+               const float* const* arrays, const uint64_t* counts, int n_arrays) {
+    std::ofstream f(path, std::ios::binary);
+    if (!f) return fail(TFG_ERR_INVALID, std::string("checkpoint: cannot open ") + path);
+    int32_t rc2[2] = {row, col};
+    uint64_t hdr[4] = {n_params, n_occ, step0, step1};
+    f.write(kCkptMagic, 8);
+    f.write(reinterpret_cast<const char*>(&kCkptVersion), 4);
+    f.write(reinterpret_cast<const char*>(&kind), 4);
+    f.write(reinterpret_cast<const char*>(&cfg), sizeof(cfg));
+    f.write(reinterpret_cast<const char*>(rc2), 8);
+    f.write(reinterpret_cast<const char*>(hdr), 32);
+    for (int i = 0; i < n_arrays; ++i) {
+        static const std::vector<float> zeros(1 << 16, 0.f);
+        if (arrays[i]) {
+            f.write(reinterpret_cast<const char*>(arrays[i]), counts[i] * 4);
+        } else {  // absent moments are written as zeros
+            for (uint64_t k = 0; k < counts[i]; k += zeros.size())
+                f.write(reinterpret_cast<const char*>(zeros.data()),
+                        std::min<uint64_t>(zeros.size(), counts[i] - k) * 4);
+        }
+    }
+    if (!f.good()) return fail(TFG_ERR_INVALID, std::string("checkpoint: write failed for ") + path);
+    return 0;
+}
+
+int read_ckpt_header(std::ifstream& f, const char* path, uint32_t kind, const tfg_field_config& cfg,
+                     int* row, int* col, uint64_t* hdr) {
+    char magic[8];
+    uint32_t ver = 0, k = 0;
+    tfg_field_config c{};
+    int32_t rc2[2];
+    f.read(magic, 8);
+    f.read(reinterpret_cast<char*>(&ver), 4);
+    f.read(reinterpret_cast<char*>(&k), 4);
+    f.read(reinterpret_cast<char*>(&c), sizeof(c));
+    f.read(reinterpret_cast<char*>(rc2), 8);
+    f.read(reinterpret_cast<char*>(hdr), 32);
+    if (!f.good() || std::memcmp(magic, kCkptMagic, 8) != 0)
+        return fail(TFG_ERR_INVALID, std::string("checkpoint: bad magic in ") + path);
+    if (ver != kCkptVersion || k != kind)
+        return fail(TFG_ERR_INVALID, std::string("checkpoint: unsupported version/kind in ") + path);
+    if (!same_cfg(c, cfg))
+        return fail(TFG_ERR_INVALID, std::string("checkpoint: FieldConfig mismatch in ") + path);
+    if (row) *row = rc2[0];
+    if (col) *col = rc2[1];
+    return 0;
+}
+
+int read_arrays(std::ifstream& f, const char* path, float* const* arrays, const uint64_t* counts, int n) {
+    for (int i = 0; i < n; ++i) {
+        if (arrays[i]) {
+            f.read(reinterpret_cast<char*>(arrays[i]), counts[i] * 4);
+        } else {
+            f.seekg(std::streamoff(counts[i] * 4), std::ios::cur);
+        }
+    }
+    if (!f.good()) return fail(TFG_ERR_INVALID, std::string("checkpoint: truncated ") + path);
+    return 0;
+}
+} // namespace
+
+extern "C" {
+
+TFG_API int tfg_save_tile_checkpoint(const char* path, const tfg_field_config* cfg, int row, int col,
+                                     const tfg_tile_state* st) {
+    uint64_t enc, dn;
+    tfg_param_counts(cfg, &enc, &dn, nullptr);
+    uint64_t occ = uint64_t(cfg->occupancy_resolution) * cfg->occupancy_resolution * cfg->occupancy_resolution;
+    const float* arr[7] = {st->enc, st->dnet, st->enc_m, st->enc_v, st->dnet_m, st->dnet_v, st->occupancy};
+    const uint64_t cnt[7] = {enc, dn, enc, enc, dn, dn, occ};
+    if (!st->enc || !st->dnet || !st->occupancy)
+        return fail(TFG_ERR_INVALID, "save_tile_checkpoint: params and occupancy are required");
+    return write_ckpt(path, 1, *cfg, row, col, enc + dn, occ, st->enc_step, st->dnet_step, arr, cnt, 7);
+}
+
+TFG_API int tfg_load_tile_checkpoint(const char* path, const tfg_field_config* cfg, int* row, int* col,
+                                     tfg_tile_state* st) {
+    std::ifstream f(path, std::ios::binary);
+    if (!f) return fail(TFG_ERR_INVALID, std::string("checkpoint: cannot open ") + path);
+    uint64_t hdr[4];
+    int rc = read_ckpt_header(f, path, 1, *cfg, row, col, hdr);
+    if (rc) return rc;
+    uint64_t enc, dn;
+    tfg_param_counts(cfg, &enc, &dn, nullptr);
+    if (hdr[0] != enc + dn) return fail(TFG_ERR_INVALID, "checkpoint: parameter count mismatch");
+    float* arr[7] = {st->enc, st->dnet, st->enc_m, st->enc_v, st->dnet_m, st->dnet_v, st->occupancy};
+    const uint64_t cnt[7] = {enc, dn, enc, enc, dn, dn, hdr[1]};
+    st->enc_step = hdr[2];
+    st->dnet_step = hdr[3];
+    return read_arrays(f, path, arr, cnt, 7);
+}
+
+TFG_API int tfg_save_color_checkpoint(const char* path, const tfg_field_config* cfg, const float* params,
+                                      const float* m, const float* v, uint64_t step) {
+    uint64_t col;
+    tfg_param_counts(cfg, nullptr, nullptr, &col);
+    const float* arr[3] = {params, m, v};
+    const uint64_t cnt[3] = {col, col, col};
+    return write_ckpt(path, 2, *cfg, -1, -1, col, 0, step, 0, arr, cnt, 3);
+}
+
+TFG_API int tfg_load_color_checkpoint(const char* path, const tfg_field_config* cfg, float* params,
+                                      float* m, float* v, uint64_t* step) {
+    std::ifstream f(path, std::ios::binary);
+    if (!f) return fail(TFG_ERR_INVALID, std::string("checkpoint: cannot open ") + path);
+    uint64_t hdr[4];
+    int rc = read_ckpt_header(f, path, 2, *cfg, nullptr, nullptr, hdr);
+    if (rc) return rc;
+    uint64_t col;
+    tfg_param_counts(cfg, nullptr, nullptr, &col);
+    if (hdr[0] != col) return fail(TFG_ERR_INVALID, "checkpoint: parameter count mismatch");
+    float* arr[3] = {params, m, v};
+    const uint64_t cnt[3] = {col, col, col};
+    if (step) *step = hdr[2];
+    return read_arrays(f, path, arr, cnt, 3);
+}
+
+// Saves the run: the window slots are copied back to their host records
+// first, then every record that was ever materialised and the colour net.
+TFG_API int tfg_save_run(tfg_ctx* c, const char* dir) {
+    if (!c || c->n_views == 0) return fail(TFG_ERR_STATE, "save_run: no scene");
+    CK(cudaSetDevice(c->device));
+    CK(cudaEventRecord(c->ev_main, c->st));
+    CK(cudaStreamWaitEvent(c->side, c->ev_main, 0));
+    for (int s = 0; s < c->nslots; ++s)
+        if (slot_copy(c, s, c->slot_tile[s], true)) return TFG_ERR_CUDA;
+    CK(cudaStreamSynchronize(c->side));
+    std::string d(dir);
+    for (size_t ti = 0; ti < c->tiles.size(); ++ti) {
+        TileHost& t = c->tiles[ti];
+        if (!c->init.ready[ti].load() || !t.created) continue;
+        float* p = t.rec;
+        tfg_tile_state st{};
+        st.enc = p;
+        st.dnet = p + c->enc_n;
+        st.enc_m = p + c->stride;
+        st.dnet_m = p + c->stride + c->enc_n;
+        st.enc_v = p + 2 * c->stride;
+        st.dnet_v = p + 2 * c->stride + c->enc_n;
+        st.occupancy = p + 3 * c->stride;
+        st.enc_step = t.enc_step;
+        st.dnet_step = t.dnet_step;
+        char name[64];
+        std::snprintf(name, sizeof name, "/tiles/r%d_c%d.ckpt", int(ti) / c->cols, int(ti) % c->cols);
+        int rc = tfg_save_tile_checkpoint((d + name).c_str(), &c->fc, int(ti) / c->cols,
+                                          int(ti) % c->cols, &st);
+        if (rc) return rc;
+    }
+    uint64_t n = c->n_params - c->color_off;
+    std::vector<float> p(n), m(n), v(n);
+    int rc = tfg_get_color(c, p.data(), m.data(), v.data(), nullptr);
+    if (rc) return rc;
+    return tfg_save_color_checkpoint((d + "/color_net.ckpt").c_str(), &c->fc, p.data(), m.data(), v.data(),
+                                     c->color_step);
+}
+
+// Restores a saved run into the host records (tiles absent from `dir` keep
+// their fresh initialisation) and the colour net; call before set_window.
+TFG_API int tfg_load_run(tfg_ctx* c, const char* dir) {
+    if (!c || c->n_views == 0) return fail(TFG_ERR_STATE, "load_run: no scene");
+    if (c->nslots) return fail(TFG_ERR_STATE, "load_run: call before the first set_window");
+    std::string d(dir);
+    for (size_t ti = 0; ti < c->tiles.size(); ++ti) {
+        char name[64];
+        std::snprintf(name, sizeof name, "/tiles/r%d_c%d.ckpt", int(ti) / c->cols, int(ti) % c->cols);
+        std::string path = d + name;
+        std::ifstream probe(path, std::ios::binary);
+        if (!probe) continue;
+        probe.close();
+        if (ensure_record(c, int(ti))) return TFG_ERR_CUDA;
+        TileHost& t = c->tiles[ti];
+        float* p = t.rec;
+        tfg_tile_state st{};
+        st.enc = p;
+        st.dnet = p + c->enc_n;
+        st.enc_m = p + c->stride;
+        st.dnet_m = p + c->stride + c->enc_n;
+        st.enc_v = p + 2 * c->stride;
+        st.dnet_v = p + 2 * c->stride + c->enc_n;
+        st.occupancy = p + 3 * c->stride;
+        int row, col;
+        int rc = tfg_load_tile_checkpoint(path.c_str(), &c->fc, &row, &col, &st);
+        if (rc) return rc;
+        if (row * c->cols + col != int(ti)) return fail(TFG_ERR_INVALID, "load_run: tile id mismatch in " + path);
+        t.enc_step = st.enc_step;
+        t.dnet_step = st.dnet_step;
+    }
+    uint64_t n = c->n_params - c->color_off;
+    std::vector<float> p(n), m(n), v(n);
+    uint64_t step = 0;
+    int rc = tfg_load_color_checkpoint((d + "/color_net.ckpt").c_str(), &c->fc, p.data(), m.data(), v.data(),
+                                       &step);
+    if (rc) return rc;
+    return tfg_set_color(c, p.data(), m.data(), v.data(), step);
 }
 
 } // extern "C"

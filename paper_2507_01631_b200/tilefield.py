@@ -97,6 +97,12 @@ def lib() -> C.CDLL:
         "tfg_param_counts": [_vp, _vp, _vp, _vp],
         "tfg_default_field_config": [_vp],
         "tfg_default_train_config": [_vp],
+        "tfg_save_tile_checkpoint": [C.c_char_p, _vp, C.c_int, C.c_int, _vp],
+        "tfg_load_tile_checkpoint": [C.c_char_p, _vp, _vp, _vp, _vp],
+        "tfg_save_color_checkpoint": [C.c_char_p, _vp, _vp, _vp, _vp, C.c_uint64],
+        "tfg_load_color_checkpoint": [C.c_char_p, _vp, _vp, _vp, _vp, _vp],
+        "tfg_save_run": [_vp, C.c_char_p],
+        "tfg_load_run": [_vp, C.c_char_p],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -125,6 +131,43 @@ def tile_init(fcfg: FieldConfig, seed: int, row: int, col: int) -> dict:
     _check(lib().tfg_tile_init(C.byref(fcfg), seed, row, col, C.byref(ts)))
     a["enc_step"], a["dnet_step"] = 0, 0
     return a
+
+
+def _state_struct(a: dict) -> TileState:
+    return TileState(*[ptr(a.get(k)) for k in ("enc", "dnet", "enc_m", "enc_v", "dnet_m", "dnet_v")],
+                     a.get("enc_step", 0), a.get("dnet_step", 0), ptr(a.get("occupancy")))
+
+
+def save_tile_checkpoint(path: str, fcfg: FieldConfig, row: int, col: int, state: dict) -> None:
+    """save_tile_checkpoint (field.hpp:206); layout in include/tilefield_gpu.h."""
+    _check(lib().tfg_save_tile_checkpoint(os.fsencode(path), C.byref(fcfg), row, col, C.byref(_state_struct(state))))
+
+
+def load_tile_checkpoint(path: str, fcfg: FieldConfig) -> tuple[int, int, dict]:
+    """load_tile_checkpoint (field.hpp:207): rejects a mismatching FieldConfig."""
+    enc_n, dnet_n, _, _ = field_sizes(fcfg)
+    a = {k: np.zeros(enc_n, np.float32) for k in ("enc", "enc_m", "enc_v")}
+    a.update({k: np.zeros(dnet_n, np.float32) for k in ("dnet", "dnet_m", "dnet_v")})
+    a["occupancy"] = np.zeros(fcfg.occupancy_resolution ** 3, np.float32)
+    ts = _state_struct(a)
+    r, c = C.c_int(), C.c_int()
+    _check(lib().tfg_load_tile_checkpoint(os.fsencode(path), C.byref(fcfg), C.byref(r), C.byref(c), C.byref(ts)))
+    a["enc_step"], a["dnet_step"] = ts.enc_step, ts.dnet_step
+    return r.value, c.value, a
+
+
+def save_color_checkpoint(path: str, fcfg: FieldConfig, p, m=None, v=None, step: int = 0) -> None:
+    """save_color_checkpoint (field.hpp:209)."""
+    _check(lib().tfg_save_color_checkpoint(os.fsencode(path), C.byref(fcfg), ptr(p), ptr(m), ptr(v), step))
+
+
+def load_color_checkpoint(path: str, fcfg: FieldConfig):
+    """load_color_checkpoint (field.hpp:210) -> (params, m, v, step)."""
+    n = field_sizes(fcfg)[2]
+    p, m, v = (np.zeros(n, np.float32) for _ in range(3))
+    st = C.c_uint64()
+    _check(lib().tfg_load_color_checkpoint(os.fsencode(path), C.byref(fcfg), ptr(p), ptr(m), ptr(v), C.byref(st)))
+    return p, m, v, st.value
 
 
 def snake_path(H: int, W: int) -> list[tuple[int, int]]:
@@ -301,6 +344,16 @@ class Context:
 
     def set_color(self, p, m=None, v=None, step=0) -> None:
         _check(lib().tfg_set_color(self.h, ptr(p), ptr(m), ptr(v), step))
+
+    def save_run(self, directory: str) -> None:
+        """Checkpoint every materialised tile (tiles/r{R}_c{C}.ckpt) and the
+        colour net (color_net.ckpt) — the run layout of SPEC.md:470."""
+        os.makedirs(os.path.join(directory, "tiles"), exist_ok=True)
+        _check(lib().tfg_save_run(self.h, os.fsencode(directory)))
+
+    def load_run(self, directory: str) -> None:
+        """Resume a saved run (before the first set_window)."""
+        _check(lib().tfg_load_run(self.h, os.fsencode(directory)))
 
     def update_occupancy(self) -> None:
         _check(lib().tfg_update_occupancy(self.h))
