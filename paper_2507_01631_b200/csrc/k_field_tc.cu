@@ -85,7 +85,7 @@ constexpr uint32_t kWeightsBytes = ((kW1dBytes + 127) & ~127u) + ((kW2dBytes + 1
 // chunk-major tile, zero padded.
 __device__ __forceinline__ void stage_matrix(uint8_t* dst, const float* __restrict__ W, int rows_src,
                                              int cols_src, int rows, int cols) {
-    for (int i = threadIdx.x; i < rows * cols; i += blockDim.x) {
+    for (int i = threadIdx.x; i < rows * cols; i += kT) {
         int r = i / cols, c = i - r * cols;
         float v = (r < rows_src && c < cols_src) ? W[r * cols_src + c] : 0.f;
         *reinterpret_cast<__nv_bfloat16*>(dst + umma::off(rows, r, c)) = __float2bfloat16_rn(v);
@@ -94,18 +94,18 @@ __device__ __forceinline__ void stage_matrix(uint8_t* dst, const float* __restri
 __device__ __forceinline__ void stage_density(const Weights& w, const float* __restrict__ p) {
     stage_matrix(w.w1d, p + kDW1, kDHidden, kFeatDim, 64, 16);
     stage_matrix(w.w2d, p + kDW2, kDOut, kDHidden, 16, 64);
-    for (int i = threadIdx.x; i < 64; i += blockDim.x) w.b1d[i] = p[kDB1 + i];
-    for (int i = threadIdx.x; i < 16; i += blockDim.x) w.b2d[i] = p[kDB2 + i];
+    for (int i = threadIdx.x; i < 64; i += kT) w.b1d[i] = p[kDB1 + i];
+    for (int i = threadIdx.x; i < 16; i += kT) w.b2d[i] = p[kDB2 + i];
 }
 __device__ __forceinline__ void stage_color(const Weights& w, const float* __restrict__ p) {
     stage_matrix(w.wc1, p + kCW1, kCHidden, kCIn, 64, 48);
     stage_matrix(w.wc2, p + kCW2, kCHidden, kCHidden, 64, 64);
     stage_matrix(w.wc3, p + kCW3, 3, kCHidden, 16, 64);
-    for (int i = threadIdx.x; i < 64; i += blockDim.x) {
+    for (int i = threadIdx.x; i < 64; i += kT) {
         w.bc1[i] = p[kCB1 + i];
         w.bc2[i] = p[kCB2 + i];
     }
-    for (int i = threadIdx.x; i < 16; i += blockDim.x) w.bc3[i] = i < 3 ? p[kCB3 + i] : 0.f;
+    for (int i = threadIdx.x; i < 16; i += kT) w.bc3[i] = i < 3 ? p[kCB3 + i] : 0.f;
 }
 
 __device__ __forceinline__ uint32_t pack2(float a, float b) {
@@ -134,6 +134,13 @@ __device__ __forceinline__ void sync_for_mma() {
     umma::fence_async_smem();
     umma::fence_before_sync();
     __syncthreads();
+    umma::fence_after_sync();
+}
+// Same, over the 128 MLP threads of a warp-specialised CTA (named barrier 1).
+__device__ __forceinline__ void sync_mlp() {
+    umma::fence_async_smem();
+    umma::fence_before_sync();
+    asm volatile("bar.sync 1, 128;\n" ::: "memory");
     umma::fence_after_sync();
 }
 __device__ __forceinline__ void wait_mma(uint64_t* bar, uint32_t& phase) {
@@ -465,6 +472,13 @@ constexpr uint32_t kBufA = 9 * kChunk;  // 18432
 constexpr uint32_t kBwdSmem = 3 * kBufA + 4 * kChunk + 6 * kChunk + 2 * kChunk + 2 * kChunk + kWeightsBytes + 128;
 constexpr uint32_t kBwdTmemCols = 256;
 constexpr int kColWc2 = 64, kColWc1 = 128, kColW1d = 176, kColWc3 = 208, kColW2d = 224;
+constexpr int kColDX = 240;  // d(features) of the last tile, read by the scatter warps
+// Warp specialisation: warps 0-3 run the MLP chain (one thread per tile row,
+// thread 0 issues the MMAs), warps 4-7 run the hash-table scatter of the
+// previous tile's d(features) from TMEM, so the L2-atomic-bound scatter
+// overlaps the latency-bound MMA chain instead of extending it.
+constexpr int kBwdThreads = 256;
+constexpr uint32_t kRegsMlp = 176, kRegsScatter = 80;  // 4 x 32 x (176 + 80) = 32768 per CTA
 
 __device__ __forceinline__ void set_ones_chunk(uint8_t* buf, int chunk, int r) {
     float v[8] = {1.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
@@ -522,11 +536,11 @@ __device__ __forceinline__ void flush_color(uint32_t tmem, float* __restrict__ g
         for (int o = 0; o < 3; ++o) atomicAdd(gc + kCB3 + o, v[o]);
 }
 
-__global__ void __launch_bounds__(128) mlp_bwd_kernel(FieldArgs a, FieldGradArgs g,
+__global__ void __launch_bounds__(kBwdThreads, 2) mlp_bwd_kernel(FieldArgs a, FieldGradArgs g,
                                                       const uint8_t* __restrict__ feat,
                                                       const int32_t* __restrict__ rays) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
-    __shared__ uint64_t bar_mma, bar_ld, bar_w;
+    __shared__ uint64_t bar_mma, bar_ld, bar_w, bar_e, bar_free;
     __shared__ uint32_t tmem_slot;
     uint8_t* p = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
     uint8_t* H1 = carve(p, kBufA);
@@ -542,25 +556,52 @@ __global__ void __launch_bounds__(128) mlp_bwd_kernel(FieldArgs a, FieldGradArgs
         umma::mbar_init(&bar_mma, 1);
         umma::mbar_init(&bar_ld, 1);
         umma::mbar_init(&bar_w, 1);
+        umma::mbar_init(&bar_e, 1);
+        umma::mbar_init(&bar_free, 4);
         umma::fence_mbar_init();
     }
     if (r < 32) umma::tmem_alloc<kBwdTmemCols>(&tmem_slot);
-    stage_color(W, a.f.color);
-    // constant ones chunks
-    set_ones_chunk(H1, 8, r);
-    set_ones_chunk(C1, 8, r);
-    set_ones_chunk(C2, 8, r);
-    set_ones_chunk(X0, 2, r);
-    {
+    if (r < kT) {
+        stage_color(W, a.f.color);
+        // constant ones chunks
+        set_ones_chunk(H1, 8, r);
+        set_ones_chunk(C1, 8, r);
+        set_ones_chunk(C2, 8, r);
+        set_ones_chunk(X0, 2, r);
         float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         st_chunk(X0, r, 3, z);
     }
-    uint32_t ph_mma = 0, ph_ld = 0, ph_w = 0;
-    int cur = -1;
-    bool first_d = true, first_c = true;
     uint32_t n_tiles = a.status->n_tiles;
     sync_for_mma();
     const uint32_t tmem = tmem_slot;
+    if (r >= kT) {
+        // ================= scatter warps
+        umma::reg_dealloc<kRegsScatter>();
+        const int row = r - kT;
+        const uint32_t quad = uint32_t(row >> 5);
+        uint32_t ph_e = 0;
+        for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+            TileDesc td = a.tiles[t];
+            bool live = row < td.n;
+            float4 L = live ? a.s.local[uint64_t(td.start) + row] : make_float4(0.f, 0.f, 0.f, 0.f);
+            umma::mbar_wait(&bar_e, ph_e);
+            ph_e ^= 1u;
+            umma::fence_after_sync();
+            float v[16];
+            umma::ld16(tmem + ((32u * quad) << 16) + uint32_t(kColDX), v);
+            umma::ld_wait();
+            umma::fence_before_sync();
+            __syncwarp();
+            if ((row & 31) == 0) umma::mbar_arrive(&bar_free);  // TMEM columns free again
+            scatter_row(a.hl, g.g_enc[td.slot], L.x, L.y, L.z, v, live);
+        }
+        __syncthreads();  // pairs with the MLP warps' final barrier before tmem_free
+        return;
+    }
+    umma::reg_alloc<kRegsMlp>();
+    uint32_t ph_mma = 0, ph_ld = 0, ph_w = 0, ph_free = 0;
+    int cur = -1;
+    bool first_d = true, first_c = true, first_e = true;
     const uint32_t id64 = umma::idesc_bf16(128, 64, 0, 0);
     const uint32_t id16 = umma::idesc_bf16(128, 16, 0, 0);
     const uint32_t id64_kmn = umma::idesc_bf16(128, 64, 0, 1);  // A K-major, B MN-major
@@ -584,7 +625,6 @@ __global__ void __launch_bounds__(128) mlp_bwd_kernel(FieldArgs a, FieldGradArgs
         bool live = r < td.n;
         int ray = rays[uint64_t(t) * kT + r];
         float4 dio = live ? a.s.io[uint64_t(td.start) + r] : make_float4(0.f, 0.f, 0.f, 0.f);
-        float4 L = live ? a.s.local[uint64_t(td.start) + r] : make_float4(0.f, 0.f, 0.f, 0.f);
         float ve[kViewDim];
         {
             const float4* v4 = a.venc + uint64_t(ray < 0 ? 0 : ray) * 6;
@@ -597,7 +637,7 @@ __global__ void __launch_bounds__(128) mlp_bwd_kernel(FieldArgs a, FieldGradArgs
                 ve[4 * q + 3] = v.w;
             }
         }
-        sync_for_mma();
+        sync_mlp();
         umma::mbar_wait(&bar_ld, ph_ld);
         ph_ld ^= 1u;
         uint32_t mh[2], mc1[2], mc2[2];  // ReLU masks of H1, C1, C2
@@ -624,7 +664,7 @@ __global__ void __launch_bounds__(128) mlp_bwd_kernel(FieldArgs a, FieldGradArgs
 #pragma unroll
             for (int c = 0; c < 8; ++c) st_chunk(H1, r, c, v + 8 * c);
         }
-        sync_for_mma();
+        sync_mlp();
         if (r == 0) {
 #pragma unroll
             for (int k = 0; k < 4; ++k)
@@ -647,7 +687,7 @@ __global__ void __launch_bounds__(128) mlp_bwd_kernel(FieldArgs a, FieldGradArgs
 #pragma unroll
             for (int c = 0; c < 6; ++c) st_chunk(CIN, r, c, cin + 8 * c);
         }
-        sync_for_mma();
+        sync_mlp();
         if (r == 0) {
 #pragma unroll
             for (int k = 0; k < 3; ++k)
@@ -672,7 +712,7 @@ __global__ void __launch_bounds__(128) mlp_bwd_kernel(FieldArgs a, FieldGradArgs
 #pragma unroll
             for (int c = 0; c < 8; ++c) st_chunk(C1, r, c, v + 8 * c);
         }
-        sync_for_mma();
+        sync_mlp();
         if (r == 0) {
 #pragma unroll
             for (int k = 0; k < 4; ++k)
@@ -697,7 +737,7 @@ __global__ void __launch_bounds__(128) mlp_bwd_kernel(FieldArgs a, FieldGradArgs
 #pragma unroll
             for (int c = 0; c < 8; ++c) st_chunk(C2, r, c, v + 8 * c);
         }
-        sync_for_mma();
+        sync_mlp();
         {
             // K3 already applied the sigmoid derivative: io = (d raw sigma,
             // d pre-sigmoid r, g, b), so the colour output layer is not recomputed
@@ -710,7 +750,7 @@ __global__ void __launch_bounds__(128) mlp_bwd_kernel(FieldArgs a, FieldGradArgs
             st_chunk(D3, r, 0, d3);
             st_chunk(D3, r, 1, d3 + 8);
         }
-        sync_for_mma();
+        sync_mlp();
         // ================= backward
         // (A) dC2pre = D3 . Wc3 ; dWc3^T += [C2|1]^T . D3
         if (r == 0) {
@@ -735,7 +775,7 @@ __global__ void __launch_bounds__(128) mlp_bwd_kernel(FieldArgs a, FieldGradArgs
 #pragma unroll
             for (int c = 0; c < 8; ++c) st_chunk(C2, r, c, v + 8 * c);  // DC2 over C2
         }
-        sync_for_mma();
+        sync_mlp();
         // (B) dC1pre = DC2 . Wc2 ; dWc2^T += [C1|1]^T . DC2
         if (r == 0) {
 #pragma unroll
@@ -761,7 +801,7 @@ __global__ void __launch_bounds__(128) mlp_bwd_kernel(FieldArgs a, FieldGradArgs
 #pragma unroll
             for (int c = 0; c < 8; ++c) st_chunk(C1, r, c, v + 8 * c);  // DC1 over C1
         }
-        sync_for_mma();
+        sync_mlp();
         // (C) dCIN[0:16] = DC1 . Wc1[:, 0:16] ; dWc1 += DC1^T . CIN
         if (r == 0) {
 #pragma unroll
@@ -787,7 +827,7 @@ __global__ void __launch_bounds__(128) mlp_bwd_kernel(FieldArgs a, FieldGradArgs
             st_chunk(DO, r, 0, d);
             st_chunk(DO, r, 1, d + 8);
         }
-        sync_for_mma();
+        sync_mlp();
         // (D) dH1pre = DO . W2d ; dW2d^T += [H1|1]^T . DO
         if (r == 0) {
             umma::mma(tmem, kmaj(DO, kT, 0), mnmaj(W.w2d, kW2dRows, 0), id64_kmn, 0);
@@ -811,32 +851,30 @@ __global__ void __launch_bounds__(128) mlp_bwd_kernel(FieldArgs a, FieldGradArgs
 #pragma unroll
             for (int c = 0; c < 8; ++c) st_chunk(H1, r, c, v + 8 * c);  // DH1 over H1
         }
-        sync_for_mma();
-        // (E) dX0 = DH1 . W1d ; dW1d += DH1^T . [X0|1|0]
+        sync_mlp();
+        // (E) dX0 = DH1 . W1d into the scatter warps' columns (once they have
+        // read the previous tile's) ; dW1d += DH1^T . [X0|1|0]
         if (r == 0) {
+            if (!first_e) {
+                umma::mbar_wait(&bar_free, ph_free);
+                ph_free ^= 1u;
+                umma::fence_after_sync();
+            }
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-                umma::mma(tmem, kmaj(H1, kT, k), mnmaj(W.w1d, kW1dRows, k), id16_kmn, k > 0);
-            umma::commit(&bar_mma);
+                umma::mma(tmem + kColDX, kmaj(H1, kT, k), mnmaj(W.w1d, kW1dRows, k), id16_kmn, k > 0);
+            umma::commit(&bar_e);
 #pragma unroll
             for (int k = 0; k < 8; ++k)
                 umma::mma(tmem + kColW1d, mnmaj(H1, kT, k), mnmaj(X0, kT, k), idw32, (first_d && k == 0) ? 0 : 1);
             umma::commit(&bar_w);
         }
-        wait_mma(&bar_mma, ph_mma);
         first_d = false;
-        {
-            // d(features) -> hash-table scatter straight from the epilogue
-            // (fire-and-forget red atomics overlap the other CTA's MMAs)
-            float v[16];
-            tld16(tmem, 0, v);
-            umma::ld_wait();
-            scatter_row(a.hl, g.g_enc[td.slot], L.x, L.y, L.z, v, live);
-        }
+        first_e = false;
         wait_mma(&bar_w, ph_w);  // dW1d has read H1 / X0 before the next tile
     }
     umma::fence_before_sync();
-    __syncthreads();
+    asm volatile("bar.sync 1, 128;\n" ::: "memory");
     umma::fence_after_sync();
     if (cur >= 0) flush_density(tmem, g.g_dnet[cur]);
     if (!first_c) flush_color(tmem, g.g_color);
@@ -872,7 +910,7 @@ void launch_field_backward_tc(const FieldArgs& a, const FieldGradArgs& g, uint8_
     }
     // the feature tiles of the forward pass (same batch) are still resident;
     // the hash-table scatter is fused into the backward's last epilogue
-    mlp_bwd_kernel<<<sms * 2, 128, kBwdSmem, st>>>(a, g, feat, rays);
+    mlp_bwd_kernel<<<sms * 2, kBwdThreads, kBwdSmem, st>>>(a, g, feat, rays);
     *launches += 1;
 }
 
