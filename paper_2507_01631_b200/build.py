@@ -39,18 +39,24 @@ def _newer(src_files, target):
     return any(os.path.getmtime(s) > t for s in src_files)
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+def build(verbose: bool = False, force: bool = False, defines: list[str] | None = None,
+          out: str | None = None, build_dir: str | None = None) -> str:
+    """Compiles every unit for sm_100a and links the C-ABI library.  `defines`
+    / `out` / `build_dir` build an A/B variant (tools/variants.py)."""
+    lib_out = out or OUT
+    bdir = build_dir or BUILD
+    dflags = [f"-D{d}" for d in (defines or [])]
+    os.makedirs(bdir, exist_ok=True)
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
     headers.append(os.path.join(HERE, "..", "include", "tilefield_gpu.h"))
     objs = []
     procs = []
     for src, extra in UNITS:
         s = os.path.join(CSRC, src)
-        o = os.path.join(BUILD, src.replace(".cu", ".o"))
+        o = os.path.join(bdir, src.replace(".cu", ".o"))
         objs.append(o)
         if force or _newer([s] + headers, o):
-            cmd = [NVCC] + COMMON + extra + ["-c", s, "-o", o]
+            cmd = [NVCC] + COMMON + extra + dflags + ["-c", s, "-o", o]
             if verbose:
                 cmd.insert(1, "-Xptxas=-v")
                 print(" ".join(cmd), flush=True)
@@ -62,10 +68,10 @@ def build(verbose: bool = False, force: bool = False) -> str:
             raise RuntimeError(f"nvcc failed on {src}")
         if verbose and out:
             sys.stdout.write(out.decode())
-    if force or procs or not os.path.exists(OUT):
-        cmd = [NVCC] + ARCH + ["-shared", "-o", OUT] + objs + ["-cudart", "static", "-lpthread", "-ldl", "-lrt"]
+    if force or procs or not os.path.exists(lib_out):
+        cmd = [NVCC] + ARCH + ["-shared", "-o", lib_out] + objs + ["-cudart", "static", "-lpthread", "-ldl", "-lrt"]
         subprocess.check_call(cmd)
-    return OUT
+    return lib_out
 
 
 def build_examples() -> str:

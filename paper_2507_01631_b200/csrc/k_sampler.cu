@@ -266,7 +266,10 @@ __device__ __forceinline__ bool occ_test(const uint32_t* bits, float x, float y,
 // results are exchanged by shuffle and both lanes finish the ray with the
 // same arithmetic (same bits); the interior-sample counting is split by
 // sample parity; the odd lane also writes the view encoding.
-__global__ void __launch_bounds__(128) raygen_kernel(RaygenArgs a, RayRec* __restrict__ rays,
+#ifndef TFG_RAYGEN_MINB
+#define TFG_RAYGEN_MINB 4
+#endif
+__global__ void __launch_bounds__(128, TFG_RAYGEN_MINB) raygen_kernel(RaygenArgs a, RayRec* __restrict__ rays,
                                                      float4* __restrict__ venc,
                                                      uint32_t* __restrict__ counts,
                                                      Status* __restrict__ status) {
