@@ -128,7 +128,10 @@ int scan_exclusive(const uint32_t* in, uint64_t n, uint32_t* out, uint32_t* bloc
 // ------------------------------------------------------------------ accept list
 // One thread per candidate pixel of the per-view crop-union rects; flag = 1 iff
 // the ray exists, hits >= 1 tile and every hit tile is loaded.
-__global__ void __launch_bounds__(128) accept_kernel(AcceptArgs a, uint32_t* __restrict__ flags) {
+#ifndef TFG_ACCEPT_MINB
+#define TFG_ACCEPT_MINB 3
+#endif
+__global__ void __launch_bounds__(128, TFG_ACCEPT_MINB) accept_kernel(AcceptArgs a, uint32_t* __restrict__ flags) {
     // two threads per candidate: one Newton localisation each (z_max / z_min)
     const uint64_t gt = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     const uint64_t idx = gt >> 1;
@@ -194,6 +197,15 @@ __global__ void __launch_bounds__(128) accept_kernel(AcceptArgs a, uint32_t* __r
                             all_loaded &= ld;
                         }
                     ok = (hits >= 1 && all_loaded) ? 1u : 0u;
+                    if (ok) {  // memoised for the ray draw (bit-identical to raygen's solve)
+                        double* cr = a.cand_rays + 6 * idx;
+                        cr[0] = o[0];
+                        cr[1] = o[1];
+                        cr[2] = o[2];
+                        cr[3] = d[0];
+                        cr[4] = d[1];
+                        cr[5] = d[2];
+                    }
                 }
             }
         }
@@ -203,7 +215,7 @@ __global__ void __launch_bounds__(128) accept_kernel(AcceptArgs a, uint32_t* __r
 
 __global__ void accept_scatter_kernel(AcceptArgs a, const uint32_t* __restrict__ flags,
                                       const uint32_t* __restrict__ pos,
-                                      uint64_t* __restrict__ out) {
+                                      uint64_t* __restrict__ out, double* __restrict__ out_rays) {
     uint64_t idx = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (idx >= a.n_candidates || !flags[idx]) return;
     int v = 0;
@@ -214,6 +226,10 @@ __global__ void accept_scatter_kernel(AcceptArgs a, const uint32_t* __restrict__
     uint64_t row = uint64_t(u[0]) + local / uint64_t(ncols);
     uint64_t col = uint64_t(u[2]) + local % uint64_t(ncols);
     out[pos[idx]] = (uint64_t(v) << 40) | (row << 20) | col;
+    const double* cr = a.cand_rays + 6 * idx;
+    double* orr = out_rays + 6 * uint64_t(pos[idx]);
+#pragma unroll
+    for (int k = 0; k < 6; ++k) orr[k] = cr[k];
 }
 
 // ------------------------------------------------------------------ K1a
@@ -280,6 +296,7 @@ __global__ void __launch_bounds__(128, TFG_RAYGEN_MINB) raygen_kernel(RaygenArgs
     const int ii = valid ? i : 0;
     uint64_t g = a.ray_begin + uint64_t(ii);
     int v, row, col;
+    const double* memo = nullptr;  // the accept pass already solved accepted pixels
     if (a.pixels) {
         v = a.pixels[3 * ii];
         row = a.pixels[3 * ii + 1];
@@ -287,27 +304,38 @@ __global__ void __launch_bounds__(128, TFG_RAYGEN_MINB) raygen_kernel(RaygenArgs
     } else {
         uint64_t na = *a.n_accept_dev;
         Rng r(hash_combine(hash_combine(hash_combine(a.seed, kPurposePixels), a.iter), g));
-        uint64_t e = na ? a.accept[r.below(na)] : 0;
+        uint64_t k = na ? r.below(na) : 0;
+        uint64_t e = na ? a.accept[k] : 0;
         v = int(e >> 40);
         row = int((e >> 20) & 0xFFFFF);
         col = int(e & 0xFFFFF);
         if (na == 0 && valid && hi == 0) atomicOr(&status->bits, kStatusRayFail);
+        if (na && a.acc_rays) memo = a.acc_rays + 6 * k;
     }
-    double gx = 0.0, gy = 0.0;
-    int st = rpc_localize(a.cams[v], double(row), double(col), hi ? a.z_min : a.z_max, &gx, &gy);
-    double ox = __shfl_xor_sync(pair, gx, 1), oy = __shfl_xor_sync(pair, gy, 1);
-    int ost = __shfl_xor_sync(pair, st, 1);
     RayRec R;
     R.view = v;
     R.row = row;
     R.col = col;
     R.target[0] = R.target[1] = R.target[2] = 0.f;
-    // status of the top (z_max) localisation first, as ray_from_pixel throws
-    int st_top = hi ? ost : st, st_bot = hi ? st : ost;
-    R.status = st_top ? st_top : st_bot;
-    if (R.status == 0) {
-        double tx = hi ? ox : gx, ty = hi ? oy : gy, bx = hi ? gx : ox, by = hi ? gy : oy;
-        R.status = rpc_ray_finish(tx, ty, bx, by, a.z_min, a.z_max, R.o, R.d);
+    if (memo) {
+        R.status = 0;
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            R.o[q] = memo[q];
+            R.d[q] = memo[3 + q];
+        }
+    } else {
+        double gx = 0.0, gy = 0.0;
+        int st = rpc_localize(a.cams[v], double(row), double(col), hi ? a.z_min : a.z_max, &gx, &gy);
+        double ox = __shfl_xor_sync(pair, gx, 1), oy = __shfl_xor_sync(pair, gy, 1);
+        int ost = __shfl_xor_sync(pair, st, 1);
+        // status of the top (z_max) localisation first, as ray_from_pixel throws
+        int st_top = hi ? ost : st, st_bot = hi ? st : ost;
+        R.status = st_top ? st_top : st_bot;
+        if (R.status == 0) {
+            double tx = hi ? ox : gx, ty = hi ? oy : gy, bx = hi ? gx : ox, by = hi ? gy : oy;
+            R.status = rpc_ray_finish(tx, ty, bx, by, a.z_min, a.z_max, R.o, R.d);
+        }
     }
     if (valid && hi == 0)
         for (int s = 0; s < a.slots.n; ++s) counts[uint64_t(s) * a.n_rays + i] = 0;
@@ -517,7 +545,7 @@ __global__ void __launch_bounds__(256) write_kernel(RaygenArgs a, const RayRec* 
 
 // ------------------------------------------------------------------ host launchers
 int launch_accept(const AcceptArgs& a, uint32_t* flags, uint32_t* pos, uint32_t* block_sums,
-                  uint32_t* n_out, uint64_t* out, cudaStream_t st, uint64_t* launches) {
+                  uint32_t* n_out, uint64_t* out, double* out_rays, cudaStream_t st, uint64_t* launches) {
     if (a.n_candidates == 0) {
         cudaMemsetAsync(n_out, 0, 4, st);
         return 0;
@@ -525,7 +553,7 @@ int launch_accept(const AcceptArgs& a, uint32_t* flags, uint32_t* pos, uint32_t*
     int nb = int((a.n_candidates + 127) / 128);
     accept_kernel<<<int((2 * a.n_candidates + 127) / 128), 128, 0, st>>>(a, flags);
     if (scan_exclusive(flags, a.n_candidates, pos, block_sums, n_out, st, launches)) return 1;
-    accept_scatter_kernel<<<nb, 128, 0, st>>>(a, flags, pos, out);
+    accept_scatter_kernel<<<nb, 128, 0, st>>>(a, flags, pos, out, out_rays);
     *launches += 2;
     return 0;
 }

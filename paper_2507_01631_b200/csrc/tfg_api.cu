@@ -97,6 +97,7 @@ struct WinBuf {
     int* d_crop_rect = nullptr;      // r0, c0, cols, rows per view
     uint64_t* d_crop_off = nullptr;  // byte offset of each view's crop
     uint64_t* d_accept = nullptr;    // packed (view, row, col)
+    double* d_acc_rays = nullptr;    // o[3], d[3] per accepted entry (memoised RPC rays)
     uint32_t* d_n = nullptr;         // accepted count (read by the ray draw on device)
     std::vector<int> h_crop_rect;
     std::vector<uint64_t> h_crop_off;
@@ -161,6 +162,7 @@ struct tfg_ctx {
     uint64_t crop_cap = 0, accept_cap = 0, cand_cap = 0;
     // accepted-list build scratch (one build at a time)
     uint32_t *d_flags = nullptr, *d_pos = nullptr, *d_block_sums = nullptr, *d_acc_sums = nullptr;
+    double* d_cand_rays = nullptr;  // accept-pass ray memo per candidate (scratch)
     uint64_t* d_view_start = nullptr;
     int *d_union = nullptr, *d_crop4 = nullptr;
 
@@ -522,7 +524,9 @@ int stage_window(tfg_ctx* c, WinBuf& w, int pr, int pc, cudaStream_t st) {
     a.n_loaded = int(want.size());
     a.z_min = c->roi.z_min;
     a.z_max = c->roi.z_max;
-    if (launch_accept(a, c->d_flags, c->d_pos, c->d_acc_sums, w.d_n, w.d_accept, st, &c->launches))
+    a.cand_rays = c->d_cand_rays;
+    if (launch_accept(a, c->d_flags, c->d_pos, c->d_acc_sums, w.d_n, w.d_accept, w.d_acc_rays, st,
+                      &c->launches))
         return fail(TFG_ERR_INVALID, "accept: scan capacity exceeded");
     CK(cudaGetLastError());
     CK(cudaEventRecord(w.ready, st));
@@ -870,7 +874,7 @@ TFG_API int tfg_destroy(tfg_ctx* c) {
                    c->d_rays, c->d_venc,
                    c->d_counts, c->d_P, c->d_tiles, c->s.local, c->s.td, c->s.endpoint, c->s.io,
                    c->d_ray_out, c->d_pixels, c->d_rparams, c->d_rbits, c->d_rcolor, c->d_rcam,
-                   c->d_feat, c->d_tile_rays, c->d_export};
+                   c->d_feat, c->d_tile_rays, c->d_export, c->d_cand_rays};
     for (void* p : dev)
         if (p) cudaFree(p);
     stop_init_pool(c);
@@ -879,7 +883,7 @@ TFG_API int tfg_destroy(tfg_ctx* c) {
         if (im) cudaFreeHost(im);
     if (c->h_status) cudaFreeHost(c->h_status);
     for (WinBuf& w : c->win) {
-        void* wo[] = {w.d_crops, w.d_crop_rect, w.d_crop_off, w.d_accept, w.d_n};
+        void* wo[] = {w.d_crops, w.d_crop_rect, w.d_crop_off, w.d_accept, w.d_n, w.d_acc_rays};
         for (void* p : wo)
             if (p) cudaFree(p);
         if (w.ready) cudaEventDestroy(w.ready);
@@ -969,16 +973,17 @@ TFG_API int tfg_set_scene(tfg_ctx* c, const tfg_rpc* cams, int n_views,
     c->crop_cap = cropb;
     int rc = 0;
     void* olds[] = {c->d_cams, c->d_east, c->d_north, c->d_flags, c->d_pos, c->d_view_start,
-                    c->d_union, c->d_crop4};
+                    c->d_union, c->d_crop4, c->d_cand_rays};
     for (void* p : olds)
         if (p) cudaFree(p);
     rc |= dalloc(c, &c->d_cams, n_views);
     rc |= dalloc(c, &c->d_east, grid_cols + 1);
     rc |= dalloc(c, &c->d_north, grid_rows + 1);
     for (WinBuf& w : c->win) {
-        void* wo[] = {w.d_crops, w.d_crop_rect, w.d_crop_off, w.d_accept, w.d_n};
+        void* wo[] = {w.d_crops, w.d_crop_rect, w.d_crop_off, w.d_accept, w.d_n, w.d_acc_rays};
         for (void* p : wo)
             if (p) cudaFree(p);
+        rc |= dalloc(c, &w.d_acc_rays, 6 * c->accept_cap);
         rc |= dalloc(c, &w.d_crops, c->crop_cap);
         rc |= dalloc(c, &w.d_crop_rect, 4 * n_views);
         rc |= dalloc(c, &w.d_crop_off, n_views);
@@ -988,6 +993,7 @@ TFG_API int tfg_set_scene(tfg_ctx* c, const tfg_rpc* cams, int n_views,
         w.pos_r = w.pos_c = -1;
     }
     rc |= dalloc(c, &c->d_flags, c->cand_cap);
+    rc |= dalloc(c, &c->d_cand_rays, 6 * c->cand_cap);
     rc |= dalloc(c, &c->d_pos, c->cand_cap + 1);
     rc |= dalloc(c, &c->d_view_start, n_views);
     rc |= dalloc(c, &c->d_union, 4 * n_views);
@@ -1153,6 +1159,7 @@ TFG_API int tfg_sample(tfg_ctx* c, uint64_t iter, uint64_t ray_begin, int n_rays
     RaygenArgs a = base_raygen(c);
     a.accept = c->win[c->front].d_accept;
     a.n_accept_dev = c->win[c->front].d_n;
+    a.acc_rays = c->win[c->front].d_acc_rays;
     a.iter = iter;
     a.ray_begin = ray_begin;
     a.n_rays = n_rays;
@@ -1506,7 +1513,7 @@ TFG_API int tfg_get_memory_report(tfg_ctx* c, tfg_memory_report* o) {
     o->optimizer_moments = 2 * kTrainSlots * c->stride * 4 + kTrainSlots * c->stride * 4;  // m, v, grads
     o->occupancy = uint64_t(kTrainSlots) * kOccVox * 4 + uint64_t(kMaxSlots) * kOccWords * 4;
     o->crops = 2 * c->crop_cap;
-    o->accept_list = 2 * c->accept_cap * 8 + c->cand_cap * 8;
+    o->accept_list = 2 * c->accept_cap * (8 + 48) + c->cand_cap * (8 + 48);  // lists + ray memo
     o->batch_buffers = uint64_t(c->max_rays) * (sizeof(RayRec) + 96 + 8 * kMaxSlots + 20 + 12) +
                        c->sample_cap * (16 + 8 + 1 + 16);
     o->color_net = (c->n_params - c->color_off) * 4;

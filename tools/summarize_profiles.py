@@ -2,7 +2,7 @@
 metrics, and profiles/traffic.json = measured DRAM bytes per launch of each
 bench kernel family, read by bench.py's roofline 'traffic' field).
 
-usage: python tools/summarize_profiles.py <launches.csv> <prof.ncu-rep> <tag>
+usage: python tools/summarize_profiles.py <launches.csv> <tag> <prof.ncu-rep> [more.ncu-rep ...]
 """
 import collections
 import csv
@@ -98,20 +98,45 @@ def raw(rep):
     return res
 
 
+def stalls(rep, top=3):
+    """Top warp-stall reasons (sampled, all instructions) of the kernel in `rep`."""
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hi = [i for i, r in enumerate(rows) if "Address" in r and "Source" in r]
+    if not hi:
+        return ""
+    h = rows[hi[0]]
+    cols = [i for i, c in enumerate(h) if c.startswith("stall_") and "Not Issued" not in c]
+    tot = collections.Counter()
+    for r in rows[hi[0] + 1:]:
+        for i in cols:
+            try:
+                tot[h[i][6:]] += float(r[i] or 0)
+            except (ValueError, IndexError):
+                pass
+    n = sum(tot.values()) or 1.0
+    return ", ".join(f"{k} {100 * v / n:.0f}%" for k, v in tot.most_common(top))
+
+
 def main():
-    lpath, rep, tag = sys.argv[1], sys.argv[2], sys.argv[3]
+    lpath, tag, reps = sys.argv[1], sys.argv[2], sys.argv[3:]
     agg = launches(lpath)
     tot = sum(v[1] for v in agg.values())
     lines = [f"# ncu summary {tag}", "", "Launch list (`ncu --metrics gpu__time_duration.sum --clock-control none`,",
-             "`python bench.py --steps 2 --warmup 3 --no-render --no-cpu`; cold-cache, serialised:",
+             "`python bench.py --steps 2 --warmup 3 --no-render --no-cpu`, `tools/profile_round.sh`; cold-cache, serialised:",
              "compare shares, not absolute times).", "",
              "| kernel | family | launches | ms/launch | share |", "|---|---|---|---|---|"]
     for k, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
         lines.append(f"| {k} | {FAMILY.get(k, '-')} | {n} | {t / 1e6 / n:.3f} | {100 * t / tot:.1f}% |")
-    r = raw(rep)
+    r = collections.defaultdict(list)
+    st = {}
+    for rep in reps:
+        for k, v in raw(rep).items():
+            r[k] += v
+            st[k] = stalls(rep)
     lines += ["", "Full captures (`ncu --set full --clock-control none`), one launch each:", "",
-              "| kernel | time ms | DRAM read MB | DRAM write MB | SM % | DRAM % | L2 % | L1 % | tensor % | warps % | issue % | regs |",
-              "|---|---|---|---|---|---|---|---|---|---|---|---|"]
+              "| kernel | time ms | DRAM read MB | DRAM write MB | SM % | DRAM % | L2 % | L1 % | tensor % | warps % | issue % | regs | top stalls |",
+              "|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
     traffic = collections.defaultdict(float)
     for k, ds in r.items():
         d = ds[0]
@@ -124,7 +149,7 @@ def main():
                      f"{g('sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active'):.1f} | "
                      f"{g('sm__warps_active.avg.pct_of_peak_sustained_active'):.1f} | "
                      f"{g('smsp__issue_active.avg.pct_of_peak_sustained_active'):.1f} | "
-                     f"{g('launch__registers_per_thread'):.0f} |")
+                     f"{g('launch__registers_per_thread'):.0f} | {st.get(k, '')} |")
         fam = FAMILY.get(k)
         if fam:
             traffic[fam] += g("dram__bytes_read.sum") + g("dram__bytes_write.sum")
