@@ -151,12 +151,25 @@ __global__ void __launch_bounds__(128, TFG_ACCEPT_MINB) accept_kernel(AcceptArgs
         const int* r = a.crop_rect + 4 * (v * kTrainSlots + k);
         if (r[0] < r[1] && row >= r[0] && row < r[1] && col >= r[2] && col < r[3]) in = true;
     }
-    if (in) {
+    uint64_t pidx = 0;
+    uint32_t info = 0;
+    if (in && a.pix_info) {
+        pidx = a.pix_off[v] + uint64_t(row) * uint64_t(a.cams[v].image_cols) + uint64_t(col);
+        info = a.pix_info[pidx];
+    }
+    if (in && (info & kMemoDone)) {
+        // solved for an earlier window: only the window test remains
+        if (info & kMemoHit) {
+            int rmin = info & 127, rmax = (info >> 7) & 127, cmin = (info >> 14) & 127, cmax = (info >> 21) & 127;
+            ok = (rmin >= a.win_r0 && rmax <= a.win_r1 && cmin >= a.win_c0 && cmax <= a.win_c1) ? 1u : 0u;
+        }
+    } else if (in) {
         double gx = 0.0, gy = 0.0;
         int st = rpc_localize(a.cams[v], double(row), double(col), hi ? a.z_min : a.z_max, &gx, &gy);
         double ox = __shfl_xor_sync(pair, gx, 1), oy = __shfl_xor_sync(pair, gy, 1);
         int ost = __shfl_xor_sync(pair, st, 1);
         double o[3], d[3];
+        uint32_t memo = kMemoDone;
         if (hi == 0 && st == 0 && ost == 0 &&
             rpc_ray_finish(gx, gy, ox, oy, a.z_min, a.z_max, o, d) == 0) {
             // candidate_tiles (tiler.cpp:70-100): XY shadow between z bounds
@@ -184,6 +197,7 @@ __global__ void __launch_bounds__(128, TFG_ACCEPT_MINB) accept_kernel(AcceptArgs
                     int r0 = cell(a.north, a.grid_rows, nylo), r1 = cell(a.north, a.grid_rows, nyhi);
                     int hits = 0;
                     bool all_loaded = true;
+                    int hr0 = 127, hr1 = 0, hc0 = 127, hc1 = 0;
                     for (int tr = r0; tr <= r1; ++tr)
                         for (int tc = c0; tc <= c1; ++tc) {
                             double box[6] = {a.east[tc],     a.north[tr],     a.z_min,
@@ -191,31 +205,38 @@ __global__ void __launch_bounds__(128, TFG_ACCEPT_MINB) accept_kernel(AcceptArgs
                             double t0, t1;
                             if (!slab(o, d, box, &t0, &t1)) continue;
                             ++hits;
+                            hr0 = tr < hr0 ? tr : hr0;
+                            hr1 = tr > hr1 ? tr : hr1;
+                            hc0 = tc < hc0 ? tc : hc0;
+                            hc1 = tc > hc1 ? tc : hc1;
                             int ti = tr * a.grid_cols + tc;
                             bool ld = false;
                             for (int k = 0; k < a.n_loaded; ++k) ld |= (a.loaded_tile[k] == ti);
                             all_loaded &= ld;
                         }
                     ok = (hits >= 1 && all_loaded) ? 1u : 0u;
-                    if (ok) {  // memoised for the ray draw (bit-identical to raygen's solve)
-                        double* cr = a.cand_rays + 6 * idx;
-                        cr[0] = o[0];
-                        cr[1] = o[1];
-                        cr[2] = o[2];
-                        cr[3] = d[0];
-                        cr[4] = d[1];
-                        cr[5] = d[2];
+                    if (hits >= 1 && a.pix_info) {
+                        memo |= kMemoHit | uint32_t(hr0) | (uint32_t(hr1) << 7) | (uint32_t(hc0) << 14) |
+                                (uint32_t(hc1) << 21);
+                        double* pr = a.pix_rays + 6 * pidx;
+                        pr[0] = o[0];
+                        pr[1] = o[1];
+                        pr[2] = o[2];
+                        pr[3] = d[0];
+                        pr[4] = d[1];
+                        pr[5] = d[2];
                     }
                 }
             }
         }
+        if (hi == 0 && a.pix_info) a.pix_info[pidx] = memo;
     }
     if (hi == 0) flags[idx] = ok;
 }
 
 __global__ void accept_scatter_kernel(AcceptArgs a, const uint32_t* __restrict__ flags,
                                       const uint32_t* __restrict__ pos,
-                                      uint64_t* __restrict__ out, double* __restrict__ out_rays) {
+                                      uint64_t* __restrict__ out) {
     uint64_t idx = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (idx >= a.n_candidates || !flags[idx]) return;
     int v = 0;
@@ -226,10 +247,6 @@ __global__ void accept_scatter_kernel(AcceptArgs a, const uint32_t* __restrict__
     uint64_t row = uint64_t(u[0]) + local / uint64_t(ncols);
     uint64_t col = uint64_t(u[2]) + local % uint64_t(ncols);
     out[pos[idx]] = (uint64_t(v) << 40) | (row << 20) | col;
-    const double* cr = a.cand_rays + 6 * idx;
-    double* orr = out_rays + 6 * uint64_t(pos[idx]);
-#pragma unroll
-    for (int k = 0; k < 6; ++k) orr[k] = cr[k];
 }
 
 // ------------------------------------------------------------------ K1a
@@ -304,13 +321,13 @@ __global__ void __launch_bounds__(128, TFG_RAYGEN_MINB) raygen_kernel(RaygenArgs
     } else {
         uint64_t na = *a.n_accept_dev;
         Rng r(hash_combine(hash_combine(hash_combine(a.seed, kPurposePixels), a.iter), g));
-        uint64_t k = na ? r.below(na) : 0;
-        uint64_t e = na ? a.accept[k] : 0;
+        uint64_t e = na ? a.accept[r.below(na)] : 0;
         v = int(e >> 40);
         row = int((e >> 20) & 0xFFFFF);
         col = int(e & 0xFFFFF);
         if (na == 0 && valid && hi == 0) atomicOr(&status->bits, kStatusRayFail);
-        if (na && a.acc_rays) memo = a.acc_rays + 6 * k;
+        if (na && a.pix_rays)
+            memo = a.pix_rays + 6 * (a.pix_off[v] + uint64_t(row) * uint64_t(a.cams[v].image_cols) + uint64_t(col));
     }
     RayRec R;
     R.view = v;
@@ -545,7 +562,7 @@ __global__ void __launch_bounds__(256) write_kernel(RaygenArgs a, const RayRec* 
 
 // ------------------------------------------------------------------ host launchers
 int launch_accept(const AcceptArgs& a, uint32_t* flags, uint32_t* pos, uint32_t* block_sums,
-                  uint32_t* n_out, uint64_t* out, double* out_rays, cudaStream_t st, uint64_t* launches) {
+                  uint32_t* n_out, uint64_t* out, cudaStream_t st, uint64_t* launches) {
     if (a.n_candidates == 0) {
         cudaMemsetAsync(n_out, 0, 4, st);
         return 0;
@@ -553,7 +570,7 @@ int launch_accept(const AcceptArgs& a, uint32_t* flags, uint32_t* pos, uint32_t*
     int nb = int((a.n_candidates + 127) / 128);
     accept_kernel<<<int((2 * a.n_candidates + 127) / 128), 128, 0, st>>>(a, flags);
     if (scan_exclusive(flags, a.n_candidates, pos, block_sums, n_out, st, launches)) return 1;
-    accept_scatter_kernel<<<nb, 128, 0, st>>>(a, flags, pos, out, out_rays);
+    accept_scatter_kernel<<<nb, 128, 0, st>>>(a, flags, pos, out);
     *launches += 2;
     return 0;
 }

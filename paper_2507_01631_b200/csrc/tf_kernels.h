@@ -38,14 +38,22 @@ struct AcceptArgs {
     int loaded_tile[kTrainSlots];
     int n_loaded;
     double z_min, z_max;
-    double* cand_rays;           // out: o[3], d[3] of every accepted candidate (scratch)
+    // Per-pixel memo of the scene (null: off).  The RPC inversion and the
+    // tile-incidence test of a pixel depend only on the scene, so each pixel
+    // is solved once: info = done | hit | bbox of the hit tiles, rays = o[3], d[3].
+    uint32_t* pix_info;
+    double* pix_rays;
+    const uint64_t* pix_off;     // first pixel of each view
+    int win_r0, win_r1, win_c0, win_c1;  // the loaded tiles' rectangle (inclusive)
 };
+constexpr uint32_t kMemoDone = 1u << 31, kMemoHit = 1u << 30;
 
 struct RaygenArgs {
     const tfg_rpc* cams;
     const uint64_t* accept;  // draw mode: accepted list
     const uint32_t* n_accept_dev;  // its length, read on device (no host sync per move)
-    const double* acc_rays;  // draw mode: o[3], d[3] of each accepted entry (memoised by K0)
+    const double* pix_rays;  // draw mode: per-pixel ray memo of the accept pass (K0)
+    const uint64_t* pix_off;
     const int32_t* pixels;   // pixel mode (render/eval): view,row,col triplets
     const uint8_t* crop_bytes;
     const int* crop_rect;        // r0, c0, cols, rows per view
@@ -128,7 +136,7 @@ struct OccArgs {
 int scan_exclusive(const uint32_t* in, uint64_t n, uint32_t* out, uint32_t* block_sums,
                    uint32_t* grand_total, cudaStream_t st, uint64_t* launches);
 int launch_accept(const AcceptArgs& a, uint32_t* flags, uint32_t* pos, uint32_t* block_sums,
-                  uint32_t* n_out, uint64_t* out, double* out_rays, cudaStream_t st, uint64_t* launches);
+                  uint32_t* n_out, uint64_t* out, cudaStream_t st, uint64_t* launches);
 int launch_sampler(const RaygenArgs& a, RayRec* rays, float4* venc, uint32_t* counts,
                    uint32_t* P, uint32_t* block_sums, TileDesc* tiles, int max_tiles,
                    SampleArrays out, uint64_t capacity, Status* status, cudaStream_t st,

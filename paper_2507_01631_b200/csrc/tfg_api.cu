@@ -97,7 +97,6 @@ struct WinBuf {
     int* d_crop_rect = nullptr;      // r0, c0, cols, rows per view
     uint64_t* d_crop_off = nullptr;  // byte offset of each view's crop
     uint64_t* d_accept = nullptr;    // packed (view, row, col)
-    double* d_acc_rays = nullptr;    // o[3], d[3] per accepted entry (memoised RPC rays)
     uint32_t* d_n = nullptr;         // accepted count (read by the ray draw on device)
     std::vector<int> h_crop_rect;
     std::vector<uint64_t> h_crop_off;
@@ -162,7 +161,11 @@ struct tfg_ctx {
     uint64_t crop_cap = 0, accept_cap = 0, cand_cap = 0;
     // accepted-list build scratch (one build at a time)
     uint32_t *d_flags = nullptr, *d_pos = nullptr, *d_block_sums = nullptr, *d_acc_sums = nullptr;
-    double* d_cand_rays = nullptr;  // accept-pass ray memo per candidate (scratch)
+    // per-pixel memo of the scene (AcceptArgs): state, rays, view offsets
+    uint32_t* d_pix_info = nullptr;
+    double* d_pix_rays = nullptr;
+    uint64_t* d_pix_off = nullptr;
+    uint64_t pix_total = 0;
     uint64_t* d_view_start = nullptr;
     int *d_union = nullptr, *d_crop4 = nullptr;
 
@@ -524,9 +527,27 @@ int stage_window(tfg_ctx* c, WinBuf& w, int pr, int pc, cudaStream_t st) {
     a.n_loaded = int(want.size());
     a.z_min = c->roi.z_min;
     a.z_max = c->roi.z_max;
-    a.cand_rays = c->d_cand_rays;
-    if (launch_accept(a, c->d_flags, c->d_pos, c->d_acc_sums, w.d_n, w.d_accept, w.d_acc_rays, st,
-                      &c->launches))
+    // the memo applies when the loaded tiles form a rectangle (every window does)
+    {
+        int r0 = 1 << 30, r1 = -1, c0 = 1 << 30, c1 = -1;
+        for (int ti : want) {
+            r0 = std::min(r0, ti / c->cols);
+            r1 = std::max(r1, ti / c->cols);
+            c0 = std::min(c0, ti % c->cols);
+            c1 = std::max(c1, ti % c->cols);
+        }
+        bool rect = !want.empty() && int(want.size()) == (r1 - r0 + 1) * (c1 - c0 + 1);
+        if (rect && c->d_pix_info) {
+            a.pix_info = c->d_pix_info;
+            a.pix_rays = c->d_pix_rays;
+            a.pix_off = c->d_pix_off;
+            a.win_r0 = r0;
+            a.win_r1 = r1;
+            a.win_c0 = c0;
+            a.win_c1 = c1;
+        }
+    }
+    if (launch_accept(a, c->d_flags, c->d_pos, c->d_acc_sums, w.d_n, w.d_accept, st, &c->launches))
         return fail(TFG_ERR_INVALID, "accept: scan capacity exceeded");
     CK(cudaGetLastError());
     CK(cudaEventRecord(w.ready, st));
@@ -874,7 +895,7 @@ TFG_API int tfg_destroy(tfg_ctx* c) {
                    c->d_rays, c->d_venc,
                    c->d_counts, c->d_P, c->d_tiles, c->s.local, c->s.td, c->s.endpoint, c->s.io,
                    c->d_ray_out, c->d_pixels, c->d_rparams, c->d_rbits, c->d_rcolor, c->d_rcam,
-                   c->d_feat, c->d_tile_rays, c->d_export, c->d_cand_rays};
+                   c->d_feat, c->d_tile_rays, c->d_export, c->d_pix_info, c->d_pix_rays, c->d_pix_off};
     for (void* p : dev)
         if (p) cudaFree(p);
     stop_init_pool(c);
@@ -883,7 +904,7 @@ TFG_API int tfg_destroy(tfg_ctx* c) {
         if (im) cudaFreeHost(im);
     if (c->h_status) cudaFreeHost(c->h_status);
     for (WinBuf& w : c->win) {
-        void* wo[] = {w.d_crops, w.d_crop_rect, w.d_crop_off, w.d_accept, w.d_n, w.d_acc_rays};
+        void* wo[] = {w.d_crops, w.d_crop_rect, w.d_crop_off, w.d_accept, w.d_n};
         for (void* p : wo)
             if (p) cudaFree(p);
         if (w.ready) cudaEventDestroy(w.ready);
@@ -973,17 +994,16 @@ TFG_API int tfg_set_scene(tfg_ctx* c, const tfg_rpc* cams, int n_views,
     c->crop_cap = cropb;
     int rc = 0;
     void* olds[] = {c->d_cams, c->d_east, c->d_north, c->d_flags, c->d_pos, c->d_view_start,
-                    c->d_union, c->d_crop4, c->d_cand_rays};
+                    c->d_union, c->d_crop4, c->d_pix_info, c->d_pix_rays, c->d_pix_off};
     for (void* p : olds)
         if (p) cudaFree(p);
     rc |= dalloc(c, &c->d_cams, n_views);
     rc |= dalloc(c, &c->d_east, grid_cols + 1);
     rc |= dalloc(c, &c->d_north, grid_rows + 1);
     for (WinBuf& w : c->win) {
-        void* wo[] = {w.d_crops, w.d_crop_rect, w.d_crop_off, w.d_accept, w.d_n, w.d_acc_rays};
+        void* wo[] = {w.d_crops, w.d_crop_rect, w.d_crop_off, w.d_accept, w.d_n};
         for (void* p : wo)
             if (p) cudaFree(p);
-        rc |= dalloc(c, &w.d_acc_rays, 6 * c->accept_cap);
         rc |= dalloc(c, &w.d_crops, c->crop_cap);
         rc |= dalloc(c, &w.d_crop_rect, 4 * n_views);
         rc |= dalloc(c, &w.d_crop_off, n_views);
@@ -993,12 +1013,44 @@ TFG_API int tfg_set_scene(tfg_ctx* c, const tfg_rpc* cams, int n_views,
         w.pos_r = w.pos_c = -1;
     }
     rc |= dalloc(c, &c->d_flags, c->cand_cap);
-    rc |= dalloc(c, &c->d_cand_rays, 6 * c->cand_cap);
     rc |= dalloc(c, &c->d_pos, c->cand_cap + 1);
     rc |= dalloc(c, &c->d_view_start, n_views);
     rc |= dalloc(c, &c->d_union, 4 * n_views);
     rc |= dalloc(c, &c->d_crop4, 4 * n_views * kTrainSlots);
     if (rc) return TFG_ERR_CUDA;
+    // per-pixel memo (52 B per image pixel, e.g. 2.3 GB for config 5): sized
+    // for HBM; skipped (pixels re-solved per window) if it does not fit
+    c->d_pix_info = nullptr;
+    c->d_pix_rays = nullptr;
+    c->d_pix_off = nullptr;
+    c->pix_total = 0;
+    {
+        std::vector<uint64_t> off(n_views);
+        uint64_t tot = 0;
+        for (int v = 0; v < n_views; ++v) {
+            off[v] = tot;
+            tot += uint64_t(cams[v].image_rows) * uint64_t(cams[v].image_cols);
+        }
+        size_t fr = 0, total = 0;
+        cudaMemGetInfo(&fr, &total);
+        bool fits = grid_rows <= 128 && grid_cols <= 128 && tot * 52 + (size_t(4) << 30) < fr;
+        if (fits && cudaMalloc(&c->d_pix_info, tot * 4) == cudaSuccess &&
+            cudaMalloc(&c->d_pix_rays, tot * 48) == cudaSuccess &&
+            cudaMalloc(&c->d_pix_off, n_views * 8) == cudaSuccess) {
+            c->pix_total = tot;
+            CK(cudaMemsetAsync(c->d_pix_info, 0, tot * 4, c->st));
+            CK(cudaMemcpyAsync(c->d_pix_off, off.data(), n_views * 8, cudaMemcpyHostToDevice, c->st));
+            CK(cudaStreamSynchronize(c->st));
+        } else {
+            cudaGetLastError();
+            for (void* p : {static_cast<void*>(c->d_pix_info), static_cast<void*>(c->d_pix_rays),
+                            static_cast<void*>(c->d_pix_off)})
+                if (p) cudaFree(p);
+            c->d_pix_info = nullptr;
+            c->d_pix_rays = nullptr;
+            c->d_pix_off = nullptr;
+        }
+    }
     CK(cudaMemcpyAsync(c->d_cams, c->cams.data(), n_views * sizeof(tfg_rpc), cudaMemcpyHostToDevice, c->st));
     CK(cudaMemcpyAsync(c->d_east, c->east.data(), (grid_cols + 1) * 8, cudaMemcpyHostToDevice, c->st));
     CK(cudaMemcpyAsync(c->d_north, c->north.data(), (grid_rows + 1) * 8, cudaMemcpyHostToDevice, c->st));
@@ -1159,7 +1211,8 @@ TFG_API int tfg_sample(tfg_ctx* c, uint64_t iter, uint64_t ray_begin, int n_rays
     RaygenArgs a = base_raygen(c);
     a.accept = c->win[c->front].d_accept;
     a.n_accept_dev = c->win[c->front].d_n;
-    a.acc_rays = c->win[c->front].d_acc_rays;
+    a.pix_rays = c->d_pix_rays;
+    a.pix_off = c->d_pix_off;
     a.iter = iter;
     a.ray_begin = ray_begin;
     a.n_rays = n_rays;
@@ -1513,7 +1566,7 @@ TFG_API int tfg_get_memory_report(tfg_ctx* c, tfg_memory_report* o) {
     o->optimizer_moments = 2 * kTrainSlots * c->stride * 4 + kTrainSlots * c->stride * 4;  // m, v, grads
     o->occupancy = uint64_t(kTrainSlots) * kOccVox * 4 + uint64_t(kMaxSlots) * kOccWords * 4;
     o->crops = 2 * c->crop_cap;
-    o->accept_list = 2 * c->accept_cap * (8 + 48) + c->cand_cap * (8 + 48);  // lists + ray memo
+    o->accept_list = 2 * c->accept_cap * 8 + c->cand_cap * 8 + c->pix_total * (4 + 48);  // lists + pixel memo
     o->batch_buffers = uint64_t(c->max_rays) * (sizeof(RayRec) + 96 + 8 * kMaxSlots + 20 + 12) +
                        c->sample_cap * (16 + 8 + 1 + 16);
     o->color_net = (c->n_params - c->color_off) * 4;
