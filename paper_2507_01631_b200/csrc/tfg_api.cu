@@ -1033,7 +1033,9 @@ TFG_API int tfg_set_scene(tfg_ctx* c, const tfg_rpc* cams, int n_views,
         }
         size_t fr = 0, total = 0;
         cudaMemGetInfo(&fr, &total);
-        bool fits = grid_rows <= 128 && grid_cols <= 128 && tot * 52 + (size_t(4) << 30) < fr;
+        const char* off_env = std::getenv("TFG_NO_PIXEL_MEMO");  // A/B + the memo-off parity test
+        bool fits = grid_rows <= 128 && grid_cols <= 128 && tot * 52 + (size_t(4) << 30) < fr &&
+                    !(off_env && off_env[0] == '1');
         if (fits && cudaMalloc(&c->d_pix_info, tot * 4) == cudaSuccess &&
             cudaMalloc(&c->d_pix_rays, tot * 48) == cudaSuccess &&
             cudaMalloc(&c->d_pix_off, n_views * 8) == cudaSuccess) {

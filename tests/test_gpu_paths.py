@@ -183,3 +183,42 @@ def test_nonfinite_gradient_names_the_group():
     # the step was not applied and the step counters were rolled back
     np.testing.assert_array_equal(after["enc"], before["enc"])
     assert after["enc_step"] == before["enc_step"]
+
+
+def test_pixel_memo_matches_resolving():
+    """The per-pixel scene memo (rays + hit-tile bbox) gives the same accepted
+    lists and batches as re-solving every pixel per window (memo disabled via
+    TFG_NO_PIXEL_MEMO in a subprocess), along a snake that revisits pixels."""
+    _need_gpu()
+    import json
+    import os
+    import subprocess
+    import sys
+
+    code = r"""
+import json, sys
+import numpy as np
+sys.path.insert(0, %r)
+from paper_2507_01631_b200 import synth
+from paper_2507_01631_b200.abi import FieldConfig, TrainConfig
+from paper_2507_01631_b200.tilefield import Context, snake_path
+scene = synth.make_scene(3, 3, tile_side=96.0, n_views=3, gsd=1.0, seed=21, max_off_nadir=30.0)
+ctx = Context(scene, FieldConfig.defaults(), TrainConfig.defaults(batch_rays=2048, seed=5), max_rays=2048)
+out = []
+for it, pos in enumerate(snake_path(3, 3) + [(0, 0), (1, 1)]):
+    ctx.set_window(*pos)
+    acc = ctx.accept_list()
+    ctx.sample(it, 0, 2048, True)
+    b = ctx.batch()
+    out.append([int(acc.size), int(np.bitwise_xor.reduce(acc)) if acc.size else 0,
+                float(b["rays"]["origin"].sum()), float(b["t"].sum()), int(b["offsets"][-1])])
+print(json.dumps(out))
+""" % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for memo in ("0", "1"):
+        env = dict(os.environ, TFG_NO_PIXEL_MEMO=memo)
+        p = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+        assert p.returncode == 0, p.stderr[-2000:]
+        res[memo] = json.loads(p.stdout.strip().splitlines()[-1])
+    assert res["0"] == res["1"]
+    assert all(r[0] > 0 for r in res["0"])
