@@ -232,6 +232,23 @@ TFG_API int tfg_get_grads(tfg_ctx* ctx, int slot, float* enc, float* dnet, float
 TFG_API int tfg_update_occupancy(tfg_ctx* ctx);
 TFG_API int tfg_get_memory_report(tfg_ctx* ctx, tfg_memory_report* out);
 
+/* ---- evaluation (evalio; §8(f) row 2) --------------------
+ * Host buffers in, computed on the context's GPU (FP64 sums).
+ *   psnr: a, b hold n values in [0,1]; 10 log10(1/MSE), capped at 99 dB.
+ *   ssim: rows x cols x 3 RGB; grey = channel mean, 11x11 Gaussian sigma 1.5,
+ *         K1 0.01, K2 0.03, L 1; mean over the valid windows.
+ *   depth_mae: mean |d1 - d2| over mask != 0 (mask may be NULL = all).
+ *   edge_band_mask: 1 within +-band_px of the projected tile edges (the grid
+ *         boundary lines at z_min and z_max) in view `cam`, else 0.
+ *   render_view: full-frame render of `cam` (row-major, every pixel) through
+ *         the render path (render_setup first). */
+TFG_API int tfg_psnr(tfg_ctx* ctx, const float* a, const float* b, uint64_t n, double* db);
+TFG_API int tfg_ssim(tfg_ctx* ctx, const float* a, const float* b, int rows, int cols, double* ssim);
+TFG_API int tfg_depth_mae(tfg_ctx* ctx, const float* d1, const float* d2, const uint8_t* mask, uint64_t n,
+                          double* mae);
+TFG_API int tfg_edge_band_mask(tfg_ctx* ctx, const tfg_rpc* cam, int band_px, uint8_t* mask);
+TFG_API int tfg_render_view(tfg_ctx* ctx, const tfg_rpc* cam, float* rgb, float* depth, float* opacity);
+
 /* ---- checkpoints (save/load_tile_checkpoint, save/load_color_checkpoint,
  * field.hpp:202-210) ---------------------------------------
  * Versioned little-endian binary: "TFCKPT01" | u32 version (1) | u32 kind

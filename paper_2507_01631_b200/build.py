@@ -29,6 +29,7 @@ UNITS = [
     ("k_field.cu", []),
     ("k_field_tc.cu", []),
     ("k_composite.cu", []),
+    ("k_eval.cu", ["-fmad=false"]),
 ]
 
 

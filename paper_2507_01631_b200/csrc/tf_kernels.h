@@ -150,4 +150,14 @@ void launch_adam(const AdamArgs& a, uint64_t total, cudaStream_t st, uint64_t* l
 void launch_occupancy(const OccArgs& a, cudaStream_t st, uint64_t* launches);
 
 
+// evaluation metrics (k_eval.cu)
+void launch_sq_diff(const float* a, const float* b, uint64_t n, double* out, int sms, cudaStream_t st);
+void launch_abs_diff(const float* a, const float* b, const uint8_t* mask, uint64_t n, double* out, int sms,
+                     cudaStream_t st);
+void launch_ssim(const float* a, const float* b, int rows, int cols, const float* gw, double* out,
+                 cudaStream_t st);
+void launch_edge_band(const tfg_rpc* cam, const double* east, const double* north, int grid_rows,
+                      int grid_cols, double z0, double z1, double step, uint64_t per_line, int band,
+                      uint8_t* mask, cudaStream_t st);
+
 } // namespace tfg

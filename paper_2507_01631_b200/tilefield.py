@@ -102,6 +102,11 @@ def lib() -> C.CDLL:
         "tfg_save_color_checkpoint": [C.c_char_p, _vp, _vp, _vp, _vp, C.c_uint64],
         "tfg_load_color_checkpoint": [C.c_char_p, _vp, _vp, _vp, _vp, _vp],
         "tfg_save_run": [_vp, C.c_char_p],
+        "tfg_psnr": [_vp, _vp, _vp, C.c_uint64, _vp],
+        "tfg_ssim": [_vp, _vp, _vp, C.c_int, C.c_int, _vp],
+        "tfg_depth_mae": [_vp, _vp, _vp, _vp, C.c_uint64, _vp],
+        "tfg_edge_band_mask": [_vp, _vp, C.c_int, _vp],
+        "tfg_render_view": [_vp, _vp, _vp, _vp, _vp],
         "tfg_load_run": [_vp, C.c_char_p],
     }
     for name, args in sig.items():
@@ -408,3 +413,46 @@ class Context:
         rgb, dep, op = np.zeros(3 * n, np.float32), np.zeros(n, np.float32), np.zeros(n, np.float32)
         _check(lib().tfg_render_pixels(self.h, C.byref(cam), ptr(px), n, ptr(rgb), ptr(dep), ptr(op)))
         return rgb.reshape(n, 3), dep, op
+
+    def render_view(self, cam: Rpc):
+        """Full-frame render of `cam` (cmd_render): (rows, cols, 3)
+        rgb, (rows, cols) depth and opacity."""
+        R, W = cam.image_rows, cam.image_cols
+        rgb = np.zeros((R, W, 3), np.float32)
+        dep, op = np.zeros((R, W), np.float32), np.zeros((R, W), np.float32)
+        _check(lib().tfg_render_view(self.h, C.byref(cam), ptr(rgb), ptr(dep), ptr(op)))
+        return rgb, dep, op
+
+    # ---- evaluation (evalio, SPEC.md:582-608) ---------------------------------
+    def psnr(self, a, b) -> float:
+        a = np.ascontiguousarray(a, np.float32)
+        b = np.ascontiguousarray(b, np.float32)
+        if a.shape != b.shape:
+            raise TileFieldError("psnr: shape mismatch")
+        out = C.c_double()
+        _check(lib().tfg_psnr(self.h, ptr(a), ptr(b), a.size, C.byref(out)))
+        return out.value
+
+    def ssim(self, a, b) -> float:
+        a = np.ascontiguousarray(a, np.float32)
+        b = np.ascontiguousarray(b, np.float32)
+        if a.shape != b.shape or a.ndim != 3 or a.shape[2] != 3:
+            raise TileFieldError("ssim: expects two (rows, cols, 3) images")
+        out = C.c_double()
+        _check(lib().tfg_ssim(self.h, ptr(a), ptr(b), a.shape[0], a.shape[1], C.byref(out)))
+        return out.value
+
+    def depth_mae(self, d1, d2, mask=None) -> float:
+        d1 = np.ascontiguousarray(d1, np.float32)
+        d2 = np.ascontiguousarray(d2, np.float32)
+        if d1.shape != d2.shape:
+            raise TileFieldError("depth_mae: shape mismatch")
+        m = None if mask is None else np.ascontiguousarray(mask, np.uint8)
+        out = C.c_double()
+        _check(lib().tfg_depth_mae(self.h, ptr(d1), ptr(d2), ptr(m), d1.size, C.byref(out)))
+        return out.value
+
+    def edge_band_mask(self, cam: Rpc, band_px: int = 8) -> np.ndarray:
+        m = np.zeros((cam.image_rows, cam.image_cols), np.uint8)
+        _check(lib().tfg_edge_band_mask(self.h, C.byref(cam), band_px, ptr(m)))
+        return m
