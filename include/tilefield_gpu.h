@@ -232,6 +232,22 @@ TFG_API int tfg_get_grads(tfg_ctx* ctx, int slot, float* enc, float* dnet, float
 TFG_API int tfg_update_occupancy(tfg_ctx* ctx);
 TFG_API int tfg_get_memory_report(tfg_ctx* ctx, tfg_memory_report* out);
 
+/* ---- crop cache (build_crop_cache; §8(f) row 3) --------
+ * Per-(view, tile) crop rasters of the scene (crop_for_tile, camera.cpp:
+ * 126-146, with TrainConfig.margin_px) and an index, little-endian:
+ *   "TFCROP01" | u32 version (1) | u32 n_views | u32 grid_rows | u32 grid_cols
+ *   | i32 margin_px | u32 0 | u64 n_entries | u64 data_offset
+ *   | n_entries x { i32 view, tile_row, tile_col, r0, r1, c0, c1, 0;
+ *                   u64 offset, u64 bytes }      (view-major, then row, col)
+ *   | u8 RGB crops, row-major, at data_offset + offset.
+ * Empty crops have r0 = r1 = c0 = c1 = 0 and 0 bytes.  load_crop_cache
+ * rejects a cache whose grid, margin or any rect differs from this scene's,
+ * then fills the pinned host images (after set_scene, which may take NULL
+ * images) so that training reads only cached crops. */
+TFG_API int tfg_build_crop_cache(tfg_ctx* ctx, const char* path, uint64_t* total_crop_bytes);
+TFG_API int tfg_load_crop_cache(tfg_ctx* ctx, const char* path);
+TFG_API int tfg_crop_rect(tfg_ctx* ctx, int view, int tile_row, int tile_col, int32_t* r0r1c0c1);
+
 /* ---- evaluation (evalio; §8(f) row 2) --------------------
  * Host buffers in, computed on the context's GPU (FP64 sums).
  *   psnr: a, b hold n values in [0,1]; 10 log10(1/MSE), capped at 99 dB.

@@ -2091,3 +2091,124 @@ TFG_API int tfg_render_view(tfg_ctx* c, const tfg_rpc* cam, float* rgb, float* d
 }
 
 } // extern "C"
+
+// ---------------------------------------------------------------- crop cache
+namespace {
+constexpr char kCropMagic[8] = {'T', 'F', 'C', 'R', 'O', 'P', '0', '1'};
+struct CropEntry {
+    int32_t view, row, col, r0, r1, c0, c1, pad;
+    uint64_t offset, bytes;
+};
+static_assert(sizeof(CropEntry) == 48, "crop index entry");
+
+void crop_index(const tfg_ctx* c, std::vector<CropEntry>& idx) {
+    idx.clear();
+    uint64_t off = 0;
+    for (int v = 0; v < c->n_views; ++v)
+        for (int ti = 0; ti < c->rows * c->cols; ++ti) {
+            CropEntry e{};
+            e.view = v;
+            e.row = ti / c->cols;
+            e.col = ti % c->cols;
+            double b[6];
+            tile_box(c, ti, b);
+            Crop cr;
+            if (crop_for_tile(c->cams[v], b, c->tc.margin_px, &cr)) {
+                e.r0 = cr.r0;
+                e.r1 = cr.r1;
+                e.c0 = cr.c0;
+                e.c1 = cr.c1;
+                e.offset = off;
+                e.bytes = uint64_t(cr.r1 - cr.r0) * uint64_t(cr.c1 - cr.c0) * 3;
+                off += e.bytes;
+            }
+            idx.push_back(e);
+        }
+}
+} // namespace
+
+extern "C" {
+
+TFG_API int tfg_crop_rect(tfg_ctx* c, int view, int row, int col, int32_t* out) {
+    if (!c || c->n_views == 0) return fail(TFG_ERR_STATE, "crop_rect: call set_scene first");
+    if (view < 0 || view >= c->n_views || row < 0 || row >= c->rows || col < 0 || col >= c->cols || !out)
+        return fail(TFG_ERR_INVALID, "crop_rect: bad view or tile");
+    double b[6];
+    tile_box(c, row * c->cols + col, b);
+    Crop cr;
+    if (!crop_for_tile(c->cams[view], b, c->tc.margin_px, &cr)) cr = Crop{};
+    out[0] = cr.r0;
+    out[1] = cr.r1;
+    out[2] = cr.c0;
+    out[3] = cr.c1;
+    return 0;
+}
+
+TFG_API int tfg_build_crop_cache(tfg_ctx* c, const char* path, uint64_t* total) {
+    if (!c || c->n_views == 0) return fail(TFG_ERR_STATE, "build_crop_cache: call set_scene first");
+    std::vector<CropEntry> idx;
+    crop_index(c, idx);
+    std::ofstream f(path, std::ios::binary);
+    if (!f) return fail(TFG_ERR_INVALID, std::string("crop cache: cannot open ") + path);
+    uint32_t hdr32[6] = {1u, uint32_t(c->n_views), uint32_t(c->rows), uint32_t(c->cols),
+                         uint32_t(c->tc.margin_px), 0u};
+    uint64_t n = idx.size(), data_off = 8 + sizeof(hdr32) + 16 + n * sizeof(CropEntry);
+    f.write(kCropMagic, 8);
+    f.write(reinterpret_cast<const char*>(hdr32), sizeof(hdr32));
+    f.write(reinterpret_cast<const char*>(&n), 8);
+    f.write(reinterpret_cast<const char*>(&data_off), 8);
+    f.write(reinterpret_cast<const char*>(idx.data()), n * sizeof(CropEntry));
+    uint64_t tot = 0;
+    for (const CropEntry& e : idx) {
+        if (!e.bytes) continue;
+        const uint8_t* im = c->h_images[e.view];
+        size_t W = size_t(c->cams[e.view].image_cols);
+        for (int r = e.r0; r < e.r1; ++r)
+            f.write(reinterpret_cast<const char*>(im + 3 * (size_t(r) * W + size_t(e.c0))),
+                    std::streamsize(3 * (e.c1 - e.c0)));
+        tot += e.bytes;
+    }
+    if (!f.good()) return fail(TFG_ERR_INVALID, std::string("crop cache: write failed for ") + path);
+    if (total) *total = tot;
+    return 0;
+}
+
+TFG_API int tfg_load_crop_cache(tfg_ctx* c, const char* path) {
+    if (!c || c->n_views == 0) return fail(TFG_ERR_STATE, "load_crop_cache: call set_scene first");
+    if (c->nslots) return fail(TFG_ERR_STATE, "load_crop_cache: call before the first set_window");
+    std::ifstream f(path, std::ios::binary);
+    if (!f) return fail(TFG_ERR_INVALID, std::string("crop cache: cannot open ") + path);
+    char magic[8];
+    uint32_t hdr32[6];
+    uint64_t n = 0, data_off = 0;
+    f.read(magic, 8);
+    f.read(reinterpret_cast<char*>(hdr32), sizeof(hdr32));
+    f.read(reinterpret_cast<char*>(&n), 8);
+    f.read(reinterpret_cast<char*>(&data_off), 8);
+    if (!f.good() || std::memcmp(magic, kCropMagic, 8) != 0 || hdr32[0] != 1u)
+        return fail(TFG_ERR_INVALID, std::string("crop cache: bad header in ") + path);
+    if (hdr32[1] != uint32_t(c->n_views) || hdr32[2] != uint32_t(c->rows) || hdr32[3] != uint32_t(c->cols) ||
+        hdr32[4] != uint32_t(c->tc.margin_px))
+        return fail(TFG_ERR_INVALID, "crop cache: views / grid / margin differ from the scene");
+    std::vector<CropEntry> want, got(n);
+    crop_index(c, want);
+    f.read(reinterpret_cast<char*>(got.data()), std::streamsize(n * sizeof(CropEntry)));
+    if (!f.good() || n != want.size() ||
+        std::memcmp(got.data(), want.data(), n * sizeof(CropEntry)) != 0)
+        return fail(TFG_ERR_INVALID, "crop cache: index differs from this scene's crop_for_tile rects");
+    std::vector<uint8_t> buf;
+    for (const CropEntry& e : got) {
+        if (!e.bytes) continue;
+        buf.resize(e.bytes);
+        f.seekg(std::streamoff(data_off + e.offset));
+        f.read(reinterpret_cast<char*>(buf.data()), std::streamsize(e.bytes));
+        if (!f.good()) return fail(TFG_ERR_INVALID, std::string("crop cache: truncated ") + path);
+        uint8_t* im = c->h_images[e.view];
+        size_t W = size_t(c->cams[e.view].image_cols), w3 = size_t(3 * (e.c1 - e.c0));
+        for (int r = e.r0; r < e.r1; ++r)
+            std::memcpy(im + 3 * (size_t(r) * W + size_t(e.c0)), buf.data() + size_t(r - e.r0) * w3, w3);
+    }
+    return 0;
+}
+
+} // extern "C"

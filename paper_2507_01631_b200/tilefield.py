@@ -108,6 +108,9 @@ def lib() -> C.CDLL:
         "tfg_edge_band_mask": [_vp, _vp, C.c_int, _vp],
         "tfg_render_view": [_vp, _vp, _vp, _vp, _vp],
         "tfg_load_run": [_vp, C.c_char_p],
+        "tfg_build_crop_cache": [_vp, C.c_char_p, _vp],
+        "tfg_load_crop_cache": [_vp, C.c_char_p],
+        "tfg_crop_rect": [_vp, C.c_int, C.c_int, C.c_int, _vp],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -200,8 +203,10 @@ class Context:
             _check(lib().tfg_set_stream(self.h, C.c_void_p(stream)))
         self.scene = scene
         self._cams = (Rpc * scene.n_views)(*scene.cams)
-        imgs = [np.ascontiguousarray(im) for im in scene.images]
-        imgp = (C.c_void_p * scene.n_views)(*[im.ctypes.data for im in imgs])
+        # images may be None: the pinned host images start black and a crop
+        # cache (load_crop_cache) fills the only pixels training reads
+        imgs = [None if im is None else np.ascontiguousarray(im) for im in (scene.images or [None] * scene.n_views)]
+        imgp = (C.c_void_p * scene.n_views)(*[None if im is None else im.ctypes.data for im in imgs])
         _check(lib().tfg_set_scene(self.h, self._cams, scene.n_views, imgp, C.byref(scene.roi),
                                    scene.grid_rows, scene.grid_cols))
         self.n_rays = 0
@@ -422,6 +427,25 @@ class Context:
         dep, op = np.zeros((R, W), np.float32), np.zeros((R, W), np.float32)
         _check(lib().tfg_render_view(self.h, C.byref(cam), ptr(rgb), ptr(dep), ptr(op)))
         return rgb, dep, op
+
+    # ---- crop cache (build_crop_cache) ------------------------
+    def build_crop_cache(self, path: str) -> int:
+        """Writes every (view, tile) crop of the scene + an index; returns the
+        total crop bytes."""
+        n = C.c_uint64()
+        _check(lib().tfg_build_crop_cache(self.h, os.fsencode(path), C.byref(n)))
+        return n.value
+
+    def load_crop_cache(self, path: str) -> None:
+        """Fills the pinned host images from a crop cache of this scene (before
+        the first set_window); training then reads only cached crops."""
+        _check(lib().tfg_load_crop_cache(self.h, os.fsencode(path)))
+
+    def crop_rect(self, view: int, row: int, col: int):
+        """crop_for_tile of (view, tile) as (r0, r1, c0, c1); None if empty."""
+        r = np.zeros(4, np.int32)
+        _check(lib().tfg_crop_rect(self.h, view, row, col, ptr(r)))
+        return None if r[0] >= r[1] or r[2] >= r[3] else tuple(int(x) for x in r)
 
     # ---- evaluation (evalio, SPEC.md:582-608) ---------------------------------
     def psnr(self, a, b) -> float:
