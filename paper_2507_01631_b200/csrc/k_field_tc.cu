@@ -188,10 +188,6 @@ __global__ void __launch_bounds__(128) hash_fwd_kernel(FieldArgs a, uint8_t* __r
 // ------------------------------------------------------------------ K4a
 // Hash-table scatter-add (HashGridT::backward, nn.hpp:231-245), run by the
 // backward's scatter warps.
-#ifndef TFG_FUSED_GATHER
-#define TFG_FUSED_GATHER 0
-#endif
-
 // Pair-vectorised scatter of one level's 8 corners (see hash_encode): one
 // red.global.add.v4.f32 for an aligned x-neighbour pair, else two v2.
 __device__ __forceinline__ void scatter_pairs(float* __restrict__ genc, const Corner& c, float d0,
@@ -371,40 +367,29 @@ __global__ void __launch_bounds__(128, 4) mlp_fwd_kernel(FieldArgs a, const uint
     const uint32_t tmem = tmem_slot;
     const uint32_t id64 = umma::idesc_bf16(128, 64, 0, 0);
     const uint32_t id16 = umma::idesc_bf16(128, 16, 0, 0);
+    // the next tile's descriptor and ray ids are loaded one tile ahead (their
+    // latency was the largest single stall of the chain)
+    TileDesc td_next{};
+    int ray_next = -1;
+    if (blockIdx.x < n_tiles) {
+        td_next = a.tiles[blockIdx.x];
+        ray_next = rays[uint64_t(blockIdx.x) * kT + r];
+    }
     for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-        TileDesc td = a.tiles[t];
+        const TileDesc td = td_next;
+        const int ray = ray_next;
+        if (t + gridDim.x < n_tiles) {
+            td_next = a.tiles[t + gridDim.x];
+            ray_next = rays[uint64_t(t + gridDim.x) * kT + r];
+        }
         if (td.slot != cur) {
             stage_density(W, a.f.dnet[td.slot]);
             cur = td.slot;
         }
-#if TFG_FUSED_GATHER
-        // hash gather of this row straight into the X0 operand tile; the tile
-        // (and the ray id) also goes to global memory for the backward pass
-        int ray = -1;
-        {
-            float f[kFeatDim];
-            if (r < td.n) {
-                float4 L = a.s.local[uint64_t(td.start) + r];
-                ray = __float_as_int(L.w);
-                hash_encode(a.hl, a.f.enc[td.slot], L.x, L.y, L.z, f);
-            } else {
-#pragma unroll
-                for (int i = 0; i < kFeatDim; ++i) f[i] = 0.f;
-            }
-            st_chunk(X0, r, 0, f);
-            st_chunk(X0, r, 1, f + 8);
-            uint8_t* gbase = const_cast<uint8_t*>(feat) + uint64_t(t) * kFeatTile;
-            st_chunk(gbase, r, 0, f);
-            st_chunk(gbase, r, 1, f + 8);
-            const_cast<int32_t*>(rays)[uint64_t(t) * kT + r] = ray;
-        }
-#else
         if (r == 0) {
             umma::mbar_expect_tx(&bar_ld, kFeatTile);
             umma::bulk_g2s(X0, feat + uint64_t(t) * kFeatTile, kFeatTile, &bar_ld);
         }
-        int ray = rays[uint64_t(t) * kT + r];
-#endif
         float ve[kViewDim];
         {
             const float4* v4 = a.venc + uint64_t(ray < 0 ? 0 : ray) * 6;
@@ -418,10 +403,8 @@ __global__ void __launch_bounds__(128, 4) mlp_fwd_kernel(FieldArgs a, const uint
             }
         }
         sync_for_mma();  // density weights staged, previous tile's TMEM reads done
-#if !TFG_FUSED_GATHER
         umma::mbar_wait(&bar_ld, ph_ld);
         ph_ld ^= 1u;
-#endif
         // ---- density layer 1: [128x16] x W1d^T -> 64
         if (r == 0) {
             umma::mma(tmem, kmaj(X0, kT, 0), kmaj(W.w1d, kW1dRows, 0), id64, 0);
@@ -968,14 +951,9 @@ void launch_field_forward_tc(const FieldArgs& a, uint8_t* feat, int32_t* rays, i
         cudaFuncSetAttribute(mlp_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kFwdSmem));
         attr = true;
     }
-#if TFG_FUSED_GATHER
-    mlp_fwd_kernel<<<sms * 4, 128, kFwdSmem, st>>>(a, feat, rays);
-    *launches += 1;
-#else
     hash_fwd_kernel<<<sms * 8, 128, 0, st>>>(a, feat, rays);
     mlp_fwd_kernel<<<sms * 4, 128, kFwdSmem, st>>>(a, feat, rays);  // 4 resident per SM
     *launches += 2;
-#endif
 }
 
 void launch_field_backward_tc(const FieldArgs& a, const FieldGradArgs& g, uint8_t* feat,
