@@ -26,6 +26,8 @@ UNITS = [
     ("k_sampler.cu", ["-fmad=false"]),
     ("k_adam.cu", ["-fmad=false"]),
     ("tfg_api.cu", ["-fmad=false"]),
+    ("tfg_io.cu", ["-fmad=false"]),
+    ("tfg_eval.cu", ["-fmad=false"]),
     ("k_field.cu", []),
     ("k_field_tc.cu", []),
     ("k_composite.cu", []),

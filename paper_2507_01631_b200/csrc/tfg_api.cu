@@ -2,6 +2,8 @@
 // context and HBM layout, scene + crops, the out-of-core window slide
 // (scheduler advance) between pinned host records and HBM on a
 // side stream, the training-iteration driver and the render path.
+// Persistence is in tfg_io.cu, evaluation in tfg_eval.cu (shared internals:
+// tfg_internal.h).
 //
 // HBM layout (allocated once in tfg_create / tfg_set_scene; constant across
 // the snake progression):
@@ -13,26 +15,10 @@
 //   batch                  : RayRec per ray, 24-float view encoding per ray,
 //                            slot-bucketed SoA samples (local+ray, t+delta,
 //                            endpoint, sigma/rgb -> dsigma/drgb)
-#include <cuda_runtime.h>
+#include "tfg_internal.h"
 
-#include <algorithm>
-#include <atomic>
-#include <memory>
-#include <thread>
-#include <cmath>
-#include <cstdio>
-#include <fstream>
-#include <cstdlib>
-#include <cstring>
-#include <string>
-#include <vector>
-
-#include "tf_common.cuh"
-#include "tf_kernels.h"
-
-using namespace tfg;
-
-namespace {
+namespace tfg {
+namespace host {
 
 thread_local std::string g_err;
 
@@ -40,13 +26,6 @@ int fail(int code, const std::string& msg) {
     g_err = msg;
     return code;
 }
-
-#define CK(call)                                                                            \
-    do {                                                                                    \
-        cudaError_t e_ = (call);                                                            \
-        if (e_ != cudaSuccess)                                                              \
-            return fail(TFG_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
-    } while (0)
 
 // ---------------------------------------------------------------- host-side field init
 // TileField::create / GlobalColorNet::create (field.hpp:93,118) with the
@@ -67,154 +46,6 @@ int level_resolution(const tfg_field_config& c, int l) {
     double b = std::exp((std::log(double(c.n_max)) - std::log(double(c.n_min))) /
                         double(c.levels - 1));
     return int(std::floor(c.n_min * std::pow(b, l) + 0.5));
-}
-
-struct TileHost {
-    bool created = false;
-    float* rec = nullptr;  // pinned: [params(stride) | m(stride) | v(stride) | ema(32^3)]
-    uint64_t enc_step = 0, dnet_step = 0;
-};
-
-// Background TileField::create of the host records (the Rng stream of a tile
-// is inherently sequential: 434k draws whose state is the previous output).
-// Workers initialise tiles in snake first-visit order; ensure_record waits
-// for a tile that is not ready yet.
-struct InitPool {
-    std::vector<std::thread> workers;
-    std::vector<int> order;
-    std::atomic<size_t> next{0};
-    std::unique_ptr<std::atomic<int>[]> ready;
-    std::atomic<bool> stop{false};
-};
-
-enum Phase { kPhSampler, kPhFieldFwd, kPhComposite, kPhFieldBwd, kPhAdam, kPhOccupancy,
-             kPhAccept, kNumPhases };
-const char* kPhaseNames[kNumPhases] = {"sampler", "field_fwd", "composite", "field_bwd",
-                                       "adam", "occupancy", "accept"};
-
-struct WinBuf {
-    uint8_t* d_crops = nullptr;      // per-view union crop, u8 RGB
-    int* d_crop_rect = nullptr;      // r0, c0, cols, rows per view
-    uint64_t* d_crop_off = nullptr;  // byte offset of each view's crop
-    uint64_t* d_accept = nullptr;    // packed (view, row, col)
-    uint32_t* d_n = nullptr;         // accepted count (read by the ray draw on device)
-    std::vector<int> h_crop_rect;
-    std::vector<uint64_t> h_crop_off;
-    int pos_r = -1, pos_c = -1;
-    cudaEvent_t ready = nullptr;
-};
-
-struct Crop {
-    int r0 = 0, r1 = 0, c0 = 0, c1 = 0;
-    bool empty() const { return r0 >= r1 || c0 >= c1; }
-};
-
-} // namespace
-
-struct tfg_ctx {
-    int device = 0;
-    int sms = 148;
-    cudaStream_t st = nullptr, side = nullptr;
-    bool own_stream = true;
-    cudaEvent_t ev_main = nullptr, ev_side = nullptr;
-    tfg_field_config fc{};
-    tfg_train_config tc{};
-    HashLayout hl{};
-    uint64_t enc_n = 0, stride = 0, n_params = 0, color_off = 0;
-    float density_lim = 0.f;
-    int max_rays = 0;
-    uint64_t sample_cap = 0;
-    int max_tiles = 0;
-    uint64_t launches = 0;
-
-    // parameters / optimizer
-    float *d_params = nullptr, *d_grads = nullptr, *d_m = nullptr, *d_v = nullptr;
-    float* d_ema = nullptr;
-    uint32_t* d_bits = nullptr;
-    uint32_t* d_group_flags = nullptr;
-    Status* d_status = nullptr;
-    Status* h_status = nullptr;
-    uint64_t color_step = 0;
-
-    // scene
-    int n_views = 0;
-    std::vector<tfg_rpc> cams;
-    tfg_rpc* d_cams = nullptr;
-    std::vector<uint8_t*> h_images;
-    tfg_roi roi{};
-    int rows = 0, cols = 0;
-    std::vector<double> east, north;
-    double *d_east = nullptr, *d_north = nullptr;
-    std::vector<TileHost> tiles;
-
-    // window
-    int pos_r = -1, pos_c = -1;
-    int nslots = 0;
-    int slot_tile[kTrainSlots] = {-1, -1, -1, -1};
-    SlotTable slots{};
-
-    // per-window staging (crops + accepted-ray list), double buffered so the
-    // next position can be staged on the side stream while this one trains
-    WinBuf win[2];
-    int front = 0;
-    cudaEvent_t ev_swap = nullptr;  // main-stream point after which the back buffer is free
-    uint64_t crop_cap = 0, accept_cap = 0, cand_cap = 0;
-    // accepted-list build scratch (one build at a time)
-    uint32_t *d_flags = nullptr, *d_pos = nullptr, *d_block_sums = nullptr, *d_acc_sums = nullptr;
-    // per-pixel memo of the scene (AcceptArgs): state, rays, view offsets
-    uint32_t* d_pix_info = nullptr;
-    double* d_pix_rays = nullptr;
-    uint64_t* d_pix_off = nullptr;
-    uint64_t pix_total = 0;
-    uint64_t* d_view_start = nullptr;
-    int *d_union = nullptr, *d_crop4 = nullptr;
-
-    // batch
-    RayRec* d_rays = nullptr;
-    float4* d_venc = nullptr;
-    uint32_t *d_counts = nullptr, *d_P = nullptr;
-    TileDesc* d_tiles = nullptr;
-    SampleArrays s{};
-    float* d_ray_out = nullptr;  // rgb(3) | depth | opacity per ray
-    int32_t* d_pixels = nullptr;
-    uint8_t* d_feat = nullptr;    // bf16 feature tiles (4 KB per 128-sample tile)
-    int32_t* d_tile_rays = nullptr;
-    float4* d_export = nullptr;   // parity export of (d_sigma, d_rgb) in ray semantics
-    int cur_rays = 0;
-    bool have_batch = false;
-    bool fwd_done = false;  // feature tiles of the current batch are resident
-    bool render_mode = false;
-
-    // render
-    float* d_rparams = nullptr;  // kMaxSlots * stride
-    uint32_t* d_rbits = nullptr;
-    float* d_rcolor = nullptr;
-    int rn = 0;
-    SlotTable rslots{};
-    tfg_rpc* d_rcam = nullptr;
-
-    uint64_t bytes_total = 0;
-    uint64_t h2d_bytes = 0, d2h_bytes = 0;
-    float* h_records = nullptr;  // one pinned block for every tile record
-    InitPool init;
-
-    // per-phase device timing (CUDA events on the context stream)
-    bool prof = false;
-    std::vector<cudaEvent_t> ev_pool;
-    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_open;
-    double prof_ms[kNumPhases] = {};
-    uint64_t prof_n[kNumPhases] = {};
-    uint64_t prof_launch[kNumPhases] = {};
-};
-
-namespace {
-
-template <typename T>
-int dalloc(tfg_ctx* c, T** p, uint64_t n) {
-    if (n == 0) n = 1;
-    CK(cudaMalloc(reinterpret_cast<void**>(p), n * sizeof(T)));
-    c->bytes_total += n * sizeof(T);
-    return 0;
 }
 
 cudaEvent_t pool_event(tfg_ctx* c) {
@@ -727,7 +558,8 @@ void for_samples(const tfg_ctx* c, const HostBatch& hb, F fn) {
     }
 }
 
-} // namespace
+} // namespace host
+} // namespace tfg
 
 extern "C" {
 
@@ -1749,466 +1581,3 @@ TFG_API int tfg_copy_bytes(tfg_ctx* c, uint64_t* h2d, uint64_t* d2h) {
 
 } // extern "C"
 
-// ---------------------------------------------------------------- checkpoints
-namespace {
-constexpr char kCkptMagic[8] = {'T', 'F', 'C', 'K', 'P', 'T', '0', '1'};
-constexpr uint32_t kCkptVersion = 1;
-
-bool same_cfg(const tfg_field_config& a, const tfg_field_config& b) {
-    return std::memcmp(&a, &b, sizeof(a)) == 0;
-}
-
-int write_ckpt(const char* path, uint32_t kind, const tfg_field_config& cfg, int row, int col,
-               uint64_t n_params, uint64_t n_occ, uint64_t step0, uint64_t step1,
-               const float* const* arrays, const uint64_t* counts, int n_arrays) {
-    std::ofstream f(path, std::ios::binary);
-    if (!f) return fail(TFG_ERR_INVALID, std::string("checkpoint: cannot open ") + path);
-    int32_t rc2[2] = {row, col};
-    uint64_t hdr[4] = {n_params, n_occ, step0, step1};
-    f.write(kCkptMagic, 8);
-    f.write(reinterpret_cast<const char*>(&kCkptVersion), 4);
-    f.write(reinterpret_cast<const char*>(&kind), 4);
-    f.write(reinterpret_cast<const char*>(&cfg), sizeof(cfg));
-    f.write(reinterpret_cast<const char*>(rc2), 8);
-    f.write(reinterpret_cast<const char*>(hdr), 32);
-    for (int i = 0; i < n_arrays; ++i) {
-        static const std::vector<float> zeros(1 << 16, 0.f);
-        if (arrays[i]) {
-            f.write(reinterpret_cast<const char*>(arrays[i]), counts[i] * 4);
-        } else {  // absent moments are written as zeros
-            for (uint64_t k = 0; k < counts[i]; k += zeros.size())
-                f.write(reinterpret_cast<const char*>(zeros.data()),
-                        std::min<uint64_t>(zeros.size(), counts[i] - k) * 4);
-        }
-    }
-    if (!f.good()) return fail(TFG_ERR_INVALID, std::string("checkpoint: write failed for ") + path);
-    return 0;
-}
-
-int read_ckpt_header(std::ifstream& f, const char* path, uint32_t kind, const tfg_field_config& cfg,
-                     int* row, int* col, uint64_t* hdr) {
-    char magic[8];
-    uint32_t ver = 0, k = 0;
-    tfg_field_config c{};
-    int32_t rc2[2];
-    f.read(magic, 8);
-    f.read(reinterpret_cast<char*>(&ver), 4);
-    f.read(reinterpret_cast<char*>(&k), 4);
-    f.read(reinterpret_cast<char*>(&c), sizeof(c));
-    f.read(reinterpret_cast<char*>(rc2), 8);
-    f.read(reinterpret_cast<char*>(hdr), 32);
-    if (!f.good() || std::memcmp(magic, kCkptMagic, 8) != 0)
-        return fail(TFG_ERR_INVALID, std::string("checkpoint: bad magic in ") + path);
-    if (ver != kCkptVersion || k != kind)
-        return fail(TFG_ERR_INVALID, std::string("checkpoint: unsupported version/kind in ") + path);
-    if (!same_cfg(c, cfg))
-        return fail(TFG_ERR_INVALID, std::string("checkpoint: FieldConfig mismatch in ") + path);
-    if (row) *row = rc2[0];
-    if (col) *col = rc2[1];
-    return 0;
-}
-
-int read_arrays(std::ifstream& f, const char* path, float* const* arrays, const uint64_t* counts, int n) {
-    for (int i = 0; i < n; ++i) {
-        if (arrays[i]) {
-            f.read(reinterpret_cast<char*>(arrays[i]), counts[i] * 4);
-        } else {
-            f.seekg(std::streamoff(counts[i] * 4), std::ios::cur);
-        }
-    }
-    if (!f.good()) return fail(TFG_ERR_INVALID, std::string("checkpoint: truncated ") + path);
-    return 0;
-}
-} // namespace
-
-extern "C" {
-
-TFG_API int tfg_save_tile_checkpoint(const char* path, const tfg_field_config* cfg, int row, int col,
-                                     const tfg_tile_state* st) {
-    uint64_t enc, dn;
-    tfg_param_counts(cfg, &enc, &dn, nullptr);
-    uint64_t occ = uint64_t(cfg->occupancy_resolution) * cfg->occupancy_resolution * cfg->occupancy_resolution;
-    const float* arr[7] = {st->enc, st->dnet, st->enc_m, st->enc_v, st->dnet_m, st->dnet_v, st->occupancy};
-    const uint64_t cnt[7] = {enc, dn, enc, enc, dn, dn, occ};
-    if (!st->enc || !st->dnet || !st->occupancy)
-        return fail(TFG_ERR_INVALID, "save_tile_checkpoint: params and occupancy are required");
-    return write_ckpt(path, 1, *cfg, row, col, enc + dn, occ, st->enc_step, st->dnet_step, arr, cnt, 7);
-}
-
-TFG_API int tfg_load_tile_checkpoint(const char* path, const tfg_field_config* cfg, int* row, int* col,
-                                     tfg_tile_state* st) {
-    std::ifstream f(path, std::ios::binary);
-    if (!f) return fail(TFG_ERR_INVALID, std::string("checkpoint: cannot open ") + path);
-    uint64_t hdr[4];
-    int rc = read_ckpt_header(f, path, 1, *cfg, row, col, hdr);
-    if (rc) return rc;
-    uint64_t enc, dn;
-    tfg_param_counts(cfg, &enc, &dn, nullptr);
-    if (hdr[0] != enc + dn) return fail(TFG_ERR_INVALID, "checkpoint: parameter count mismatch");
-    float* arr[7] = {st->enc, st->dnet, st->enc_m, st->enc_v, st->dnet_m, st->dnet_v, st->occupancy};
-    const uint64_t cnt[7] = {enc, dn, enc, enc, dn, dn, hdr[1]};
-    st->enc_step = hdr[2];
-    st->dnet_step = hdr[3];
-    return read_arrays(f, path, arr, cnt, 7);
-}
-
-TFG_API int tfg_save_color_checkpoint(const char* path, const tfg_field_config* cfg, const float* params,
-                                      const float* m, const float* v, uint64_t step) {
-    uint64_t col;
-    tfg_param_counts(cfg, nullptr, nullptr, &col);
-    const float* arr[3] = {params, m, v};
-    const uint64_t cnt[3] = {col, col, col};
-    return write_ckpt(path, 2, *cfg, -1, -1, col, 0, step, 0, arr, cnt, 3);
-}
-
-TFG_API int tfg_load_color_checkpoint(const char* path, const tfg_field_config* cfg, float* params,
-                                      float* m, float* v, uint64_t* step) {
-    std::ifstream f(path, std::ios::binary);
-    if (!f) return fail(TFG_ERR_INVALID, std::string("checkpoint: cannot open ") + path);
-    uint64_t hdr[4];
-    int rc = read_ckpt_header(f, path, 2, *cfg, nullptr, nullptr, hdr);
-    if (rc) return rc;
-    uint64_t col;
-    tfg_param_counts(cfg, nullptr, nullptr, &col);
-    if (hdr[0] != col) return fail(TFG_ERR_INVALID, "checkpoint: parameter count mismatch");
-    float* arr[3] = {params, m, v};
-    const uint64_t cnt[3] = {col, col, col};
-    if (step) *step = hdr[2];
-    return read_arrays(f, path, arr, cnt, 3);
-}
-
-// Saves the run: the window slots are copied back to their host records
-// first, then every record that was ever materialised and the colour net.
-TFG_API int tfg_save_run(tfg_ctx* c, const char* dir) {
-    if (!c || c->n_views == 0) return fail(TFG_ERR_STATE, "save_run: no scene");
-    CK(cudaSetDevice(c->device));
-    CK(cudaEventRecord(c->ev_main, c->st));
-    CK(cudaStreamWaitEvent(c->side, c->ev_main, 0));
-    for (int s = 0; s < c->nslots; ++s)
-        if (slot_copy(c, s, c->slot_tile[s], true)) return TFG_ERR_CUDA;
-    CK(cudaStreamSynchronize(c->side));
-    std::string d(dir);
-    for (size_t ti = 0; ti < c->tiles.size(); ++ti) {
-        TileHost& t = c->tiles[ti];
-        if (!c->init.ready[ti].load() || !t.created) continue;
-        float* p = t.rec;
-        tfg_tile_state st{};
-        st.enc = p;
-        st.dnet = p + c->enc_n;
-        st.enc_m = p + c->stride;
-        st.dnet_m = p + c->stride + c->enc_n;
-        st.enc_v = p + 2 * c->stride;
-        st.dnet_v = p + 2 * c->stride + c->enc_n;
-        st.occupancy = p + 3 * c->stride;
-        st.enc_step = t.enc_step;
-        st.dnet_step = t.dnet_step;
-        char name[64];
-        std::snprintf(name, sizeof name, "/tiles/r%d_c%d.ckpt", int(ti) / c->cols, int(ti) % c->cols);
-        int rc = tfg_save_tile_checkpoint((d + name).c_str(), &c->fc, int(ti) / c->cols,
-                                          int(ti) % c->cols, &st);
-        if (rc) return rc;
-    }
-    uint64_t n = c->n_params - c->color_off;
-    std::vector<float> p(n), m(n), v(n);
-    int rc = tfg_get_color(c, p.data(), m.data(), v.data(), nullptr);
-    if (rc) return rc;
-    return tfg_save_color_checkpoint((d + "/color_net.ckpt").c_str(), &c->fc, p.data(), m.data(), v.data(),
-                                     c->color_step);
-}
-
-// Restores a saved run into the host records (tiles absent from `dir` keep
-// their fresh initialisation) and the colour net; call before set_window.
-TFG_API int tfg_load_run(tfg_ctx* c, const char* dir) {
-    if (!c || c->n_views == 0) return fail(TFG_ERR_STATE, "load_run: no scene");
-    if (c->nslots) return fail(TFG_ERR_STATE, "load_run: call before the first set_window");
-    std::string d(dir);
-    for (size_t ti = 0; ti < c->tiles.size(); ++ti) {
-        char name[64];
-        std::snprintf(name, sizeof name, "/tiles/r%d_c%d.ckpt", int(ti) / c->cols, int(ti) % c->cols);
-        std::string path = d + name;
-        std::ifstream probe(path, std::ios::binary);
-        if (!probe) continue;
-        probe.close();
-        if (ensure_record(c, int(ti))) return TFG_ERR_CUDA;
-        TileHost& t = c->tiles[ti];
-        float* p = t.rec;
-        tfg_tile_state st{};
-        st.enc = p;
-        st.dnet = p + c->enc_n;
-        st.enc_m = p + c->stride;
-        st.dnet_m = p + c->stride + c->enc_n;
-        st.enc_v = p + 2 * c->stride;
-        st.dnet_v = p + 2 * c->stride + c->enc_n;
-        st.occupancy = p + 3 * c->stride;
-        int row, col;
-        int rc = tfg_load_tile_checkpoint(path.c_str(), &c->fc, &row, &col, &st);
-        if (rc) return rc;
-        if (row * c->cols + col != int(ti)) return fail(TFG_ERR_INVALID, "load_run: tile id mismatch in " + path);
-        t.enc_step = st.enc_step;
-        t.dnet_step = st.dnet_step;
-    }
-    uint64_t n = c->n_params - c->color_off;
-    std::vector<float> p(n), m(n), v(n);
-    uint64_t step = 0;
-    int rc = tfg_load_color_checkpoint((d + "/color_net.ckpt").c_str(), &c->fc, p.data(), m.data(), v.data(),
-                                       &step);
-    if (rc) return rc;
-    return tfg_set_color(c, p.data(), m.data(), v.data(), step);
-}
-
-} // extern "C"
-
-// ---------------------------------------------------------------- evaluation
-namespace {
-template <typename T>
-int dcopy_in(tfg_ctx* c, T** d, const T* h, uint64_t n) {
-    CK(cudaMallocAsync(reinterpret_cast<void**>(d), n * sizeof(T), c->st));
-    CK(cudaMemcpyAsync(*d, h, n * sizeof(T), cudaMemcpyHostToDevice, c->st));
-    return 0;
-}
-} // namespace
-
-extern "C" {
-
-TFG_API int tfg_psnr(tfg_ctx* c, const float* a, const float* b, uint64_t n, double* db) {
-    if (!c || !a || !b || n == 0 || !db) return fail(TFG_ERR_INVALID, "psnr: empty or null input");
-    CK(cudaSetDevice(c->device));
-    float *da = nullptr, *dbuf = nullptr;
-    double* acc = nullptr;
-    if (dcopy_in(c, &da, a, n) || dcopy_in(c, &dbuf, b, n)) return TFG_ERR_CUDA;
-    CK(cudaMallocAsync(reinterpret_cast<void**>(&acc), 8, c->st));
-    CK(cudaMemsetAsync(acc, 0, 8, c->st));
-    launch_sq_diff(da, dbuf, n, acc, c->sms, c->st);
-    c->launches += 1;
-    double s = 0.0;
-    CK(cudaMemcpyAsync(&s, acc, 8, cudaMemcpyDeviceToHost, c->st));
-    for (void* p : {static_cast<void*>(da), static_cast<void*>(dbuf), static_cast<void*>(acc)})
-        CK(cudaFreeAsync(p, c->st));
-    CK(cudaStreamSynchronize(c->st));
-    double mse = s / double(n);
-    *db = mse > 0.0 ? std::min(99.0, 10.0 * std::log10(1.0 / mse)) : 99.0;
-    return 0;
-}
-
-TFG_API int tfg_ssim(tfg_ctx* c, const float* a, const float* b, int rows, int cols, double* out) {
-    if (!c || !a || !b || !out) return fail(TFG_ERR_INVALID, "ssim: null input");
-    if (rows < 11 || cols < 11) return fail(TFG_ERR_INVALID, "ssim: image smaller than the 11x11 window");
-    CK(cudaSetDevice(c->device));
-    uint64_t n = uint64_t(rows) * uint64_t(cols) * 3;
-    float *da = nullptr, *dbuf = nullptr, *gw = nullptr;
-    double* acc = nullptr;
-    if (dcopy_in(c, &da, a, n) || dcopy_in(c, &dbuf, b, n)) return TFG_ERR_CUDA;
-    float w[11];
-    {
-        double g[11], sum = 0.0;
-        for (int k = 0; k < 11; ++k) {
-            double x = k - 5;
-            g[k] = std::exp(-(x * x) / (2.0 * 1.5 * 1.5));
-            sum += g[k];
-        }
-        for (int k = 0; k < 11; ++k) w[k] = float(g[k] / sum);
-    }
-    if (dcopy_in(c, &gw, w, 11)) return TFG_ERR_CUDA;
-    CK(cudaMallocAsync(reinterpret_cast<void**>(&acc), 8, c->st));
-    CK(cudaMemsetAsync(acc, 0, 8, c->st));
-    launch_ssim(da, dbuf, rows, cols, gw, acc, c->st);
-    c->launches += 1;
-    double s = 0.0;
-    CK(cudaMemcpyAsync(&s, acc, 8, cudaMemcpyDeviceToHost, c->st));
-    for (void* p : {static_cast<void*>(da), static_cast<void*>(dbuf), static_cast<void*>(gw),
-                    static_cast<void*>(acc)})
-        CK(cudaFreeAsync(p, c->st));
-    CK(cudaStreamSynchronize(c->st));
-    *out = s / (double(rows - 10) * double(cols - 10));
-    return 0;
-}
-
-TFG_API int tfg_depth_mae(tfg_ctx* c, const float* d1, const float* d2, const uint8_t* mask, uint64_t n,
-                          double* out) {
-    if (!c || !d1 || !d2 || n == 0 || !out) return fail(TFG_ERR_INVALID, "depth_mae: empty or null input");
-    CK(cudaSetDevice(c->device));
-    float *a = nullptr, *b = nullptr;
-    uint8_t* m = nullptr;
-    double* acc = nullptr;
-    if (dcopy_in(c, &a, d1, n) || dcopy_in(c, &b, d2, n)) return TFG_ERR_CUDA;
-    if (mask && dcopy_in(c, &m, mask, n)) return TFG_ERR_CUDA;
-    CK(cudaMallocAsync(reinterpret_cast<void**>(&acc), 16, c->st));
-    CK(cudaMemsetAsync(acc, 0, 16, c->st));
-    launch_abs_diff(a, b, m, n, acc, c->sms, c->st);
-    c->launches += 1;
-    double s[2] = {0.0, 0.0};
-    CK(cudaMemcpyAsync(s, acc, 16, cudaMemcpyDeviceToHost, c->st));
-    for (void* p : {static_cast<void*>(a), static_cast<void*>(b), static_cast<void*>(m), static_cast<void*>(acc)})
-        if (p) CK(cudaFreeAsync(p, c->st));
-    CK(cudaStreamSynchronize(c->st));
-    if (s[1] == 0.0) return fail(TFG_ERR_INVALID, "depth_mae: empty mask");
-    *out = s[0] / s[1];
-    return 0;
-}
-
-TFG_API int tfg_edge_band_mask(tfg_ctx* c, const tfg_rpc* cam, int band_px, uint8_t* mask) {
-    if (!c || c->n_views == 0) return fail(TFG_ERR_STATE, "edge_band_mask: call set_scene first");
-    if (!cam || !mask || band_px < 0) return fail(TFG_ERR_INVALID, "edge_band_mask: bad arguments");
-    CK(cudaSetDevice(c->device));
-    uint64_t npx = uint64_t(cam->image_rows) * uint64_t(cam->image_cols);
-    uint8_t* dm = nullptr;
-    tfg_rpc* dcam = nullptr;
-    CK(cudaMallocAsync(reinterpret_cast<void**>(&dm), npx, c->st));
-    CK(cudaMemsetAsync(dm, 0, npx, c->st));
-    if (dcopy_in(c, &dcam, cam, 1)) return TFG_ERR_CUDA;
-    // sample the boundary lines at 1/8 of the view's ground footprint per pixel
-    double ext = std::max(c->roi.easting_max - c->roi.easting_min, c->roi.northing_max - c->roi.northing_min);
-    double gsd = std::fabs(cam->long_scale) / std::max(1.0, std::fabs(cam->samp_scale));
-    double step = std::max(gsd / 8.0, ext / 1.0e6);
-    uint64_t per_line = uint64_t(ext / step) + 2;
-    launch_edge_band(dcam, c->d_east, c->d_north, c->rows, c->cols, c->roi.z_min, c->roi.z_max, step, per_line,
-                     band_px, dm, c->st);
-    c->launches += 1;
-    CK(cudaMemcpyAsync(mask, dm, npx, cudaMemcpyDeviceToHost, c->st));
-    CK(cudaFreeAsync(dm, c->st));
-    CK(cudaFreeAsync(dcam, c->st));
-    CK(cudaStreamSynchronize(c->st));
-    return 0;
-}
-
-TFG_API int tfg_render_view(tfg_ctx* c, const tfg_rpc* cam, float* rgb, float* depth, float* opacity) {
-    if (!c || !cam) return fail(TFG_ERR_INVALID, "render_view: null input");
-    uint64_t npx = uint64_t(cam->image_rows) * uint64_t(cam->image_cols);
-    const uint64_t chunk = 1u << 22;
-    std::vector<int32_t> px;
-    for (uint64_t p0 = 0; p0 < npx; p0 += chunk) {
-        uint64_t nb = std::min<uint64_t>(chunk, npx - p0);
-        px.resize(2 * nb);
-        for (uint64_t i = 0; i < nb; ++i) {
-            px[2 * i] = int32_t((p0 + i) / uint64_t(cam->image_cols));
-            px[2 * i + 1] = int32_t((p0 + i) % uint64_t(cam->image_cols));
-        }
-        int rc = tfg_render_pixels(c, cam, px.data(), int(nb), rgb ? rgb + 3 * p0 : nullptr,
-                                   depth ? depth + p0 : nullptr, opacity ? opacity + p0 : nullptr);
-        if (rc) return rc;
-    }
-    return 0;
-}
-
-} // extern "C"
-
-// ---------------------------------------------------------------- crop cache
-namespace {
-constexpr char kCropMagic[8] = {'T', 'F', 'C', 'R', 'O', 'P', '0', '1'};
-struct CropEntry {
-    int32_t view, row, col, r0, r1, c0, c1, pad;
-    uint64_t offset, bytes;
-};
-static_assert(sizeof(CropEntry) == 48, "crop index entry");
-
-void crop_index(const tfg_ctx* c, std::vector<CropEntry>& idx) {
-    idx.clear();
-    uint64_t off = 0;
-    for (int v = 0; v < c->n_views; ++v)
-        for (int ti = 0; ti < c->rows * c->cols; ++ti) {
-            CropEntry e{};
-            e.view = v;
-            e.row = ti / c->cols;
-            e.col = ti % c->cols;
-            double b[6];
-            tile_box(c, ti, b);
-            Crop cr;
-            if (crop_for_tile(c->cams[v], b, c->tc.margin_px, &cr)) {
-                e.r0 = cr.r0;
-                e.r1 = cr.r1;
-                e.c0 = cr.c0;
-                e.c1 = cr.c1;
-                e.offset = off;
-                e.bytes = uint64_t(cr.r1 - cr.r0) * uint64_t(cr.c1 - cr.c0) * 3;
-                off += e.bytes;
-            }
-            idx.push_back(e);
-        }
-}
-} // namespace
-
-extern "C" {
-
-TFG_API int tfg_crop_rect(tfg_ctx* c, int view, int row, int col, int32_t* out) {
-    if (!c || c->n_views == 0) return fail(TFG_ERR_STATE, "crop_rect: call set_scene first");
-    if (view < 0 || view >= c->n_views || row < 0 || row >= c->rows || col < 0 || col >= c->cols || !out)
-        return fail(TFG_ERR_INVALID, "crop_rect: bad view or tile");
-    double b[6];
-    tile_box(c, row * c->cols + col, b);
-    Crop cr;
-    if (!crop_for_tile(c->cams[view], b, c->tc.margin_px, &cr)) cr = Crop{};
-    out[0] = cr.r0;
-    out[1] = cr.r1;
-    out[2] = cr.c0;
-    out[3] = cr.c1;
-    return 0;
-}
-
-TFG_API int tfg_build_crop_cache(tfg_ctx* c, const char* path, uint64_t* total) {
-    if (!c || c->n_views == 0) return fail(TFG_ERR_STATE, "build_crop_cache: call set_scene first");
-    std::vector<CropEntry> idx;
-    crop_index(c, idx);
-    std::ofstream f(path, std::ios::binary);
-    if (!f) return fail(TFG_ERR_INVALID, std::string("crop cache: cannot open ") + path);
-    uint32_t hdr32[6] = {1u, uint32_t(c->n_views), uint32_t(c->rows), uint32_t(c->cols),
-                         uint32_t(c->tc.margin_px), 0u};
-    uint64_t n = idx.size(), data_off = 8 + sizeof(hdr32) + 16 + n * sizeof(CropEntry);
-    f.write(kCropMagic, 8);
-    f.write(reinterpret_cast<const char*>(hdr32), sizeof(hdr32));
-    f.write(reinterpret_cast<const char*>(&n), 8);
-    f.write(reinterpret_cast<const char*>(&data_off), 8);
-    f.write(reinterpret_cast<const char*>(idx.data()), n * sizeof(CropEntry));
-    uint64_t tot = 0;
-    for (const CropEntry& e : idx) {
-        if (!e.bytes) continue;
-        const uint8_t* im = c->h_images[e.view];
-        size_t W = size_t(c->cams[e.view].image_cols);
-        for (int r = e.r0; r < e.r1; ++r)
-            f.write(reinterpret_cast<const char*>(im + 3 * (size_t(r) * W + size_t(e.c0))),
-                    std::streamsize(3 * (e.c1 - e.c0)));
-        tot += e.bytes;
-    }
-    if (!f.good()) return fail(TFG_ERR_INVALID, std::string("crop cache: write failed for ") + path);
-    if (total) *total = tot;
-    return 0;
-}
-
-TFG_API int tfg_load_crop_cache(tfg_ctx* c, const char* path) {
-    if (!c || c->n_views == 0) return fail(TFG_ERR_STATE, "load_crop_cache: call set_scene first");
-    if (c->nslots) return fail(TFG_ERR_STATE, "load_crop_cache: call before the first set_window");
-    std::ifstream f(path, std::ios::binary);
-    if (!f) return fail(TFG_ERR_INVALID, std::string("crop cache: cannot open ") + path);
-    char magic[8];
-    uint32_t hdr32[6];
-    uint64_t n = 0, data_off = 0;
-    f.read(magic, 8);
-    f.read(reinterpret_cast<char*>(hdr32), sizeof(hdr32));
-    f.read(reinterpret_cast<char*>(&n), 8);
-    f.read(reinterpret_cast<char*>(&data_off), 8);
-    if (!f.good() || std::memcmp(magic, kCropMagic, 8) != 0 || hdr32[0] != 1u)
-        return fail(TFG_ERR_INVALID, std::string("crop cache: bad header in ") + path);
-    if (hdr32[1] != uint32_t(c->n_views) || hdr32[2] != uint32_t(c->rows) || hdr32[3] != uint32_t(c->cols) ||
-        hdr32[4] != uint32_t(c->tc.margin_px))
-        return fail(TFG_ERR_INVALID, "crop cache: views / grid / margin differ from the scene");
-    std::vector<CropEntry> want, got(n);
-    crop_index(c, want);
-    f.read(reinterpret_cast<char*>(got.data()), std::streamsize(n * sizeof(CropEntry)));
-    if (!f.good() || n != want.size() ||
-        std::memcmp(got.data(), want.data(), n * sizeof(CropEntry)) != 0)
-        return fail(TFG_ERR_INVALID, "crop cache: index differs from this scene's crop_for_tile rects");
-    std::vector<uint8_t> buf;
-    for (const CropEntry& e : got) {
-        if (!e.bytes) continue;
-        buf.resize(e.bytes);
-        f.seekg(std::streamoff(data_off + e.offset));
-        f.read(reinterpret_cast<char*>(buf.data()), std::streamsize(e.bytes));
-        if (!f.good()) return fail(TFG_ERR_INVALID, std::string("crop cache: truncated ") + path);
-        uint8_t* im = c->h_images[e.view];
-        size_t W = size_t(c->cams[e.view].image_cols), w3 = size_t(3 * (e.c1 - e.c0));
-        for (int r = e.r0; r < e.r1; ++r)
-            std::memcpy(im + 3 * (size_t(r) * W + size_t(e.c0)), buf.data() + size_t(r - e.r0) * w3, w3);
-    }
-    return 0;
-}
-
-} // extern "C"
