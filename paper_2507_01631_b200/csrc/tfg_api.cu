@@ -243,6 +243,22 @@ int slot_copy(tfg_ctx* c, int slot, int ti, bool to_host) {
     return 0;
 }
 
+// D2D between a device slot (params / m / v / EMA spans) and a contiguous
+// staged record (the host record layout), on stream st.
+int slot_record_d2d(tfg_ctx* c, int slot, float* rec, bool to_record, cudaStream_t st) {
+    uint64_t off = uint64_t(slot) * c->stride;
+    size_t bytes = c->stride * sizeof(float);
+    float* dev[4] = {c->d_params + off, c->d_m + off, c->d_v + off, c->d_ema + uint64_t(slot) * kOccVox};
+    size_t nb[4] = {bytes, bytes, bytes, kOccVox * sizeof(float)};
+    for (int a = 0; a < 4; ++a) {
+        float* r = rec + a * c->stride;
+        CK(cudaMemcpyAsync(to_record ? static_cast<void*>(r) : static_cast<void*>(dev[a]),
+                           to_record ? static_cast<const void*>(dev[a]) : static_cast<const void*>(r), nb[a],
+                           cudaMemcpyDeviceToDevice, st));
+    }
+    return 0;
+}
+
 void fill_slots(tfg_ctx* c) {
     c->slots.n = c->nslots;
     for (int k = 0; k < c->nslots; ++k) {
@@ -672,7 +688,13 @@ TFG_API int tfg_create(const tfg_field_config* fcfg, const tfg_train_config* tcf
     CK(cudaEventCreateWithFlags(&c->ev_side, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->ev_swap, cudaEventDisableTiming));
     CK(cudaEventRecord(c->ev_swap, c->st));
+    for (cudaEvent_t* e : {&c->ev_stage_in, &c->ev_stage_read, &c->ev_out_done}) {
+        CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+        CK(cudaEventRecord(*e, c->st));
+    }
     rc |= dalloc(c, &c->d_params, c->n_params);
+    rc |= dalloc(c, &c->d_stage_in, uint64_t(kTrainSlots) * (3 * c->stride + kOccVox));
+    rc |= dalloc(c, &c->d_stage_out, uint64_t(kTrainSlots) * (3 * c->stride + kOccVox));
     rc |= dalloc(c, &c->d_grads, c->n_params);
     rc |= dalloc(c, &c->d_m, c->n_params);
     rc |= dalloc(c, &c->d_v, c->n_params);
@@ -727,7 +749,8 @@ TFG_API int tfg_destroy(tfg_ctx* c) {
                    c->d_rays, c->d_venc,
                    c->d_counts, c->d_P, c->d_tiles, c->s.local, c->s.td, c->s.endpoint, c->s.io,
                    c->d_ray_out, c->d_pixels, c->d_rparams, c->d_rbits, c->d_rcolor, c->d_rcam,
-                   c->d_feat, c->d_tile_rays, c->d_export, c->d_pix_info, c->d_pix_rays, c->d_pix_off};
+                   c->d_feat, c->d_tile_rays, c->d_export, c->d_pix_info, c->d_pix_rays, c->d_pix_off,
+                   c->d_stage_in, c->d_stage_out};
     for (void* p : dev)
         if (p) cudaFree(p);
     stop_init_pool(c);
@@ -742,6 +765,8 @@ TFG_API int tfg_destroy(tfg_ctx* c) {
         if (w.ready) cudaEventDestroy(w.ready);
     }
     if (c->ev_swap) cudaEventDestroy(c->ev_swap);
+    for (cudaEvent_t e : {c->ev_stage_in, c->ev_stage_read, c->ev_out_done})
+        if (e) cudaEventDestroy(e);
     if (c->ev_main) cudaEventDestroy(c->ev_main);
     if (c->ev_side) cudaEventDestroy(c->ev_side);
     if (c->side) cudaStreamDestroy(c->side);
@@ -958,21 +983,53 @@ TFG_API int tfg_set_window(tfg_ctx* c, int pr, int pc) {
     } else {
         for (int k = 0; k < ns; ++k) next[k] = want[k];
     }
+    // Entering tiles staged by prefetch_window move in by D2D on the main
+    // stream (the evicted state goes out the same way and reaches its host
+    // record asynchronously); any other slot change copies through the side
+    // stream, which the main stream then waits for.
+    const uint64_t rec_n = 3 * c->stride + kOccVox;
+    int staged_k[kTrainSlots] = {-1, -1, -1, -1};
+    bool any_staged = false, any_plain = false;
+    for (int s = 0; s < ns; ++s) {
+        bool stays = (s < c->nslots && c->slot_tile[s] == next[s]);
+        if (stays) continue;
+        for (int k = 0; k < kTrainSlots; ++k)
+            if (c->stage_tile[k] == next[s]) staged_k[s] = k;
+        if (staged_k[s] >= 0 && s < c->nslots) any_staged = true;
+        else staged_k[s] = -1, any_plain = true;
+    }
     // main-stream work on the old window must finish before its state moves
     CK(cudaEventRecord(c->ev_main, c->st));
     CK(cudaStreamWaitEvent(c->side, c->ev_main, 0));
+    std::vector<std::pair<int, int>> evicted;  // (out record index, tile)
+    if (any_staged) {
+        CK(cudaStreamWaitEvent(c->st, c->ev_out_done, 0));  // out records free
+        CK(cudaStreamWaitEvent(c->st, c->ev_stage_in, 0));  // staged records complete
+        for (int s = 0; s < ns; ++s) {
+            if (staged_k[s] < 0) continue;
+            int old = c->slot_tile[s];
+            if (slot_record_d2d(c, s, c->d_stage_out + uint64_t(s) * rec_n, true, c->st)) return TFG_ERR_CUDA;
+            evicted.push_back({s, old});
+            if (slot_record_d2d(c, s, c->d_stage_in + uint64_t(staged_k[s]) * rec_n, false, c->st))
+                return TFG_ERR_CUDA;
+            c->h2d_bytes += rec_n * sizeof(float);  // (staged ahead by prefetch_window)
+        }
+        CK(cudaEventRecord(c->ev_stage_read, c->st));
+    }
+    for (int k = 0; k < kTrainSlots; ++k) c->stage_tile[k] = -1;
     for (int s = 0; s < c->nslots; ++s) {
         int old = c->slot_tile[s];
-        if (old >= 0 && (s >= ns || next[s] != old)) {
+        if (old >= 0 && (s >= ns || next[s] != old) && !(s < ns && staged_k[s] >= 0)) {
             if (slot_copy(c, s, old, true)) return TFG_ERR_CUDA;
         }
     }
     for (int s = 0; s < ns; ++s) {
         bool stays = (s < c->nslots && c->slot_tile[s] == next[s]);
-        if (stays) continue;
+        if (stays || staged_k[s] >= 0) continue;
         if (ensure_record(c, next[s])) return TFG_ERR_CUDA;
         if (slot_copy(c, s, next[s], false)) return TFG_ERR_CUDA;
     }
+    (void)any_plain;
     for (int s = 0; s < ns; ++s) c->slot_tile[s] = next[s];
     c->nslots = ns;
     c->pos_r = pr;
@@ -987,6 +1044,16 @@ TFG_API int tfg_set_window(tfg_ctx* c, int pr, int pc) {
         if (rc) return rc;
     }
     CK(cudaEventRecord(c->ev_side, c->side));
+    if (!evicted.empty()) {
+        // evicted records: D2H behind the main stream's D2D, off the critical path
+        CK(cudaStreamWaitEvent(c->side, c->ev_stage_read, 0));
+        for (auto& e : evicted) {
+            CK(cudaMemcpyAsync(c->tiles[e.second].rec, c->d_stage_out + uint64_t(e.first) * rec_n,
+                               rec_n * sizeof(float), cudaMemcpyDeviceToHost, c->side));
+            c->d2h_bytes += rec_n * sizeof(float);
+        }
+        CK(cudaEventRecord(c->ev_out_done, c->side));
+    }
     CK(cudaStreamWaitEvent(c->st, c->ev_side, 0));
     CK(cudaStreamWaitEvent(c->st, back.ready, 0));
     c->front ^= 1;
@@ -1010,6 +1077,25 @@ TFG_API int tfg_prefetch_window(tfg_ctx* c, int pr, int pc) {
     WinBuf& back = c->win[c->front ^ 1];
     if (back.pos_r == pr && back.pos_c == pc) return 0;
     back.pos_r = back.pos_c = -1;
+    // entering tiles first: their host records (final while not resident) go
+    // to the staging records, so the move itself only does D2D copies
+    if (c->nslots == kTrainSlots) {
+        std::vector<int> want = window_tiles(c, single ? 0 : pr, single ? 0 : pc);
+        const uint64_t rec_n = 3 * c->stride + kOccVox;
+        CK(cudaStreamWaitEvent(c->side, c->ev_stage_read, 0));  // previous staged records consumed
+        for (int k = 0; k < kTrainSlots; ++k) c->stage_tile[k] = -1;
+        int k = 0;
+        for (int ti : want) {
+            bool resident = false;
+            for (int s = 0; s < c->nslots; ++s) resident |= (c->slot_tile[s] == ti);
+            if (resident || k >= kTrainSlots) continue;
+            if (ensure_record(c, ti)) return TFG_ERR_CUDA;
+            CK(cudaMemcpyAsync(c->d_stage_in + uint64_t(k) * rec_n, c->tiles[ti].rec, rec_n * sizeof(float),
+                               cudaMemcpyHostToDevice, c->side));
+            c->stage_tile[k++] = ti;
+        }
+        CK(cudaEventRecord(c->ev_stage_in, c->side));
+    }
     CK(cudaStreamWaitEvent(c->side, c->ev_swap, 0));
     return stage_window(c, back, pr, pc, c->side);
 }

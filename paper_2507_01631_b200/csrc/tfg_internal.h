@@ -126,6 +126,15 @@ struct tfg_ctx {
     WinBuf win[2];
     int front = 0;
     cudaEvent_t ev_swap = nullptr;  // main-stream point after which the back buffer is free
+    // Tile records staged by prefetch_window (H2D ahead of the move) and the
+    // evicted records awaiting their asynchronous D2H; record layout as the
+    // host's: params | m | v (stride each) | occupancy EMA.
+    float* d_stage_in = nullptr;
+    float* d_stage_out = nullptr;
+    int stage_tile[kTrainSlots] = {-1, -1, -1, -1};
+    cudaEvent_t ev_stage_in = nullptr;   // side stream: staged H2D done
+    cudaEvent_t ev_stage_read = nullptr; // main stream: staged records consumed
+    cudaEvent_t ev_out_done = nullptr;   // side stream: evicted D2H done
     uint64_t crop_cap = 0, accept_cap = 0, cand_cap = 0;
     // accepted-list build scratch (one build at a time)
     uint32_t *d_flags = nullptr, *d_pos = nullptr, *d_block_sums = nullptr, *d_acc_sums = nullptr;

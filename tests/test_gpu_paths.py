@@ -222,3 +222,33 @@ print(json.dumps(out))
         res[memo] = json.loads(p.stdout.strip().splitlines()[-1])
     assert res["0"] == res["1"]
     assert all(r[0] > 0 for r in res["0"])
+
+
+def test_prefetched_slide_round_trips_state_bit_exactly():
+    """A prefetched move stages the entering tiles' records ahead and moves
+    them in by D2D; the evicted state reaches its host record asynchronously.
+    Tiles that leave and come back (without training elsewhere) return
+    bit-identically, with their Adam step counts."""
+    _need_gpu()
+    from paper_2507_01631_b200.tilefield import Context
+
+    scene = synth.make_scene(3, 3, tile_side=96.0, n_views=2, gsd=1.5, seed=14)
+    ctx = Context(scene, FieldConfig.defaults(), TrainConfig.defaults(batch_rays=1024, seed=8), max_rays=1024)
+    ctx.set_window(0, 0)
+    for it in range(3):
+        ctx.train_step(it, 0, 1024)
+    before = {t: ctx.tile_state(k) for k, t in enumerate(ctx.window_tiles())}
+    ctx.prefetch_window(0, 1)
+    ctx.set_window(0, 1)  # (0,0) and (1,0) leave via the staged path
+    ctx.train_step(3, 0, 1024)
+    ctx.prefetch_window(1, 1)
+    ctx.set_window(1, 1)  # (0,1)... leave; (0,0) and (1,0) stay out
+    ctx.prefetch_window(0, 0)
+    ctx.set_window(0, 0)  # (0,0), (1,0) come back from their host records
+    after = {t: ctx.tile_state(k) for k, t in enumerate(ctx.window_tiles())}
+    for t in ((0, 0), (1, 0)):
+        for key in ("enc", "dnet", "enc_m", "enc_v", "dnet_m", "dnet_v", "occupancy"):
+            assert before[t][key].tobytes() == after[t][key].tobytes(), (t, key)
+        assert after[t]["enc_step"] == before[t]["enc_step"] == 3
+    # the tiles trained at (0,1) carry that step too
+    assert after[(0, 1)]["enc_step"] == 4 and after[(1, 1)]["enc_step"] == 4
