@@ -314,7 +314,11 @@ __global__ void __launch_bounds__(128, TFG_RAYGEN_MINB) raygen_kernel(RaygenArgs
     uint64_t g = a.ray_begin + uint64_t(ii);
     int v, row, col;
     const double* memo = nullptr;  // the accept pass already solved accepted pixels
-    if (a.pixels) {
+    if (a.pixels && a.pixel_pairs) {  // render: (row, col) pairs of the one render view
+        v = 0;
+        row = a.pixels[2 * ii];
+        col = a.pixels[2 * ii + 1];
+    } else if (a.pixels) {
         v = a.pixels[3 * ii];
         row = a.pixels[3 * ii + 1];
         col = a.pixels[3 * ii + 2];

@@ -55,6 +55,7 @@ struct RaygenArgs {
     const double* pix_rays;  // draw mode: per-pixel ray memo of the accept pass (K0)
     const uint64_t* pix_off;
     const int32_t* pixels;   // pixel mode (render/eval): view,row,col triplets
+    int pixel_pairs;         // ... or (row, col) pairs of view 0 (the render camera)
     const uint8_t* crop_bytes;
     const int* crop_rect;        // r0, c0, cols, rows per view
     const uint64_t* crop_offset; // byte offset of each view's crop

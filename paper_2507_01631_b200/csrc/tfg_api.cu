@@ -1542,7 +1542,6 @@ TFG_API int tfg_render_pixels(tfg_ctx* c, const tfg_rpc* cam, const int32_t* pix
     if (!c || c->rn == 0) return fail(TFG_ERR_STATE, "render_pixels: call render_setup first");
     CK(cudaSetDevice(c->device));
     CK(cudaMemcpyAsync(c->d_rcam, cam, sizeof(tfg_rpc), cudaMemcpyHostToDevice, c->st));
-    std::vector<int32_t> px3;
     FieldPtrs f{};
     for (int k = 0; k < c->rn; ++k) {
         f.enc[k] = c->d_rparams + uint64_t(k) * c->stride;
@@ -1550,19 +1549,14 @@ TFG_API int tfg_render_pixels(tfg_ctx* c, const tfg_rpc* cam, const int32_t* pix
         f.occ_bits[k] = c->d_rbits + uint64_t(k) * kOccWords;
     }
     f.color = c->d_rcolor;
-    std::vector<float> ro;
     for (int b0 = 0; b0 < n_rays; b0 += c->max_rays) {
         int nb = std::min(c->max_rays, n_rays - b0);
-        px3.resize(size_t(nb) * 3);
-        for (int i = 0; i < nb; ++i) {
-            px3[3 * i] = 0;
-            px3[3 * i + 1] = pixels[2 * (b0 + i)];
-            px3[3 * i + 2] = pixels[2 * (b0 + i) + 1];
-        }
-        CK(cudaMemcpyAsync(c->d_pixels, px3.data(), px3.size() * 4, cudaMemcpyHostToDevice, c->st));
+        CK(cudaMemcpyAsync(c->d_pixels, pixels + 2 * uint64_t(b0), size_t(nb) * 8, cudaMemcpyHostToDevice,
+                           c->st));
         RaygenArgs a{};
         a.cams = c->d_rcam;
         a.pixels = c->d_pixels;
+        a.pixel_pairs = 1;
         a.n_rays = nb;
         a.z_min = c->roi.z_min;
         a.z_max = c->roi.z_max;
@@ -1577,16 +1571,18 @@ TFG_API int tfg_render_pixels(tfg_ctx* c, const tfg_rpc* cam, const int32_t* pix
         if ((rc = run_forward(c, f))) return rc;
         c->fwd_done = false;
         if ((rc = run_composite(c, false))) return rc;
-        ro.resize(5 * uint64_t(c->max_rays));
-        CK(cudaMemcpyAsync(ro.data(), c->d_ray_out, ro.size() * 4, cudaMemcpyDeviceToHost, c->st));
+        // outputs straight into the caller's buffers (rgb interleaved as on device)
+        const float* ro = c->d_ray_out;
+        if (rgb)
+            CK(cudaMemcpyAsync(rgb + 3 * uint64_t(b0), ro, size_t(nb) * 12, cudaMemcpyDeviceToHost, c->st));
+        if (depth)
+            CK(cudaMemcpyAsync(depth + b0, ro + 3 * uint64_t(c->max_rays), size_t(nb) * 4, cudaMemcpyDeviceToHost,
+                               c->st));
+        if (opacity)
+            CK(cudaMemcpyAsync(opacity + b0, ro + 4 * uint64_t(c->max_rays), size_t(nb) * 4,
+                               cudaMemcpyDeviceToHost, c->st));
         if ((rc = sync_status(c)) && rc != TFG_ERR_INVALID) return rc;
         if (c->h_status->bits & (kStatusSampleOverflow | kStatusSegOverflow)) return check_status(c);
-        for (int i = 0; i < nb; ++i) {
-            if (rgb)
-                for (int k = 0; k < 3; ++k) rgb[3 * (b0 + i) + k] = ro[3 * i + k];
-            if (depth) depth[b0 + i] = ro[3 * uint64_t(c->max_rays) + i];
-            if (opacity) opacity[b0 + i] = ro[4 * uint64_t(c->max_rays) + i];
-        }
     }
     c->have_batch = false;
     return 0;
