@@ -252,3 +252,62 @@ def test_prefetched_slide_round_trips_state_bit_exactly():
         assert after[t]["enc_step"] == before[t]["enc_step"] == 3
     # the tiles trained at (0,1) carry that step too
     assert after[(0, 1)]["enc_step"] == 4 and after[(1, 1)]["enc_step"] == 4
+
+
+def test_config3_full_snake_constant_memory_linear_time():
+    """Config 3 shape (8x8 grid of 128 m tiles, 49 window positions; 4 of the
+    16 views to bound the CPU oracle): the whole snake runs with a constant
+    HBM footprint, every tile's Adam steps match its visit count, each move
+    costs about the same (time linear in positions), and the accepted list
+    and batch are bit-exact against the oracle at the first, a middle and the
+    last position."""
+    _need_gpu()
+    import time
+
+    import torch
+
+    from oracle.pyoracle import Oracle, Session
+    from paper_2507_01631_b200.tilefield import Context, snake_path
+
+    c3 = synth.CONFIGS[3]
+    scene = synth.make_scene(8, 8, c3["tile_side"], 40.0, 4, 1.0, seed=3)
+    fc, tc = FieldConfig.defaults(), TrainConfig.defaults(batch_rays=2048, seed=2)
+    ctx = Context(scene, fc, tc, max_rays=2048)
+    path = snake_path(8, 8)
+    assert len(path) == 49
+    check = {0, 24, 48}
+    ses = Session(Oracle(), scene, fc, tc, workers=16)
+    visits, mem, dt = {}, None, []
+    for it, pos in enumerate(path):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        ctx.set_window(*pos)
+        if it + 1 < len(path):
+            ctx.prefetch_window(*path[it + 1])
+        torch.cuda.synchronize()
+        dt.append(time.perf_counter() - t0)
+        if it in check:
+            # the oracle jumps here directly, so its slot numbering differs
+            # from the GPU's (slots keep their tiles across moves): compare
+            # samples by tile
+            ses.set_window(*pos)
+            np.testing.assert_array_equal(ctx.accept_list(), ses.build_accept())
+            assert ctx.sample(it, 0, 2048, True) == ses.sample(it, 0, 2048, True)
+            ga, gb = ctx.batch(), ses.batch()
+            ta, tb = np.array(ctx.window_tiles()), np.array(ses.window_tiles())
+            np.testing.assert_array_equal(ta[ga["slot"]], tb[gb["slot"]])
+            ga["slot"] = gb["slot"]
+            _cmp_batch(ga, gb)
+        ctx.train_step(it, 0, 2048)
+        for t in ctx.window_tiles():
+            visits[t] = visits.get(t, 0) + 1
+        m = ctx.memory_report()["total_device"]
+        mem = mem or m
+        assert m == mem
+    # persistent optimizer state: steps == visits for every resident tile
+    for k, t in enumerate(ctx.window_tiles()):
+        assert ctx.tile_state(k)["enc_step"] == visits[t]
+    assert len(visits) == 64
+    # moves (after the first, which builds the initial state) cost about the same
+    steady = sorted(dt[1:])
+    assert steady[len(steady) * 9 // 10] < 4 * steady[len(steady) // 2] + 0.02
