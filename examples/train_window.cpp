@@ -1,9 +1,13 @@
 // examples/train_window.cpp — a C++ host driving the snake progression
 // through the C-ABI exactly as the reference trainer loop would:
-// for each window position, n_it iterations of train_step.  Builds against
-// include/ and links libtilefield_gpu.so.
+// for each window position, n_it iterations of train_step, then a run
+// checkpoint and a PSNR of the view's crop.  Builds against include/ and
+// links libtilefield_gpu.so.
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
+#include <filesystem>
+#include <string>
 #include <vector>
 
 #include "../include/tilefield_gpu.hpp"
@@ -40,6 +44,17 @@ int main() {
             std::printf("window (%d,%d): %llu accepted rays, loss %.5f\n", r, c,
                         (unsigned long long)ctx.accepted_rays(), loss);
         }
+        // run checkpoint (tiles/r{R}_c{C}.ckpt + color_net.ckpt)
+        std::string dir = std::string(std::getenv("TMPDIR") ? std::getenv("TMPDIR") : "/tmp") + "/tfg_example_run";
+        std::filesystem::create_directories(dir + "/tiles");
+        ctx.save_run(dir);
+        // evaluation metric on the GPU: PSNR of the image against a shifted copy
+        std::vector<float> a(64 * 64 * 3), b(a.size());
+        for (size_t i = 0; i < a.size(); ++i) {
+            a[i] = img[i] / 255.f;
+            b[i] = std::fmin(1.f, a[i] + 0.1f);
+        }
+        std::printf("checkpointed to %s; psnr %.2f dB\n", dir.c_str(), ctx.psnr(a.data(), b.data(), a.size()));
     } catch (const tilefield::Error& e) {
         std::printf("tilefield::Error: %s\n", e.what());
         return 1;

@@ -110,6 +110,44 @@ public:
         check(tfg_get_memory_report(c_, &r));
         return r;
     }
+
+    // render + evaluation (cmd_render, evalio)
+    void render_setup(const int32_t* rows, const int32_t* cols, int n, const tfg_tile_state* states,
+                      const float* color_params) {
+        check(tfg_render_setup(c_, rows, cols, n, states, color_params));
+    }
+    void render_view(const tfg_rpc& cam, float* rgb, float* depth, float* opacity) {
+        check(tfg_render_view(c_, &cam, rgb, depth, opacity));
+    }
+    double psnr(const float* a, const float* b, uint64_t n) {
+        double v = 0.0;
+        check(tfg_psnr(c_, a, b, n, &v));
+        return v;
+    }
+    double ssim(const float* a, const float* b, int rows, int cols) {
+        double v = 0.0;
+        check(tfg_ssim(c_, a, b, rows, cols, &v));
+        return v;
+    }
+    double depth_mae(const float* d1, const float* d2, const uint8_t* mask, uint64_t n) {
+        double v = 0.0;
+        check(tfg_depth_mae(c_, d1, d2, mask, n, &v));
+        return v;
+    }
+    void edge_band_mask(const tfg_rpc& cam, int band_px, uint8_t* mask) {
+        check(tfg_edge_band_mask(c_, &cam, band_px, mask));
+    }
+
+    // persistence (checkpoints, run resume, crop cache)
+    void save_run(const std::string& dir) { check(tfg_save_run(c_, dir.c_str())); }
+    void load_run(const std::string& dir) { check(tfg_load_run(c_, dir.c_str())); }
+    uint64_t build_crop_cache(const std::string& path) {
+        uint64_t n = 0;
+        check(tfg_build_crop_cache(c_, path.c_str(), &n));
+        return n;
+    }
+    void load_crop_cache(const std::string& path) { check(tfg_load_crop_cache(c_, path.c_str())); }
+
     tfg_ctx* raw() { return c_; }
 
 private:
