@@ -915,6 +915,7 @@ TFG_API int tfg_set_scene(tfg_ctx* c, const tfg_rpc* cams, int n_views,
     CK(cudaMemcpyAsync(c->d_north, c->north.data(), (grid_rows + 1) * 8, cudaMemcpyHostToDevice, c->st));
     CK(cudaStreamSynchronize(c->st));
     c->nslots = 0;
+    for (int k = 0; k < kTrainSlots; ++k) c->stage_tile[k] = -1;
     c->pos_r = c->pos_c = -1;
     start_init_pool(c);
     return 0;
