@@ -795,6 +795,10 @@ TFG_API int tfg_set_scene(tfg_ctx* c, const tfg_rpc* cams, int n_views,
     if ((grid_rows == 1) != (grid_cols == 1))
         return fail(TFG_ERR_INVALID, "set_scene: 1xN grids need the experimental 1x2 window");
     CK(cudaSetDevice(c->device));
+    // pending copies (e.g. an evicted tile's asynchronous D2H) target buffers
+    // that are about to be freed
+    CK(cudaStreamSynchronize(c->side));
+    CK(cudaStreamSynchronize(c->st));
     c->n_views = n_views;
     c->cams.assign(cams, cams + n_views);
     c->roi = *roi;
