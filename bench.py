@@ -288,8 +288,8 @@ def run_ours(args):
 
     # ---- render (config 4: 4x4-tile ROI, random-init weights, occupancy all on)
     render = None
-    if rank == 0 and not args.no_render:
-        render = bench_render(args)
+    if not args.no_render:
+        render = bench_render(args, rank, world, dev)
 
     out = None
     if rank == 0:
@@ -313,11 +313,15 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def bench_render(args):
+def bench_render(args, rank=0, world=1, dev=None):
+    """Config 4: the full 4096^2-class novel view of a 4x4-tile ROI from
+    random-init tiles (render_view: every pixel, chunks of 2^20 rays).  With N
+    ranks the view's rows are split across the GPUs (no collective); time is
+    the max over ranks."""
     import numpy as np
     import torch
+    import torch.distributed as dist
 
-    from paper_2507_01631_b200 import synth
     from paper_2507_01631_b200.abi import FieldConfig, Roi, TrainConfig
     from paper_2507_01631_b200.synth import Scene, make_camera
     from paper_2507_01631_b200.tilefield import Context, tile_init
@@ -333,29 +337,35 @@ def bench_render(args):
     states = [tile_init(fc, 1, r, c) for r, c in tiles]
     color = ctx.color()[0]
     ctx.render_setup(tiles, states, color)
-    # a 1024 x 1024 block of the 4096^2-class novel view
-    r0, c0 = cam.image_rows // 2 - 512, cam.image_cols // 2 - 512
-    rr, cc = np.meshgrid(np.arange(r0, r0 + 1024), np.arange(c0, c0 + 1024), indexing="ij")
+    # this rank's share of the view: a contiguous band of rows
+    R, W = cam.image_rows, cam.image_cols
+    r0, r1 = R * rank // world, R * (rank + 1) // world
+    rr, cc = np.meshgrid(np.arange(r0, r1), np.arange(W), indexing="ij")
     px = np.stack([rr.ravel(), cc.ravel()], axis=1).astype(np.int32)
-    ctx.render_pixels(cam, px)  # warm-up
+    n = px.shape[0]
+    ctx.render_pixels(cam, px[:chunk])  # warm-up
     ctx.profile_enable(True)
+    if world > 1:
+        dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    reps = 3
-    for _ in range(reps):
-        rgb, dep, op = ctx.render_pixels(cam, px)
+    rgb, dep, op = ctx.render_pixels(cam, px)
     wall = time.perf_counter() - t0
     prof = ctx.profile_read()
     dev_ms = sum(prof[p][0] for p in ("sampler", "field_fwd", "composite"))
-    _, ns = ctx.last_batch()
     ctx.close()
-    return {"value": reps * chunk / (dev_ms / 1e3), "unit": "rays/s",
-            "e2e": {"value": reps * chunk / wall, "unit": "rays/s", "h2d_bytes_per_step": chunk * 12,
-                    "d2h_bytes_per_step": chunk * 20},
-            "config": "cfg4: 4x4-tile ROI (512 m), novel view at 0.125 m, 1024^2-ray block, random-init "
-                      "weights, occupancy all on, midpoint samples",
-            "samples_per_ray": ns / chunk,
-            "phases_ms": {p: prof[p][0] / reps for p in ("sampler", "field_fwd", "composite")}}
+    t = torch.tensor([dev_ms, wall], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dev_ms, wall = float(t[0]), float(t[1])
+    total = R * W
+    return {"value": total / (dev_ms / 1e3), "unit": "rays/s",
+            "e2e": {"value": total / wall, "unit": "rays/s", "h2d_bytes_per_step": total * 8,
+                    "d2h_bytes_per_step": total * 20},
+            "config": f"cfg4: 4x4-tile ROI (512 m), full {R}x{W} novel view at 0.125 m over {world} GPU(s) "
+                      "(row bands, no collective), random-init weights, occupancy all on, midpoint samples",
+            "rays": total,
+            "phases_ms": {p: prof[p][0] for p in ("sampler", "field_fwd", "composite")}}
 
 
 def main():
