@@ -2,8 +2,9 @@
 //
 // The per-tile NeRF field (forward_batch / backward_batch, field.hpp:185-197;
 // MlpT nn.hpp:90-157; HashGridT nn.hpp:213-245) split by bound:
-//   K2a hash_fwd_kernel   hash-grid gather (L2-latency bound): 16 features per
-//                         sample -> bf16 tile in UMMA operand layout (4 KB/tile)
+//   K2a hash_fwd_kernel   hash-grid gather (L1-throughput bound): 16 features
+//                         per sample -> bf16 tile in UMMA operand layout
+//                         (4 KB/tile), reused by K4b
 //   K2b mlp_fwd_kernel    density MLP 16->64->16 + colour MLP 39->64->64->3 as
 //                         tcgen05.mma (bf16 x bf16 -> fp32 in TMEM), operands
 //                         staged by the bulk-copy engine, epilogues
@@ -13,8 +14,11 @@
 //                         read from the same smem tiles) accumulated in TMEM
 //                         across all tiles of a persistent CTA, flushed with
 //                         one fp32 atomic per weight per CTA
-//   (K4a)                 hash-table scatter-add fused into K4b's last epilogue
-//                         (red.global.add.v4/v2.f32, aligned x-neighbour pairs)
+//   (K4a)                 hash-table scatter-add on K4b's own scatter warps
+//                         (warp specialisation: they drain d(features) from
+//                         TMEM while the MLP warps run the next tile;
+//                         red.global.add.v4/v2.f32 on aligned x-neighbour
+//                         pairs, same-cell lane pairs merged on levels 0-2)
 // A tile is <= 128 samples of one slot bucket (K1), so the density weights of
 // a tile are one tile's.  Precision: bf16 operands, fp32 accumulation (tests
 // state the tolerance against the fp32 oracle).
