@@ -758,6 +758,10 @@ TFG_API int tfg_destroy(tfg_ctx* c) {
     for (auto* im : c->h_images)
         if (im) cudaFreeHost(im);
     if (c->h_status) cudaFreeHost(c->h_status);
+    for (void* p : {static_cast<void*>(c->h_rpix), static_cast<void*>(c->h_rout), static_cast<void*>(c->h_rstat)})
+        if (p) cudaFreeHost(p);
+    for (cudaEvent_t e : c->ev_rdone)
+        if (e) cudaEventDestroy(e);
     for (WinBuf& w : c->win) {
         void* wo[] = {w.d_crops, w.d_crop_rect, w.d_crop_off, w.d_accept, w.d_n};
         for (void* p : wo)
@@ -1554,10 +1558,41 @@ TFG_API int tfg_render_pixels(tfg_ctx* c, const tfg_rpc* cam, const int32_t* pix
         f.occ_bits[k] = c->d_rbits + uint64_t(k) * kOccWords;
     }
     f.color = c->d_rcolor;
-    for (int b0 = 0; b0 < n_rays; b0 += c->max_rays) {
-        int nb = std::min(c->max_rays, n_rays - b0);
-        CK(cudaMemcpyAsync(c->d_pixels, pixels + 2 * uint64_t(b0), size_t(nb) * 8, cudaMemcpyHostToDevice,
-                           c->st));
+    // Chunks of max_rays rays, software-pipelined: while the GPU renders chunk
+    // i, the host stages chunk i+1's pixels into one pinned buffer and copies
+    // chunk i-1's outputs out of the other; the GPU side copies only pinned
+    // memory.
+    const uint64_t M = uint64_t(c->max_rays);
+    if (!c->h_rpix) {
+        CK(cudaHostAlloc(reinterpret_cast<void**>(&c->h_rpix), 2 * M * 8, cudaHostAllocDefault));
+        CK(cudaHostAlloc(reinterpret_cast<void**>(&c->h_rout), 2 * M * 20, cudaHostAllocDefault));
+        CK(cudaHostAlloc(reinterpret_cast<void**>(&c->h_rstat), 2 * sizeof(Status), cudaHostAllocDefault));
+        for (auto& e : c->ev_rdone) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    const int nch = int((uint64_t(n_rays) + M - 1) / M);
+    auto chunk_n = [&](int i) { return int(std::min<uint64_t>(M, uint64_t(n_rays) - uint64_t(i) * M)); };
+    auto stage_in = [&](int i) {
+        std::memcpy(c->h_rpix + (i & 1) * 2 * M, pixels + 2 * uint64_t(i) * M, size_t(chunk_n(i)) * 8);
+    };
+    auto drain = [&](int i) -> int {
+        CK(cudaEventSynchronize(c->ev_rdone[i & 1]));
+        const Status& st = c->h_rstat[i & 1];
+        if (st.bits & (kStatusSampleOverflow | kStatusSegOverflow)) {
+            *c->h_status = st;
+            return check_status(c);
+        }
+        const float* ro = c->h_rout + (i & 1) * 5 * M;
+        uint64_t b0 = uint64_t(i) * M, nb = uint64_t(chunk_n(i));
+        if (rgb) std::memcpy(rgb + 3 * b0, ro, nb * 12);
+        if (depth) std::memcpy(depth + b0, ro + 3 * M, nb * 4);
+        if (opacity) std::memcpy(opacity + b0, ro + 4 * M, nb * 4);
+        return 0;
+    };
+    if (nch > 0) stage_in(0);
+    int drained = 0;  // chunks [0, drained) are copied out
+    for (int i = 0; i < nch; ++i) {
+        const int b = i & 1, nb = chunk_n(i);
+        CK(cudaMemcpyAsync(c->d_pixels, c->h_rpix + b * 2 * M, size_t(nb) * 8, cudaMemcpyHostToDevice, c->st));
         RaygenArgs a{};
         a.cams = c->d_rcam;
         a.pixels = c->d_pixels;
@@ -1576,18 +1611,23 @@ TFG_API int tfg_render_pixels(tfg_ctx* c, const tfg_rpc* cam, const int32_t* pix
         if ((rc = run_forward(c, f))) return rc;
         c->fwd_done = false;
         if ((rc = run_composite(c, false))) return rc;
-        // outputs straight into the caller's buffers (rgb interleaved as on device)
-        const float* ro = c->d_ray_out;
-        if (rgb)
-            CK(cudaMemcpyAsync(rgb + 3 * uint64_t(b0), ro, size_t(nb) * 12, cudaMemcpyDeviceToHost, c->st));
-        if (depth)
-            CK(cudaMemcpyAsync(depth + b0, ro + 3 * uint64_t(c->max_rays), size_t(nb) * 4, cudaMemcpyDeviceToHost,
-                               c->st));
-        if (opacity)
-            CK(cudaMemcpyAsync(opacity + b0, ro + 4 * uint64_t(c->max_rays), size_t(nb) * 4,
-                               cudaMemcpyDeviceToHost, c->st));
-        if ((rc = sync_status(c)) && rc != TFG_ERR_INVALID) return rc;
-        if (c->h_status->bits & (kStatusSampleOverflow | kStatusSegOverflow)) return check_status(c);
+        float* ho = c->h_rout + b * 5 * M;
+        CK(cudaMemcpyAsync(ho, c->d_ray_out, size_t(nb) * 12, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaMemcpyAsync(ho + 3 * M, c->d_ray_out + 3 * M, size_t(nb) * 4, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaMemcpyAsync(ho + 4 * M, c->d_ray_out + 4 * M, size_t(nb) * 4, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaMemcpyAsync(c->h_rstat + b, c->d_status, sizeof(Status), cudaMemcpyDeviceToHost, c->st));
+        CK(cudaEventRecord(c->ev_rdone[b], c->st));
+        c->d2h_bytes += uint64_t(nb) * 20 + sizeof(Status);
+        if (i + 1 < nch) {
+            // chunk i-1 used the buffers chunk i+1 is about to take
+            if (i >= 1 && (rc = drain(i - 1))) return rc;
+            drained = i;
+            stage_in(i + 1);
+        }
+    }
+    for (int i = drained; i < nch; ++i) {
+        int rc = drain(i);
+        if (rc) return rc;
     }
     c->have_batch = false;
     return 0;

@@ -153,6 +153,11 @@ struct tfg_ctx {
     TileDesc* d_tiles = nullptr;
     SampleArrays s{};
     float* d_ray_out = nullptr;  // rgb(3) | depth | opacity per ray
+    // render pipeline: pinned double buffers (pixels in, outputs + status out)
+    int32_t* h_rpix = nullptr;   // 2 x max_rays x (row, col)
+    float* h_rout = nullptr;     // 2 x max_rays x 5
+    Status* h_rstat = nullptr;   // 2
+    cudaEvent_t ev_rdone[2] = {nullptr, nullptr};
     int32_t* d_pixels = nullptr;
     uint8_t* d_feat = nullptr;    // bf16 feature tiles (4 KB per 128-sample tile)
     int32_t* d_tile_rays = nullptr;
