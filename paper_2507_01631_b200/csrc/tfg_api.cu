@@ -1588,6 +1588,9 @@ TFG_API int tfg_render_pixels(tfg_ctx* c, const tfg_rpc* cam, const int32_t* pix
         if (opacity) std::memcpy(opacity + b0, ro + 4 * M, nb * 4);
         return 0;
     };
+    // a previous call that stopped on an error may still have copies queued
+    // from the pinned buffers
+    CK(cudaStreamSynchronize(c->st));
     if (nch > 0) stage_in(0);
     int drained = 0;  // chunks [0, drained) are copied out
     for (int i = 0; i < nch; ++i) {
