@@ -120,17 +120,4 @@ __device__ __forceinline__ void hash_encode(const HashLayout& hl, const float* _
     }
 }
 
-__device__ __forceinline__ void hash_scatter(const HashLayout& hl, float* __restrict__ g, float x,
-                                             float y, float z, const float* d) {
-    float2* g2 = reinterpret_cast<float2*>(g);
-#pragma unroll
-    for (int l = 0; l < kLevels; ++l) {
-        Corner c;
-        hash_level(hl, l, x, y, z, c);
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-            atomicAdd(g2 + c.idx[k], make_float2(c.w[k] * d[2 * l], c.w[k] * d[2 * l + 1]));
-    }
-}
-
 } // namespace tfg
