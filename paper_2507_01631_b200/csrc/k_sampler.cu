@@ -302,10 +302,15 @@ __device__ __forceinline__ bool occ_test(const uint32_t* bits, float x, float y,
 #ifndef TFG_RAYGEN_MINB
 #define TFG_RAYGEN_MINB 4
 #endif
-__global__ void __launch_bounds__(128, TFG_RAYGEN_MINB) raygen_kernel(RaygenArgs a, RayRec* __restrict__ rays,
-                                                     float4* __restrict__ venc,
-                                                     uint32_t* __restrict__ counts,
-                                                     Status* __restrict__ status) {
+// kSolve = false: drawn pixels with the pixel memo only (no Newton code, so
+// fewer registers and more resident warps); true: explicit pixels or no memo.
+#ifndef TFG_RAYGEN_MEMO_MINB
+#define TFG_RAYGEN_MEMO_MINB 8
+#endif
+template <bool kSolve>
+__global__ void __launch_bounds__(128, kSolve ? TFG_RAYGEN_MINB : TFG_RAYGEN_MEMO_MINB)
+    raygen_kernel(RaygenArgs a, RayRec* __restrict__ rays, float4* __restrict__ venc,
+                  uint32_t* __restrict__ counts, Status* __restrict__ status) {
     const int gt = blockIdx.x * blockDim.x + threadIdx.x;
     const int i = gt >> 1, hi = gt & 1;
     const uint32_t pair = 3u << ((threadIdx.x & 31) & ~1);
@@ -345,6 +350,8 @@ __global__ void __launch_bounds__(128, TFG_RAYGEN_MINB) raygen_kernel(RaygenArgs
             R.o[q] = memo[q];
             R.d[q] = memo[3 + q];
         }
+    } else if constexpr (!kSolve) {
+        R.status = 1;  // empty accepted list (flagged above)
     } else {
         double gx = 0.0, gy = 0.0;
         int st = rpc_localize(a.cams[v], double(row), double(col), hi ? a.z_min : a.z_max, &gx, &gy);
@@ -583,7 +590,10 @@ int launch_sampler(const RaygenArgs& a, RayRec* rays, float4* venc, uint32_t* co
                    uint32_t* P, uint32_t* block_sums, TileDesc* tiles, int max_tiles,
                    SampleArrays out, uint64_t capacity, Status* status, cudaStream_t st,
                    uint64_t* launches) {
-    raygen_kernel<<<(2 * a.n_rays + 127) / 128, 128, 0, st>>>(a, rays, venc, counts, status);
+    if (!a.pixels && a.pix_rays)
+        raygen_kernel<false><<<(2 * a.n_rays + 127) / 128, 128, 0, st>>>(a, rays, venc, counts, status);
+    else
+        raygen_kernel<true><<<(2 * a.n_rays + 127) / 128, 128, 0, st>>>(a, rays, venc, counts, status);
     uint64_t n = uint64_t(a.slots.n) * a.n_rays;
     if (scan_exclusive(counts, n, P, block_sums, nullptr, st, launches)) return 1;
     tiles_kernel<<<1, 256, 0, st>>>(P, a.n_rays, a.slots.n, capacity, max_tiles, tiles, status);
