@@ -278,12 +278,13 @@ __device__ __forceinline__ void plan_intervals(SegPlan& p, double spm, int cap) 
     }
 }
 
+// step = (tf - tn) / n of the segment, computed once per segment by the
+// caller (the same FP64 quotient for every sample of the segment)
 __device__ __forceinline__ double sample_t(const SegPlan& p, int k, int j, bool jitter,
-                                           uint64_t key) {
+                                           uint64_t key, double step) {
     int n = p.nint[k];
     if (j == 0) return p.tn[k];
     if (j == n) return p.tf[k];
-    double step = (p.tf[k] - p.tn[k]) / n;
     float u = 0.5f;
     if (jitter) u = Rng(hash_combine(key, (uint64_t(k) << 16) | uint64_t(j))).flt();
     return p.tn[k] + (double(j) + (double(u) - 0.5)) * step;
@@ -411,9 +412,10 @@ __global__ void __launch_bounds__(128, kSolve ? TFG_RAYGEN_MINB : TFG_RAYGEN_MEM
         const double* fr = a.slots.frame[p.slot[k]];
         const uint32_t* bits = a.occ_bits[p.slot[k]];
         int n = p.nint[k];
+        const double step = (p.tf[k] - p.tn[k]) / n;
         int cnt = 0;
         for (int j = 1 + hi; j < n; j += 2) {
-            double t = sample_t(p, k, j, a.jitter, key);
+            double t = sample_t(p, k, j, a.jitter, key, step);
             float lx = float((R.o[0] + t * R.d[0] - fr[0]) * fr[3]);
             float ly = float((R.o[1] + t * R.d[1] - fr[1]) * fr[4]);
             float lz = float((R.o[2] + t * R.d[2] - fr[2]) * fr[5]);
@@ -525,6 +527,7 @@ __global__ void __launch_bounds__(256) write_kernel(RaygenArgs a, const RayRec* 
         uint64_t base = P[uint64_t(s) * a.n_rays + warp];
         uint32_t written = 0;
         int n = p.nint[k];
+        const double step = (p.tf[k] - p.tn[k]) / n;
         for (int j0 = 0; j0 <= n; j0 += 32) {
             int j = j0 + lane;
             bool valid = j <= n;
@@ -533,7 +536,7 @@ __global__ void __launch_bounds__(256) write_kernel(RaygenArgs a, const RayRec* 
             bool endp = (j == 0 || j == n);
             bool keep = false;
             if (valid) {
-                t = sample_t(p, k, j, a.jitter, key);
+                t = sample_t(p, k, j, a.jitter, key, step);
                 lx = float((R.o[0] + t * R.d[0] - fr[0]) * fr[3]);
                 ly = float((R.o[1] + t * R.d[1] - fr[1]) * fr[4]);
                 lz = float((R.o[2] + t * R.d[2] - fr[2]) * fr[5]);
