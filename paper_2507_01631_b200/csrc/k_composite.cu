@@ -45,6 +45,7 @@ __global__ void __launch_bounds__(256) composite_kernel(CompositeArgs a) {
     float4 cio[kCache];
     float2 ctd[kCache];
     uint64_t cpos[kCache];
+    float cw[kCache], ct1[kCache];  // weight w_k and T_{k+1} of the cached samples
     auto fetch = [&](int q, float4& io, float2& td, uint64_t& pos) {
         io = make_float4(0.f, 0.f, 0.f, 0.f);
         td = make_float2(0.f, 0.f);
@@ -59,6 +60,7 @@ __global__ void __launch_bounds__(256) composite_kernel(CompositeArgs a) {
     };
     // ---------------- forward
     float T = 1.f, cr = 0.f, cg = 0.f, cb = 0.f, dep = 0.f, op = 0.f;
+    float w_last = 0.f, t1_last = 0.f;  // of the lane's sample in the last chunk processed
     auto fwd_chunk = [&](const float4& io, const float2& td) {
         float alpha = 1.f - expf(-(io.x * td.y));
         float keep = 1.f - alpha;
@@ -76,6 +78,8 @@ __global__ void __launch_bounds__(256) composite_kernel(CompositeArgs a) {
         cb += w * io.w;
         dep += w * td.x;
         op += w;
+        w_last = w;
+        t1_last = T * incl;
         T *= __shfl_sync(FULL, incl, 31);
     };
 #pragma unroll
@@ -83,8 +87,11 @@ __global__ void __launch_bounds__(256) composite_kernel(CompositeArgs a) {
         if (ci * 32 < m) {
             fetch(ci * 32 + lane, cio[ci], ctd[ci], cpos[ci]);
             fwd_chunk(cio[ci], ctd[ci]);
+            cw[ci] = w_last;
+            ct1[ci] = t1_last;
         }
     }
+    const float T_after_cache = T;
     for (int q0 = kCache * 32; q0 < m; q0 += 32) {
         float4 io;
         float2 td;
@@ -114,9 +121,10 @@ __global__ void __launch_bounds__(256) composite_kernel(CompositeArgs a) {
     // ---------------- backward
     float T2 = 1.f, pr = 0.f, pg = 0.f, pb = 0.f;
     float Rbr = T * a.bg.x, Rbg = T * a.bg.y, Rbb = T * a.bg.z;
-    auto bwd_chunk = [&](int q, const float4& io, const float2& td, uint64_t pos) {
-        float sg = io.x, de = td.y;
-        float alpha = 1.f - expf(-(sg * de));
+    // w and T_{k+1} of a chunk: recomputed exactly as the forward sweep did
+    // (same operations, same order), or taken from the forward's cache
+    auto chunk_weights = [&](const float4& io, const float2& td, float& w, float& Tk1) {
+        float alpha = 1.f - expf(-(io.x * td.y));
         float keep = 1.f - alpha;
         float incl = keep;
 #pragma unroll
@@ -126,9 +134,12 @@ __global__ void __launch_bounds__(256) composite_kernel(CompositeArgs a) {
         }
         float excl = __shfl_up_sync(FULL, incl, 1);
         if (lane == 0) excl = 1.f;
-        float Tk = T2 * excl;
-        float w = Tk * alpha;
-        float Tk1 = T2 * incl;
+        w = T2 * excl * alpha;
+        Tk1 = T2 * incl;
+        T2 *= __shfl_sync(FULL, incl, 31);
+    };
+    auto bwd_chunk = [&](int q, const float4& io, const float2& td, uint64_t pos, float w, float Tk1) {
+        float sg = io.x, de = td.y;
         // inclusive prefix of w*c
         float sr = w * io.y, sgc = w * io.z, sbc = w * io.w;
 #pragma unroll
@@ -155,17 +166,19 @@ __global__ void __launch_bounds__(256) composite_kernel(CompositeArgs a) {
         pr += __shfl_sync(FULL, sr, 31);
         pg += __shfl_sync(FULL, sgc, 31);
         pb += __shfl_sync(FULL, sbc, 31);
-        T2 *= __shfl_sync(FULL, incl, 31);
     };
 #pragma unroll
     for (int ci = 0; ci < kCache; ++ci)
-        if (ci * 32 < m) bwd_chunk(ci * 32 + lane, cio[ci], ctd[ci], cpos[ci]);
+        if (ci * 32 < m) bwd_chunk(ci * 32 + lane, cio[ci], ctd[ci], cpos[ci], cw[ci], ct1[ci]);
+    T2 = T_after_cache;  // the uncached tail continues from the forward's transmittance
     for (int q0 = kCache * 32; q0 < m; q0 += 32) {
         float4 io;
         float2 td;
         uint64_t pos;
         fetch(q0 + lane, io, td, pos);
-        bwd_chunk(q0 + lane, io, td, pos);
+        float w, Tk1;
+        chunk_weights(io, td, w, Tk1);
+        bwd_chunk(q0 + lane, io, td, pos, w, Tk1);
     }
 }
 
