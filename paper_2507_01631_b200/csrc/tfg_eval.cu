@@ -5,12 +5,27 @@
 
 // ---------------------------------------------------------------- evaluation
 namespace {
-template <typename T>
-int dcopy_in(tfg_ctx* c, T** d, const T* h, uint64_t n) {
-    CK(cudaMallocAsync(reinterpret_cast<void**>(d), n * sizeof(T), c->st));
-    CK(cudaMemcpyAsync(*d, h, n * sizeof(T), cudaMemcpyHostToDevice, c->st));
-    return 0;
-}
+// Stream-ordered device scratch of one call, released on every exit path.
+struct Scratch {
+    tfg_ctx* c;
+    std::vector<void*> ptrs;
+    explicit Scratch(tfg_ctx* ctx) : c(ctx) {}
+    ~Scratch() {
+        for (void* p : ptrs) cudaFreeAsync(p, c->st);
+    }
+    template <typename T>
+    int alloc(T** d, uint64_t n) {
+        CK(cudaMallocAsync(reinterpret_cast<void**>(d), n * sizeof(T), c->st));
+        ptrs.push_back(*d);
+        return 0;
+    }
+    template <typename T>
+    int upload(T** d, const T* h, uint64_t n) {
+        if (alloc(d, n)) return TFG_ERR_CUDA;
+        CK(cudaMemcpyAsync(*d, h, n * sizeof(T), cudaMemcpyHostToDevice, c->st));
+        return 0;
+    }
+};
 } // namespace
 
 extern "C" {
@@ -18,17 +33,15 @@ extern "C" {
 TFG_API int tfg_psnr(tfg_ctx* c, const float* a, const float* b, uint64_t n, double* db) {
     if (!c || !a || !b || n == 0 || !db) return fail(TFG_ERR_INVALID, "psnr: empty or null input");
     CK(cudaSetDevice(c->device));
+    Scratch sc(c);
     float *da = nullptr, *dbuf = nullptr;
     double* acc = nullptr;
-    if (dcopy_in(c, &da, a, n) || dcopy_in(c, &dbuf, b, n)) return TFG_ERR_CUDA;
-    CK(cudaMallocAsync(reinterpret_cast<void**>(&acc), 8, c->st));
+    if (sc.upload(&da, a, n) || sc.upload(&dbuf, b, n) || sc.alloc(&acc, 1)) return TFG_ERR_CUDA;
     CK(cudaMemsetAsync(acc, 0, 8, c->st));
     launch_sq_diff(da, dbuf, n, acc, c->sms, c->st);
     c->launches += 1;
     double s = 0.0;
     CK(cudaMemcpyAsync(&s, acc, 8, cudaMemcpyDeviceToHost, c->st));
-    for (void* p : {static_cast<void*>(da), static_cast<void*>(dbuf), static_cast<void*>(acc)})
-        CK(cudaFreeAsync(p, c->st));
     CK(cudaStreamSynchronize(c->st));
     double mse = s / double(n);
     *db = mse > 0.0 ? std::min(99.0, 10.0 * std::log10(1.0 / mse)) : 99.0;
@@ -40,9 +53,10 @@ TFG_API int tfg_ssim(tfg_ctx* c, const float* a, const float* b, int rows, int c
     if (rows < 11 || cols < 11) return fail(TFG_ERR_INVALID, "ssim: image smaller than the 11x11 window");
     CK(cudaSetDevice(c->device));
     uint64_t n = uint64_t(rows) * uint64_t(cols) * 3;
+    Scratch sc(c);
     float *da = nullptr, *dbuf = nullptr, *gw = nullptr;
     double* acc = nullptr;
-    if (dcopy_in(c, &da, a, n) || dcopy_in(c, &dbuf, b, n)) return TFG_ERR_CUDA;
+    if (sc.upload(&da, a, n) || sc.upload(&dbuf, b, n)) return TFG_ERR_CUDA;
     float w[11];
     {
         double g[11], sum = 0.0;
@@ -53,16 +67,12 @@ TFG_API int tfg_ssim(tfg_ctx* c, const float* a, const float* b, int rows, int c
         }
         for (int k = 0; k < 11; ++k) w[k] = float(g[k] / sum);
     }
-    if (dcopy_in(c, &gw, w, 11)) return TFG_ERR_CUDA;
-    CK(cudaMallocAsync(reinterpret_cast<void**>(&acc), 8, c->st));
+    if (sc.upload(&gw, static_cast<const float*>(w), 11) || sc.alloc(&acc, 1)) return TFG_ERR_CUDA;
     CK(cudaMemsetAsync(acc, 0, 8, c->st));
     launch_ssim(da, dbuf, rows, cols, gw, acc, c->st);
     c->launches += 1;
     double s = 0.0;
     CK(cudaMemcpyAsync(&s, acc, 8, cudaMemcpyDeviceToHost, c->st));
-    for (void* p : {static_cast<void*>(da), static_cast<void*>(dbuf), static_cast<void*>(gw),
-                    static_cast<void*>(acc)})
-        CK(cudaFreeAsync(p, c->st));
     CK(cudaStreamSynchronize(c->st));
     *out = s / (double(rows - 10) * double(cols - 10));
     return 0;
@@ -72,19 +82,17 @@ TFG_API int tfg_depth_mae(tfg_ctx* c, const float* d1, const float* d2, const ui
                           double* out) {
     if (!c || !d1 || !d2 || n == 0 || !out) return fail(TFG_ERR_INVALID, "depth_mae: empty or null input");
     CK(cudaSetDevice(c->device));
+    Scratch sc(c);
     float *a = nullptr, *b = nullptr;
     uint8_t* m = nullptr;
     double* acc = nullptr;
-    if (dcopy_in(c, &a, d1, n) || dcopy_in(c, &b, d2, n)) return TFG_ERR_CUDA;
-    if (mask && dcopy_in(c, &m, mask, n)) return TFG_ERR_CUDA;
-    CK(cudaMallocAsync(reinterpret_cast<void**>(&acc), 16, c->st));
+    if (sc.upload(&a, d1, n) || sc.upload(&b, d2, n) || sc.alloc(&acc, 2)) return TFG_ERR_CUDA;
+    if (mask && sc.upload(&m, mask, n)) return TFG_ERR_CUDA;
     CK(cudaMemsetAsync(acc, 0, 16, c->st));
     launch_abs_diff(a, b, m, n, acc, c->sms, c->st);
     c->launches += 1;
     double s[2] = {0.0, 0.0};
     CK(cudaMemcpyAsync(s, acc, 16, cudaMemcpyDeviceToHost, c->st));
-    for (void* p : {static_cast<void*>(a), static_cast<void*>(b), static_cast<void*>(m), static_cast<void*>(acc)})
-        if (p) CK(cudaFreeAsync(p, c->st));
     CK(cudaStreamSynchronize(c->st));
     if (s[1] == 0.0) return fail(TFG_ERR_INVALID, "depth_mae: empty mask");
     *out = s[0] / s[1];
@@ -96,11 +104,11 @@ TFG_API int tfg_edge_band_mask(tfg_ctx* c, const tfg_rpc* cam, int band_px, uint
     if (!cam || !mask || band_px < 0) return fail(TFG_ERR_INVALID, "edge_band_mask: bad arguments");
     CK(cudaSetDevice(c->device));
     uint64_t npx = uint64_t(cam->image_rows) * uint64_t(cam->image_cols);
+    Scratch sc(c);
     uint8_t* dm = nullptr;
     tfg_rpc* dcam = nullptr;
-    CK(cudaMallocAsync(reinterpret_cast<void**>(&dm), npx, c->st));
+    if (sc.alloc(&dm, npx) || sc.upload(&dcam, cam, 1)) return TFG_ERR_CUDA;
     CK(cudaMemsetAsync(dm, 0, npx, c->st));
-    if (dcopy_in(c, &dcam, cam, 1)) return TFG_ERR_CUDA;
     // sample the boundary lines at 1/8 of the view's ground footprint per pixel
     double ext = std::max(c->roi.easting_max - c->roi.easting_min, c->roi.northing_max - c->roi.northing_min);
     double gsd = std::fabs(cam->long_scale) / std::max(1.0, std::fabs(cam->samp_scale));
@@ -110,8 +118,6 @@ TFG_API int tfg_edge_band_mask(tfg_ctx* c, const tfg_rpc* cam, int band_px, uint
                      band_px, dm, c->st);
     c->launches += 1;
     CK(cudaMemcpyAsync(mask, dm, npx, cudaMemcpyDeviceToHost, c->st));
-    CK(cudaFreeAsync(dm, c->st));
-    CK(cudaFreeAsync(dcam, c->st));
     CK(cudaStreamSynchronize(c->st));
     return 0;
 }
