@@ -681,60 +681,68 @@ TFG_API int tfg_create(const tfg_field_config* fcfg, const tfg_train_config* tcf
     c->density_lim = std::log(fcfg->density_max);
     c->sample_cap = uint64_t(max_rays) * 128;
     c->max_tiles = int(c->sample_cap / 128 + kMaxSlots + 1);
-    int rc = 0;
-    CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
-    CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
-    CK(cudaEventCreateWithFlags(&c->ev_main, cudaEventDisableTiming));
-    CK(cudaEventCreateWithFlags(&c->ev_side, cudaEventDisableTiming));
-    CK(cudaEventCreateWithFlags(&c->ev_swap, cudaEventDisableTiming));
-    CK(cudaEventRecord(c->ev_swap, c->st));
-    for (cudaEvent_t* e : {&c->ev_stage_in, &c->ev_stage_read, &c->ev_out_done}) {
-        CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
-        CK(cudaEventRecord(*e, c->st));
-    }
-    rc |= dalloc(c, &c->d_params, c->n_params);
-    rc |= dalloc(c, &c->d_stage_in, uint64_t(kTrainSlots) * (3 * c->stride + kOccVox));
-    rc |= dalloc(c, &c->d_stage_out, uint64_t(kTrainSlots) * (3 * c->stride + kOccVox));
-    rc |= dalloc(c, &c->d_grads, c->n_params);
-    rc |= dalloc(c, &c->d_m, c->n_params);
-    rc |= dalloc(c, &c->d_v, c->n_params);
-    rc |= dalloc(c, &c->d_ema, uint64_t(kTrainSlots) * kOccVox);
-    rc |= dalloc(c, &c->d_bits, uint64_t(kMaxSlots) * kOccWords);
-    rc |= dalloc(c, &c->d_group_flags, 16);
-    rc |= dalloc(c, &c->d_status, 1);
-    rc |= dalloc(c, &c->d_rays, max_rays);
-    rc |= dalloc(c, &c->d_venc, uint64_t(max_rays) * 6);
-    rc |= dalloc(c, &c->d_counts, uint64_t(max_rays) * kMaxSlots);
-    rc |= dalloc(c, &c->d_P, uint64_t(max_rays) * kMaxSlots + 1);
-    rc |= dalloc(c, &c->d_tiles, c->max_tiles);
-    rc |= dalloc(c, &c->s.local, c->sample_cap);
-    rc |= dalloc(c, &c->s.td, c->sample_cap);
-    rc |= dalloc(c, &c->s.endpoint, c->sample_cap);
-    rc |= dalloc(c, &c->s.io, c->sample_cap);
-    rc |= dalloc(c, &c->d_ray_out, uint64_t(max_rays) * 5);
-    rc |= dalloc(c, &c->d_pixels, uint64_t(max_rays) * 3);
-    rc |= dalloc(c, &c->d_feat, uint64_t(c->max_tiles) * 4096);
-    rc |= dalloc(c, &c->d_tile_rays, uint64_t(c->max_tiles) * 128);
-    rc |= dalloc(c, &c->d_block_sums, 4096 + 64);
-    rc |= dalloc(c, &c->d_acc_sums, 4096 + 64);
-    rc |= dalloc(c, &c->d_rcam, 1);
+    // everything below may fail part-way: tfg_destroy releases what was made
+    auto init = [&]() -> int {
+        int rc = 0;
+        CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&c->ev_main, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->ev_side, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->ev_swap, cudaEventDisableTiming));
+        CK(cudaEventRecord(c->ev_swap, c->st));
+        for (cudaEvent_t* e : {&c->ev_stage_in, &c->ev_stage_read, &c->ev_out_done}) {
+            CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+            CK(cudaEventRecord(*e, c->st));
+        }
+        rc |= dalloc(c, &c->d_params, c->n_params);
+        rc |= dalloc(c, &c->d_stage_in, uint64_t(kTrainSlots) * (3 * c->stride + kOccVox));
+        rc |= dalloc(c, &c->d_stage_out, uint64_t(kTrainSlots) * (3 * c->stride + kOccVox));
+        rc |= dalloc(c, &c->d_grads, c->n_params);
+        rc |= dalloc(c, &c->d_m, c->n_params);
+        rc |= dalloc(c, &c->d_v, c->n_params);
+        rc |= dalloc(c, &c->d_ema, uint64_t(kTrainSlots) * kOccVox);
+        rc |= dalloc(c, &c->d_bits, uint64_t(kMaxSlots) * kOccWords);
+        rc |= dalloc(c, &c->d_group_flags, 16);
+        rc |= dalloc(c, &c->d_status, 1);
+        rc |= dalloc(c, &c->d_rays, max_rays);
+        rc |= dalloc(c, &c->d_venc, uint64_t(max_rays) * 6);
+        rc |= dalloc(c, &c->d_counts, uint64_t(max_rays) * kMaxSlots);
+        rc |= dalloc(c, &c->d_P, uint64_t(max_rays) * kMaxSlots + 1);
+        rc |= dalloc(c, &c->d_tiles, c->max_tiles);
+        rc |= dalloc(c, &c->s.local, c->sample_cap);
+        rc |= dalloc(c, &c->s.td, c->sample_cap);
+        rc |= dalloc(c, &c->s.endpoint, c->sample_cap);
+        rc |= dalloc(c, &c->s.io, c->sample_cap);
+        rc |= dalloc(c, &c->d_ray_out, uint64_t(max_rays) * 5);
+        rc |= dalloc(c, &c->d_pixels, uint64_t(max_rays) * 3);
+        rc |= dalloc(c, &c->d_feat, uint64_t(c->max_tiles) * 4096);
+        rc |= dalloc(c, &c->d_tile_rays, uint64_t(c->max_tiles) * 128);
+        rc |= dalloc(c, &c->d_block_sums, 4096 + 64);
+        rc |= dalloc(c, &c->d_acc_sums, 4096 + 64);
+        rc |= dalloc(c, &c->d_rcam, 1);
+        if (rc) return TFG_ERR_CUDA;
+        CK(cudaHostAlloc(reinterpret_cast<void**>(&c->h_status), sizeof(Status), cudaHostAllocDefault));
+        CK(cudaMemsetAsync(c->d_params, 0, c->n_params * 4, c->st));
+        CK(cudaMemsetAsync(c->d_m, 0, c->n_params * 4, c->st));
+        CK(cudaMemsetAsync(c->d_v, 0, c->n_params * 4, c->st));
+        CK(cudaMemsetAsync(c->d_grads, 0, c->n_params * 4, c->st));
+        CK(cudaMemsetAsync(c->d_status, 0, sizeof(Status), c->st));
+        // GlobalColorNet::create (field.hpp:118)
+        std::vector<float> color(col);
+        Rng rcn(hash_combine(c->tc.seed, kPurposeColor));
+        const int cw[4] = {kCIn, kCHidden, kCHidden, 3};
+        mlp_init_host(cw, 4, rcn, color.data());
+        CK(cudaMemcpyAsync(c->d_params + c->color_off, color.data(), col * 4, cudaMemcpyHostToDevice, c->st));
+        CK(cudaStreamSynchronize(c->st));
+        return 0;
+    };
+    int rc = init();
     if (rc) {
-        delete c;
-        return TFG_ERR_CUDA;
+        std::string msg = g_err;
+        tfg_destroy(c);
+        g_err = msg;
+        return rc;
     }
-    CK(cudaHostAlloc(reinterpret_cast<void**>(&c->h_status), sizeof(Status), cudaHostAllocDefault));
-    CK(cudaMemsetAsync(c->d_params, 0, c->n_params * 4, c->st));
-    CK(cudaMemsetAsync(c->d_m, 0, c->n_params * 4, c->st));
-    CK(cudaMemsetAsync(c->d_v, 0, c->n_params * 4, c->st));
-    CK(cudaMemsetAsync(c->d_grads, 0, c->n_params * 4, c->st));
-    CK(cudaMemsetAsync(c->d_status, 0, sizeof(Status), c->st));
-    // GlobalColorNet::create (field.hpp:118)
-    std::vector<float> color(col);
-    Rng rcn(hash_combine(c->tc.seed, kPurposeColor));
-    const int cw[4] = {kCIn, kCHidden, kCHidden, 3};
-    mlp_init_host(cw, 4, rcn, color.data());
-    CK(cudaMemcpyAsync(c->d_params + c->color_off, color.data(), col * 4, cudaMemcpyHostToDevice, c->st));
-    CK(cudaStreamSynchronize(c->st));
     *out = c;
     return 0;
 }
