@@ -25,6 +25,7 @@ __device__ __forceinline__ float warp_sum(float v) {
 __global__ void __launch_bounds__(256) composite_kernel(CompositeArgs a) {
     int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     int lane = threadIdx.x & 31;
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");  // the forward's sigma/rgb
     if (i >= a.n_rays) return;
     if (a.status_in->bits & kStatusSampleOverflow) return;
     const RayRec& R = a.rays[i];
@@ -184,7 +185,7 @@ __global__ void __launch_bounds__(256) composite_kernel(CompositeArgs a) {
 
 void launch_composite(const CompositeArgs& a, cudaStream_t st, uint64_t* launches) {
     int blocks = (a.n_rays * 32 + 255) / 256;
-    composite_kernel<<<blocks, 256, 0, st>>>(a);
+    launch_pdl(composite_kernel, dim3(blocks), dim3(256), 0, st, a);
     *launches += 1;
 }
 

@@ -366,6 +366,7 @@ __global__ void __launch_bounds__(128, 4) mlp_fwd_kernel(FieldArgs a, const uint
     stage_color(W, a.f.color);
     uint32_t ph_mma = 0, ph_ld = 0;
     int cur = -1;
+    umma::griddep_wait();  // hash_fwd's feature tiles and ray ids
     uint32_t n_tiles = a.status->n_tiles;
     sync_for_mma();
     const uint32_t tmem = tmem_slot;
@@ -635,6 +636,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2) mlp_bwd_kernel(FieldArgs a, Fi
         float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         st_chunk(X0, r, 3, z);
     }
+    umma::griddep_wait();  // the composite's gradients
     uint32_t n_tiles = a.status->n_tiles;
     sync_for_mma();
     const uint32_t tmem = tmem_slot;
@@ -956,7 +958,7 @@ void launch_field_forward_tc(const FieldArgs& a, uint8_t* feat, int32_t* rays, i
         attr = true;
     }
     hash_fwd_kernel<<<sms * 8, 128, 0, st>>>(a, feat, rays);
-    mlp_fwd_kernel<<<sms * 4, 128, kFwdSmem, st>>>(a, feat, rays);  // 4 resident per SM
+    launch_pdl(mlp_fwd_kernel, dim3(sms * 4), dim3(128), kFwdSmem, st, a, feat, rays);  // 4 per SM
     *launches += 2;
 }
 
@@ -969,7 +971,7 @@ void launch_field_backward_tc(const FieldArgs& a, const FieldGradArgs& g, uint8_
     }
     // the feature tiles of the forward pass (same batch) are still resident;
     // the hash-table scatter is fused into the backward's last epilogue
-    mlp_bwd_kernel<<<sms * 2, kBwdThreads, kBwdSmem, st>>>(a, g, feat, rays);
+    launch_pdl(mlp_bwd_kernel, dim3(sms * 2), dim3(kBwdThreads), kBwdSmem, st, a, g, feat, rays);
     *launches += 1;
 }
 

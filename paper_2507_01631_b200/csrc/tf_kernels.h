@@ -151,6 +151,29 @@ void launch_adam(const AdamArgs& a, uint64_t total, cudaStream_t st, uint64_t* l
 void launch_occupancy(const OccArgs& a, cudaStream_t st, uint64_t* launches);
 
 
+// Launch with programmatic stream serialization (the kernel calls
+// umma::griddep_wait() before reading its predecessor's outputs).
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+#ifdef TFG_NO_PDL
+    k<<<grid, block, smem, st>>>(static_cast<KArgs>(args)...);
+    return cudaGetLastError();
+#else
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+#endif
+}
+
 // evaluation metrics (k_eval.cu)
 void launch_sq_diff(const float* a, const float* b, uint64_t n, double* out, int sms, cudaStream_t st);
 void launch_abs_diff(const float* a, const float* b, const uint8_t* mask, uint64_t n, double* out, int sms,
