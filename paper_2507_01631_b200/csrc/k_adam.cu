@@ -21,6 +21,7 @@ __device__ __forceinline__ int group_of(const AdamArgs& a, uint64_t i) {
 }
 
 __global__ void __launch_bounds__(256) grad_check_kernel(AdamArgs a, uint64_t total) {
+    pdl_wait();
     uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
     uint32_t bad = 0;  // bitmask of groups
     for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
@@ -35,6 +36,7 @@ __global__ void __launch_bounds__(256) grad_check_kernel(AdamArgs a, uint64_t to
 }
 
 __global__ void __launch_bounds__(256) adam_kernel(AdamArgs a, uint64_t total) {
+    pdl_wait();
     __shared__ int skip;
     if (threadIdx.x == 0) {
         int s = 0;
@@ -68,8 +70,8 @@ __global__ void __launch_bounds__(256) adam_kernel(AdamArgs a, uint64_t total) {
 void launch_adam(const AdamArgs& a, uint64_t total, cudaStream_t st, uint64_t* launches) {
     int blocks = int((total + 255) / 256);
     if (blocks > 148 * 8) blocks = 148 * 8;
-    grad_check_kernel<<<blocks, 256, 0, st>>>(a, total);
-    adam_kernel<<<blocks, 256, 0, st>>>(a, total);
+    launch_pdl(grad_check_kernel, dim3(blocks), dim3(256), 0, st, a, total);
+    launch_pdl(adam_kernel, dim3(blocks), dim3(256), 0, st, a, total);
     *launches += 2;
 }
 

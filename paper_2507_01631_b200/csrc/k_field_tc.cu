@@ -168,6 +168,7 @@ __device__ __forceinline__ float sigm(float x) { return 1.f / (1.f + __expf(-x))
 // chunk-major layout (the A operand of the first density layer) + ray id.
 __global__ void __launch_bounds__(128) hash_fwd_kernel(FieldArgs a, uint8_t* __restrict__ feat,
                                                        int32_t* __restrict__ rays) {
+    pdl_wait();
     uint32_t n_tiles = a.status->n_tiles;
     int r = threadIdx.x;
     for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
@@ -957,7 +958,7 @@ void launch_field_forward_tc(const FieldArgs& a, uint8_t* feat, int32_t* rays, i
         cudaFuncSetAttribute(mlp_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kFwdSmem));
         attr = true;
     }
-    hash_fwd_kernel<<<sms * 8, 128, 0, st>>>(a, feat, rays);
+    launch_pdl(hash_fwd_kernel, dim3(sms * 8), dim3(128), 0, st, a, feat, rays);
     launch_pdl(mlp_fwd_kernel, dim3(sms * 4), dim3(128), kFwdSmem, st, a, feat, rays);  // 4 per SM
     *launches += 2;
 }

@@ -56,6 +56,7 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* t
 __global__ void __launch_bounds__(kScanThreads) scan_reduce_kernel(const uint32_t* __restrict__ in,
                                                                    uint64_t n,
                                                                    uint32_t* __restrict__ sums) {
+    pdl_wait();
     uint64_t base = uint64_t(blockIdx.x) * kScanTile;
     uint32_t s = 0;
 #pragma unroll
@@ -70,6 +71,7 @@ __global__ void __launch_bounds__(kScanThreads) scan_reduce_kernel(const uint32_
 
 __global__ void __launch_bounds__(kScanThreads) scan_sums_kernel(uint32_t* sums, int nb,
                                                                  uint32_t* grand_total) {
+    pdl_wait();
     // single block: exclusive scan of up to kScanTile block sums
     uint32_t v[kScanItems];
     uint32_t s = 0;
@@ -94,6 +96,7 @@ __global__ void __launch_bounds__(kScanThreads) scan_apply_kernel(const uint32_t
                                                                   uint64_t n,
                                                                   const uint32_t* __restrict__ sums,
                                                                   uint32_t* __restrict__ out) {
+    pdl_wait();
     uint64_t base = uint64_t(blockIdx.x) * kScanTile;
     uint32_t v[kScanItems];
     uint32_t s = 0;
@@ -118,9 +121,9 @@ int scan_exclusive(const uint32_t* in, uint64_t n, uint32_t* out, uint32_t* bloc
     int nb = int((n + kScanTile - 1) / kScanTile);
     if (nb < 1) nb = 1;
     if (nb > kScanTile) return 1;
-    scan_reduce_kernel<<<nb, kScanThreads, 0, st>>>(in, n, block_sums);
-    scan_sums_kernel<<<1, kScanThreads, 0, st>>>(block_sums, nb, grand_total);
-    scan_apply_kernel<<<nb, kScanThreads, 0, st>>>(in, n, block_sums, out);
+    launch_pdl(scan_reduce_kernel, dim3(nb), dim3(kScanThreads), 0, st, in, n, block_sums);
+    launch_pdl(scan_sums_kernel, dim3(1), dim3(kScanThreads), 0, st, block_sums, nb, grand_total);
+    launch_pdl(scan_apply_kernel, dim3(nb), dim3(kScanThreads), 0, st, in, n, block_sums, out);
     if (launches) *launches += 3;
     return 0;
 }
@@ -312,6 +315,7 @@ template <bool kSolve>
 __global__ void __launch_bounds__(128, kSolve ? TFG_RAYGEN_MINB : TFG_RAYGEN_MEMO_MINB)
     raygen_kernel(RaygenArgs a, RayRec* __restrict__ rays, float4* __restrict__ venc,
                   uint32_t* __restrict__ counts, Status* __restrict__ status) {
+    pdl_wait();
     const int gt = blockIdx.x * blockDim.x + threadIdx.x;
     const int i = gt >> 1, hi = gt & 1;
     const uint32_t pair = 3u << ((threadIdx.x & 31) & ~1);
@@ -455,6 +459,7 @@ __global__ void __launch_bounds__(128, kSolve ? TFG_RAYGEN_MINB : TFG_RAYGEN_MEM
 __global__ void tiles_kernel(const uint32_t* __restrict__ P, int n_rays, int nslots,
                              uint64_t capacity, int max_tiles, TileDesc* __restrict__ tiles,
                              Status* __restrict__ status) {
+    pdl_wait();
     __shared__ uint32_t tile_base[kMaxSlots + 1];
     if (threadIdx.x == 0) {
         uint32_t tb = 0;
@@ -501,6 +506,7 @@ __global__ void __launch_bounds__(256) write_kernel(RaygenArgs a, const RayRec* 
                                                     const uint32_t* __restrict__ P,
                                                     const Status* __restrict__ status,
                                                     SampleArrays out) {
+    pdl_wait();
     int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     int lane = threadIdx.x & 31;
     if (warp >= a.n_rays) return;
@@ -594,13 +600,15 @@ int launch_sampler(const RaygenArgs& a, RayRec* rays, float4* venc, uint32_t* co
                    SampleArrays out, uint64_t capacity, Status* status, cudaStream_t st,
                    uint64_t* launches) {
     if (!a.pixels && a.pix_rays)
-        raygen_kernel<false><<<(2 * a.n_rays + 127) / 128, 128, 0, st>>>(a, rays, venc, counts, status);
+        launch_pdl(raygen_kernel<false>, dim3((2 * a.n_rays + 127) / 128), dim3(128), 0, st, a, rays, venc, counts,
+                   status);
     else
-        raygen_kernel<true><<<(2 * a.n_rays + 127) / 128, 128, 0, st>>>(a, rays, venc, counts, status);
+        launch_pdl(raygen_kernel<true>, dim3((2 * a.n_rays + 127) / 128), dim3(128), 0, st, a, rays, venc, counts,
+                   status);
     uint64_t n = uint64_t(a.slots.n) * a.n_rays;
     if (scan_exclusive(counts, n, P, block_sums, nullptr, st, launches)) return 1;
-    tiles_kernel<<<1, 256, 0, st>>>(P, a.n_rays, a.slots.n, capacity, max_tiles, tiles, status);
-    write_kernel<<<(a.n_rays * 32 + 255) / 256, 256, 0, st>>>(a, rays, P, status, out);
+    launch_pdl(tiles_kernel, dim3(1), dim3(256), 0, st, P, a.n_rays, a.slots.n, capacity, max_tiles, tiles, status);
+    launch_pdl(write_kernel, dim3((a.n_rays * 32 + 255) / 256), dim3(256), 0, st, a, rays, P, status, out);
     *launches += 3;
     return 0;
 }

@@ -64,6 +64,16 @@ constexpr uint64_t kPurposeTileDnet = 0x54444E54ull;
 constexpr uint64_t kPurposeColor = 0x434F4C52ull;
 constexpr uint64_t kPurposeOccupancy = 0x4F434355ull;
 
+// Programmatic dependent launch (launch_pdl): wait for the preceding grid's
+// completion and memory before the first dependent access.
+#ifdef __CUDACC__
+__device__ __forceinline__ void pdl_wait() {
+#ifndef TFG_NO_PDL
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+#endif
+}
+#endif
+
 // ---------------------------------------------------------------- rng.hpp:11-48
 TF_HD uint64_t splitmix64(uint64_t x) {
     x += 0x9e3779b97f4a7c15ull;
