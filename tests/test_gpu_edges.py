@@ -96,3 +96,29 @@ def test_invalid_arguments_raise():
     with pytest.raises(TileFieldError):
         ctx.set_window(5, 5)  # outside the grid
     assert np.isfinite(ctx.train_step(0, 0, 64))
+
+
+def test_sample_cap_and_delta_cap_bit_exact():
+    """A small per-ray sample cap (plan_intervals rescales every segment's
+    interval count) and a short last-delta cap sample
+    bit-exactly against the oracle, with and without jitter."""
+    _need_gpu()
+    from oracle.pyoracle import Oracle, Session
+    from paper_2507_01631_b200.tilefield import Context
+
+    scene = synth.make_scene(2, 2, tile_side=96.0, n_views=2, gsd=1.0, seed=44, max_off_nadir=30.0)
+    fc, tc = FieldConfig.defaults(), TrainConfig.defaults(batch_rays=2048, seed=9)
+    tc.max_samples_per_ray = 24
+    tc.delta_cap = 0.75
+    ctx = Context(scene, fc, tc, max_rays=2048)
+    ses = Session(Oracle(), scene, fc, tc, workers=8)
+    ctx.set_window(0, 0)
+    ses.set_window(0, 0)
+    ses.build_accept()
+    for it, jitter in ((0, True), (1, False)):
+        n = ctx.sample(it, 0, 2048, jitter)
+        assert n == ses.sample(it, 0, 2048, jitter)
+        b = ctx.batch()
+        _cmp(b, ses.batch())
+        per_ray = np.diff(b["offsets"])
+        assert per_ray.max() <= 24
