@@ -22,12 +22,54 @@ __device__ __forceinline__ float warp_sum(float v) {
     return v;
 }
 
+// The batch loss is summed without same-address global atomics (65,536 of
+// them, serialised in L2, cost a third of the kernel): each block sums its
+// rays in smem, the last warp to arrive stores the block's partial, and
+// loss_reduce_kernel adds the partials.  Every warp arrives exactly once.
+__device__ __forceinline__ void loss_arrive(double* blk_sum, unsigned* blk_n, double* parts, double term,
+                                            int lane) {
+    if (lane != 0) return;
+    if (term != 0.0) atomicAdd(blk_sum, term);
+    __threadfence_block();
+    if (atomicAdd(blk_n, 1u) == (blockDim.x >> 5) - 1) {
+        __threadfence_block();
+        parts[blockIdx.x] = *reinterpret_cast<volatile double*>(blk_sum);
+    }
+}
+
+__global__ void __launch_bounds__(1024) loss_reduce_kernel(const double* __restrict__ parts, int n,
+                                                           Status* __restrict__ status) {
+    __shared__ double w[32];
+    pdl_wait();
+    double v = 0.0;
+    for (int k = threadIdx.x; k < n; k += blockDim.x) v += parts[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) w[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        v = threadIdx.x < (blockDim.x >> 5) ? w[threadIdx.x] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (threadIdx.x == 0) status->loss += v;
+    }
+}
+
 __global__ void __launch_bounds__(256) composite_kernel(CompositeArgs a) {
+    __shared__ double blk_sum;
+    __shared__ unsigned blk_n;
     int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     int lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        blk_sum = 0.0;
+        blk_n = 0u;
+    }
+    __syncthreads();
     asm volatile("griddepcontrol.wait;\n" ::: "memory");  // the forward's sigma/rgb
-    if (i >= a.n_rays) return;
-    if (a.status_in->bits & kStatusSampleOverflow) return;
+    if (i >= a.n_rays || (a.status_in->bits & kStatusSampleOverflow)) {
+        loss_arrive(&blk_sum, &blk_n, a.loss_parts, 0.0, lane);
+        return;
+    }
     const RayRec& R = a.rays[i];
     int nseg = R.status == 0 ? R.nseg : 0;
     uint32_t base[kMaxSeg];
@@ -115,9 +157,12 @@ __global__ void __launch_bounds__(256) composite_kernel(CompositeArgs a) {
         if (a.ray_depth) a.ray_depth[i] = dep / fmaxf(op, 1e-10f);
         if (a.ray_opacity) a.ray_opacity[i] = op;
     }
-    if (!a.backward || R.status != 0) return;
+    if (!a.backward || R.status != 0) {
+        loss_arrive(&blk_sum, &blk_n, a.loss_parts, 0.0, lane);
+        return;
+    }
     float er = rr - R.target[0], eg = rg - R.target[1], eb = rb - R.target[2];
-    if (lane == 0) atomicAdd(&a.status->loss, double(er * er + eg * eg + eb * eb));
+    loss_arrive(&blk_sum, &blk_n, a.loss_parts, double(er * er + eg * eg + eb * eb), lane);
     float gr = 2.f * er * a.inv3b, gg = 2.f * eg * a.inv3b, gb = 2.f * eb * a.inv3b;
     // ---------------- backward
     float T2 = 1.f, pr = 0.f, pg = 0.f, pb = 0.f;
@@ -187,6 +232,11 @@ void launch_composite(const CompositeArgs& a, cudaStream_t st, uint64_t* launche
     int blocks = (a.n_rays * 32 + 255) / 256;
     launch_pdl(composite_kernel, dim3(blocks), dim3(256), 0, st, a);
     *launches += 1;
+    if (a.backward) {
+        launch_pdl(loss_reduce_kernel, dim3(1), dim3(1024), 0, st, static_cast<const double*>(a.loss_parts), blocks,
+                   a.status);
+        *launches += 1;
+    }
 }
 
 } // namespace tfg

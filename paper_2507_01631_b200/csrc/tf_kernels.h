@@ -101,6 +101,7 @@ struct CompositeArgs {
     float* ray_opacity;
     float density_max;   // sigma == density_max <=> clamped activation (zero grad)
     float4* export_io;   // optional: (d_sigma, d_rgb) per sample in reference semantics
+    double* loss_parts;  // one partial loss per block, summed by loss_reduce_kernel
 };
 
 struct AdamGroup {

@@ -517,6 +517,7 @@ int run_composite(tfg_ctx* c, bool backward, float4* export_io = nullptr) {
     a.ray_opacity = c->d_ray_out + 4 * uint64_t(c->max_rays);
     a.density_max = c->fc.density_max;
     a.export_io = export_io;
+    a.loss_parts = c->d_loss_parts;
     launch_composite(a, c->st, &c->launches);
     CK(cudaGetLastError());
     return 0;
@@ -716,6 +717,7 @@ TFG_API int tfg_create(const tfg_field_config* fcfg, const tfg_train_config* tcf
         rc |= dalloc(c, &c->d_ray_out, uint64_t(max_rays) * 5);
         rc |= dalloc(c, &c->d_pixels, uint64_t(max_rays) * 3);
         rc |= dalloc(c, &c->d_feat, uint64_t(c->max_tiles) * 4096);
+        rc |= dalloc(c, &c->d_loss_parts, uint64_t(max_rays) / 8 + 1);
         rc |= dalloc(c, &c->d_tile_rays, uint64_t(c->max_tiles) * 128);
         rc |= dalloc(c, &c->d_block_sums, 4096 + 64);
         rc |= dalloc(c, &c->d_acc_sums, 4096 + 64);
@@ -758,7 +760,7 @@ TFG_API int tfg_destroy(tfg_ctx* c) {
                    c->d_counts, c->d_P, c->d_tiles, c->s.local, c->s.td, c->s.endpoint, c->s.io,
                    c->d_ray_out, c->d_pixels, c->d_rparams, c->d_rbits, c->d_rcolor, c->d_rcam,
                    c->d_feat, c->d_tile_rays, c->d_export, c->d_pix_info, c->d_pix_rays, c->d_pix_off,
-                   c->d_stage_in, c->d_stage_out};
+                   c->d_stage_in, c->d_stage_out, c->d_loss_parts};
     for (void* p : dev)
         if (p) cudaFree(p);
     stop_init_pool(c);

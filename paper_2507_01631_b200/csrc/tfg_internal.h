@@ -150,6 +150,7 @@ struct tfg_ctx {
     RayRec* d_rays = nullptr;
     float4* d_venc = nullptr;
     uint32_t *d_counts = nullptr, *d_P = nullptr;
+    double* d_loss_parts = nullptr;  // per-block partial losses of K3
     TileDesc* d_tiles = nullptr;
     SampleArrays s{};
     float* d_ray_out = nullptr;  // rgb(3) | depth | opacity per ray
