@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(256) composite_kernel(CompositeArgs a) {
         blk_n = 0u;
     }
     __syncthreads();
-    asm volatile("griddepcontrol.wait;\n" ::: "memory");  // the forward's sigma/rgb
+    pdl_wait();  // the forward's sigma/rgb
     if (i >= a.n_rays || (a.status_in->bits & kStatusSampleOverflow)) {
         loss_arrive(&blk_sum, &blk_n, a.loss_parts, 0.0, lane);
         return;

@@ -367,7 +367,7 @@ __global__ void __launch_bounds__(128, 4) mlp_fwd_kernel(FieldArgs a, const uint
     stage_color(W, a.f.color);
     uint32_t ph_mma = 0, ph_ld = 0;
     int cur = -1;
-    umma::griddep_wait();  // hash_fwd's feature tiles and ray ids
+    pdl_wait();  // hash_fwd's feature tiles and ray ids
     uint32_t n_tiles = a.status->n_tiles;
     sync_for_mma();
     const uint32_t tmem = tmem_slot;
@@ -637,7 +637,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2) mlp_bwd_kernel(FieldArgs a, Fi
         float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         st_chunk(X0, r, 3, z);
     }
-    umma::griddep_wait();  // the composite's gradients
+    pdl_wait();  // the composite's gradients
     uint32_t n_tiles = a.status->n_tiles;
     sync_for_mma();
     const uint32_t tmem = tmem_slot;

@@ -79,15 +79,6 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* mbar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(mbar)) : "memory");
 }
 
-// Programmatic dependent launch: the kernel's prologue (barrier init, TMEM
-// allocation, weight staging) may overlap the previous kernel's tail; this
-// waits for the previous grid's completion and memory before dependent reads.
-__device__ __forceinline__ void griddep_wait() {
-#ifndef TFG_NO_PDL
-    asm volatile("griddepcontrol.wait;\n" ::: "memory");
-#endif
-}
-
 // Warpgroup register reallocation (warp-specialised kernels).
 template <uint32_t N>
 __device__ __forceinline__ void reg_alloc() {
