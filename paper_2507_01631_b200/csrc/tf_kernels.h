@@ -153,7 +153,7 @@ void launch_occupancy(const OccArgs& a, cudaStream_t st, uint64_t* launches);
 
 
 // Launch with programmatic stream serialization (the kernel calls
-// umma::griddep_wait() before reading its predecessor's outputs).
+// pdl_wait() (tf_common.cuh) before reading its predecessor's outputs).
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                               Args&&... args) {
