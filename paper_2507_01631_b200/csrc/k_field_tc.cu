@@ -552,7 +552,15 @@ __device__ __forceinline__ void set_ones_chunk(uint8_t* buf, int chunk, int r) {
 }
 
 // Adds the CTA's TMEM weight-gradient accumulators into the global gradients.
-__device__ __forceinline__ void flush_density(uint32_t tmem, float* __restrict__ gd) {
+// Row-major blocks whose rows are per-thread (dW1d, dWc1) go through a smem
+// transpose so that their reds are coalesced (consecutive lanes, consecutive
+// addresses: 4 sectors per warp instruction instead of 32); the MN-major
+// blocks (dW2d^T, dWc2^T, dWc3^T) are coalesced as they come.  `scratch` is a
+// free activation buffer; the 128 MLP threads call these together.
+__device__ __forceinline__ void red_block_coalesced(float* __restrict__ g, const float* scratch, int n) {
+    for (int j = threadIdx.x; j < n; j += kT) atomicAdd(g + j, scratch[j]);
+}
+__device__ __forceinline__ void flush_density(uint32_t tmem, float* __restrict__ gd, float* scratch) {
     int m = threadIdx.x;  // TMEM lane row
     float v[32];
     // dW1d [o=m][i] (cols 0..15), bias at col 16
@@ -560,9 +568,13 @@ __device__ __forceinline__ void flush_density(uint32_t tmem, float* __restrict__
     tld16(tmem, kColW1d + 16, v + 16);
     umma::ld_wait();
     if (m < kDHidden) {
-        for (int i = 0; i < kFeatDim; ++i) atomicAdd(gd + kDW1 + m * kFeatDim + i, v[i]);
+#pragma unroll
+        for (int i = 0; i < kFeatDim; ++i) scratch[m * kFeatDim + i] = v[i];
         atomicAdd(gd + kDB1 + m, v[16]);
     }
+    asm volatile("bar.sync 1, 128;\n" ::: "memory");
+    red_block_coalesced(gd + kDW1, scratch, kDHidden * kFeatDim);
+    asm volatile("bar.sync 1, 128;\n" ::: "memory");  // scratch reused
     // dW2d^T [i=m][o], bias row m = 64
     tld16(tmem, kColW2d, v);
     umma::ld_wait();
@@ -571,7 +583,7 @@ __device__ __forceinline__ void flush_density(uint32_t tmem, float* __restrict__
     else if (m == kDHidden)
         for (int o = 0; o < kDOut; ++o) atomicAdd(gd + kDB2 + o, v[o]);
 }
-__device__ __forceinline__ void flush_color(uint32_t tmem, float* __restrict__ gc) {
+__device__ __forceinline__ void flush_color(uint32_t tmem, float* __restrict__ gc, float* scratch) {
     int m = threadIdx.x;
     float v[64];
     // dWc2^T [i=m][o], bias row 64
@@ -590,9 +602,12 @@ __device__ __forceinline__ void flush_color(uint32_t tmem, float* __restrict__ g
     tld16(tmem, kColWc1 + 32, v + 32);
     umma::ld_wait();
     if (m < kCHidden) {
-        for (int i = 0; i < kCIn; ++i) atomicAdd(gc + kCW1 + m * kCIn + i, v[i]);
+        for (int i = 0; i < kCIn; ++i) scratch[m * kCIn + i] = v[i];
         atomicAdd(gc + kCB1 + m, v[kCIn]);
     }
+    asm volatile("bar.sync 1, 128;\n" ::: "memory");
+    red_block_coalesced(gc + kCW1, scratch, kCHidden * kCIn);
+    asm volatile("bar.sync 1, 128;\n" ::: "memory");
     // dWc3^T [i=m][o], bias row 64
     tld16(tmem, kColWc3, v);
     umma::ld_wait();
@@ -680,7 +695,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2) mlp_bwd_kernel(FieldArgs a, Fi
     for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
         TileDesc td = a.tiles[t];
         if (td.slot != cur) {
-            if (cur >= 0) flush_density(tmem, g.g_dnet[cur]);
+            if (cur >= 0) flush_density(tmem, g.g_dnet[cur], reinterpret_cast<float*>(C1));
             stage_density(W, a.f.dnet[td.slot]);
             cur = td.slot;
             first_d = true;
@@ -943,8 +958,8 @@ __global__ void __launch_bounds__(kBwdThreads, 2) mlp_bwd_kernel(FieldArgs a, Fi
     umma::fence_before_sync();
     asm volatile("bar.sync 1, 128;\n" ::: "memory");
     umma::fence_after_sync();
-    if (cur >= 0) flush_density(tmem, g.g_dnet[cur]);
-    if (!first_c) flush_color(tmem, g.g_color);
+    if (cur >= 0) flush_density(tmem, g.g_dnet[cur], reinterpret_cast<float*>(C1));
+    if (!first_c) flush_color(tmem, g.g_color, reinterpret_cast<float*>(C1));
     umma::fence_before_sync();
     __syncthreads();
     if (r < 32) umma::tmem_free<kBwdTmemCols>(tmem);
