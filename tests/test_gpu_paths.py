@@ -311,3 +311,26 @@ def test_config3_full_snake_constant_memory_linear_time():
     # moves (after the first, which builds the initial state) cost about the same
     steady = sorted(dt[1:])
     assert steady[len(steady) * 9 // 10] < 4 * steady[len(steady) // 2] + 0.02
+
+
+def test_config2_all_positions_bit_exact():
+    """BASELINE config 2 (3x3 grid, 8 views at 0.5 m, 16,384 rays; seam
+    correctness): at every one of its 4 window positions the accepted list and
+    the full batch are bit-exact, and a training step's loss matches."""
+    _need_gpu()
+    from oracle.pyoracle import Oracle, Session
+    from paper_2507_01631_b200.tilefield import Context, snake_path
+
+    scene = synth.config_scene(2, seed=2)
+    c2 = synth.CONFIGS[2]
+    fc, tc = FieldConfig.defaults(), TrainConfig.defaults(batch_rays=c2["batch"], seed=7)
+    ctx = Context(scene, fc, tc, max_rays=c2["batch"])
+    ses = Session(Oracle(), scene, fc, tc, workers=16)
+    for it, pos in enumerate(snake_path(3, 3)):
+        ctx.set_window(*pos)
+        ses.set_window(*pos)
+        np.testing.assert_array_equal(ctx.accept_list(), ses.build_accept())
+        assert ctx.sample(it, 0, c2["batch"], True) == ses.sample(it, 0, c2["batch"], True)
+        _cmp_batch(ctx.batch(), ses.batch())
+        lg, lr = ctx.train_step(it, 0, c2["batch"]), ses.train_step(it, 0, c2["batch"])
+        assert abs(lg - lr) <= 1e-2 * lr, (pos, lg, lr)
