@@ -18,6 +18,9 @@ FAMILY = {
     "mlp_fwd_kernel": "field_fwd",
     "hash_fwd_kernel": "field_fwd",
     "raygen_kernel": "sampler",
+    "raygen_kernel<0>": "sampler",
+    "raygen_kernel<1>": "sampler",
+    "loss_reduce_kernel": "composite",
     "write_kernel": "sampler",
     "tiles_kernel": "sampler",
     "scan_reduce_kernel": "sampler",
@@ -48,7 +51,8 @@ METRICS = [
 
 def short(name):
     n = name.split("(")[0]
-    return n.split("::")[-1]
+    n = n.split("::")[-1]
+    return n[5:] if n.startswith("void ") else n
 
 
 def launches(path):
