@@ -15,6 +15,8 @@
 //                    deltas over the concatenated ray
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "tf_common.cuh"
 #include "tf_kernels.h"
 
@@ -129,44 +131,77 @@ int scan_exclusive(const uint32_t* in, uint64_t n, uint32_t* out, uint32_t* bloc
 }
 
 // ------------------------------------------------------------------ accept list
-// One thread per candidate pixel of the per-view crop-union rects; flag = 1 iff
-// the ray exists, hits >= 1 tile and every hit tile is loaded.
+// flag = 1 iff the candidate pixel's ray exists, hits >= 1 tile and every hit
+// tile is loaded.  Two kernels: accept_memo_kernel (one light
+// thread per candidate of the per-view crop-union rects) settles every pixel
+// the scene memo already holds and compacts the rest into a to-do list;
+// accept_solve_kernel runs the two Newton localisations of each listed pixel
+// on a lane pair, so no warp carries memo-hit lanes through a solve.
 #ifndef TFG_ACCEPT_MINB
-#define TFG_ACCEPT_MINB 3
+#define TFG_ACCEPT_MINB 6
 #endif
-__global__ void __launch_bounds__(128, TFG_ACCEPT_MINB) accept_kernel(AcceptArgs a, uint32_t* __restrict__ flags) {
-    // two threads per candidate: one Newton localisation each (z_max / z_min)
-    const uint64_t gt = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    const uint64_t idx = gt >> 1;
-    const int hi = int(gt & 1);
-    const uint32_t pair = 3u << ((threadIdx.x & 31) & ~1);
-    if (idx >= a.n_candidates) return;  // both lanes of a pair leave together
+
+__device__ __forceinline__ void candidate_pixel(const AcceptArgs& a, uint64_t idx, int* v_, int* row, int* col) {
     int v = 0;
     while (v + 1 < a.n_views && a.view_start[v + 1] <= idx) ++v;
     uint64_t local = idx - a.view_start[v];
     const int* u = a.union_rect + 4 * v;
     int ncols = u[3] - u[2];
-    int row = u[0] + int(local / uint64_t(ncols));
-    int col = u[2] + int(local % uint64_t(ncols));
-    uint32_t ok = 0;
-    bool in = false;
-    for (int k = 0; k < a.n_loaded; ++k) {
-        const int* r = a.crop_rect + 4 * (v * kTrainSlots + k);
-        if (r[0] < r[1] && row >= r[0] && row < r[1] && col >= r[2] && col < r[3]) in = true;
-    }
-    uint64_t pidx = 0;
-    uint32_t info = 0;
-    if (in && a.pix_info) {
-        pidx = a.pix_off[v] + uint64_t(row) * uint64_t(a.cams[v].image_cols) + uint64_t(col);
-        info = a.pix_info[pidx];
-    }
-    if (in && (info & kMemoDone)) {
-        // solved for an earlier window: only the window test remains
-        if (info & kMemoHit) {
-            int rmin = info & 127, rmax = (info >> 7) & 127, cmin = (info >> 14) & 127, cmax = (info >> 21) & 127;
-            ok = (rmin >= a.win_r0 && rmax <= a.win_r1 && cmin >= a.win_c0 && cmax <= a.win_c1) ? 1u : 0u;
+    *v_ = v;
+    *row = u[0] + int(local / uint64_t(ncols));
+    *col = u[2] + int(local % uint64_t(ncols));
+}
+
+__global__ void __launch_bounds__(256) accept_memo_kernel(AcceptArgs a, uint32_t* __restrict__ flags) {
+    const uint64_t idx = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    bool todo = false;
+    if (idx < a.n_candidates) {
+        int v, row, col;
+        candidate_pixel(a, idx, &v, &row, &col);
+        bool in = false;
+        for (int k = 0; k < a.n_loaded; ++k) {
+            const int* r = a.crop_rect + 4 * (v * kTrainSlots + k);
+            if (r[0] < r[1] && row >= r[0] && row < r[1] && col >= r[2] && col < r[3]) in = true;
         }
-    } else if (in) {
+        uint32_t info = 0;
+        if (in && a.pix_info)
+            info = a.pix_info[a.pix_off[v] + uint64_t(row) * uint64_t(a.cams[v].image_cols) + uint64_t(col)];
+        if (in && !(info & kMemoDone)) {
+            todo = true;
+        } else {
+            // outside every loaded crop, or solved for an earlier window:
+            // only the window test remains
+            uint32_t ok = 0;
+            if (info & kMemoHit) {
+                int rmin = info & 127, rmax = (info >> 7) & 127, cmin = (info >> 14) & 127, cmax = (info >> 21) & 127;
+                ok = (rmin >= a.win_r0 && rmax <= a.win_r1 && cmin >= a.win_c0 && cmax <= a.win_c1) ? 1u : 0u;
+            }
+            flags[idx] = ok;
+        }
+    }
+    // warp-aggregated append to the to-do list
+    uint32_t m = __ballot_sync(0xffffffffu, todo);
+    const int lane = threadIdx.x & 31;
+    uint32_t base = 0;
+    if (lane == 0 && m) base = atomicAdd(a.todo_n, uint32_t(__popc(m)));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (todo) a.todo[base + __popc(m & ((1u << lane) - 1u))] = uint32_t(idx);
+}
+
+__global__ void __launch_bounds__(128, TFG_ACCEPT_MINB) accept_solve_kernel(AcceptArgs a, uint32_t* __restrict__ flags) {
+    // two threads per listed pixel: one Newton localisation each (z_max / z_min)
+    const uint64_t gt = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int hi = int(gt & 1);
+    const uint32_t pair = 3u << ((threadIdx.x & 31) & ~1);
+    const uint32_t n_todo = *a.todo_n;
+    const uint64_t stride = (uint64_t(gridDim.x) * blockDim.x) >> 1;
+    for (uint64_t j = gt >> 1; j < n_todo; j += stride) {  // both lanes of a pair iterate together
+        const uint64_t idx = a.todo[j];
+        int v, row, col;
+        candidate_pixel(a, idx, &v, &row, &col);
+        uint64_t pidx = 0;
+        if (a.pix_info) pidx = a.pix_off[v] + uint64_t(row) * uint64_t(a.cams[v].image_cols) + uint64_t(col);
+        uint32_t ok = 0;
         double gx = 0.0, gy = 0.0;
         int st = rpc_localize(a.cams[v], double(row), double(col), hi ? a.z_min : a.z_max, &gx, &gy);
         double ox = __shfl_xor_sync(pair, gx, 1), oy = __shfl_xor_sync(pair, gy, 1);
@@ -232,9 +267,11 @@ __global__ void __launch_bounds__(128, TFG_ACCEPT_MINB) accept_kernel(AcceptArgs
                 }
             }
         }
-        if (hi == 0 && a.pix_info) a.pix_info[pidx] = memo;
+        if (hi == 0) {
+            if (a.pix_info) a.pix_info[pidx] = memo;
+            flags[idx] = ok;
+        }
     }
-    if (hi == 0) flags[idx] = ok;
 }
 
 __global__ void accept_scatter_kernel(AcceptArgs a, const uint32_t* __restrict__ flags,
@@ -304,7 +341,7 @@ __device__ __forceinline__ bool occ_test(const uint32_t* bits, float x, float y,
 // same arithmetic (same bits); the interior-sample counting is split by
 // sample parity; the odd lane also writes the view encoding.
 #ifndef TFG_RAYGEN_MINB
-#define TFG_RAYGEN_MINB 4
+#define TFG_RAYGEN_MINB 6
 #endif
 // kSolve = false: drawn pixels with the pixel memo only (no Newton code, so
 // fewer registers and more resident warps); true: explicit pixels or no memo.
@@ -581,17 +618,24 @@ __global__ void __launch_bounds__(256) write_kernel(RaygenArgs a, const RayRec* 
 }
 
 // ------------------------------------------------------------------ host launchers
-int launch_accept(const AcceptArgs& a, uint32_t* flags, uint32_t* pos, uint32_t* block_sums,
+int launch_accept(const AcceptArgs& args, uint32_t* flags, uint32_t* pos, uint32_t* block_sums,
                   uint32_t* n_out, uint64_t* out, cudaStream_t st, uint64_t* launches) {
+    AcceptArgs a = args;
+    a.todo = pos;
     if (a.n_candidates == 0) {
         cudaMemsetAsync(n_out, 0, 4, st);
         return 0;
     }
     int nb = int((a.n_candidates + 127) / 128);
-    accept_kernel<<<int((2 * a.n_candidates + 127) / 128), 128, 0, st>>>(a, flags);
+    cudaMemsetAsync(a.todo_n, 0, 4, st);
+    accept_memo_kernel<<<int((a.n_candidates + 255) / 256), 256, 0, st>>>(a, flags);
+    // one lane pair per candidate (the to-do list is at most that long; pairs
+    // past its end leave at once): measured faster than a persistent grid
+    uint64_t solve_blocks = (2 * a.n_candidates + 127) / 128;
+    accept_solve_kernel<<<int(solve_blocks), 128, 0, st>>>(a, flags);
     if (scan_exclusive(flags, a.n_candidates, pos, block_sums, n_out, st, launches)) return 1;
     accept_scatter_kernel<<<nb, 128, 0, st>>>(a, flags, pos, out);
-    *launches += 2;
+    *launches += 3;
     return 0;
 }
 

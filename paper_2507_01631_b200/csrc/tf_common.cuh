@@ -104,30 +104,43 @@ struct Rng {
 // ---------------------------------------------------------------- camera.cpp
 // RPC00B rational cubic (camera.cpp:22-64).  Returns false where the
 // reference's project() throws (|normalised coordinate| > 1.5).
+// Coefficient load.  On the device it is a volatile load: the Newton loops
+// would otherwise hoist all 80 loop-invariant coefficients into registers and
+// spill (the camera is warp-uniform and L1-resident, so the reload is a
+// broadcast).  The loaded value is the same either way.
+TF_HD double rpc_coef(const double* p) {
+#if defined(__CUDA_ARCH__) && !defined(TFG_RPC_HOIST)
+    double v;
+    asm volatile("ld.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+#else
+    return *p;
+#endif
+}
 TF_HD double rpc_poly(const double* c, double P, double L, double H) {
     // term order of rpc_terms (camera.cpp:22-43); left-to-right dot product
     // with each product formed in the reference's operand order.
     double s = 0;
-    s += c[0] * 1.0;
-    s += c[1] * L;
-    s += c[2] * P;
-    s += c[3] * H;
-    s += c[4] * (L * P);
-    s += c[5] * (L * H);
-    s += c[6] * (P * H);
-    s += c[7] * (L * L);
-    s += c[8] * (P * P);
-    s += c[9] * (H * H);
-    s += c[10] * (P * L * H);
-    s += c[11] * (L * L * L);
-    s += c[12] * (L * P * P);
-    s += c[13] * (L * H * H);
-    s += c[14] * (L * L * P);
-    s += c[15] * (P * P * P);
-    s += c[16] * (P * H * H);
-    s += c[17] * (L * L * H);
-    s += c[18] * (P * P * H);
-    s += c[19] * (H * H * H);
+    s += rpc_coef(c + 0) * 1.0;
+    s += rpc_coef(c + 1) * L;
+    s += rpc_coef(c + 2) * P;
+    s += rpc_coef(c + 3) * H;
+    s += rpc_coef(c + 4) * (L * P);
+    s += rpc_coef(c + 5) * (L * H);
+    s += rpc_coef(c + 6) * (P * H);
+    s += rpc_coef(c + 7) * (L * L);
+    s += rpc_coef(c + 8) * (P * P);
+    s += rpc_coef(c + 9) * (H * H);
+    s += rpc_coef(c + 10) * (P * L * H);
+    s += rpc_coef(c + 11) * (L * L * L);
+    s += rpc_coef(c + 12) * (L * P * P);
+    s += rpc_coef(c + 13) * (L * H * H);
+    s += rpc_coef(c + 14) * (L * L * P);
+    s += rpc_coef(c + 15) * (P * P * P);
+    s += rpc_coef(c + 16) * (P * H * H);
+    s += rpc_coef(c + 17) * (L * L * H);
+    s += rpc_coef(c + 18) * (P * P * H);
+    s += rpc_coef(c + 19) * (H * H * H);
     return s;
 }
 TF_HD bool rpc_project(const tfg_rpc& c, double x, double y, double z, double* row, double* col) {

@@ -45,6 +45,11 @@ struct AcceptArgs {
     double* pix_rays;
     const uint64_t* pix_off;     // first pixel of each view
     int win_r0, win_r1, win_c0, win_c1;  // the loaded tiles' rectangle (inclusive)
+    // pixels the memo does not settle: candidate indices + their count
+    // (the list lives in the scan's output buffer, which is free until the scan)
+    uint32_t* todo;
+    uint32_t* todo_n;
+    int sms;
 };
 constexpr uint32_t kMemoDone = 1u << 31, kMemoHit = 1u << 30;
 

@@ -394,6 +394,8 @@ int stage_window(tfg_ctx* c, WinBuf& w, int pr, int pc, cudaStream_t st) {
             a.win_c1 = c1;
         }
     }
+    a.todo_n = c->d_todo_n;
+    a.sms = c->sms;
     if (launch_accept(a, c->d_flags, c->d_pos, c->d_acc_sums, w.d_n, w.d_accept, st, &c->launches))
         return fail(TFG_ERR_INVALID, "accept: scan capacity exceeded");
     CK(cudaGetLastError());
@@ -721,6 +723,7 @@ TFG_API int tfg_create(const tfg_field_config* fcfg, const tfg_train_config* tcf
         rc |= dalloc(c, &c->d_tile_rays, uint64_t(c->max_tiles) * 128);
         rc |= dalloc(c, &c->d_block_sums, 4096 + 64);
         rc |= dalloc(c, &c->d_acc_sums, 4096 + 64);
+        rc |= dalloc(c, &c->d_todo_n, 1);
         rc |= dalloc(c, &c->d_rcam, 1);
         if (rc) return TFG_ERR_CUDA;
         CK(cudaHostAlloc(reinterpret_cast<void**>(&c->h_status), sizeof(Status), cudaHostAllocDefault));
@@ -755,7 +758,7 @@ TFG_API int tfg_destroy(tfg_ctx* c) {
     cudaDeviceSynchronize();
     void* dev[] = {c->d_params, c->d_grads, c->d_m, c->d_v, c->d_ema, c->d_bits, c->d_group_flags,
                    c->d_status, c->d_cams, c->d_east, c->d_north, c->d_flags, c->d_pos,
-                   c->d_block_sums, c->d_acc_sums, c->d_view_start, c->d_union, c->d_crop4,
+                   c->d_block_sums, c->d_acc_sums, c->d_todo_n, c->d_view_start, c->d_union, c->d_crop4,
                    c->d_rays, c->d_venc,
                    c->d_counts, c->d_P, c->d_tiles, c->s.local, c->s.td, c->s.endpoint, c->s.io,
                    c->d_ray_out, c->d_pixels, c->d_rparams, c->d_rbits, c->d_rcolor, c->d_rcam,

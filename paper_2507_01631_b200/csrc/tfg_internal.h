@@ -138,6 +138,7 @@ struct tfg_ctx {
     uint64_t crop_cap = 0, accept_cap = 0, cand_cap = 0;
     // accepted-list build scratch (one build at a time)
     uint32_t *d_flags = nullptr, *d_pos = nullptr, *d_block_sums = nullptr, *d_acc_sums = nullptr;
+    uint32_t* d_todo_n = nullptr;  // accept: count of pixels the memo does not settle
     // per-pixel memo of the scene (AcceptArgs): state, rays, view offsets
     uint32_t* d_pix_info = nullptr;
     double* d_pix_rays = nullptr;

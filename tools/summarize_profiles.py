@@ -30,7 +30,8 @@ FAMILY = {
     "adam_kernel": "adam",
     "grad_check_kernel": "adam",
     "occupancy_kernel": "occupancy",
-    "accept_kernel": "accept",
+    "accept_memo_kernel": "accept",
+    "accept_solve_kernel": "accept",
     "accept_scatter_kernel": "accept",
 }
 METRICS = [
