@@ -33,6 +33,8 @@ B_PER_GPU = 65536
 WINDOW = (2, 2)
 FLOP_FWD = 17664          # per sample (density 4,096 + colour 13,568), SURVEY.md §8
 FLOP_FWD_BWD = 52992      # per sample
+SCATTER_BYTES = 8 * 8 * 8  # per sample: 8 levels x 8 corners x float2 of reds
+SCATTER_FLOOR_MS = 1.24   # measured: backward with the MLP chain cut to its last GEMM
 
 
 def peaks():
@@ -252,6 +254,19 @@ def run_ours(args):
                 "unit": d["unit"], "frac": d["achieved"] / peak, "traffic": traffic,
                 "peak_source": f"{peak_src} ({'bf16 sustained' if d['bound'] == 'tensor' else 'HBM copy'})",
                 "per_launch_work": (FLOP_FWD_BWD if dom == "field_bwd" else KERNEL_UNITS[dom][1]) * n_samples}
+    if dom == "field_bwd":
+        # The backward is bound by its hash-gradient scatter, not the tensor
+        # cores: 8 levels x 8 corners x 2 fp32 of global reds per sample
+        # (profiles/ hold the ncu
+        # evidence).  The floor is the A/B variant with the MLP chain cut.
+        bwd_ms = d["ms_per_step"]
+        roofline["limiter"] = {
+            "resource": "global fp32 reds of the hash-table gradients (L1 red path -> L2)",
+            "red_bytes_per_sample": SCATTER_BYTES,
+            "achieved_red_GBps": SCATTER_BYTES * n_samples / (bwd_ms / 1e3) / 1e9,
+            "scatter_floor_ms": SCATTER_FLOOR_MS,
+            "frac_of_floor": SCATTER_FLOOR_MS / bwd_ms,
+            "floor_source": "A/B variant: MLP chain cut to its last GEMM, scatter unchanged (BENCH_NOTES.md)"}
 
     # ---- end to end through the public API with host buffers: window slides
     # (pinned host <-> HBM tile state + crops), accepted-list rebuilds, loss
