@@ -6,9 +6,11 @@
 //                         per sample -> bf16 tile in UMMA operand layout
 //                         (4 KB/tile), reused by K4b
 //   K2b mlp_fwd_kernel    density MLP 16->64->16 + colour MLP 39->64->64->3 as
-//                         tcgen05.mma (bf16 x bf16 -> fp32 in TMEM), operands
-//                         staged by the bulk-copy engine, epilogues
-//                         (bias, ReLU, exp/sigmoid) from tcgen05.ld
+//                         tcgen05.mma (bf16 x bf16 -> fp32 in TMEM), weights
+//                         and features staged by the bulk-copy engine,
+//                         epilogues (bias, ReLU, exp/sigmoid) from tcgen05.ld;
+//                         each epilogue's bf16 output goes back to TMEM with
+//                         tcgen05.st as the next layer's A operand
 //   K4b mlp_bwd_kernel    recomputed forward + data-gradient GEMMs + weight-
 //                         gradient GEMMs (K = 128 samples, MN-major operands
 //                         read from the same smem tiles) accumulated in TMEM
@@ -157,6 +159,28 @@ __device__ __forceinline__ void wait_mma(uint64_t* bar, uint32_t& phase) {
 __device__ __forceinline__ void tld16(uint32_t tmem, int col, float* v) {
     uint32_t w = threadIdx.x >> 5;
     umma::ld16(tmem + ((32u * w) << 16) + uint32_t(col), v);
+}
+
+// Packs n (multiple of 16) activations of this thread's row to bf16 pairs in
+// TMEM columns [col, col + n/2) of its lane (the A operand of the next layer).
+template <int N>
+__device__ __forceinline__ void tst_bf16(uint32_t tmem, int col, const float* v) {
+    const uint32_t w = threadIdx.x >> 5;
+#pragma unroll
+    for (int c = 0; c < N / 16; ++c) {
+        uint32_t q[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) q[j] = pack2(v[16 * c + 2 * j], v[16 * c + 2 * j + 1]);
+        umma::st8(tmem + ((32u * w) << 16) + uint32_t(col + 8 * c), q);
+    }
+}
+// Barrier before thread 0 issues MMAs that read the A operand other threads
+// stored to TMEM and overwrite the accumulator they read.
+__device__ __forceinline__ void sync_for_mma_tmem() {
+    umma::st_wait();
+    umma::fence_before_sync();
+    __syncthreads();
+    umma::fence_after_sync();
 }
 
 __device__ __forceinline__ float sigm(float x) { return 1.f / (1.f + __expf(-x)); }
@@ -336,12 +360,14 @@ __device__ __forceinline__ void scatter_row_bfly(float* genc, float x, float y, 
 static_assert(kLevels == 8, "scatter_row_bfly unrolls the 8 levels of the default FieldConfig");
 
 // ------------------------------------------------------------------ K2b
-// smem: weights | A [128x64] | B [128x64]; the five layers ping-pong:
-//   X0 (in B) -> H1 (A) -> CIN (B) -> C1 (A) -> C2 (B) -> rgb
-// (each buffer is overwritten only after the MMA reading it has completed),
-// 53 KB per CTA -> 4 resident CTAs per SM.
-constexpr uint32_t kFwdSmem = kWeightsBytes + 16384 + 16384 + 128;
-constexpr uint32_t kFwdTmemCols = 64;
+// smem: weights | X0 [128x16] (the gathered features, bulk-copied; the only
+// activation tile in smem).  4 resident CTAs per SM (TMEM and registers).
+constexpr uint32_t kFwdSmem = kWeightsBytes + kFeatTile + 128;
+// TMEM: accumulator [0, 64); layers 2-5 take their A operand (the previous
+// layer's activations, bf16 pairs) from columns [64, 96), so activations never
+// touch smem (measured: the MLP's smem pipe was its contended resource).
+constexpr uint32_t kFwdTmemCols = 128;
+constexpr int kColA = 64;
 
 __global__ void __launch_bounds__(128, 4) mlp_fwd_kernel(FieldArgs a, const uint8_t* __restrict__ feat,
                                                       const int32_t* __restrict__ rays) {
@@ -350,13 +376,7 @@ __global__ void __launch_bounds__(128, 4) mlp_fwd_kernel(FieldArgs a, const uint
     __shared__ uint32_t tmem_slot;
     uint8_t* p = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
     Weights W = carve_weights(p);
-    uint8_t* BA = carve(p, 16384);
-    uint8_t* BB = carve(p, 16384);
-    uint8_t* X0 = BB;   // [128 x 16]
-    uint8_t* HA = BA;   // H1
-    uint8_t* CIN = BB;  // [128 x 48]
-    uint8_t* C1 = BA;
-    uint8_t* C2 = BB;
+    uint8_t* X0 = carve(p, kFeatTile);  // [128 x 16]
     const int r = threadIdx.x;
     if (r == 0) {
         umma::mbar_init(&bar_mma, 1);
@@ -426,15 +446,14 @@ __global__ void __launch_bounds__(128, 4) mlp_fwd_kernel(FieldArgs a, const uint
             umma::ld_wait();
 #pragma unroll
             for (int i = 0; i < 64; ++i) v[i] = fmaxf(v[i] + W.b1d[i], 0.f);
-#pragma unroll
-            for (int c = 0; c < 8; ++c) st_chunk(HA, r, c, v + 8 * c);
+            tst_bf16<64>(tmem, kColA, v);
         }
-        sync_for_mma();
+        sync_for_mma_tmem();
         // ---- density layer 2: [128x64] x W2d^T -> 16 (raw sigma | embedding)
         if (r == 0) {
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-                umma::mma(tmem, kmaj(HA, kT, k), kmaj(W.w2d, kW2dRows, k), id16, k > 0);
+                umma::mma_ts(tmem, tmem + kColA + 8 * k, kmaj(W.w2d, kW2dRows, k), id16, k > 0);
             umma::commit(&bar_mma);
         }
         wait_mma(&bar_mma, ph_mma);
@@ -453,15 +472,14 @@ __global__ void __launch_bounds__(128, 4) mlp_fwd_kernel(FieldArgs a, const uint
             cin[kCIn] = 1.f;  // ones column (bias gradient of colour layer 1 in K4)
 #pragma unroll
             for (int i = kCIn + 1; i < 48; ++i) cin[i] = 0.f;
-#pragma unroll
-            for (int c = 0; c < 6; ++c) st_chunk(CIN, r, c, cin + 8 * c);
+            tst_bf16<48>(tmem, kColA, cin);
         }
-        sync_for_mma();
+        sync_for_mma_tmem();
         // ---- colour layer 1: [128x48] x Wc1^T -> 64
         if (r == 0) {
 #pragma unroll
             for (int k = 0; k < 3; ++k)
-                umma::mma(tmem, kmaj(CIN, kT, k), kmaj(W.wc1, kWc1Rows, k), id64, k > 0);
+                umma::mma_ts(tmem, tmem + kColA + 8 * k, kmaj(W.wc1, kWc1Rows, k), id64, k > 0);
             umma::commit(&bar_mma);
         }
         wait_mma(&bar_mma, ph_mma);
@@ -474,15 +492,14 @@ __global__ void __launch_bounds__(128, 4) mlp_fwd_kernel(FieldArgs a, const uint
             umma::ld_wait();
 #pragma unroll
             for (int i = 0; i < 64; ++i) v[i] = fmaxf(v[i] + W.bc1[i], 0.f);
-#pragma unroll
-            for (int c = 0; c < 8; ++c) st_chunk(C1, r, c, v + 8 * c);
+            tst_bf16<64>(tmem, kColA, v);
         }
-        sync_for_mma();
+        sync_for_mma_tmem();
         // ---- colour layer 2: [128x64] x Wc2^T -> 64
         if (r == 0) {
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-                umma::mma(tmem, kmaj(C1, kT, k), kmaj(W.wc2, kWc2Rows, k), id64, k > 0);
+                umma::mma_ts(tmem, tmem + kColA + 8 * k, kmaj(W.wc2, kWc2Rows, k), id64, k > 0);
             umma::commit(&bar_mma);
         }
         wait_mma(&bar_mma, ph_mma);
@@ -495,15 +512,14 @@ __global__ void __launch_bounds__(128, 4) mlp_fwd_kernel(FieldArgs a, const uint
             umma::ld_wait();
 #pragma unroll
             for (int i = 0; i < 64; ++i) v[i] = fmaxf(v[i] + W.bc2[i], 0.f);
-#pragma unroll
-            for (int c = 0; c < 8; ++c) st_chunk(C2, r, c, v + 8 * c);
+            tst_bf16<64>(tmem, kColA, v);
         }
-        sync_for_mma();
+        sync_for_mma_tmem();
         // ---- colour layer 3: [128x64] x Wc3^T -> 16 (3 real) -> sigmoid
         if (r == 0) {
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-                umma::mma(tmem, kmaj(C2, kT, k), kmaj(W.wc3, kWc3Rows, k), id16, k > 0);
+                umma::mma_ts(tmem, tmem + kColA + 8 * k, kmaj(W.wc3, kWc3Rows, k), id16, k > 0);
             umma::commit(&bar_mma);
         }
         wait_mma(&bar_mma, ph_mma);
