@@ -203,6 +203,22 @@ TFG_API int tfg_grad_buffer(tfg_ctx* ctx, void** dptr, uint64_t* count);
  * divided by 3*B); copies to host and synchronises. */
 TFG_API int tfg_read_loss(tfg_ctx* ctx, float* loss_out);
 
+/* ---- multi-GPU: ray-sharded data parallelism (SURVEY.md §8b tfg_comm_init,
+ * §8e).  One context per GPU; every rank holds the same window and draws rays
+ * [rank * B, (rank + 1) * B) of each iteration, with batch_rays = B * nranks
+ * in the train config, so the summed gradient is the global-batch gradient.
+ * NCCL is loaded at run time (libnccl.so.2).  Usage per iteration:
+ *   tfg_forward_backward; tfg_allreduce_grads; tfg_optimizer_step.
+ * Rank 0 creates the id and the host distributes its 128 bytes. */
+#define TFG_COMM_ID_BYTES 128
+TFG_API int tfg_comm_unique_id(uint8_t* id /* TFG_COMM_ID_BYTES */);
+TFG_API int tfg_comm_init(tfg_ctx* ctx, const uint8_t* id, int rank, int nranks);
+/* In-place sum of the flat gradient buffer over the ranks, on the context's
+ * stream (ordered between the backward and the optimizer step). */
+TFG_API int tfg_allreduce_grads(tfg_ctx* ctx);
+/* Releases the communicator (tfg_destroy does too). */
+TFG_API int tfg_comm_destroy(tfg_ctx* ctx);
+
 /* ---- sub-steps exposed for parity (reference-facing operator surface) ---- */
 /* sample_segments over the current window: builds the device batch. */
 TFG_API int tfg_sample(tfg_ctx* ctx, uint64_t iter, uint64_t ray_begin, int n_rays, int jitter,

@@ -9,6 +9,7 @@
 // implements forward_batch / backward_batch / adam_step on top of this.
 #pragma once
 
+#include <array>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -83,6 +84,18 @@ public:
         return {static_cast<float*>(p), n};
     }
     void optimizer_step(uint64_t iter) { check(tfg_optimizer_step(c_, iter)); }
+    // the library's own NCCL communicator: rank 0 calls comm_unique_id() and
+    // the host distributes the 128 bytes; then per iteration
+    // forward_backward, allreduce_grads, optimizer_step
+    static std::array<uint8_t, TFG_COMM_ID_BYTES> comm_unique_id() {
+        std::array<uint8_t, TFG_COMM_ID_BYTES> id{};
+        check(tfg_comm_unique_id(id.data()));
+        return id;
+    }
+    void comm_init(const std::array<uint8_t, TFG_COMM_ID_BYTES>& id, int rank, int nranks) {
+        check(tfg_comm_init(c_, id.data(), rank, nranks));
+    }
+    void allreduce_grads() { check(tfg_allreduce_grads(c_)); }
     float read_loss() {
         float l = 0.f;
         check(tfg_read_loss(c_, &l));

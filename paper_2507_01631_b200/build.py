@@ -32,6 +32,7 @@ UNITS = [
     ("k_field_tc.cu", []),
     ("k_composite.cu", []),
     ("k_eval.cu", ["-fmad=false"]),
+    ("tfg_comm.cu", []),
 ]
 
 

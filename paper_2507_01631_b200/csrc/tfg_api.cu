@@ -756,6 +756,7 @@ TFG_API int tfg_destroy(tfg_ctx* c) {
     if (!c) return 0;
     cudaSetDevice(c->device);
     cudaDeviceSynchronize();
+    comm_release(c);
     void* dev[] = {c->d_params, c->d_grads, c->d_m, c->d_v, c->d_ema, c->d_bits, c->d_group_flags,
                    c->d_status, c->d_cams, c->d_east, c->d_north, c->d_flags, c->d_pos,
                    c->d_block_sums, c->d_acc_sums, c->d_todo_n, c->d_view_start, c->d_union, c->d_crop4,

@@ -25,6 +25,7 @@ namespace host {
 
 // Records the thread-local message returned by tfg_last_error.
 int fail(int code, const std::string& msg);
+void comm_release(tfg_ctx* c);  // tfg_comm.cu
 
 #define CK(call)                                                                            \
     do {                                                                                    \
@@ -81,6 +82,8 @@ using namespace tfg::host;
 
 struct tfg_ctx {
     int device = 0;
+    void* comm = nullptr;  // ncclComm_t of tfg_comm_init (tfg_comm.cu)
+    int comm_rank = 0, comm_ranks = 0;
     int sms = 148;
     cudaStream_t st = nullptr, side = nullptr;
     bool own_stream = true;

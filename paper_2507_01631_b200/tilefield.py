@@ -111,6 +111,10 @@ def lib() -> C.CDLL:
         "tfg_build_crop_cache": [_vp, C.c_char_p, _vp],
         "tfg_load_crop_cache": [_vp, C.c_char_p],
         "tfg_crop_rect": [_vp, C.c_int, C.c_int, C.c_int, _vp],
+        "tfg_comm_unique_id": [_vp],
+        "tfg_comm_init": [_vp, _vp, C.c_int, C.c_int],
+        "tfg_allreduce_grads": [_vp],
+        "tfg_comm_destroy": [_vp],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -312,6 +316,34 @@ class Context:
         l = C.c_float()
         _check(lib().tfg_train_step(self.h, it, ray_begin, n_rays or self.max_rays, C.byref(l)))
         return l.value
+
+    # ---- multi-GPU through the C-ABI's own NCCL communicator.  torch is
+    # imported first so that the library binds torch's libnccl.so.2 instead of
+    # loading the system copy under the same soname (torch would then fail to
+    # import against the older one).
+    @staticmethod
+    def comm_unique_id() -> bytes:
+        """128-byte NCCL id (rank 0 creates it; the host distributes it)."""
+        import torch  # noqa: F401  (see above)
+
+        buf = (C.c_uint8 * 128)()
+        _check(lib().tfg_comm_unique_id(buf))
+        return bytes(buf)
+
+    def comm_init(self, uid: bytes, rank: int, nranks: int) -> None:
+        if len(uid) != 128:
+            raise ValueError("comm_init: the NCCL id is 128 bytes")
+        import torch  # noqa: F401  (see comm_unique_id)
+
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        _check(lib().tfg_comm_init(self.h, buf, rank, nranks))
+
+    def allreduce_grads(self) -> None:
+        """In-place sum of the flat gradient buffer over the ranks (context stream)."""
+        _check(lib().tfg_allreduce_grads(self.h))
+
+    def comm_destroy(self) -> None:
+        _check(lib().tfg_comm_destroy(self.h))
 
     def grad_buffer(self) -> tuple[int, int]:
         p, n = C.c_void_p(), C.c_uint64()
