@@ -138,7 +138,7 @@ int scan_exclusive(const uint32_t* in, uint64_t n, uint32_t* out, uint32_t* bloc
 // accept_solve_kernel runs the two Newton localisations of each listed pixel
 // on a lane pair, so no warp carries memo-hit lanes through a solve.
 #ifndef TFG_ACCEPT_MINB
-#define TFG_ACCEPT_MINB 6
+#define TFG_ACCEPT_MINB 4
 #endif
 
 __device__ __forceinline__ void candidate_pixel(const AcceptArgs& a, uint64_t idx, int* v_, int* row, int* col) {
@@ -341,7 +341,7 @@ __device__ __forceinline__ bool occ_test(const uint32_t* bits, float x, float y,
 // same arithmetic (same bits); the interior-sample counting is split by
 // sample parity; the odd lane also writes the view encoding.
 #ifndef TFG_RAYGEN_MINB
-#define TFG_RAYGEN_MINB 6
+#define TFG_RAYGEN_MINB 5
 #endif
 // kSolve = false: drawn pixels with the pixel memo only (no Newton code, so
 // fewer registers and more resident warps); true: explicit pixels or no memo.

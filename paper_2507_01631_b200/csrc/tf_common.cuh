@@ -143,6 +143,68 @@ TF_HD double rpc_poly(const double* c, double P, double L, double H) {
     s += rpc_coef(c + 19) * (H * H * H);
     return s;
 }
+// The four central-difference projections of a Newton iteration at once:
+// every coefficient is loaded once and applied to the four points (the
+// solve's bound is the L1 writeback of its coefficient loads).  Each point's
+// arithmetic is exactly rpc_project's, in the same order.  Returns false if
+// any point falls outside the valid cube (where project() would throw).
+TF_HD void rpc_poly4(const double* c, const double* P, const double* L, double H, double* s) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) s[i] = 0;
+    double k;
+#define TFG_TERM4(n, expr)                                         \
+    k = rpc_coef(c + n);                                           \
+    _Pragma("unroll") for (int i = 0; i < 4; ++i) {                \
+        const double Li = L[i], Pi = P[i];                         \
+        (void)Li;                                                  \
+        (void)Pi;                                                  \
+        s[i] += k * (expr);                                        \
+    }
+    TFG_TERM4(0, 1.0)
+    TFG_TERM4(1, Li)
+    TFG_TERM4(2, Pi)
+    TFG_TERM4(3, H)
+    TFG_TERM4(4, Li * Pi)
+    TFG_TERM4(5, Li * H)
+    TFG_TERM4(6, Pi * H)
+    TFG_TERM4(7, Li * Li)
+    TFG_TERM4(8, Pi * Pi)
+    TFG_TERM4(9, H * H)
+    TFG_TERM4(10, Pi * Li * H)
+    TFG_TERM4(11, Li * Li * Li)
+    TFG_TERM4(12, Li * Pi * Pi)
+    TFG_TERM4(13, Li * H * H)
+    TFG_TERM4(14, Li * Li * Pi)
+    TFG_TERM4(15, Pi * Pi * Pi)
+    TFG_TERM4(16, Pi * H * H)
+    TFG_TERM4(17, Li * Li * H)
+    TFG_TERM4(18, Pi * Pi * H)
+    TFG_TERM4(19, H * H * H)
+#undef TFG_TERM4
+}
+TF_HD bool rpc_project4(const tfg_rpc& c, const double* x, const double* y, double z, double* row, double* col) {
+    double L[4], P[4];
+    const double H = (z - c.height_off) / c.height_scale;
+    bool ok = fabs(H) <= 1.5;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        L[i] = (x[i] - c.long_off) / c.long_scale;
+        P[i] = (y[i] - c.lat_off) / c.lat_scale;
+        ok = ok && fabs(L[i]) <= 1.5 && fabs(P[i]) <= 1.5;
+    }
+    if (!ok) return false;
+    double ln[4], ld[4], sn[4], sd[4];
+    rpc_poly4(c.line_num, P, L, H, ln);
+    rpc_poly4(c.line_den, P, L, H, ld);
+    rpc_poly4(c.samp_num, P, L, H, sn);
+    rpc_poly4(c.samp_den, P, L, H, sd);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        row[i] = c.line_off + c.line_scale * (ln[i] / ld[i]);
+        col[i] = c.samp_off + c.samp_scale * (sn[i] / sd[i]);
+    }
+    return true;
+}
 TF_HD bool rpc_project(const tfg_rpc& c, double x, double y, double z, double* row, double* col) {
     double L = (x - c.long_off) / c.long_scale;
     double P = (y - c.lat_off) / c.lat_scale;
@@ -214,10 +276,16 @@ TF_HD int rpc_localize(const tfg_rpc& c, double pr, double pc, double h, double*
         double fn = hyp2(f0, f1);
         if (fn < 1e-4) { *gx = x; *gy = y; return 0; }
         double a0, a1, b0, b1, c0, c1, d0, d1;
-        if (!rpc_project(c, x + hx, y + 0.0, h, &a0, &a1)) return 1;
-        if (!rpc_project(c, x - hx, y - 0.0, h, &b0, &b1)) return 1;
-        if (!rpc_project(c, x + 0.0, y + hy, h, &c0, &c1)) return 1;
-        if (!rpc_project(c, x - 0.0, y - hy, h, &d0, &d1)) return 1;
+        {
+            const double px[4] = {x + hx, x - hx, x + 0.0, x - 0.0};
+            const double py[4] = {y + 0.0, y - 0.0, y + hy, y - hy};
+            double pr4[4], pc4[4];
+            if (!rpc_project4(c, px, py, h, pr4, pc4)) return 1;
+            a0 = pr4[0]; a1 = pc4[0];
+            b0 = pr4[1]; b1 = pc4[1];
+            c0 = pr4[2]; c1 = pc4[2];
+            d0 = pr4[3]; d1 = pc4[3];
+        }
         // residual differences: (p_a - px) - (p_b - px)
         double j00 = ((a0 - pr) - (b0 - pr)) / (2 * hx);
         double j10 = ((a1 - pc) - (b1 - pc)) / (2 * hx);
