@@ -362,7 +362,7 @@ static_assert(kLevels == 8, "scatter_row_bfly unrolls the 8 levels of the defaul
 // ------------------------------------------------------------------ K2b
 // smem: weights | X0 [128x16] (the gathered features, bulk-copied; the only
 // activation tile in smem).  4 resident CTAs per SM (TMEM and registers).
-constexpr uint32_t kFwdSmem = kWeightsBytes + kFeatTile + 128;
+constexpr uint32_t kFwdSmem = kWeightsBytes + 2 * kFeatTile + 128;
 // TMEM: accumulator [0, 64); layers 2-5 take their A operand (the previous
 // layer's activations, bf16 pairs) from columns [64, 96), so activations never
 // touch smem (measured: the MLP's smem pipe was its contended resource).
@@ -372,20 +372,24 @@ constexpr int kColA = 64;
 __global__ void __launch_bounds__(128, 4) mlp_fwd_kernel(FieldArgs a, const uint8_t* __restrict__ feat,
                                                       const int32_t* __restrict__ rays) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
-    __shared__ uint64_t bar_mma, bar_ld;
+    __shared__ uint64_t bar_mma, bar_ld[2];
     __shared__ uint32_t tmem_slot;
     uint8_t* p = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
     Weights W = carve_weights(p);
-    uint8_t* X0 = carve(p, kFeatTile);  // [128 x 16]
+    // [128 x 16] feature tiles, double-buffered: tile i+1's bulk copy is in
+    // flight while tile i runs
+    uint8_t* const X0b0 = carve(p, kFeatTile);
+    uint8_t* const X0b1 = carve(p, kFeatTile);
     const int r = threadIdx.x;
     if (r == 0) {
         umma::mbar_init(&bar_mma, 1);
-        umma::mbar_init(&bar_ld, 1);
+        umma::mbar_init(&bar_ld[0], 1);
+        umma::mbar_init(&bar_ld[1], 1);
         umma::fence_mbar_init();
     }
     if (r < 32) umma::tmem_alloc<kFwdTmemCols>(&tmem_slot);
     stage_color(W, a.f.color);
-    uint32_t ph_mma = 0, ph_ld = 0;
+    uint32_t ph_mma = 0, ph_ld = 0;  // bit b: phase of bar_ld[b]
     int cur = -1;
     pdl_wait();  // hash_fwd's feature tiles and ray ids
     uint32_t n_tiles = a.status->n_tiles;
@@ -400,21 +404,30 @@ __global__ void __launch_bounds__(128, 4) mlp_fwd_kernel(FieldArgs a, const uint
     if (blockIdx.x < n_tiles) {
         td_next = a.tiles[blockIdx.x];
         ray_next = rays[uint64_t(blockIdx.x) * kT + r];
+        if (r == 0) {
+            umma::mbar_expect_tx(&bar_ld[0], kFeatTile);
+            umma::bulk_g2s(X0b0, feat + uint64_t(blockIdx.x) * kFeatTile, kFeatTile, &bar_ld[0]);
+        }
     }
-    for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+    uint32_t it = 0;
+    for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
         const TileDesc td = td_next;
         const int ray = ray_next;
+        const uint32_t b = it & 1u;
+        uint8_t* X0 = b ? X0b1 : X0b0;
         if (t + gridDim.x < n_tiles) {
             td_next = a.tiles[t + gridDim.x];
             ray_next = rays[uint64_t(t + gridDim.x) * kT + r];
+            // the other buffer's last reader (the previous tile's layer-1
+            // MMA) has completed
+            if (r == 0) {
+                umma::mbar_expect_tx(&bar_ld[b ^ 1u], kFeatTile);
+                umma::bulk_g2s(b ? X0b0 : X0b1, feat + uint64_t(t + gridDim.x) * kFeatTile, kFeatTile, &bar_ld[b ^ 1u]);
+            }
         }
         if (td.slot != cur) {
             stage_density(W, a.f.dnet[td.slot]);
             cur = td.slot;
-        }
-        if (r == 0) {
-            umma::mbar_expect_tx(&bar_ld, kFeatTile);
-            umma::bulk_g2s(X0, feat + uint64_t(t) * kFeatTile, kFeatTile, &bar_ld);
         }
         float ve[kViewDim];
         {
@@ -429,8 +442,8 @@ __global__ void __launch_bounds__(128, 4) mlp_fwd_kernel(FieldArgs a, const uint
             }
         }
         sync_for_mma();  // density weights staged, previous tile's TMEM reads done
-        umma::mbar_wait(&bar_ld, ph_ld);
-        ph_ld ^= 1u;
+        umma::mbar_wait(&bar_ld[b], (ph_ld >> b) & 1u);
+        ph_ld ^= 1u << b;
         // ---- density layer 1: [128x16] x W1d^T -> 64
         if (r == 0) {
             umma::mma(tmem, kmaj(X0, kT, 0), kmaj(W.w1d, kW1dRows, 0), id64, 0);
