@@ -1002,8 +1002,14 @@ void launch_field_forward_tc(const FieldArgs& a, uint8_t* feat, int32_t* rays, i
         cudaFuncSetAttribute(mlp_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kFwdSmem));
         attr = true;
     }
-    launch_pdl(hash_fwd_kernel, dim3(sms * 8), dim3(128), 0, st, a, feat, rays);
-    launch_pdl(mlp_fwd_kernel, dim3(sms * 4), dim3(128), kFwdSmem, st, a, feat, rays);  // 4 per SM
+#ifndef TFG_GATHER_CTAS
+#define TFG_GATHER_CTAS 5
+#endif
+#ifndef TFG_MLPF_CTAS
+#define TFG_MLPF_CTAS 4
+#endif
+    launch_pdl(hash_fwd_kernel, dim3(sms * TFG_GATHER_CTAS), dim3(128), 0, st, a, feat, rays);
+    launch_pdl(mlp_fwd_kernel, dim3(sms * TFG_MLPF_CTAS), dim3(128), kFwdSmem, st, a, feat, rays);  // 4 per SM
     *launches += 2;
 }
 
