@@ -497,38 +497,38 @@ __global__ void tiles_kernel(const uint32_t* __restrict__ P, int n_rays, int nsl
                              uint64_t capacity, int max_tiles, TileDesc* __restrict__ tiles,
                              Status* __restrict__ status) {
     pdl_wait();
-    __shared__ uint32_t tile_base[kMaxSlots + 1];
+    // every CTA derives the slot buckets' tile bases from P (a few loads);
+    // block 0 publishes the totals, all CTAs write their share of the tiles
+    __shared__ uint32_t tile_base[kMaxSlots + 1], bucket[kMaxSlots + 1];
+    __shared__ int ok;
     if (threadIdx.x == 0) {
         uint32_t tb = 0;
+        for (int s = 0; s <= nslots; ++s) bucket[s] = P[uint64_t(s) * n_rays];
         for (int s = 0; s < nslots; ++s) {
-            uint32_t b = P[uint64_t(s) * n_rays];
-            uint32_t e = P[uint64_t(s + 1) * n_rays];
             tile_base[s] = tb;
-            tb += (e - b + 127) / 128;
+            tb += (bucket[s + 1] - bucket[s] + 127) / 128;
         }
         tile_base[nslots] = tb;
-        uint64_t total = P[uint64_t(nslots) * n_rays];
-        status->n_samples = total;
-        status->n_tiles = tb;
-        if (total > capacity || int(tb) > max_tiles) {
-            atomicOr(&status->bits, kStatusSampleOverflow);
-            status->n_tiles = 0;
+        const uint64_t total = bucket[nslots];
+        ok = !(total > capacity || int(tb) > max_tiles);
+        if (blockIdx.x == 0) {
+            status->n_samples = total;
+            status->n_tiles = ok ? tb : 0;
+            if (!ok) atomicOr(&status->bits, kStatusSampleOverflow);
         }
     }
     __syncthreads();
-    if (status->n_tiles == 0) return;
-    for (int s = 0; s < nslots; ++s) {
-        uint32_t b = P[uint64_t(s) * n_rays];
-        uint32_t e = P[uint64_t(s + 1) * n_rays];
-        uint32_t nt = tile_base[s + 1] - tile_base[s];
-        for (uint32_t t = threadIdx.x; t < nt; t += blockDim.x) {
-            TileDesc d;
-            d.start = b + 128 * t;
-            uint32_t rem = e - d.start;
-            d.n = uint16_t(rem < 128 ? rem : 128);
-            d.slot = uint16_t(s);
-            tiles[tile_base[s] + t] = d;
-        }
+    if (!ok) return;
+    const uint32_t n_tiles = tile_base[nslots];
+    for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < n_tiles; g += gridDim.x * blockDim.x) {
+        int s = 0;
+        while (s + 1 < nslots && g >= tile_base[s + 1]) ++s;
+        TileDesc d;
+        d.start = bucket[s] + 128 * (g - tile_base[s]);
+        const uint32_t rem = bucket[s + 1] - d.start;
+        d.n = uint16_t(rem < 128 ? rem : 128);
+        d.slot = uint16_t(s);
+        tiles[g] = d;
     }
 }
 
@@ -651,7 +651,8 @@ int launch_sampler(const RaygenArgs& a, RayRec* rays, float4* venc, uint32_t* co
                    status);
     uint64_t n = uint64_t(a.slots.n) * a.n_rays;
     if (scan_exclusive(counts, n, P, block_sums, nullptr, st, launches)) return 1;
-    launch_pdl(tiles_kernel, dim3(1), dim3(256), 0, st, P, a.n_rays, a.slots.n, capacity, max_tiles, tiles, status);
+    launch_pdl(tiles_kernel, dim3(std::min(148, (max_tiles + 255) / 256)), dim3(256), 0, st, P, a.n_rays, a.slots.n,
+               capacity, max_tiles, tiles, status);
     launch_pdl(write_kernel, dim3((a.n_rays * 32 + 255) / 256), dim3(256), 0, st, a, rays, P, status, out);
     *launches += 3;
     return 0;
