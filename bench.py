@@ -286,6 +286,13 @@ def run_ours(args):
     # prefetched move (the one-off initial load of a run is not timed, like
     # the device metric's).
     path = snake_path(scene.grid_rows, scene.grid_cols)
+    # run setup (untimed, reported): every pixel's ray solved once for the
+    # whole scene, so window moves only run the accept pass's memo kernel
+    torch.cuda.synchronize()
+    tp0 = time.perf_counter()
+    ctx.precompute_rays()
+    torch.cuda.synchronize()
+    precompute_ms = 1e3 * (time.perf_counter() - tp0)
     ctx.set_window(*path[0])
     ctx.prefetch_window(*path[1])
     h0, d0 = ctx.copy_bytes()
@@ -306,13 +313,21 @@ def run_ours(args):
         ctx.read_loss()
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
+    # the run setup's share: the whole-scene ray fill amortised over one full
+    # snake (every position once, move_every iterations each)
+    snake_steps = len(path) * args.move_every
+    e2e_s += (precompute_ms / 1e3) * min(1.0, e2e_steps / snake_steps)
     h1, d1 = ctx.copy_bytes()
     te = torch.tensor([e2e_s], device=dev)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e = {"value": world * B * e2e_steps / float(te.item()), "unit": UNIT,
            "h2d_bytes_per_step": (h1 - h0) // e2e_steps, "d2h_bytes_per_step": (d1 - d0) // e2e_steps,
-           "window_move_every": args.move_every, "window_moves": (e2e_steps - 1) // args.move_every}
+           "window_move_every": args.move_every, "window_moves": (e2e_steps - 1) // args.move_every,
+           "setup": {"precompute_rays_ms": precompute_ms,
+                     "what": "one-off per run: tfg_precompute_rays solves every pixel ray of the scene; "
+                             "its share over one full snake (len(path) x move_every iterations) is "
+                             "added to the e2e time"}}
 
     # ---- render (config 4: 4x4-tile ROI, random-init weights, occupancy all on)
     render = None

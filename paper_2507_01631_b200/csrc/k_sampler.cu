@@ -633,6 +633,10 @@ int launch_accept(const AcceptArgs& args, uint32_t* flags, uint32_t* pos, uint32
     // past its end leave at once): measured faster than a persistent grid
     uint64_t solve_blocks = (2 * a.n_candidates + 127) / 128;
     accept_solve_kernel<<<int(solve_blocks), 128, 0, st>>>(a, flags);
+    if (!out) {  // memo fill only (tfg_precompute_rays): no accepted list
+        *launches += 2;
+        return 0;
+    }
     if (scan_exclusive(flags, a.n_candidates, pos, block_sums, n_out, st, launches)) return 1;
     accept_scatter_kernel<<<nb, 128, 0, st>>>(a, flags, pos, out);
     *launches += 3;

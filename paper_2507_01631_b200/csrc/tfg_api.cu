@@ -1088,6 +1088,63 @@ TFG_API int tfg_set_window(tfg_ctx* c, int pr, int pc) {
     return 0;
 }
 
+// Solves the ray of every pixel of every view once into the per-pixel memo
+// (the same kernels as the accept pass, over whole views in row bands that
+// fit the candidate buffers, with no tile loaded so no list is built).  Each
+// later window position then only runs the memo pass.  Runs on the side
+// stream, ordered with window staging; the main stream waits for it.
+TFG_API int tfg_precompute_rays(tfg_ctx* c) {
+    if (!c || c->n_views == 0) return fail(TFG_ERR_STATE, "precompute_rays: call set_scene first");
+    if (!c->d_pix_info) return 0;  // memo off (TFG_NO_PIXEL_MEMO): nothing to fill
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = c->side;
+    CK(cudaEventRecord(c->ev_main, c->st));
+    CK(cudaStreamWaitEvent(st, c->ev_main, 0));
+    for (int v = 0; v < c->n_views; ++v) {
+        const int rows = c->cams[v].image_rows, cols = c->cams[v].image_cols;
+        const int band = int(std::max<uint64_t>(1, std::min<uint64_t>(uint64_t(rows), c->cand_cap / uint64_t(cols))));
+        for (int r0 = 0; r0 < rows; r0 += band) {
+            const int r1 = std::min(rows, r0 + band);
+            const uint64_t vs = 0;
+            int urect[4] = {r0, r1, 0, cols};
+            std::vector<int> crect(4 * kTrainSlots, 0);
+            crect[0] = r0, crect[1] = r1, crect[2] = 0, crect[3] = cols;  // slot 0: the band; others empty
+            // pageable copies are staged before the call returns
+            CK(cudaMemcpyAsync(c->d_view_start, &vs, 8, cudaMemcpyHostToDevice, st));
+            CK(cudaMemcpyAsync(c->d_union, urect, 16, cudaMemcpyHostToDevice, st));
+            CK(cudaMemcpyAsync(c->d_crop4, crect.data(), crect.size() * 4, cudaMemcpyHostToDevice, st));
+            AcceptArgs a{};
+            a.cams = c->d_cams + v;
+            a.n_views = 1;
+            a.view_start = c->d_view_start;
+            a.union_rect = c->d_union;
+            a.crop_rect = c->d_crop4;
+            a.n_candidates = uint64_t(r1 - r0) * uint64_t(cols);
+            a.east = c->d_east;
+            a.north = c->d_north;
+            a.grid_rows = c->rows;
+            a.grid_cols = c->cols;
+            for (int k = 0; k < kTrainSlots; ++k) a.loaded_tile[k] = -1;
+            a.n_loaded = 1;
+            a.z_min = c->roi.z_min;
+            a.z_max = c->roi.z_max;
+            a.pix_info = c->d_pix_info;
+            a.pix_rays = c->d_pix_rays;
+            a.pix_off = c->d_pix_off + v;
+            a.win_r0 = a.win_c0 = 1;  // no window: nothing is accepted
+            a.win_r1 = a.win_c1 = 0;
+            a.todo_n = c->d_todo_n;
+            a.sms = c->sms;
+            if (launch_accept(a, c->d_flags, c->d_pos, c->d_acc_sums, nullptr, nullptr, st, &c->launches))
+                return fail(TFG_ERR_INVALID, "precompute_rays: launch failed");
+            CK(cudaGetLastError());
+        }
+    }
+    CK(cudaEventRecord(c->ev_side, st));
+    CK(cudaStreamWaitEvent(c->st, c->ev_side, 0));
+    return 0;
+}
+
 // Stages the next window position (crops + accepted-ray list) into the back
 // buffer on the side stream while the current position trains; the entering
 // tiles' host records are materialised by the init pool.

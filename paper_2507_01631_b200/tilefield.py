@@ -111,6 +111,7 @@ def lib() -> C.CDLL:
         "tfg_build_crop_cache": [_vp, C.c_char_p, _vp],
         "tfg_load_crop_cache": [_vp, C.c_char_p],
         "tfg_crop_rect": [_vp, C.c_int, C.c_int, C.c_int, _vp],
+        "tfg_precompute_rays": [_vp],
         "tfg_comm_unique_id": [_vp],
         "tfg_comm_init": [_vp, _vp, C.c_int, C.c_int],
         "tfg_allreduce_grads": [_vp],
@@ -316,6 +317,11 @@ class Context:
         l = C.c_float()
         _check(lib().tfg_train_step(self.h, it, ray_begin, n_rays or self.max_rays, C.byref(l)))
         return l.value
+
+    def precompute_rays(self) -> None:
+        """Solve every pixel's ray of the scene once (optional; window moves
+        then only run the accept pass's memo kernel)."""
+        _check(lib().tfg_precompute_rays(self.h))
 
     # ---- multi-GPU through the C-ABI's own NCCL communicator.  torch is
     # imported first so that the library binds torch's libnccl.so.2 instead of

@@ -188,7 +188,8 @@ def test_nonfinite_gradient_names_the_group():
 def test_pixel_memo_matches_resolving():
     """The per-pixel scene memo (rays + hit-tile bbox) gives the same accepted
     lists and batches as re-solving every pixel per window (memo disabled via
-    TFG_NO_PIXEL_MEMO in a subprocess), along a snake that revisits pixels."""
+    TFG_NO_PIXEL_MEMO in a subprocess), along a snake that revisits pixels;
+    and so does filling the whole memo up front (tfg_precompute_rays)."""
     _need_gpu()
     import json
     import os
@@ -204,6 +205,9 @@ from paper_2507_01631_b200.abi import FieldConfig, TrainConfig
 from paper_2507_01631_b200.tilefield import Context, snake_path
 scene = synth.make_scene(3, 3, tile_side=96.0, n_views=3, gsd=1.0, seed=21, max_off_nadir=30.0)
 ctx = Context(scene, FieldConfig.defaults(), TrainConfig.defaults(batch_rays=2048, seed=5), max_rays=2048)
+import os
+if os.environ.get("TFG_TEST_PRECOMPUTE") == "1":
+    ctx.precompute_rays()
 out = []
 for it, pos in enumerate(snake_path(3, 3) + [(0, 0), (1, 1)]):
     ctx.set_window(*pos)
@@ -215,13 +219,14 @@ for it, pos in enumerate(snake_path(3, 3) + [(0, 0), (1, 1)]):
 print(json.dumps(out))
 """ % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     res = {}
-    for memo in ("0", "1"):
-        env = dict(os.environ, TFG_NO_PIXEL_MEMO=memo)
+    for mode, memo, pre in (("memo", "0", "0"), ("solve", "1", "0"), ("pre", "0", "1")):
+        env = dict(os.environ, TFG_NO_PIXEL_MEMO=memo, TFG_TEST_PRECOMPUTE=pre)
         p = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
         assert p.returncode == 0, p.stderr[-2000:]
-        res[memo] = json.loads(p.stdout.strip().splitlines()[-1])
-    assert res["0"] == res["1"]
-    assert all(r[0] > 0 for r in res["0"])
+        res[mode] = json.loads(p.stdout.strip().splitlines()[-1])
+    assert res["memo"] == res["solve"]
+    assert res["pre"] == res["memo"]
+    assert all(r[0] > 0 for r in res["memo"])
 
 
 def test_prefetched_slide_round_trips_state_bit_exactly():

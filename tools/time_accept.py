@@ -24,3 +24,19 @@ for pos in path[:9]:
     torch.cuda.synchronize()
     ts.append(1e3 * (time.perf_counter() - t0))
 print("first window ms %.2f, moves:" % ts[0], " ".join(f"{t:.2f}" for t in ts[1:]), "sum %.2f" % sum(ts))
+
+# the same moves after the whole-scene memo fill (tfg_precompute_rays)
+ctx2 = Context(scene, FieldConfig.defaults(), TrainConfig.defaults(batch_rays=65536, seed=2), max_rays=65536)
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+ctx2.precompute_rays()
+torch.cuda.synchronize()
+pre = 1e3 * (time.perf_counter() - t0)
+ts = []
+for pos in path[:9]:
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    ctx2.set_window(*pos)
+    torch.cuda.synchronize()
+    ts.append(1e3 * (time.perf_counter() - t0))
+print("precompute ms %.2f; first window ms %.2f, moves:" % (pre, ts[0]), " ".join(f"{t:.2f}" for t in ts[1:]))
