@@ -320,14 +320,17 @@ __device__ __forceinline__ void plan_intervals(SegPlan& p, double spm, int cap) 
 
 // step = (tf - tn) / n of the segment, computed once per segment by the
 // caller (the same FP64 quotient for every sample of the segment)
-__device__ __forceinline__ double sample_t(const SegPlan& p, int k, int j, bool jitter,
+__device__ __forceinline__ double sample_t(double tn, double tf, int n, int k, int j, bool jitter,
                                            uint64_t key, double step) {
-    int n = p.nint[k];
-    if (j == 0) return p.tn[k];
-    if (j == n) return p.tf[k];
+    if (j == 0) return tn;
+    if (j == n) return tf;
     float u = 0.5f;
     if (jitter) u = Rng(hash_combine(key, (uint64_t(k) << 16) | uint64_t(j))).flt();
-    return p.tn[k] + (double(j) + (double(u) - 0.5)) * step;
+    return tn + (double(j) + (double(u) - 0.5)) * step;
+}
+__device__ __forceinline__ double sample_t(const SegPlan& p, int k, int j, bool jitter,
+                                           uint64_t key, double step) {
+    return sample_t(p.tn[k], p.tf[k], p.nint[k], k, j, jitter, key, step);
 }
 
 __device__ __forceinline__ bool occ_test(const uint32_t* bits, float x, float y, float z) {
@@ -552,25 +555,23 @@ __global__ void __launch_bounds__(256) write_kernel(RaygenArgs a, const RayRec* 
     if (R.status != 0) return;
     uint64_t g = a.ray_begin + uint64_t(warp);
     uint64_t key = hash_combine(hash_combine(hash_combine(a.seed, kPurposeJitter), a.iter), g);
-    SegPlan p;
-    p.nseg = R.nseg;
-    for (int k = 0; k < R.nseg; ++k) {
-        p.slot[k] = R.slot[k];
-        p.tn[k] = R.tn[k];
-        p.tf[k] = R.tf[k];
-        p.nint[k] = R.nint[k];
-    }
+    // segment fields straight from the (warp-uniform) ray record and the
+    // slot frame from the kernel parameters: no local-memory copies
+    const int nseg = R.nseg;
+    const double o0 = R.o[0], o1 = R.o[1], o2 = R.o[2], d0 = R.d[0], d1 = R.d[1], d2 = R.d[2];
     const uint32_t lt = (1u << lane) - 1u;
     long long pend_pos = -1;
     double pend_t = 0.0;
-    for (int k = 0; k < p.nseg; ++k) {
-        int s = p.slot[k];
-        const double* fr = a.slots.frame[s];
+    for (int k = 0; k < nseg; ++k) {
+        const int s = R.slot[k];
+        const double f0 = a.slots.frame[s][0], f1 = a.slots.frame[s][1], f2 = a.slots.frame[s][2];
+        const double f3 = a.slots.frame[s][3], f4 = a.slots.frame[s][4], f5 = a.slots.frame[s][5];
         const uint32_t* bits = a.occ_bits[s];
         uint64_t base = P[uint64_t(s) * a.n_rays + warp];
         uint32_t written = 0;
-        int n = p.nint[k];
-        const double step = (p.tf[k] - p.tn[k]) / n;
+        const int n = R.nint[k];
+        const double tn = R.tn[k], tf = R.tf[k];
+        const double step = (tf - tn) / n;
         for (int j0 = 0; j0 <= n; j0 += 32) {
             int j = j0 + lane;
             bool valid = j <= n;
@@ -579,10 +580,10 @@ __global__ void __launch_bounds__(256) write_kernel(RaygenArgs a, const RayRec* 
             bool endp = (j == 0 || j == n);
             bool keep = false;
             if (valid) {
-                t = sample_t(p, k, j, a.jitter, key, step);
-                lx = float((R.o[0] + t * R.d[0] - fr[0]) * fr[3]);
-                ly = float((R.o[1] + t * R.d[1] - fr[1]) * fr[4]);
-                lz = float((R.o[2] + t * R.d[2] - fr[2]) * fr[5]);
+                t = sample_t(tn, tf, n, k, j, a.jitter, key, step);
+                lx = float((o0 + t * d0 - f0) * f3);
+                ly = float((o1 + t * d1 - f1) * f4);
+                lz = float((o2 + t * d2 - f2) * f5);
                 keep = endp || occ_test(bits, lx, ly, lz);
             }
             uint32_t mask = __ballot_sync(0xffffffffu, keep);
@@ -609,7 +610,7 @@ __global__ void __launch_bounds__(256) write_kernel(RaygenArgs a, const RayRec* 
         }
     }
     if (lane == 0 && pend_pos >= 0) {
-        double texit = (a.z_min - R.o[2]) / R.d[2];
+        double texit = (a.z_min - o2) / d2;
         double r = texit - pend_t;
         if (r < 0) r = 0;
         if (r > a.delta_cap) r = a.delta_cap;
