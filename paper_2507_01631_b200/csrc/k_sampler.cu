@@ -432,7 +432,10 @@ __global__ void __launch_bounds__(128, kSolve ? TFG_RAYGEN_MINB : TFG_RAYGEN_MEM
     bool overflow = false;
     for (int s = 0; s < a.slots.n; ++s) {
         double t0, t1;
-        if (!slab(R.o, R.d, a.slots.box[s], &t0, &t1)) continue;
+        double box[6];  // from the kernel parameters by value (a pointer into them would copy the block to local memory)
+#pragma unroll
+        for (int q = 0; q < 6; ++q) box[q] = a.slots.box[s][q];
+        if (!slab(R.o, R.d, box, &t0, &t1)) continue;
         if (p.nseg == kMaxSeg) {
             overflow = true;
             break;
@@ -452,17 +455,23 @@ __global__ void __launch_bounds__(128, kSolve ? TFG_RAYGEN_MINB : TFG_RAYGEN_MEM
     plan_intervals(p, a.spm, a.cap);
     uint64_t key = hash_combine(hash_combine(hash_combine(a.seed, kPurposeJitter), a.iter), g);
     R.nseg = p.nseg;
+    const double o0 = R.o[0], o1 = R.o[1], o2 = R.o[2], d0 = R.d[0], d1 = R.d[1], d2 = R.d[2];
     for (int k = 0; k < p.nseg; ++k) {
-        const double* fr = a.slots.frame[p.slot[k]];
-        const uint32_t* bits = a.occ_bits[p.slot[k]];
-        int n = p.nint[k];
-        const double step = (p.tf[k] - p.tn[k]) / n;
+        // slot frame values from the kernel parameters (no pointer into them,
+        // which would copy the parameter block to local memory)
+        const int sl = p.slot[k];
+        const double f0 = a.slots.frame[sl][0], f1 = a.slots.frame[sl][1], f2 = a.slots.frame[sl][2];
+        const double f3 = a.slots.frame[sl][3], f4 = a.slots.frame[sl][4], f5 = a.slots.frame[sl][5];
+        const uint32_t* bits = a.occ_bits[sl];
+        const int n = p.nint[k];
+        const double tn = p.tn[k], tf = p.tf[k];
+        const double step = (tf - tn) / n;
         int cnt = 0;
         for (int j = 1 + hi; j < n; j += 2) {
-            double t = sample_t(p, k, j, a.jitter, key, step);
-            float lx = float((R.o[0] + t * R.d[0] - fr[0]) * fr[3]);
-            float ly = float((R.o[1] + t * R.d[1] - fr[1]) * fr[4]);
-            float lz = float((R.o[2] + t * R.d[2] - fr[2]) * fr[5]);
+            double t = sample_t(tn, tf, n, k, j, a.jitter, key, step);
+            float lx = float((o0 + t * d0 - f0) * f3);
+            float ly = float((o1 + t * d1 - f1) * f4);
+            float lz = float((o2 + t * d2 - f2) * f5);
             cnt += occ_test(bits, lx, ly, lz);
         }
         cnt += __shfl_xor_sync(pair, cnt, 1);
