@@ -20,11 +20,20 @@ __device__ __forceinline__ int group_of(const AdamArgs& a, uint64_t i) {
     return g;
 }
 
+// Both kernels stream float4s: every group offset is a multiple of 4
+// (tfg_optimizer_step checks), so a float4 never straddles two groups; the
+// last total % 4 elements go one by one.
 __global__ void __launch_bounds__(256) grad_check_kernel(AdamArgs a, uint64_t total) {
     pdl_wait();
     uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
     uint32_t bad = 0;  // bitmask of groups
-    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
+    const uint64_t n4 = total >> 2;
+    const float4* g4 = reinterpret_cast<const float4*>(a.grads);
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n4; i += stride) {
+        float4 g = g4[i];
+        if (!(isfinite(g.x) && isfinite(g.y) && isfinite(g.z) && isfinite(g.w))) bad |= 1u << group_of(a, 4 * i);
+    }
+    for (uint64_t i = 4 * n4 + uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
         float g = a.grads[i];
         if (!isfinite(g)) bad |= 1u << group_of(a, i);
     }
@@ -54,21 +63,44 @@ __global__ void __launch_bounds__(256) adam_kernel(AdamArgs a, uint64_t total) {
     __syncthreads();
     if (skip) return;
     uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
-    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
-        const AdamGroup& G = a.g[group_of(a, i)];
-        float g = a.grads[i];
-        float m = a.beta1 * a.m[i] + a.omb1 * g;
-        float v = a.beta2 * a.v[i] + a.omb2 * (g * g);
-        a.m[i] = m;
-        a.v[i] = v;
+    // the update of one element (adam_step's formula and rounding)
+    auto upd = [&](const AdamGroup& G, float g, float& m, float& v, float& p) {
+        m = a.beta1 * m + a.omb1 * g;
+        v = a.beta2 * v + a.omb2 * (g * g);
         float mh = m / G.bc1;
         float vh = v / G.bc2;
-        a.params[i] = a.params[i] - G.lr * mh / (sqrtf(vh) + a.eps);
+        p = p - G.lr * mh / (sqrtf(vh) + a.eps);
+    };
+    const uint64_t n4 = total >> 2;
+    const float4* g4 = reinterpret_cast<const float4*>(a.grads);
+    float4* m4 = reinterpret_cast<float4*>(a.m);
+    float4* v4 = reinterpret_cast<float4*>(a.v);
+    float4* p4 = reinterpret_cast<float4*>(a.params);
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n4; i += stride) {
+        const AdamGroup& G = a.g[group_of(a, 4 * i)];
+        const float4 g = g4[i];
+        float4 m = m4[i], v = v4[i], p = p4[i];
+        upd(G, g.x, m.x, v.x, p.x);
+        upd(G, g.y, m.y, v.y, p.y);
+        upd(G, g.z, m.z, v.z, p.z);
+        upd(G, g.w, m.w, v.w, p.w);
+        m4[i] = m;
+        v4[i] = v;
+        p4[i] = p;
+    }
+    for (uint64_t i = 4 * n4 + uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
+        const AdamGroup& G = a.g[group_of(a, i)];
+        float m = a.m[i], v = a.v[i], p = a.params[i];
+        upd(G, a.grads[i], m, v, p);
+        a.m[i] = m;
+        a.v[i] = v;
+        a.params[i] = p;
     }
 }
 
 void launch_adam(const AdamArgs& a, uint64_t total, cudaStream_t st, uint64_t* launches) {
-    int blocks = int((total + 255) / 256);
+    int blocks = int((total / 4 + 255) / 256);
+    if (blocks < 1) blocks = 1;
     if (blocks > 148 * 8) blocks = 148 * 8;
     launch_pdl(grad_check_kernel, dim3(blocks), dim3(256), 0, st, a, total);
     launch_pdl(adam_kernel, dim3(blocks), dim3(256), 0, st, a, total);

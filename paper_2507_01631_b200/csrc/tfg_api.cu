@@ -1304,6 +1304,8 @@ TFG_API int tfg_optimizer_step(tfg_ctx* c, uint64_t iter) {
         a.g[2 * c->nslots] = gap;
         a.n_groups = ng + 1;
     }
+    for (int g = 0; g < a.n_groups; ++g)  // the Adam kernels stream float4s within one group
+        if (a.g[g].offset % 4 != 0) return fail(TFG_ERR_INVALID, "optimizer_step: group offset not 4-aligned");
     {
         PhaseScope ps(c, kPhAdam);
         launch_adam(a, total, c->st, &c->launches);
