@@ -633,7 +633,7 @@ int launch_accept(const AcceptArgs& args, uint32_t* flags, uint32_t* pos, uint32
     AcceptArgs a = args;
     a.todo = pos;
     if (a.n_candidates == 0) {
-        cudaMemsetAsync(n_out, 0, 4, st);
+        if (n_out) cudaMemsetAsync(n_out, 0, 4, st);
         return 0;
     }
     int nb = int((a.n_candidates + 127) / 128);
@@ -665,7 +665,7 @@ int launch_sampler(const RaygenArgs& a, RayRec* rays, float4* venc, uint32_t* co
                    status);
     uint64_t n = uint64_t(a.slots.n) * a.n_rays;
     if (scan_exclusive(counts, n, P, block_sums, nullptr, st, launches)) return 1;
-    launch_pdl(tiles_kernel, dim3(std::min(148, (max_tiles + 255) / 256)), dim3(256), 0, st, P, a.n_rays, a.slots.n,
+    launch_pdl(tiles_kernel, dim3(std::max(1, std::min(148, (max_tiles + 255) / 256))), dim3(256), 0, st, P, a.n_rays, a.slots.n,
                capacity, max_tiles, tiles, status);
     launch_pdl(write_kernel, dim3((a.n_rays * 32 + 255) / 256), dim3(256), 0, st, a, rays, P, status, out);
     *launches += 3;

@@ -1102,6 +1102,7 @@ TFG_API int tfg_precompute_rays(tfg_ctx* c) {
     CK(cudaStreamWaitEvent(st, c->ev_main, 0));
     for (int v = 0; v < c->n_views; ++v) {
         const int rows = c->cams[v].image_rows, cols = c->cams[v].image_cols;
+        if (uint64_t(cols) > c->cand_cap) return fail(TFG_ERR_INVALID, "precompute_rays: view wider than the candidate buffers");
         const int band = int(std::max<uint64_t>(1, std::min<uint64_t>(uint64_t(rows), c->cand_cap / uint64_t(cols))));
         for (int r0 = 0; r0 < rows; r0 += band) {
             const int r1 = std::min(rows, r0 + band);
