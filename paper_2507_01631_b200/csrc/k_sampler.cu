@@ -5,7 +5,9 @@
 // Compiled with -fmad=false: every double/float operation here rounds once,
 // matching the reference's x86-64 build (see tf_common.cuh).
 //
-//   accept_kernel    accept_rays over the window's crop union
+//   accept_memo_kernel + accept_solve_kernel + accept_scatter_kernel
+//                    accept_rays over the window's crop union:
+//                    settle memoised pixels / Newton-solve the rest / compact
 //   raygen_kernel    pixel draw (rng.hpp:42-46) + ray_from_pixel (camera.cpp:105)
 //                    + TileBoxSet::segments (geometry.cpp:39-48) + per-slot
 //                    sample counts (sample_segments)
