@@ -571,7 +571,7 @@ constexpr int kColDX = 240;  // d(features) of the last tile, read by the scatte
 // overlaps the latency-bound MMA chain instead of extending it.
 constexpr int kBwdThreads = 256;
 #ifndef TFG_REGS_MLP
-#define TFG_REGS_MLP 176
+#define TFG_REGS_MLP 168
 #endif
 constexpr uint32_t kRegsMlp = TFG_REGS_MLP, kRegsScatter = 256 - TFG_REGS_MLP;  // 4 x 32 x 256 = 32768 per CTA
 
