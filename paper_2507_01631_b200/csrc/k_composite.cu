@@ -55,7 +55,10 @@ __global__ void __launch_bounds__(1024) loss_reduce_kernel(const double* __restr
     }
 }
 
-__global__ void __launch_bounds__(256) composite_kernel(CompositeArgs a) {
+#ifndef TFG_COMPOSITE_THREADS
+#define TFG_COMPOSITE_THREADS 256  // >= 256: d_loss_parts holds max_rays / 8 block partials
+#endif
+__global__ void __launch_bounds__(TFG_COMPOSITE_THREADS) composite_kernel(CompositeArgs a) {
     __shared__ double blk_sum;
     __shared__ unsigned blk_n;
     int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -229,8 +232,8 @@ __global__ void __launch_bounds__(256) composite_kernel(CompositeArgs a) {
 }
 
 void launch_composite(const CompositeArgs& a, cudaStream_t st, uint64_t* launches) {
-    int blocks = (a.n_rays * 32 + 255) / 256;
-    launch_pdl(composite_kernel, dim3(blocks), dim3(256), 0, st, a);
+    int blocks = (a.n_rays * 32 + TFG_COMPOSITE_THREADS - 1) / TFG_COMPOSITE_THREADS;
+    launch_pdl(composite_kernel, dim3(blocks), dim3(TFG_COMPOSITE_THREADS), 0, st, a);
     *launches += 1;
     if (a.backward) {
         launch_pdl(loss_reduce_kernel, dim3(1), dim3(1024), 0, st, static_cast<const double*>(a.loss_parts), blocks,

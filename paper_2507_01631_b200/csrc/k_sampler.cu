@@ -553,7 +553,10 @@ __global__ void tiles_kernel(const uint32_t* __restrict__ P, int n_rays, int nsl
 // (double, then rounded; duplicate boundary samples get delta = 0); the last
 // kept sample's delta is the remaining distance to the z_min exit capped at
 // delta_cap.
-__global__ void __launch_bounds__(256) write_kernel(RaygenArgs a, const RayRec* __restrict__ rays,
+#ifndef TFG_WRITE_THREADS
+#define TFG_WRITE_THREADS 128
+#endif
+__global__ void __launch_bounds__(TFG_WRITE_THREADS) write_kernel(RaygenArgs a, const RayRec* __restrict__ rays,
                                                     const uint32_t* __restrict__ P,
                                                     const Status* __restrict__ status,
                                                     SampleArrays out) {
@@ -669,7 +672,8 @@ int launch_sampler(const RaygenArgs& a, RayRec* rays, float4* venc, uint32_t* co
     if (scan_exclusive(counts, n, P, block_sums, nullptr, st, launches)) return 1;
     launch_pdl(tiles_kernel, dim3(std::max(1, std::min(148, (max_tiles + 255) / 256))), dim3(256), 0, st, P, a.n_rays, a.slots.n,
                capacity, max_tiles, tiles, status);
-    launch_pdl(write_kernel, dim3((a.n_rays * 32 + 255) / 256), dim3(256), 0, st, a, rays, P, status, out);
+    launch_pdl(write_kernel, dim3((a.n_rays * 32 + TFG_WRITE_THREADS - 1) / TFG_WRITE_THREADS), dim3(TFG_WRITE_THREADS), 0,
+               st, a, rays, P, status, out);
     *launches += 3;
     return 0;
 }
