@@ -126,6 +126,35 @@ def cpu_baseline(scene, n_rays: int, steps: int, warmup: int):
                       f"(after {warmup} warm-up; accepted-ray list of {n_acc} built once in {t_accept:.1f} s, untimed)"}
 
 
+def cpu_render_baseline(scene, fc, R: int, W: int, n: int = 8192):
+    """The oracle's render path (sample_pixels -> field forward -> composite)
+    on the host cores for a bounded sample of the render view's pixels: the
+    central half of the image, which the centre 2x2 window covers (the oracle
+    holds one 2x2 window; the GPU render holds all 16 tiles)."""
+    import numpy as np
+
+    from oracle.pyoracle import Oracle, Session
+    from paper_2507_01631_b200.abi import TrainConfig
+
+    cores = os.cpu_count() or 1
+    ses = Session(Oracle(), scene, fc, TrainConfig.defaults(batch_rays=n), workers=cores)
+    ses.set_window(1, 1)
+    rng = np.random.default_rng(0)
+    px = np.stack([np.zeros(n, np.int64), rng.integers(R // 4, 3 * R // 4, n), rng.integers(W // 4, 3 * W // 4, n)],
+                  axis=1).astype(np.int32)
+    ses.sample_pixels(px[:512])  # warm-up
+    ses.forward()
+    ses.composite()
+    t0 = time.perf_counter()
+    ses.sample_pixels(px)
+    ses.forward()
+    ses.composite()
+    dt = time.perf_counter() - t0
+    return {"value": n / dt, "unit": "rays/s", "cores": cores, "kind": "port",
+            "sample": f"oracle render of {n} pixels of the config-4 view's central half (window (1, 1)), "
+                      "sample + field forward + composite"}
+
+
 def run_reference(args):
     """The reference arm: the CPU oracle trainer (restated reference algorithm,
     primitives pinned bit-for-bit to the reference sources) on all host cores,
@@ -404,7 +433,10 @@ def bench_render(args, rank=0, world=1, dev=None):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     dev_ms, wall = float(t[0]), float(t[1])
     total = R * W
-    return {"value": total / (dev_ms / 1e3), "unit": "rays/s",
+    cpu = None
+    if rank == 0 and world == 1 and not getattr(args, "no_cpu", False):
+        cpu = cpu_render_baseline(scene, fc, R, W)
+    return {"value": total / (dev_ms / 1e3), "unit": "rays/s", "cpu_baseline": cpu,
             "e2e": {"value": total / wall, "unit": "rays/s", "h2d_bytes_per_step": total * 8,
                     "d2h_bytes_per_step": total * 20},
             "config": f"cfg4: 4x4-tile ROI (512 m), full {R}x{W} novel view at 0.125 m over {world} GPU(s) "

@@ -8,6 +8,6 @@ import argparse  # noqa: E402
 
 import bench  # noqa: E402
 
-r = bench.bench_render(argparse.Namespace())
+r = bench.bench_render(argparse.Namespace(no_cpu=True))
 print(f"render {r['value'] / 1e6:.2f} M rays/s device, {r['e2e']['value'] / 1e6:.2f} M e2e;",
       {k: round(v, 2) for k, v in r["phases_ms"].items()})
