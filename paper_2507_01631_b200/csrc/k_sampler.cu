@@ -25,7 +25,8 @@
 namespace tfg {
 
 // ------------------------------------------------------------------ scans
-// Three-phase exclusive scan of uint32 (values and sums < 2^32).
+// Two-kernel exclusive scan of uint32 (values and sums < 2^32): block totals,
+// then per-block prefix + apply.
 constexpr int kScanThreads = 512;
 constexpr int kScanItems = 8;
 constexpr int kScanTile = kScanThreads * kScanItems;
@@ -73,34 +74,26 @@ __global__ void __launch_bounds__(kScanThreads) scan_reduce_kernel(const uint32_
     if (threadIdx.x == 0) sums[blockIdx.x] = tot;
 }
 
-__global__ void __launch_bounds__(kScanThreads) scan_sums_kernel(uint32_t* sums, int nb,
-                                                                 uint32_t* grand_total) {
-    pdl_wait();
-    // single block: exclusive scan of up to kScanTile block sums
-    uint32_t v[kScanItems];
-    uint32_t s = 0;
-#pragma unroll
-    for (int k = 0; k < kScanItems; ++k) {
-        int i = threadIdx.x * kScanItems + k;
-        v[k] = i < nb ? sums[i] : 0;
-        s += v[k];
-    }
-    uint32_t tot;
-    uint32_t pre = block_exclusive_scan(s, &tot);
-#pragma unroll
-    for (int k = 0; k < kScanItems; ++k) {
-        int i = threadIdx.x * kScanItems + k;
-        if (i < nb) sums[i] = pre;
-        pre += v[k];
-    }
-    if (threadIdx.x == 0 && grand_total) *grand_total = tot;
-}
-
+// Applies the block prefixes.  Each block sums the raw block totals before
+// it itself (at most kScanTile of them, kScanItems per thread), so there is
+// no separate pass over the block sums; the last block also writes the grand
+// total.
 __global__ void __launch_bounds__(kScanThreads) scan_apply_kernel(const uint32_t* __restrict__ in,
                                                                   uint64_t n,
                                                                   const uint32_t* __restrict__ sums,
-                                                                  uint32_t* __restrict__ out) {
+                                                                  uint32_t* __restrict__ out,
+                                                                  uint32_t* __restrict__ grand_total) {
     pdl_wait();
+    __shared__ uint32_t s_block_pre;
+    {
+        uint32_t acc = 0;
+        for (int j = threadIdx.x; j < int(blockIdx.x); j += blockDim.x) acc += sums[j];
+        uint32_t tot;
+        block_exclusive_scan(acc, &tot);
+        if (threadIdx.x == 0) s_block_pre = tot;
+        __syncthreads();
+    }
+    const uint32_t block_pre = s_block_pre;
     uint64_t base = uint64_t(blockIdx.x) * kScanTile;
     uint32_t v[kScanItems];
     uint32_t s = 0;
@@ -110,14 +103,17 @@ __global__ void __launch_bounds__(kScanThreads) scan_apply_kernel(const uint32_t
         v[k] = i < n ? in[i] : 0;
         s += v[k];
     }
-    uint32_t pre = block_exclusive_scan(s, nullptr) + sums[blockIdx.x];
+    uint32_t pre = block_exclusive_scan(s, nullptr) + block_pre;
 #pragma unroll
     for (int k = 0; k < kScanItems; ++k) {
         uint64_t i = base + uint64_t(threadIdx.x) * kScanItems + k;
         if (i < n) out[i] = pre;
         pre += v[k];
     }
-    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == blockDim.x - 1) out[n] = pre;
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == blockDim.x - 1) {
+        out[n] = pre;
+        if (grand_total) *grand_total = pre;
+    }
 }
 
 int scan_exclusive(const uint32_t* in, uint64_t n, uint32_t* out, uint32_t* block_sums,
@@ -126,9 +122,9 @@ int scan_exclusive(const uint32_t* in, uint64_t n, uint32_t* out, uint32_t* bloc
     if (nb < 1) nb = 1;
     if (nb > kScanTile) return 1;
     launch_pdl(scan_reduce_kernel, dim3(nb), dim3(kScanThreads), 0, st, in, n, block_sums);
-    launch_pdl(scan_sums_kernel, dim3(1), dim3(kScanThreads), 0, st, block_sums, nb, grand_total);
-    launch_pdl(scan_apply_kernel, dim3(nb), dim3(kScanThreads), 0, st, in, n, block_sums, out);
-    if (launches) *launches += 3;
+    launch_pdl(scan_apply_kernel, dim3(nb), dim3(kScanThreads), 0, st, in, n, static_cast<const uint32_t*>(block_sums),
+               out, grand_total);
+    if (launches) *launches += 2;
     return 0;
 }
 
