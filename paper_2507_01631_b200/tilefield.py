@@ -450,10 +450,19 @@ class Context:
         self._rarr = arr
         _check(lib().tfg_render_setup(self.h, ptr(rows), ptr(cols), n, arr, ptr(np.ascontiguousarray(color, np.float32))))
 
-    def render_pixels(self, cam: Rpc, pixels):
+    def render_pixels(self, cam: Rpc, pixels, out=None):
+        """Renders (row, col) pixels of `cam`.  `out` = (rgb[n*3], depth[n],
+        opacity[n]) float32 arrays to fill (reused buffers avoid the page
+        faults of fresh ones); else new arrays are returned."""
         px = np.ascontiguousarray(pixels, np.int32).reshape(-1, 2)
         n = px.shape[0]
-        rgb, dep, op = np.zeros(3 * n, np.float32), np.zeros(n, np.float32), np.zeros(n, np.float32)
+        if out is None:
+            rgb, dep, op = np.empty(3 * n, np.float32), np.empty(n, np.float32), np.empty(n, np.float32)
+        else:
+            rgb, dep, op = out
+            if not all(a.dtype == np.float32 and a.flags.c_contiguous for a in (rgb, dep, op)) or \
+                    rgb.size != 3 * n or dep.size != n or op.size != n:
+                raise ValueError("render_pixels: out must be contiguous float32 arrays of 3n, n, n")
         _check(lib().tfg_render_pixels(self.h, C.byref(cam), ptr(px), n, ptr(rgb), ptr(dep), ptr(op)))
         return rgb.reshape(n, 3), dep, op
 
