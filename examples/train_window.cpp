@@ -36,7 +36,6 @@ int main() {
     try {
         tilefield::gpu::Context ctx(f, t, 0, 4096);
         ctx.set_scene({cam}, {img.data()}, roi, 3, 3);
-        ctx.precompute_rays();  // every pixel ray once; window moves then only check the memo
         uint64_t it = 0;
         for (auto [r, c] : tilefield::gpu::Context::snake_path(3, 3)) {
             ctx.advance(r, c);

@@ -179,13 +179,13 @@ TFG_API int tfg_window_tiles(tfg_ctx* ctx, int32_t* rows4, int32_t* cols4);
 TFG_API int tfg_snake_path(int grid_rows, int grid_cols, int32_t* out_pairs, int* n_out);
 /* Prefetch of the next window position's tiles + crops on the side stream. */
 TFG_API int tfg_prefetch_window(tfg_ctx* ctx, int pos_row, int pos_col);
-/* Optional: solves the ray of every pixel of every view once into the
- * per-pixel memo (the accept pass's FP64 Newton solves, done up front for the
- * whole scene instead of per window move; same results).  Later window
- * positions then run only the memo pass.  Asynchronous on the context. */
-TFG_API int tfg_precompute_rays(tfg_ctx* ctx);
 
-/* Accepted-ray list of the current window: packed
+/* The accept pass solves every candidate pixel's ray once per window position
+ * into a per-window pixel memo (sized by the window's crop union, so HBM is
+ * O(1) in the grid size); pixels the previous position already solved are
+ * copied from its memo instead of re-solved.  The ray draw reads the memo.
+ *
+ * Accepted-ray list of the current window: packed
  * (view << 40) | (row << 20) | col, enumerated view, row, col ascending. */
 TFG_API int tfg_accept_count(tfg_ctx* ctx, uint64_t* n);
 TFG_API int tfg_accept_export(tfg_ctx* ctx, uint64_t* out, uint64_t capacity);

@@ -84,7 +84,6 @@ public:
         return {static_cast<float*>(p), n};
     }
     void optimizer_step(uint64_t iter) { check(tfg_optimizer_step(c_, iter)); }
-    void precompute_rays() { check(tfg_precompute_rays(c_)); }
     // the library's own NCCL communicator: rank 0 calls comm_unique_id() and
     // the host distributes the 128 bytes; then per iteration
     // forward_backward, allreduce_grads, optimizer_step

@@ -50,14 +50,19 @@ __global__ void __launch_bounds__(256) adam_kernel(AdamArgs a, uint64_t total) {
     if (threadIdx.x == 0) {
         int s = 0;
         for (int g = 0; g < a.n_groups; ++g) s |= a.group_flags[g] ? 1 : 0;
-        skip = s;
-        if (s && blockIdx.x == 0) {
+        // an earlier step's non-finite error not yet read by the host: the
+        // reference would have thrown, so no later step is applied either
+        const int pending = a.sticky[0] != 0;
+        skip = s | pending;
+        if (s && !pending && blockIdx.x == 0) {
             for (int g = 0; g < a.n_groups; ++g)
                 if (a.group_flags[g]) {
-                    a.status->nonfinite_group = uint32_t(g);
+                    a.sticky[1] = uint32_t(g);
                     break;
                 }
-            atomicOr(&a.status->bits, kStatusNonFinite);
+            a.sticky[2] = a.seq;
+            __threadfence();
+            a.sticky[0] = 1u;
         }
     }
     __syncthreads();

@@ -25,7 +25,7 @@ __global__ void __launch_bounds__(256) occupancy_kernel(OccArgs a) {
     __syncthreads();
     int v = blockIdx.x * blockDim.x + threadIdx.x;
     float e = a.ema[slot][v];
-    if (a.update) {
+    if (a.update && !(a.sticky && a.sticky[0])) {
         int x = v % kOccRes, y = (v / kOccRes) % kOccRes, z = v / (kOccRes * kOccRes);
         Rng rng(hash_combine(a.base_key[slot], uint64_t(v)));
         float ux = rng.flt(), uy = rng.flt(), uz = rng.flt();

@@ -132,7 +132,8 @@ int scan_exclusive(const uint32_t* in, uint64_t n, uint32_t* out, uint32_t* bloc
 // flag = 1 iff the candidate pixel's ray exists, hits >= 1 tile and every hit
 // tile is loaded.  Two kernels: accept_memo_kernel (one light
 // thread per candidate of the per-view crop-union rects) settles every pixel
-// the scene memo already holds and compacts the rest into a to-do list;
+// the previous window position already solved (copying its memo entry into
+// this window's memo) and compacts the rest into a to-do list;
 // accept_solve_kernel runs the two Newton localisations of each listed pixel
 // on a lane pair, so no warp carries memo-hit lanes through a solve.
 #ifndef TFG_ACCEPT_MINB
@@ -162,12 +163,26 @@ __global__ void __launch_bounds__(256) accept_memo_kernel(AcceptArgs a, uint32_t
             if (r[0] < r[1] && row >= r[0] && row < r[1] && col >= r[2] && col < r[3]) in = true;
         }
         uint32_t info = 0;
-        if (in && a.pix_info)
-            info = a.pix_info[a.pix_off[v] + uint64_t(row) * uint64_t(a.cams[v].image_cols) + uint64_t(col)];
+        if (in && a.o_info) {
+            // solved for the previous window position: copy its memo entry
+            const int* o = a.o_rect + 4 * v;  // r0, c0, cols, rows
+            if (row >= o[0] && row < o[0] + o[3] && col >= o[1] && col < o[1] + o[2]) {
+                const uint64_t oi = a.o_off[v] / 3 + uint64_t(row - o[0]) * uint64_t(o[2]) + uint64_t(col - o[1]);
+                info = a.o_info[oi];
+                if (info & kMemoHit) {
+                    const double2* src = reinterpret_cast<const double2*>(a.o_rays + 6 * oi);
+                    double2* dst = reinterpret_cast<double2*>(a.m_rays + 6 * idx);
+                    dst[0] = src[0];
+                    dst[1] = src[1];
+                    dst[2] = src[2];
+                }
+            }
+        }
+        a.m_info[idx] = info;
         if (in && !(info & kMemoDone)) {
             todo = true;
         } else {
-            // outside every loaded crop, or solved for an earlier window:
+            // outside every loaded crop, or solved for the previous window:
             // only the window test remains
             uint32_t ok = 0;
             if (info & kMemoHit) {
@@ -197,8 +212,6 @@ __global__ void __launch_bounds__(128, TFG_ACCEPT_MINB) accept_solve_kernel(Acce
         const uint64_t idx = a.todo[j];
         int v, row, col;
         candidate_pixel(a, idx, &v, &row, &col);
-        uint64_t pidx = 0;
-        if (a.pix_info) pidx = a.pix_off[v] + uint64_t(row) * uint64_t(a.cams[v].image_cols) + uint64_t(col);
         uint32_t ok = 0;
         double gx = 0.0, gy = 0.0;
         int st = rpc_localize(a.cams[v], double(row), double(col), hi ? a.z_min : a.z_max, &gx, &gy);
@@ -251,10 +264,10 @@ __global__ void __launch_bounds__(128, TFG_ACCEPT_MINB) accept_solve_kernel(Acce
                             all_loaded &= ld;
                         }
                     ok = (hits >= 1 && all_loaded) ? 1u : 0u;
-                    if (hits >= 1 && a.pix_info) {
+                    if (hits >= 1) {
                         memo |= kMemoHit | uint32_t(hr0) | (uint32_t(hr1) << 7) | (uint32_t(hc0) << 14) |
                                 (uint32_t(hc1) << 21);
-                        double* pr = a.pix_rays + 6 * pidx;
+                        double* pr = a.m_rays + 6 * idx;
                         pr[0] = o[0];
                         pr[1] = o[1];
                         pr[2] = o[2];
@@ -266,7 +279,7 @@ __global__ void __launch_bounds__(128, TFG_ACCEPT_MINB) accept_solve_kernel(Acce
             }
         }
         if (hi == 0) {
-            if (a.pix_info) a.pix_info[pidx] = memo;
+            a.m_info[idx] = memo;
             flags[idx] = ok;
         }
     }
@@ -378,8 +391,10 @@ __global__ void __launch_bounds__(128, kSolve ? TFG_RAYGEN_MINB : TFG_RAYGEN_MEM
         row = int((e >> 20) & 0xFFFFF);
         col = int(e & 0xFFFFF);
         if (na == 0 && valid && hi == 0) atomicOr(&status->bits, kStatusRayFail);
-        if (na && a.pix_rays)
-            memo = a.pix_rays + 6 * (a.pix_off[v] + uint64_t(row) * uint64_t(a.cams[v].image_cols) + uint64_t(col));
+        if (na && a.memo_rays) {
+            const int* cr = a.crop_rect + 4 * v;  // r0, c0, cols, rows: memo index = crop pixel index
+            memo = a.memo_rays + 6 * (a.crop_offset[v] / 3 + uint64_t(row - cr[0]) * uint64_t(cr[2]) + uint64_t(col - cr[1]));
+        }
     }
     RayRec R;
     R.view = v;
@@ -644,10 +659,6 @@ int launch_accept(const AcceptArgs& args, uint32_t* flags, uint32_t* pos, uint32
     // past its end leave at once): measured faster than a persistent grid
     uint64_t solve_blocks = (2 * a.n_candidates + 127) / 128;
     accept_solve_kernel<<<int(solve_blocks), 128, 0, st>>>(a, flags);
-    if (!out) {  // memo fill only (tfg_precompute_rays): no accepted list
-        *launches += 2;
-        return 0;
-    }
     if (scan_exclusive(flags, a.n_candidates, pos, block_sums, n_out, st, launches)) return 1;
     accept_scatter_kernel<<<nb, 128, 0, st>>>(a, flags, pos, out);
     *launches += 3;
@@ -658,7 +669,7 @@ int launch_sampler(const RaygenArgs& a, RayRec* rays, float4* venc, uint32_t* co
                    uint32_t* P, uint32_t* block_sums, TileDesc* tiles, int max_tiles,
                    SampleArrays out, uint64_t capacity, Status* status, cudaStream_t st,
                    uint64_t* launches) {
-    if (!a.pixels && a.pix_rays)
+    if (!a.pixels && a.memo_rays)
         launch_pdl(raygen_kernel<false>, dim3((2 * a.n_rays + 127) / 128), dim3(128), 0, st, a, rays, venc, counts,
                    status);
     else

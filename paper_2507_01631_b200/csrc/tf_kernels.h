@@ -38,12 +38,20 @@ struct AcceptArgs {
     int loaded_tile[kTrainSlots];
     int n_loaded;
     double z_min, z_max;
-    // Per-pixel memo of the scene (null: off).  The RPC inversion and the
-    // tile-incidence test of a pixel depend only on the scene, so each pixel
-    // is solved once: info = done | hit | bbox of the hit tiles, rays = o[3], d[3].
-    uint32_t* pix_info;
-    double* pix_rays;
-    const uint64_t* pix_off;     // first pixel of each view
+    // Per-window pixel memo (indexed like the candidates: view_start[v] +
+    // (row - r0) * ncols + (col - c0) over the union rect).  The RPC inversion
+    // and the tile-incidence test of a pixel depend only on the scene, so a
+    // pixel solved for the previous window position is copied, not re-solved:
+    // info = done | hit | bbox of the hit tiles, rays = o[3], d[3].  Bounded by
+    // the window's crop union (O(1) in the grid size).
+    uint32_t* m_info;
+    double* m_rays;
+    // the previous window's memo (null: none / reuse off), its union rects
+    // (r0, c0, cols, rows per view) and crop byte offsets (pixel offset x 3)
+    const uint32_t* o_info;
+    const double* o_rays;
+    const int* o_rect;
+    const uint64_t* o_off;
     int win_r0, win_r1, win_c0, win_c1;  // the loaded tiles' rectangle (inclusive)
     // pixels the memo does not settle: candidate indices + their count
     // (the list lives in the scan's output buffer, which is free until the scan)
@@ -57,8 +65,7 @@ struct RaygenArgs {
     const tfg_rpc* cams;
     const uint64_t* accept;  // draw mode: accepted list
     const uint32_t* n_accept_dev;  // its length, read on device (no host sync per move)
-    const double* pix_rays;  // draw mode: per-pixel ray memo of the accept pass (K0)
-    const uint64_t* pix_off;
+    const double* memo_rays;  // draw mode: the window's pixel-ray memo (accept pass), indexed like the crop pixels
     const int32_t* pixels;   // pixel mode (render/eval): view,row,col triplets
     int pixel_pairs;         // ... or (row, col) pairs of view 0 (the render camera)
     const uint8_t* crop_bytes;
@@ -124,7 +131,11 @@ struct AdamArgs {
     int n_groups;
     float beta1, beta2, omb1, omb2, eps;
     uint32_t* group_flags;  // non-finite flag per group
-    Status* status;
+    // sticky non-finite record {flag, group, seq}: not cleared by the next
+    // batch, so a skipped step stays visible (and later steps stay skipped,
+    // like the reference's throw) until the host reads it
+    uint32_t* sticky;
+    uint32_t seq;           // host sequence number of this optimizer step
 };
 
 struct OccArgs {
@@ -138,6 +149,7 @@ struct OccArgs {
     int n;
     float decay, threshold, density_max;
     int update;  // 0: only recompute bits from the EMA
+    const uint32_t* sticky;  // non-null: skip the EMA update after a skipped (non-finite) Adam step
 };
 
 int scan_exclusive(const uint32_t* in, uint64_t n, uint32_t* out, uint32_t* block_sums,

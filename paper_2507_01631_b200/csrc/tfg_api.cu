@@ -300,6 +300,7 @@ int run_occupancy(tfg_ctx* c, bool update, uint64_t* keys) {
     o.threshold = c->fc.occupancy_threshold;
     o.density_max = c->fc.density_max;
     o.update = update ? 1 : 0;
+    o.sticky = c->d_sticky;
     launch_occupancy(o, c->st, &c->launches);
     CK(cudaGetLastError());
     return 0;
@@ -384,16 +385,22 @@ int stage_window(tfg_ctx* c, WinBuf& w, int pr, int pc, cudaStream_t st) {
             c1 = std::max(c1, ti % c->cols);
         }
         bool rect = !want.empty() && int(want.size()) == (r1 - r0 + 1) * (c1 - c0 + 1);
-        if (rect && c->d_pix_info) {
-            a.pix_info = c->d_pix_info;
-            a.pix_rays = c->d_pix_rays;
-            a.pix_off = c->d_pix_off;
-            a.win_r0 = r0;
-            a.win_r1 = r1;
-            a.win_c0 = c0;
-            a.win_c1 = c1;
+        a.win_r0 = r0;
+        a.win_r1 = r1;
+        a.win_c0 = c0;
+        a.win_c1 = c1;
+        // the other window buffer holds the previous position (staged earlier
+        // on the same side stream): its solved pixels are copied, not re-solved
+        const WinBuf& o = (&w == &c->win[0]) ? c->win[1] : c->win[0];
+        if (rect && c->memo_reuse && o.pos_r >= 0) {
+            a.o_info = o.d_minfo;
+            a.o_rays = o.d_mrays;
+            a.o_rect = o.d_crop_rect;
+            a.o_off = o.d_crop_off;
         }
     }
+    a.m_info = w.d_minfo;
+    a.m_rays = w.d_mrays;
     a.todo_n = c->d_todo_n;
     a.sms = c->sms;
     if (launch_accept(a, c->d_flags, c->d_pos, c->d_acc_sums, w.d_n, w.d_accept, st, &c->launches))
@@ -424,26 +431,57 @@ int check_status(tfg_ctx* c) {
         return fail(TFG_ERR_INVALID,
                     "sample: ray generation failed (ray_from_pixel threw for a drawn pixel, or the "
                     "window's accepted-ray list is empty)");
-    if (s.bits & kStatusNonFinite) {
-        int g = int(s.nonfinite_group);
-        char nm[96];
-        if (g >= 2 * c->nslots) {
-            std::snprintf(nm, sizeof nm, "color");
-        } else {
-            int ti = c->slot_tile[g / 2];
-            std::snprintf(nm, sizeof nm, "tile(%d,%d).%s", ti / c->cols, ti % c->cols,
-                          (g % 2) ? "dnet" : "enc");
-        }
-        return fail(TFG_ERR_NONFINITE,
-                    std::string("adam_step: non-finite gradient in group ") + nm);
+    if (!c->nonfinite_pending.empty()) {
+        std::string m = c->nonfinite_pending;
+        c->nonfinite_pending.clear();
+        return fail(TFG_ERR_NONFINITE, m);
     }
     return 0;
 }
 
-int sync_status(tfg_ctx* c) {
-    c->d2h_bytes += sizeof(Status);
-    CK(cudaMemcpyAsync(c->h_status, c->d_status, sizeof(Status), cudaMemcpyDeviceToHost, c->st));
+// Consumes the sticky non-finite record once (host copy already taken): the
+// step-count increments of the failed optimizer step and of every later one
+// (skipped on the device as well) are rolled back, the group is named, and
+// the record is cleared on the device.
+void consume_sticky(tfg_ctx* c) {
+    const uint32_t* k = c->h_sticky;
+    if (k[0]) {
+        const uint32_t g = k[1], seq = k[2];
+        char nm[96];
+        std::snprintf(nm, sizeof nm, "color");
+        for (auto it = c->unverified.rbegin(); it != c->unverified.rend(); ++it) {
+            if (int32_t(it->seq - seq) < 0) break;
+            for (int s = 0; s < it->nslots; ++s) {
+                TileHost& th = c->tiles[it->tile[s]];
+                --th.enc_step;
+                --th.dnet_step;
+            }
+            --c->color_step;
+            if (it->seq == seq && int(g) < 2 * it->nslots) {
+                int ti = it->tile[g / 2];
+                std::snprintf(nm, sizeof nm, "tile(%d,%d).%s", ti / c->cols, ti % c->cols, (g % 2) ? "dnet" : "enc");
+            }
+        }
+        c->nonfinite_pending = std::string("adam_step: non-finite gradient in group ") + nm;
+        cudaMemsetAsync(c->d_sticky, 0, 16, c->st);
+    }
+    c->unverified.clear();
+}
+
+// Reads the sticky record (synchronises) and settles the unverified steps.
+int settle_steps(tfg_ctx* c) {
+    CK(cudaMemcpyAsync(c->h_sticky, c->d_sticky, 16, cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
+    consume_sticky(c);
+    return 0;
+}
+
+int sync_status(tfg_ctx* c) {
+    c->d2h_bytes += sizeof(Status) + 16;
+    CK(cudaMemcpyAsync(c->h_status, c->d_status, sizeof(Status), cudaMemcpyDeviceToHost, c->st));
+    CK(cudaMemcpyAsync(c->h_sticky, c->d_sticky, 16, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    consume_sticky(c);
     return check_status(c);
 }
 
@@ -706,6 +744,7 @@ TFG_API int tfg_create(const tfg_field_config* fcfg, const tfg_train_config* tcf
         rc |= dalloc(c, &c->d_ema, uint64_t(kTrainSlots) * kOccVox);
         rc |= dalloc(c, &c->d_bits, uint64_t(kMaxSlots) * kOccWords);
         rc |= dalloc(c, &c->d_group_flags, 16);
+        rc |= dalloc(c, &c->d_sticky, 4);
         rc |= dalloc(c, &c->d_status, 1);
         rc |= dalloc(c, &c->d_rays, max_rays);
         rc |= dalloc(c, &c->d_venc, uint64_t(max_rays) * 6);
@@ -727,6 +766,8 @@ TFG_API int tfg_create(const tfg_field_config* fcfg, const tfg_train_config* tcf
         rc |= dalloc(c, &c->d_rcam, 1);
         if (rc) return TFG_ERR_CUDA;
         CK(cudaHostAlloc(reinterpret_cast<void**>(&c->h_status), sizeof(Status), cudaHostAllocDefault));
+        CK(cudaHostAlloc(reinterpret_cast<void**>(&c->h_sticky), 16, cudaHostAllocDefault));
+        CK(cudaMemsetAsync(c->d_sticky, 0, 16, c->st));
         CK(cudaMemsetAsync(c->d_params, 0, c->n_params * 4, c->st));
         CK(cudaMemsetAsync(c->d_m, 0, c->n_params * 4, c->st));
         CK(cudaMemsetAsync(c->d_v, 0, c->n_params * 4, c->st));
@@ -757,13 +798,13 @@ TFG_API int tfg_destroy(tfg_ctx* c) {
     cudaSetDevice(c->device);
     cudaDeviceSynchronize();
     comm_release(c);
-    void* dev[] = {c->d_params, c->d_grads, c->d_m, c->d_v, c->d_ema, c->d_bits, c->d_group_flags,
+    void* dev[] = {c->d_params, c->d_grads, c->d_m, c->d_v, c->d_ema, c->d_bits, c->d_group_flags, c->d_sticky,
                    c->d_status, c->d_cams, c->d_east, c->d_north, c->d_flags, c->d_pos,
                    c->d_block_sums, c->d_acc_sums, c->d_todo_n, c->d_view_start, c->d_union, c->d_crop4,
                    c->d_rays, c->d_venc,
                    c->d_counts, c->d_P, c->d_tiles, c->s.local, c->s.td, c->s.endpoint, c->s.io,
                    c->d_ray_out, c->d_pixels, c->d_rparams, c->d_rbits, c->d_rcolor, c->d_rcam,
-                   c->d_feat, c->d_tile_rays, c->d_export, c->d_pix_info, c->d_pix_rays, c->d_pix_off,
+                   c->d_feat, c->d_tile_rays, c->d_export,
                    c->d_stage_in, c->d_stage_out, c->d_loss_parts};
     for (void* p : dev)
         if (p) cudaFree(p);
@@ -772,12 +813,13 @@ TFG_API int tfg_destroy(tfg_ctx* c) {
     for (auto* im : c->h_images)
         if (im) cudaFreeHost(im);
     if (c->h_status) cudaFreeHost(c->h_status);
+    if (c->h_sticky) cudaFreeHost(c->h_sticky);
     for (void* p : {static_cast<void*>(c->h_rpix), static_cast<void*>(c->h_rout), static_cast<void*>(c->h_rstat)})
         if (p) cudaFreeHost(p);
     for (cudaEvent_t e : c->ev_rdone)
         if (e) cudaEventDestroy(e);
     for (WinBuf& w : c->win) {
-        void* wo[] = {w.d_crops, w.d_crop_rect, w.d_crop_off, w.d_accept, w.d_n};
+        void* wo[] = {w.d_crops, w.d_crop_rect, w.d_crop_off, w.d_accept, w.d_n, w.d_minfo, w.d_mrays};
         for (void* p : wo)
             if (p) cudaFree(p);
         if (w.ready) cudaEventDestroy(w.ready);
@@ -872,22 +914,35 @@ TFG_API int tfg_set_scene(tfg_ctx* c, const tfg_rpc* cams, int n_views,
     c->accept_cap = cand;
     c->crop_cap = cropb;
     int rc = 0;
-    void* olds[] = {c->d_cams, c->d_east, c->d_north, c->d_flags, c->d_pos, c->d_view_start,
-                    c->d_union, c->d_crop4, c->d_pix_info, c->d_pix_rays, c->d_pix_off};
-    for (void* p : olds)
-        if (p) cudaFree(p);
+    dfree(c, c->d_cams);
+    dfree(c, c->d_east);
+    dfree(c, c->d_north);
+    dfree(c, c->d_flags);
+    dfree(c, c->d_pos);
+    dfree(c, c->d_view_start);
+    dfree(c, c->d_union);
+    dfree(c, c->d_crop4);
     rc |= dalloc(c, &c->d_cams, n_views);
     rc |= dalloc(c, &c->d_east, grid_cols + 1);
     rc |= dalloc(c, &c->d_north, grid_rows + 1);
+    // per window buffer: crops, accepted list and the pixel memo of the crop
+    // union (52 B per candidate pixel), all sized by the largest window union
+    // over the positions: independent of the ROI / grid size
     for (WinBuf& w : c->win) {
-        void* wo[] = {w.d_crops, w.d_crop_rect, w.d_crop_off, w.d_accept, w.d_n};
-        for (void* p : wo)
-            if (p) cudaFree(p);
+        dfree(c, w.d_crops);
+        dfree(c, w.d_crop_rect);
+        dfree(c, w.d_crop_off);
+        dfree(c, w.d_accept);
+        dfree(c, w.d_n);
+        dfree(c, w.d_minfo);
+        dfree(c, w.d_mrays);
         rc |= dalloc(c, &w.d_crops, c->crop_cap);
         rc |= dalloc(c, &w.d_crop_rect, 4 * n_views);
         rc |= dalloc(c, &w.d_crop_off, n_views);
         rc |= dalloc(c, &w.d_accept, c->accept_cap);
         rc |= dalloc(c, &w.d_n, 1);
+        rc |= dalloc(c, &w.d_minfo, c->cand_cap);
+        rc |= dalloc(c, &w.d_mrays, 6 * c->cand_cap);
         if (!w.ready) CK(cudaEventCreateWithFlags(&w.ready, cudaEventDisableTiming));
         w.pos_r = w.pos_c = -1;
     }
@@ -897,40 +952,10 @@ TFG_API int tfg_set_scene(tfg_ctx* c, const tfg_rpc* cams, int n_views,
     rc |= dalloc(c, &c->d_union, 4 * n_views);
     rc |= dalloc(c, &c->d_crop4, 4 * n_views * kTrainSlots);
     if (rc) return TFG_ERR_CUDA;
-    // per-pixel memo (52 B per image pixel, e.g. 2.3 GB for config 5): sized
-    // for HBM; skipped (pixels re-solved per window) if it does not fit
-    c->d_pix_info = nullptr;
-    c->d_pix_rays = nullptr;
-    c->d_pix_off = nullptr;
-    c->pix_total = 0;
     {
-        std::vector<uint64_t> off(n_views);
-        uint64_t tot = 0;
-        for (int v = 0; v < n_views; ++v) {
-            off[v] = tot;
-            tot += uint64_t(cams[v].image_rows) * uint64_t(cams[v].image_cols);
-        }
-        size_t fr = 0, total = 0;
-        cudaMemGetInfo(&fr, &total);
-        const char* off_env = std::getenv("TFG_NO_PIXEL_MEMO");  // A/B + the memo-off parity test
-        bool fits = grid_rows <= 128 && grid_cols <= 128 && tot * 52 + (size_t(4) << 30) < fr &&
-                    !(off_env && off_env[0] == '1');
-        if (fits && cudaMalloc(&c->d_pix_info, tot * 4) == cudaSuccess &&
-            cudaMalloc(&c->d_pix_rays, tot * 48) == cudaSuccess &&
-            cudaMalloc(&c->d_pix_off, n_views * 8) == cudaSuccess) {
-            c->pix_total = tot;
-            CK(cudaMemsetAsync(c->d_pix_info, 0, tot * 4, c->st));
-            CK(cudaMemcpyAsync(c->d_pix_off, off.data(), n_views * 8, cudaMemcpyHostToDevice, c->st));
-            CK(cudaStreamSynchronize(c->st));
-        } else {
-            cudaGetLastError();
-            for (void* p : {static_cast<void*>(c->d_pix_info), static_cast<void*>(c->d_pix_rays),
-                            static_cast<void*>(c->d_pix_off)})
-                if (p) cudaFree(p);
-            c->d_pix_info = nullptr;
-            c->d_pix_rays = nullptr;
-            c->d_pix_off = nullptr;
-        }
+        const char* off_env = std::getenv("TFG_NO_MEMO_REUSE");  // A/B + the reuse-off parity test
+        // the memo's hit-tile bbox has 7 bits per coordinate
+        c->memo_reuse = grid_rows <= 128 && grid_cols <= 128 && !(off_env && off_env[0] == '1');
     }
     CK(cudaMemcpyAsync(c->d_cams, c->cams.data(), n_views * sizeof(tfg_rpc), cudaMemcpyHostToDevice, c->st));
     CK(cudaMemcpyAsync(c->d_east, c->east.data(), (grid_cols + 1) * 8, cudaMemcpyHostToDevice, c->st));
@@ -1088,64 +1113,6 @@ TFG_API int tfg_set_window(tfg_ctx* c, int pr, int pc) {
     return 0;
 }
 
-// Solves the ray of every pixel of every view once into the per-pixel memo
-// (the same kernels as the accept pass, over whole views in row bands that
-// fit the candidate buffers, with no tile loaded so no list is built).  Each
-// later window position then only runs the memo pass.  Runs on the side
-// stream, ordered with window staging; the main stream waits for it.
-TFG_API int tfg_precompute_rays(tfg_ctx* c) {
-    if (!c || c->n_views == 0) return fail(TFG_ERR_STATE, "precompute_rays: call set_scene first");
-    if (!c->d_pix_info) return 0;  // memo off (TFG_NO_PIXEL_MEMO): nothing to fill
-    CK(cudaSetDevice(c->device));
-    cudaStream_t st = c->side;
-    CK(cudaEventRecord(c->ev_main, c->st));
-    CK(cudaStreamWaitEvent(st, c->ev_main, 0));
-    for (int v = 0; v < c->n_views; ++v) {
-        const int rows = c->cams[v].image_rows, cols = c->cams[v].image_cols;
-        if (uint64_t(cols) > c->cand_cap) return fail(TFG_ERR_INVALID, "precompute_rays: view wider than the candidate buffers");
-        const int band = int(std::max<uint64_t>(1, std::min<uint64_t>(uint64_t(rows), c->cand_cap / uint64_t(cols))));
-        for (int r0 = 0; r0 < rows; r0 += band) {
-            const int r1 = std::min(rows, r0 + band);
-            const uint64_t vs = 0;
-            int urect[4] = {r0, r1, 0, cols};
-            std::vector<int> crect(4 * kTrainSlots, 0);
-            crect[0] = r0, crect[1] = r1, crect[2] = 0, crect[3] = cols;  // slot 0: the band; others empty
-            // pageable copies are staged before the call returns
-            CK(cudaMemcpyAsync(c->d_view_start, &vs, 8, cudaMemcpyHostToDevice, st));
-            CK(cudaMemcpyAsync(c->d_union, urect, 16, cudaMemcpyHostToDevice, st));
-            CK(cudaMemcpyAsync(c->d_crop4, crect.data(), crect.size() * 4, cudaMemcpyHostToDevice, st));
-            AcceptArgs a{};
-            a.cams = c->d_cams + v;
-            a.n_views = 1;
-            a.view_start = c->d_view_start;
-            a.union_rect = c->d_union;
-            a.crop_rect = c->d_crop4;
-            a.n_candidates = uint64_t(r1 - r0) * uint64_t(cols);
-            a.east = c->d_east;
-            a.north = c->d_north;
-            a.grid_rows = c->rows;
-            a.grid_cols = c->cols;
-            for (int k = 0; k < kTrainSlots; ++k) a.loaded_tile[k] = -1;
-            a.n_loaded = 1;
-            a.z_min = c->roi.z_min;
-            a.z_max = c->roi.z_max;
-            a.pix_info = c->d_pix_info;
-            a.pix_rays = c->d_pix_rays;
-            a.pix_off = c->d_pix_off + v;
-            a.win_r0 = a.win_c0 = 1;  // no window: nothing is accepted
-            a.win_r1 = a.win_c1 = 0;
-            a.todo_n = c->d_todo_n;
-            a.sms = c->sms;
-            if (launch_accept(a, c->d_flags, c->d_pos, c->d_acc_sums, nullptr, nullptr, st, &c->launches))
-                return fail(TFG_ERR_INVALID, "precompute_rays: launch failed");
-            CK(cudaGetLastError());
-        }
-    }
-    CK(cudaEventRecord(c->ev_side, st));
-    CK(cudaStreamWaitEvent(c->st, c->ev_side, 0));
-    return 0;
-}
-
 // Stages the next window position (crops + accepted-ray list) into the back
 // buffer on the side stream while the current position trains; the entering
 // tiles' host records are materialised by the init pool.
@@ -1212,8 +1179,7 @@ TFG_API int tfg_sample(tfg_ctx* c, uint64_t iter, uint64_t ray_begin, int n_rays
     RaygenArgs a = base_raygen(c);
     a.accept = c->win[c->front].d_accept;
     a.n_accept_dev = c->win[c->front].d_n;
-    a.pix_rays = c->d_pix_rays;
-    a.pix_off = c->d_pix_off;
+    a.memo_rays = c->win[c->front].d_mrays;
     a.iter = iter;
     a.ray_begin = ray_begin;
     a.n_rays = n_rays;
@@ -1274,7 +1240,21 @@ TFG_API int tfg_optimizer_step(tfg_ctx* c, uint64_t iter) {
     a.omb2 = 1.0f - t.beta2;
     a.eps = t.eps;
     a.group_flags = c->d_group_flags;
-    a.status = c->d_status;
+    a.sticky = c->d_sticky;
+    // bound the host's list of unverified steps (callers that never read the
+    // status): settle it every 4096 steps
+    if (c->unverified.size() >= 4096) {
+        int rc = settle_steps(c);
+        if (rc) return rc;
+    }
+    a.seq = ++c->step_seq;
+    {
+        tfg_ctx::StepRec r{};
+        r.seq = a.seq;
+        r.nslots = c->nslots;
+        for (int k = 0; k < c->nslots; ++k) r.tile[k] = c->slot_tile[k];
+        c->unverified.push_back(r);
+    }
     auto group = [&](AdamGroup& G, uint64_t off, uint64_t cnt, double base, uint64_t& step) {
         uint64_t s = ++step;
         G.offset = off;
@@ -1330,17 +1310,8 @@ TFG_API int tfg_optimizer_step(tfg_ctx* c, uint64_t iter) {
 
 TFG_API int tfg_read_loss(tfg_ctx* c, float* loss) {
     if (!c) return fail(TFG_ERR_INVALID, "read_loss: null context");
-    int rc = sync_status(c);
+    int rc = sync_status(c);  // rolls back the step counts of skipped (non-finite) steps, once
     if (loss) *loss = float(c->h_status->loss / (3.0 * double(c->tc.batch_rays)));
-    if (rc == TFG_ERR_NONFINITE) {
-        // the step was not applied: roll back the step counters
-        for (int k = 0; k < c->nslots; ++k) {
-            TileHost& th = c->tiles[c->slot_tile[k]];
-            --th.enc_step;
-            --th.dnet_step;
-        }
-        --c->color_step;
-    }
     return rc;
 }
 
@@ -1487,7 +1458,7 @@ TFG_API int tfg_get_grads(tfg_ctx* c, int slot, float* enc, float* dnet, float* 
 
 TFG_API int tfg_get_tile_state(tfg_ctx* c, int slot, tfg_tile_state* o) {
     if (!c || slot < 0 || slot >= c->nslots) return fail(TFG_ERR_INVALID, "get_tile_state: bad slot");
-    CK(cudaStreamSynchronize(c->st));
+    if (settle_steps(c)) return TFG_ERR_CUDA;  // step counts of skipped steps rolled back
     CK(cudaStreamSynchronize(c->side));
     uint64_t off = uint64_t(slot) * c->stride;
     uint64_t dn = c->stride - c->enc_n;
@@ -1526,7 +1497,8 @@ TFG_API int tfg_set_tile_state(tfg_ctx* c, int slot, const tfg_tile_state* in) {
 }
 
 TFG_API int tfg_get_color(tfg_ctx* c, float* p, float* m, float* v, uint64_t* step) {
-    CK(cudaStreamSynchronize(c->st));
+    if (!c) return fail(TFG_ERR_INVALID, "get_color: null context");
+    if (settle_steps(c)) return TFG_ERR_CUDA;
     uint64_t n = c->n_params - c->color_off;
     if (p) CK(cudaMemcpy(p, c->d_params + c->color_off, n * 4, cudaMemcpyDeviceToHost));
     if (m) CK(cudaMemcpy(m, c->d_m + c->color_off, n * 4, cudaMemcpyDeviceToHost));
@@ -1569,7 +1541,8 @@ TFG_API int tfg_get_memory_report(tfg_ctx* c, tfg_memory_report* o) {
     o->optimizer_moments = 2 * kTrainSlots * c->stride * 4 + kTrainSlots * c->stride * 4;  // m, v, grads
     o->occupancy = uint64_t(kTrainSlots) * kOccVox * 4 + uint64_t(kMaxSlots) * kOccWords * 4;
     o->crops = 2 * c->crop_cap;
-    o->accept_list = 2 * c->accept_cap * 8 + c->cand_cap * 8 + c->pix_total * (4 + 48);  // lists + pixel memo
+    // accepted lists + the two window pixel memos + the build scratch
+    o->accept_list = 2 * c->accept_cap * 8 + 2 * c->cand_cap * (4 + 48) + c->cand_cap * 8;
     o->batch_buffers = uint64_t(c->max_rays) * (sizeof(RayRec) + 96 + 8 * kMaxSlots + 20 + 12) +
                        c->sample_cap * (16 + 8 + 1 + 16);
     o->color_net = (c->n_params - c->color_off) * 4;

@@ -15,6 +15,7 @@
 #include <memory>
 #include <string>
 #include <thread>
+#include <unordered_map>
 #include <vector>
 
 #include "tf_common.cuh"
@@ -63,6 +64,10 @@ struct WinBuf {
     uint64_t* d_crop_off = nullptr;  // byte offset of each view's crop
     uint64_t* d_accept = nullptr;    // packed (view, row, col)
     uint32_t* d_n = nullptr;         // accepted count (read by the ray draw on device)
+    // pixel memo of this window's crop union (indexed like the crop pixels):
+    // state (done | hit | hit-tile bbox) and the FP64 ray o[3], d[3]
+    uint32_t* d_minfo = nullptr;
+    double* d_mrays = nullptr;
     std::vector<int> h_crop_rect;
     std::vector<uint64_t> h_crop_off;
     int pos_r = -1, pos_c = -1;
@@ -106,6 +111,19 @@ struct tfg_ctx {
     Status* d_status = nullptr;
     Status* h_status = nullptr;
     uint64_t color_step = 0;
+    // Optimizer steps whose Adam status the host has not read yet: their
+    // step-count increments are rolled back (once) if the device reports a
+    // non-finite gradient at or before them (sticky record {flag, group, seq}).
+    struct StepRec {
+        uint32_t seq;
+        int tile[kTrainSlots];
+        int nslots;
+    };
+    std::vector<StepRec> unverified;
+    uint32_t step_seq = 0;
+    uint32_t* d_sticky = nullptr;
+    uint32_t* h_sticky = nullptr;  // pinned, 4 words
+    std::string nonfinite_pending;  // message of a consumed record, raised by the next status check
 
     // scene
     int n_views = 0;
@@ -142,12 +160,8 @@ struct tfg_ctx {
     // accepted-list build scratch (one build at a time)
     uint32_t *d_flags = nullptr, *d_pos = nullptr, *d_block_sums = nullptr, *d_acc_sums = nullptr;
     uint32_t* d_todo_n = nullptr;  // accept: count of pixels the memo does not settle
-    // per-pixel memo of the scene (AcceptArgs): state, rays, view offsets
-    uint32_t* d_pix_info = nullptr;
-    double* d_pix_rays = nullptr;
-    uint64_t* d_pix_off = nullptr;
-    uint64_t pix_total = 0;
     uint64_t* d_view_start = nullptr;
+    bool memo_reuse = true;  // copy pixels solved for the previous window (TFG_NO_MEMO_REUSE=1: off)
     int *d_union = nullptr, *d_crop4 = nullptr;
 
     // batch
@@ -181,6 +195,7 @@ struct tfg_ctx {
     tfg_rpc* d_rcam = nullptr;
 
     uint64_t bytes_total = 0;
+    std::unordered_map<void*, uint64_t> alloc_bytes;  // device allocations (memory_report)
     uint64_t h2d_bytes = 0, d2h_bytes = 0;
     float* h_records = nullptr;  // one pinned block for every tile record
     InitPool init;
@@ -197,12 +212,26 @@ struct tfg_ctx {
 namespace tfg {
 namespace host {
 
+// Every device buffer of a context goes through dalloc/dfree, so
+// memory_report's total_device is the live HBM footprint.
 template <typename T>
 int dalloc(tfg_ctx* c, T** p, uint64_t n) {
     if (n == 0) n = 1;
     CK(cudaMalloc(reinterpret_cast<void**>(p), n * sizeof(T)));
     c->bytes_total += n * sizeof(T);
+    c->alloc_bytes[*p] = n * sizeof(T);
     return 0;
+}
+template <typename T>
+void dfree(tfg_ctx* c, T*& p) {
+    if (!p) return;
+    auto it = c->alloc_bytes.find(static_cast<void*>(p));
+    if (it != c->alloc_bytes.end()) {
+        c->bytes_total -= it->second;
+        c->alloc_bytes.erase(it);
+    }
+    cudaFree(static_cast<void*>(p));
+    p = nullptr;
 }
 
 // shared helpers (defined in tfg_api.cu)
@@ -211,6 +240,7 @@ bool crop_for_tile(const tfg_rpc& cam, const double* box, int margin, Crop* out)
 std::vector<int> window_tiles(const tfg_ctx* c, int pr, int pc);
 int ensure_record(tfg_ctx* c, int ti);
 int slot_copy(tfg_ctx* c, int slot, int ti, bool to_host);
+int settle_steps(tfg_ctx* c);
 
 } // namespace host
 } // namespace tfg

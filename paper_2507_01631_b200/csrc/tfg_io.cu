@@ -63,7 +63,17 @@ int read_ckpt_header(std::ifstream& f, const char* path, uint32_t kind, const tf
     return 0;
 }
 
+// The payload must be exactly the arrays the header announces: checked
+// against the file size before anything is read into caller buffers.
 int read_arrays(std::ifstream& f, const char* path, float* const* arrays, const uint64_t* counts, int n) {
+    const std::streamoff here = f.tellg();
+    f.seekg(0, std::ios::end);
+    const std::streamoff end = f.tellg();
+    f.seekg(here, std::ios::beg);
+    uint64_t need = 0;
+    for (int i = 0; i < n; ++i) need += counts[i] * 4;
+    if (here < 0 || end < here || uint64_t(end - here) != need)
+        return fail(TFG_ERR_INVALID, std::string("checkpoint: payload size does not match the header in ") + path);
     for (int i = 0; i < n; ++i) {
         if (arrays[i]) {
             f.read(reinterpret_cast<char*>(arrays[i]), counts[i] * 4);
@@ -100,11 +110,18 @@ TFG_API int tfg_load_tile_checkpoint(const char* path, const tfg_field_config* c
     uint64_t enc, dn;
     tfg_param_counts(cfg, &enc, &dn, nullptr);
     if (hdr[0] != enc + dn) return fail(TFG_ERR_INVALID, "checkpoint: parameter count mismatch");
+    // the occupancy count is stored apart from the FieldConfig: it must be
+    // exactly res^3 (the caller's buffer size)
+    const uint64_t occ =
+        uint64_t(cfg->occupancy_resolution) * cfg->occupancy_resolution * cfg->occupancy_resolution;
+    if (hdr[1] != occ) return fail(TFG_ERR_INVALID, "checkpoint: occupancy count mismatch");
     float* arr[7] = {st->enc, st->dnet, st->enc_m, st->enc_v, st->dnet_m, st->dnet_v, st->occupancy};
-    const uint64_t cnt[7] = {enc, dn, enc, enc, dn, dn, hdr[1]};
+    const uint64_t cnt[7] = {enc, dn, enc, enc, dn, dn, occ};
+    rc = read_arrays(f, path, arr, cnt, 7);
+    if (rc) return rc;
     st->enc_step = hdr[2];
     st->dnet_step = hdr[3];
-    return read_arrays(f, path, arr, cnt, 7);
+    return 0;
 }
 
 TFG_API int tfg_save_color_checkpoint(const char* path, const tfg_field_config* cfg, const float* params,
@@ -125,11 +142,13 @@ TFG_API int tfg_load_color_checkpoint(const char* path, const tfg_field_config* 
     if (rc) return rc;
     uint64_t col;
     tfg_param_counts(cfg, nullptr, nullptr, &col);
-    if (hdr[0] != col) return fail(TFG_ERR_INVALID, "checkpoint: parameter count mismatch");
+    if (hdr[0] != col || hdr[1] != 0) return fail(TFG_ERR_INVALID, "checkpoint: parameter count mismatch");
     float* arr[3] = {params, m, v};
     const uint64_t cnt[3] = {col, col, col};
+    rc = read_arrays(f, path, arr, cnt, 3);
+    if (rc) return rc;
     if (step) *step = hdr[2];
-    return read_arrays(f, path, arr, cnt, 3);
+    return 0;
 }
 
 // Saves the run: the window slots are copied back to their host records
@@ -137,6 +156,7 @@ TFG_API int tfg_load_color_checkpoint(const char* path, const tfg_field_config* 
 TFG_API int tfg_save_run(tfg_ctx* c, const char* dir) {
     if (!c || c->n_views == 0) return fail(TFG_ERR_STATE, "save_run: no scene");
     CK(cudaSetDevice(c->device));
+    if (settle_steps(c)) return TFG_ERR_CUDA;  // saved step counts exclude skipped steps
     CK(cudaEventRecord(c->ev_main, c->st));
     CK(cudaStreamWaitEvent(c->side, c->ev_main, 0));
     for (int s = 0; s < c->nslots; ++s)

@@ -111,7 +111,6 @@ def lib() -> C.CDLL:
         "tfg_build_crop_cache": [_vp, C.c_char_p, _vp],
         "tfg_load_crop_cache": [_vp, C.c_char_p],
         "tfg_crop_rect": [_vp, C.c_int, C.c_int, C.c_int, _vp],
-        "tfg_precompute_rays": [_vp],
         "tfg_comm_unique_id": [_vp],
         "tfg_comm_init": [_vp, _vp, C.c_int, C.c_int],
         "tfg_allreduce_grads": [_vp],
@@ -206,6 +205,12 @@ class Context:
         self.max_rays = max_rays
         if stream is not None:
             _check(lib().tfg_set_stream(self.h, C.c_void_p(stream)))
+        self._set_scene(scene)
+        self.n_rays = 0
+        self.n_samples = 0
+
+    def _set_scene(self, scene) -> None:
+        """tfg_set_scene: cameras, pinned host images, grid (re-callable)."""
         self.scene = scene
         self._cams = (Rpc * scene.n_views)(*scene.cams)
         # images may be None: the pinned host images start black and a crop
@@ -214,8 +219,6 @@ class Context:
         imgp = (C.c_void_p * scene.n_views)(*[None if im is None else im.ctypes.data for im in imgs])
         _check(lib().tfg_set_scene(self.h, self._cams, scene.n_views, imgp, C.byref(scene.roi),
                                    scene.grid_rows, scene.grid_cols))
-        self.n_rays = 0
-        self.n_samples = 0
 
     def close(self):
         if getattr(self, "h", None):
@@ -317,11 +320,6 @@ class Context:
         l = C.c_float()
         _check(lib().tfg_train_step(self.h, it, ray_begin, n_rays or self.max_rays, C.byref(l)))
         return l.value
-
-    def precompute_rays(self) -> None:
-        """Solve every pixel's ray of the scene once (optional; window moves
-        then only run the accept pass's memo kernel)."""
-        _check(lib().tfg_precompute_rays(self.h))
 
     # ---- multi-GPU through the C-ABI's own NCCL communicator.  torch is
     # imported first so that the library binds torch's libnccl.so.2 instead of

@@ -94,7 +94,20 @@ def test_checkpoint_rejects_mismatch_and_corruption(tmp_path):
         load_color_checkpoint(p, fc)  # a tile file is not a colour file
     raw = bytearray(open(p, "rb").read())
     open(p, "wb").write(raw[:-4])
-    with pytest.raises(TileFieldError, match="truncated"):
+    with pytest.raises(TileFieldError, match="payload size"):
+        load_tile_checkpoint(p, fc)
+    open(p, "wb").write(raw + b"\0" * 64)
+    with pytest.raises(TileFieldError, match="payload size"):
+        load_tile_checkpoint(p, fc)
+    # a header whose occupancy count exceeds res^3 (stored apart
+    # from the FieldConfig) must be rejected before anything is read into the
+    # caller's res^3 buffer, even when the payload is padded to match it
+    o_nocc = 16 + C.sizeof(fc) + 8 + 8
+    bad = bytearray(raw)
+    n_occ = fc.occupancy_resolution ** 3
+    bad[o_nocc:o_nocc + 8] = np.uint64(n_occ + 1024).tobytes()
+    open(p, "wb").write(bad + b"\0" * 4096)
+    with pytest.raises(TileFieldError, match="occupancy count"):
         load_tile_checkpoint(p, fc)
     raw[0] = ord("X")
     open(p, "wb").write(raw)

@@ -183,13 +183,37 @@ def test_nonfinite_gradient_names_the_group():
     # the step was not applied and the step counters were rolled back
     np.testing.assert_array_equal(after["enc"], before["enc"])
     assert after["enc_step"] == before["enc_step"]
+    # the record is consumed once: a second read neither raises nor rolls back again
+    ctx.read_loss()
+    assert ctx.tile_state(0)["enc_step"] == before["enc_step"]
+    _, _, _, cstep = ctx.color()
+    # callers that never read the status (bench-style
+    # forward_backward + optimizer_step) keep no inflated counts either, and
+    # the occupancy update due at iteration 15 is skipped with the step
+    occ0 = ctx.tile_state(1)["occupancy"]
+    for it in (14, 15):
+        ctx.forward_backward(it, 0, 512)
+        ctx.optimizer_step(it)
+    st1 = ctx.tile_state(0)  # settles the unverified steps
+    assert st1["enc_step"] == before["enc_step"]
+    np.testing.assert_array_equal(st1["enc"], before["enc"])
+    np.testing.assert_array_equal(ctx.tile_state(1)["occupancy"], occ0)
+    assert ctx.color()[3] == cstep
+    with pytest.raises(NonFiniteGradient, match=r"tile\(1,0\)\.dnet"):
+        ctx.read_loss()
+    # a healthy tile state lets training continue with the right counts
+    st["dnet"] = ctx.tile_state(0)["dnet"]
+    ctx.set_tile_state(2, st)
+    ctx.train_step(16, 0, 512)
+    assert ctx.tile_state(0)["enc_step"] == before["enc_step"] + 1
 
 
 def test_pixel_memo_matches_resolving():
-    """The per-pixel scene memo (rays + hit-tile bbox) gives the same accepted
-    lists and batches as re-solving every pixel per window (memo disabled via
-    TFG_NO_PIXEL_MEMO in a subprocess), along a snake that revisits pixels;
-    and so does filling the whole memo up front (tfg_precompute_rays)."""
+    """The per-window pixel memo, with pixels of the previous position copied
+    (rays + hit-tile bbox), gives the same accepted lists and batches as
+    re-solving every pixel per window (reuse disabled via TFG_NO_MEMO_REUSE in
+    a subprocess), along a snake that revisits pixels, with and without the
+    prefetched (side-stream) staging of the next position."""
     _need_gpu()
     import json
     import os
@@ -206,11 +230,13 @@ from paper_2507_01631_b200.tilefield import Context, snake_path
 scene = synth.make_scene(3, 3, tile_side=96.0, n_views=3, gsd=1.0, seed=21, max_off_nadir=30.0)
 ctx = Context(scene, FieldConfig.defaults(), TrainConfig.defaults(batch_rays=2048, seed=5), max_rays=2048)
 import os
-if os.environ.get("TFG_TEST_PRECOMPUTE") == "1":
-    ctx.precompute_rays()
+pre = os.environ.get("TFG_TEST_PREFETCH") == "1"
+path = snake_path(3, 3) + [(0, 0), (1, 1)]
 out = []
-for it, pos in enumerate(snake_path(3, 3) + [(0, 0), (1, 1)]):
+for it, pos in enumerate(path):
     ctx.set_window(*pos)
+    if pre and it + 1 < len(path):
+        ctx.prefetch_window(*path[it + 1])
     acc = ctx.accept_list()
     ctx.sample(it, 0, 2048, True)
     b = ctx.batch()
@@ -220,7 +246,7 @@ print(json.dumps(out))
 """ % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     res = {}
     for mode, memo, pre in (("memo", "0", "0"), ("solve", "1", "0"), ("pre", "0", "1")):
-        env = dict(os.environ, TFG_NO_PIXEL_MEMO=memo, TFG_TEST_PRECOMPUTE=pre)
+        env = dict(os.environ, TFG_NO_MEMO_REUSE=memo, TFG_TEST_PREFETCH=pre)
         p = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
         assert p.returncode == 0, p.stderr[-2000:]
         res[mode] = json.loads(p.stdout.strip().splitlines()[-1])
