@@ -6,12 +6,16 @@ segmentation + sampling, field fwd/bwd, compositing + loss + backward, fused
 Adam, periodic occupancy update), whole job over N GPUs; plus render rays/s.
 
 Workload: config 5 (6x6 grid of 128 m tiles, 16 synthetic views ~1650^2 px at
-0.5 m, 65,536 rays per batch per GPU, window at position (2,2)).  Ray-sharded
-data parallelism (weak scaling): rank r trains rays [r*B, (r+1)*B) of the
-global counter-RNG stream with an NCCL allreduce of the 7.01 MB gradient.
+0.5 m, a 65,536-ray global batch, window at position (2,2)).  Ray-sharded data
+parallelism (strong scaling, BASELINE config 5): rank r of N trains rays
+[r*B/N, (r+1)*B/N) of the global counter-RNG stream, with an NCCL allreduce of
+the 7.01 MB gradient; the loss is normalised by the global B.
 
 `python bench.py [--gpus N --steps K --warmup W]`           (our arm)
 `python bench.py --impl reference [...]`                     (CPU reference arm)
+
+With --gpus N > 1 and no torchrun environment, bench.py re-launches itself
+under torch.distributed.run with N ranks (one process per GPU).
 """
 from __future__ import annotations
 
@@ -29,12 +33,13 @@ sys.path.insert(0, ROOT)
 
 METRIC = "training rays/sec (2x2 window, fwd+bwd+Adam)"
 UNIT = "rays/s"
-B_PER_GPU = 65536
+B_GLOBAL = 65536          # BASELINE config 5: one global batch, sharded over the ranks
 WINDOW = (2, 2)
 FLOP_FWD = 17664          # per sample (density 4,096 + colour 13,568), SURVEY.md §8
 FLOP_FWD_BWD = 52992      # per sample
+FLOP_BWD = FLOP_FWD_BWD - FLOP_FWD  # 35,328: the backward's own work (its forward recompute is credited to field_fwd)
 SCATTER_BYTES = 8 * 8 * 8  # per sample: 8 levels x 8 corners x float2 of reds
-SCATTER_FLOOR_MS = 1.24   # measured: backward with the MLP chain cut to its last GEMM
+DTYPE = "bf16 MLP operands (tcgen05, fp32 accumulate); fp32 hash grid, compositing, Adam; fp64 rays"
 
 
 def peaks():
@@ -101,10 +106,28 @@ def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
 
+def relaunch(n: int) -> int:
+    """One process per GPU: re-executes this command under torch.distributed.run
+    (rendezvous on 127.0.0.1) and returns its exit code."""
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # communicator size / NVLS visible in the log
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
 def cpu_baseline(scene, n_rays: int, steps: int, warmup: int):
     """The CPU oracle trainer (oracle/, the reference's algorithm restated; the
-    absent trainer/field bodies have no other CPU implementation) on the host
-    cores, on a bounded sample of the same workload."""
+    absent trainer/field bodies have no other CPU implementation) on all host
+    cores, on a bounded sample of the same workload (same scene, window,
+    seeds; n_rays per iteration instead of 65,536)."""
     from oracle.pyoracle import Oracle, Session
     from paper_2507_01631_b200.abi import FieldConfig, TrainConfig
 
@@ -166,11 +189,11 @@ def run_reference(args):
     from paper_2507_01631_b200 import synth
 
     scene = synth.config_scene(5, seed=0)
-    n = 2048
+    n = 4096
     cb = cpu_baseline(scene, n, args.steps, args.warmup)
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32 (fp64 rays)", "data": "synthetic",
             "config": {"workload": "cfg5 6x6 grid, 2x2 window at (2,2), 16 views ~1650^2 px, bounded ray sample",
                        "rays_per_step": n},
             "cpu_baseline": cb,
@@ -180,12 +203,23 @@ def run_reference(args):
 
 KERNEL_UNITS = {
     # phase: (bound, per-sample, per-ray, unit) algorithmic work
-    "field_bwd": ("tensor", FLOP_FWD_BWD, 0, "flop"),
+    "field_bwd": ("tensor", FLOP_BWD, 0, "flop"),
     "field_fwd": ("tensor", FLOP_FWD, 0, "flop"),
     "composite": ("hbm", 40, 36, "byte"),
     "sampler": ("hbm", 22, 79, "byte"),
     "adam": ("hbm", 0, 0, "byte"),
 }
+
+
+def red_peak():
+    """Measured red.global.add throughput of this GPU model (tools/red_peak.cu
+    on a B200, committed as profiles/red_peak.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "red_peak.json")) as f:
+            r = json.load(f)
+        return {"GBps": float(r["best_GBps"]), "source": r.get("source", "profiles/red_peak.json")}
+    except Exception:
+        return None
 
 
 def run_ours(args):
@@ -197,14 +231,18 @@ def run_ours(args):
     from paper_2507_01631_b200.tilefield import Context, snake_path, tile_init
 
     rank, world, local = dist_env()
+    if "RANK" in os.environ and world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    B = B_PER_GPU
+    if B_GLOBAL % world:
+        raise SystemExit(f"bench.py: the {B_GLOBAL}-ray batch does not split over {world} ranks")
+    B = B_GLOBAL // world  # strong scaling: this rank's shard of the global batch
     scene = synth.config_scene(5, seed=0)
     fc = FieldConfig.defaults()
-    tc = TrainConfig.defaults(batch_rays=B * world, seed=2)
+    tc = TrainConfig.defaults(batch_rays=B_GLOBAL, seed=2)
     stream = torch.cuda.current_stream(dev)
     ctx = Context(scene, fc, tc, device=local, max_rays=B, stream=stream.cuda_stream)
     ctx.set_window(*WINDOW)
@@ -257,7 +295,7 @@ def run_ours(args):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max, ms_bracket_max = float(t[0].item()), float(t[1].item())
-    value = world * B * args.steps / (ms_max / 1e3)
+    value = B_GLOBAL * args.steps / (ms_max / 1e3)
 
     hbm, tf_burst, tf_sust, peak_src = peaks()
     K = args.steps
@@ -290,20 +328,21 @@ def run_ours(args):
     roofline = {"kernel": dom, "bound": d["bound"], "achieved": d["achieved"], "peak": peak,
                 "unit": d["unit"], "frac": d["achieved"] / peak, "traffic": traffic,
                 "peak_source": f"{peak_src} ({'bf16 sustained' if d['bound'] == 'tensor' else 'HBM copy'})",
-                "per_launch_work": (FLOP_FWD_BWD if dom == "field_bwd" else KERNEL_UNITS[dom][1]) * n_samples}
-    if dom == "field_bwd":
-        # The backward is bound by its hash-gradient scatter, not the tensor
-        # cores: 8 levels x 8 corners x 2 fp32 of global reds per sample
-        # (profiles/ hold the ncu
-        # evidence).  The floor is the A/B variant with the MLP chain cut.
+                "per_launch_work": KERNEL_UNITS[dom][1] * n_samples,
+                "per_launch_work_unit": KERNEL_UNITS[dom][3],
+                "per_unit": f"{KERNEL_UNITS[dom][1]} {KERNEL_UNITS[dom][3]}/sample x {n_samples} samples/launch"}
+    red = red_peak()
+    if dom == "field_bwd" and red:
+        # The backward is bound by its hash-gradient scatter (8 levels x 8
+        # corners x float2 of global reds per sample), not the tensor cores:
+        # reported against the measured red.global throughput of this GPU
+        # (tools/red_peak.cu, profiles/red_peak.json) beside the tensor peak.
         bwd_ms = d["ms_per_step"]
+        ach = SCATTER_BYTES * n_samples / (bwd_ms / 1e3) / 1e9
         roofline["limiter"] = {
-            "resource": "global fp32 reds of the hash-table gradients (L1 red path -> L2)",
-            "red_bytes_per_sample": SCATTER_BYTES,
-            "achieved_red_GBps": SCATTER_BYTES * n_samples / (bwd_ms / 1e3) / 1e9,
-            "scatter_floor_ms": SCATTER_FLOOR_MS,
-            "frac_of_floor": SCATTER_FLOOR_MS / bwd_ms,
-            "floor_source": "A/B variant: MLP chain cut to its last GEMM, scatter unchanged (BENCH_NOTES.md)"}
+            "resource": "global fp32 reds of the hash-table gradients (random indices into the 7 MB window tables)",
+            "red_bytes_per_sample": SCATTER_BYTES, "achieved": ach, "unit": "GB/s of red payload",
+            "peak": red["GBps"], "frac": ach / red["GBps"], "peak_source": red["source"]}
 
     # ---- end to end through the public API with host buffers: window slides
     # (pinned host <-> HBM tile state + crops), accepted-list rebuilds, loss
@@ -315,13 +354,6 @@ def run_ours(args):
     # prefetched move (the one-off initial load of a run is not timed, like
     # the device metric's).
     path = snake_path(scene.grid_rows, scene.grid_cols)
-    # run setup (untimed, reported): every pixel's ray solved once for the
-    # whole scene, so window moves only run the accept pass's memo kernel
-    torch.cuda.synchronize()
-    tp0 = time.perf_counter()
-    ctx.precompute_rays()
-    torch.cuda.synchronize()
-    precompute_ms = 1e3 * (time.perf_counter() - tp0)
     ctx.set_window(*path[0])
     ctx.prefetch_window(*path[1])
     h0, d0 = ctx.copy_bytes()
@@ -342,21 +374,16 @@ def run_ours(args):
         ctx.read_loss()
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
-    # the run setup's share: the whole-scene ray fill amortised over one full
-    # snake (every position once, move_every iterations each)
-    snake_steps = len(path) * args.move_every
-    e2e_s += (precompute_ms / 1e3) * min(1.0, e2e_steps / snake_steps)
     h1, d1 = ctx.copy_bytes()
     te = torch.tensor([e2e_s], device=dev)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e = {"value": world * B * e2e_steps / float(te.item()), "unit": UNIT,
+    e2e = {"value": B_GLOBAL * e2e_steps / float(te.item()), "unit": UNIT,
            "h2d_bytes_per_step": (h1 - h0) // e2e_steps, "d2h_bytes_per_step": (d1 - d0) // e2e_steps,
            "window_move_every": args.move_every, "window_moves": (e2e_steps - 1) // args.move_every,
-           "setup": {"precompute_rays_ms": precompute_ms,
-                     "what": "one-off per run: tfg_precompute_rays solves every pixel ray of the scene; "
-                             "its share over one full snake (len(path) x move_every iterations) is "
-                             "added to the e2e time"}}
+           "what": "public API, host images/tile records: every move stages crops + tile state "
+                   "(pinned H2D/D2H) and rebuilds the accepted list (new pixels Newton-solved, the "
+                   "previous position's pixels copied from its memo); loss/status read every step"}
 
     # ---- render (config 4: 4x4-tile ROI, random-init weights, occupancy all on)
     render = None
@@ -367,13 +394,13 @@ def run_ours(args):
     if rank == 0:
         cb = None
         if world == 1 and not args.no_cpu:
-            cb = cpu_baseline(scene, 2048, 2, 1)
+            cb = cpu_baseline(scene, 16384, 6, 1)
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
-               "warmup": args.warmup, "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak",
-               "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+               "warmup": args.warmup, "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "strong",
+               "vs_baseline": None, "dtype": DTYPE, "data": "synthetic",
                "config": {"workload": "cfg5: 6x6 grid of 128 m tiles, 2x2 window at (2,2), 16 synthetic views "
                                       "~1650^2 px at 0.5 m, random-init fields",
-                          "rays_per_gpu_per_step": B, "global_batch": B * world,
+                          "rays_per_gpu_per_step": B, "global_batch": B_GLOBAL,
                           "samples_per_step_per_gpu": n_samples,
                           "samples_per_ray": n_samples / B, "parallelism": f"ray-sharded dp{world}",
                           "l2": "flushed between timed iterations (256 MB write)",
@@ -462,6 +489,8 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "RANK" not in os.environ:
+        sys.exit(relaunch(args.gpus))
     if args.impl == "reference":
         run_reference(args)
     else:

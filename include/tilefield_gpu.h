@@ -233,13 +233,43 @@ TFG_API int tfg_sample(tfg_ctx* ctx, uint64_t iter, uint64_t ray_begin, int n_ra
 TFG_API int tfg_sample_pixels(tfg_ctx* ctx, const int32_t* pixels, int n_rays,
                               uint64_t* n_samples);
 TFG_API int tfg_batch_export(tfg_ctx* ctx, tfg_batch_view* out);
+/* A caller-built RaySegmentBatch becomes the current batch (replaces the batch
+ * argument of forward_batch / backward_batch, field.hpp:186-197; layout
+ * ray_batch.hpp:13-49): rays[n_rays], offsets[n_rays+1] (offsets[0] = 0),
+ * per-sample t, delta, local (3), slot, endpoint; capacity is ignored.  Slots
+ * index the loaded tiles (set_window, or set_slot_params without a window);
+ * each ray's samples must be at most one run per slot. */
+TFG_API int tfg_batch_import(tfg_ctx* ctx, const tfg_batch_view* batch, int n_rays);
+/* FieldParamView / ColorParamView (field.hpp:130-144): caller-owned parameters
+ * into a slot (enc 434,292 + dnet 2,128 floats; NULL keeps) or the colour net
+ * (6,915).  With no window set, slots 0..3 are bound detached (forward and
+ * backward only). */
+TFG_API int tfg_set_slot_params(tfg_ctx* ctx, int slot, const float* enc, const float* dnet);
+TFG_API int tfg_set_color_params(tfg_ctx* ctx, const float* params);
+/* Caller-given per-sample sigma and rgb (ray order) as the batch's field
+ * outputs: tfg_composite then renders exactly these (render alone, SPEC.md:
+ * 361-384). */
+TFG_API int tfg_set_field_outputs(tfg_ctx* ctx, const float* sigma, const float* rgb);
+/* backward_batch (field.hpp:193-197) from caller-given d_sigma / d_rgb (ray
+ * order, gradients w.r.t. the outputs of the preceding tfg_field_forward) into
+ * the flat gradient buffer (zeroed first; read with tfg_get_grads). */
+TFG_API int tfg_field_backward_from(tfg_ctx* ctx, const float* d_sigma, const float* d_rgb);
+/* adam_step (field.hpp:45-48) over caller spans, host or device memory:
+ * AdamState = (m, v, *step), LrSchedule = (lr_base, lr_decay_rate,
+ * lr_decay_steps), AdamConfig = (beta1, beta2, eps).  Non-finite gradients:
+ * TFG_ERR_NONFINITE naming `group`, nothing updated, *step unchanged; else
+ * *step += 1.  Bit-identical to the reference formula. */
+TFG_API int tfg_adam_step(tfg_ctx* ctx, float* params, const float* grads, float* m, float* v, uint64_t n,
+                          uint64_t* step, double lr_base, double lr_decay_rate, uint64_t lr_decay_steps,
+                          float beta1, float beta2, float eps, const char* group);
 /* forward_batch: per-sample sigma and rgb in ray order (n_samples, 3*n_samples). */
 TFG_API int tfg_field_forward(tfg_ctx* ctx, float* sigma, float* rgb);
 /* render + color_loss + render backward: per-ray rgb(3)/depth/opacity, and the
  * per-sample d_sigma / d_rgb in ray order (any output may be NULL). */
 TFG_API int tfg_composite(tfg_ctx* ctx, float* ray_rgb, float* ray_depth, float* ray_opacity,
                           float* d_sigma, float* d_rgb, float* loss);
-/* backward_batch into the flat gradient buffer (zeroed first). */
+/* backward_batch of the tfg_composite gradients into the flat gradient buffer
+ * (zeroed first); needs tfg_field_forward of this batch first. */
 TFG_API int tfg_field_backward(tfg_ctx* ctx);
 
 /* ---- parameter / state access -------------------------------------------- */

@@ -79,15 +79,21 @@ def build(verbose: bool = False, force: bool = False, defines: list[str] | None 
 
 
 def build_examples() -> str:
-    """The C++ host example (examples/train_window.cpp) against the C-ABI."""
+    """The C++ host programs against the C-ABI: the example trainer
+    (examples/train_window.cpp) and the drop-in batch-operator caller of the
+    adapter test (tests/cpp/field_adapter.cpp, include/tilefield_gpu_field.hpp)."""
     lib = build()
     out_dir = os.path.join(HERE, "bin")
     os.makedirs(out_dir, exist_ok=True)
+    inc = os.path.join(HERE, "..", "include")
+    hdrs = [os.path.join(inc, f) for f in os.listdir(inc)]
     exe = os.path.join(out_dir, "train_window")
-    src = os.path.join(HERE, "..", "examples", "train_window.cpp")
-    if _newer([src, lib], exe):
-        subprocess.check_call(["g++", "-std=c++17", "-O2", "-o", exe, src, "-L", HERE, "-ltilefield_gpu",
-                               "-Wl,-rpath,$ORIGIN/.."])
+    for name, src in (("train_window", os.path.join(HERE, "..", "examples", "train_window.cpp")),
+                      ("field_adapter", os.path.join(HERE, "..", "tests", "cpp", "field_adapter.cpp"))):
+        out = os.path.join(out_dir, name)
+        if _newer([src, lib] + hdrs, out):
+            subprocess.check_call(["g++", "-std=c++20", "-O2", "-Wall", "-I", inc, "-o", out, src, "-L", HERE,
+                                   "-ltilefield_gpu", "-Wl,-rpath,$ORIGIN/.."])
     return exe
 
 

@@ -300,6 +300,22 @@ __global__ void accept_scatter_kernel(AcceptArgs a, const uint32_t* __restrict__
     out[pos[idx]] = (uint64_t(v) << 40) | (row << 20) | col;
 }
 
+// encode_direction (nn.hpp:288-298) of the float world direction: 6 float4
+__device__ __forceinline__ void write_view_encoding(const double* d, float4* ve) {
+    float d3[3] = {float(d[0]), float(d[1]), float(d[2])};
+    float e[24];
+    int jj = 0;
+    const float scales[4] = {3.14159265358979323846f, 6.28318530717958647692f,
+                             12.5663706143591729538f, 25.1327412287183459077f};
+    for (int f = 0; f < kViewFreqs; ++f)
+        for (int c = 0; c < 3; ++c) {
+            float x = scales[f] * d3[c];
+            e[jj++] = sinf(x);
+            e[jj++] = cosf(x);
+        }
+    for (int q = 0; q < 6; ++q) ve[q] = make_float4(e[4 * q], e[4 * q + 1], e[4 * q + 2], e[4 * q + 3]);
+}
+
 // ------------------------------------------------------------------ K1a
 struct SegPlan {
     int nseg;
@@ -501,20 +517,7 @@ __global__ void __launch_bounds__(128, kSolve ? TFG_RAYGEN_MINB : TFG_RAYGEN_MEM
         rays[i] = R;
         return;
     }
-    // encode_direction (nn.hpp:288-298) of the float world direction
-    float d3[3] = {float(R.d[0]), float(R.d[1]), float(R.d[2])};
-    float e[24];
-    int jj = 0;
-    const float scales[4] = {3.14159265358979323846f, 6.28318530717958647692f,
-                             12.5663706143591729538f, 25.1327412287183459077f};
-    for (int f = 0; f < kViewFreqs; ++f)
-        for (int c = 0; c < 3; ++c) {
-            float x = scales[f] * d3[c];
-            e[jj++] = sinf(x);
-            e[jj++] = cosf(x);
-        }
-    float4* ve = venc + uint64_t(i) * 6;
-    for (int q = 0; q < 6; ++q) ve[q] = make_float4(e[4 * q], e[4 * q + 1], e[4 * q + 2], e[4 * q + 3]);
+    write_view_encoding(R.d, venc + uint64_t(i) * 6);
 }
 
 // Slot buckets -> 128-sample single-slot tiles (one block).
@@ -641,6 +644,99 @@ __global__ void __launch_bounds__(TFG_WRITE_THREADS) write_kernel(RaygenArgs a, 
         if (r > a.delta_cap) r = a.delta_cap;
         out.td[pend_pos] = make_float2(float(pend_t), float(r));
     }
+}
+
+// ------------------------------------------------------------------ batch import
+// A caller-built RaySegmentBatch (tfg_batch_import; the forward_batch /
+// backward_batch drop-in) into the device batch layout the sampler writes:
+// per ray its runs of same-slot samples become the ray's segments (a ray
+// crosses each convex tile box at most once, so at most one run per slot),
+// per-slot counts -> exclusive scan -> slot buckets -> 128-sample tiles.
+__global__ void __launch_bounds__(128) import_plan_kernel(ImportArgs a, RayRec* __restrict__ rays,
+                                                          float4* __restrict__ venc, uint32_t* __restrict__ counts,
+                                                          Status* __restrict__ status) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= a.n_rays) return;
+    const tfg_ray_entry& E = a.rays[i];
+    RayRec R;
+    for (int q = 0; q < 3; ++q) {
+        R.o[q] = E.origin[q];
+        R.d[q] = E.direction[q];
+        R.target[q] = E.target[q];
+    }
+    R.view = E.image_id;
+    R.row = E.row;
+    R.col = E.col;
+    R.status = 0;
+    R.nseg = 0;
+    for (int s = 0; s < a.nslots; ++s) counts[uint64_t(s) * a.n_rays + i] = 0;
+    const uint32_t q0 = a.offsets[i], q1 = a.offsets[i + 1];
+    uint32_t seen = 0;
+    bool bad = q1 < q0;
+    for (uint32_t q = q0; q < q1 && !bad;) {
+        const int s = a.slot[q];
+        uint32_t e = q + 1;
+        while (e < q1 && a.slot[e] == s) ++e;
+        if (s >= a.nslots || (seen >> s) & 1u || R.nseg == kMaxSeg) {
+            bad = true;
+            break;
+        }
+        seen |= 1u << s;
+        const int k = R.nseg++;
+        R.slot[k] = uint8_t(s);
+        R.cnt[k] = uint16_t(e - q);
+        R.nint[k] = uint16_t(e - q - 1);
+        R.tn[k] = a.t[q];
+        R.tf[k] = a.t[e - 1];
+        counts[uint64_t(s) * a.n_rays + i] = e - q;
+        q = e;
+    }
+    if (bad) {
+        atomicOr(&status->bits, kStatusBadBatch);
+        R.status = 2;
+        R.nseg = 0;
+        for (int s = 0; s < a.nslots; ++s) counts[uint64_t(s) * a.n_rays + i] = 0;
+    }
+    rays[i] = R;
+    write_view_encoding(R.d, venc + uint64_t(i) * 6);
+}
+
+__global__ void __launch_bounds__(128) import_scatter_kernel(ImportArgs a, const RayRec* __restrict__ rays,
+                                                             const uint32_t* __restrict__ P,
+                                                             const Status* __restrict__ status, SampleArrays out) {
+    pdl_wait();
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (warp >= a.n_rays || (status->bits & kStatusSampleOverflow)) return;
+    const RayRec& R = rays[warp];
+    if (R.status != 0) return;
+    uint32_t q = a.offsets[warp];
+    for (int k = 0; k < R.nseg; ++k) {
+        const uint64_t base = P[uint64_t(R.slot[k]) * a.n_rays + warp];
+        const int n = R.cnt[k];
+        for (int j = lane; j < n; j += 32) {
+            const uint32_t s = q + j;
+            out.local[base + j] = make_float4(a.local[3 * uint64_t(s)], a.local[3 * uint64_t(s) + 1],
+                                              a.local[3 * uint64_t(s) + 2], __int_as_float(warp));
+            out.td[base + j] = make_float2(a.t[s], a.delta[s]);
+            out.endpoint[base + j] = a.endpoint[s];
+        }
+        q += n;
+    }
+}
+
+int launch_import(const ImportArgs& a, RayRec* rays, float4* venc, uint32_t* counts, uint32_t* P,
+                  uint32_t* block_sums, TileDesc* tiles, int max_tiles, SampleArrays out, uint64_t capacity,
+                  Status* status, cudaStream_t st, uint64_t* launches) {
+    import_plan_kernel<<<(a.n_rays + 127) / 128, 128, 0, st>>>(a, rays, venc, counts, status);
+    uint64_t n = uint64_t(a.nslots) * a.n_rays;
+    if (scan_exclusive(counts, n, P, block_sums, nullptr, st, launches)) return 1;
+    launch_pdl(tiles_kernel, dim3(std::max(1, std::min(148, (max_tiles + 255) / 256))), dim3(256), 0, st, P, a.n_rays,
+               a.nslots, capacity, max_tiles, tiles, status);
+    launch_pdl(import_scatter_kernel, dim3((a.n_rays * 32 + 127) / 128), dim3(128), 0, st, a,
+               static_cast<const RayRec*>(rays), static_cast<const uint32_t*>(P), static_cast<const Status*>(status),
+               out);
+    *launches += 3;
+    return 0;
 }
 
 // ------------------------------------------------------------------ host launchers

@@ -424,6 +424,7 @@ enum : uint32_t {
     kStatusSampleOverflow = 1u << 1,
     kStatusNonFinite = 1u << 2,
     kStatusSegOverflow = 1u << 3,
+    kStatusBadBatch = 1u << 4,  // imported batch: a ray's samples are not <= 1 run per loaded slot
 };
 
 struct Status {

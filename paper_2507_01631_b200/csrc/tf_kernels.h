@@ -82,6 +82,20 @@ struct RaygenArgs {
     const uint32_t* occ_bits[kMaxSlots];
 };
 
+// A caller-built RaySegmentBatch (ray_batch.hpp:13-49) in ray order, on the
+// device (tfg_batch_import).
+struct ImportArgs {
+    const tfg_ray_entry* rays;
+    const uint32_t* offsets;  // n_rays + 1
+    const float* t;
+    const float* delta;
+    const float* local;       // 3 per sample
+    const uint8_t* slot;
+    const uint8_t* endpoint;
+    int n_rays;
+    int nslots;
+};
+
 struct FieldArgs {
     FieldPtrs f;
     HashLayout hl;
@@ -160,6 +174,9 @@ int launch_sampler(const RaygenArgs& a, RayRec* rays, float4* venc, uint32_t* co
                    uint32_t* P, uint32_t* block_sums, TileDesc* tiles, int max_tiles,
                    SampleArrays out, uint64_t capacity, Status* status, cudaStream_t st,
                    uint64_t* launches);
+int launch_import(const ImportArgs& a, RayRec* rays, float4* venc, uint32_t* counts, uint32_t* P,
+                  uint32_t* block_sums, TileDesc* tiles, int max_tiles, SampleArrays out, uint64_t capacity,
+                  Status* status, cudaStream_t st, uint64_t* launches);
 void launch_field_forward_tc(const FieldArgs& a, uint8_t* feat, int32_t* rays, int sms,
                              cudaStream_t st, uint64_t* launches);
 void launch_field_backward_tc(const FieldArgs& a, const FieldGradArgs& g, uint8_t* feat,

@@ -427,6 +427,9 @@ int check_status(tfg_ctx* c) {
     if (s.bits & kStatusSampleOverflow)
         return fail(TFG_ERR_INVALID, "sample: batch exceeds the sample capacity of the context");
     if (s.bits & kStatusSegOverflow) return fail(TFG_ERR_INVALID, "sample: more than 8 segments");
+    if (s.bits & kStatusBadBatch)
+        return fail(TFG_ERR_INVALID, "batch_import: a ray's samples must form at most one run per loaded slot "
+                                     "(slot < number of slots; a ray crosses each tile box once)");
     if (s.bits & kStatusRayFail)
         return fail(TFG_ERR_INVALID,
                     "sample: ray generation failed (ray_from_pixel threw for a drawn pixel, or the "
@@ -534,6 +537,7 @@ FieldArgs field_args(tfg_ctx* c, const FieldPtrs& f) {
 int run_forward(tfg_ctx* c, const FieldPtrs& f) {
     PhaseScope ps(c, kPhFieldFwd);
     c->fwd_done = true;
+    c->io_fwd = true;
     launch_field_forward_tc(field_args(c, f), c->d_feat, c->d_tile_rays, c->sms, c->st,
                             &c->launches);
     CK(cudaGetLastError());
@@ -542,6 +546,7 @@ int run_forward(tfg_ctx* c, const FieldPtrs& f) {
 
 int run_composite(tfg_ctx* c, bool backward, float4* export_io = nullptr) {
     PhaseScope ps(c, kPhComposite);
+    if (backward) c->io_fwd = false;  // io now holds the pre-activation gradients
     CompositeArgs a{};
     a.rays = c->d_rays;
     a.P = c->d_P;
@@ -564,10 +569,9 @@ int run_composite(tfg_ctx* c, bool backward, float4* export_io = nullptr) {
 }
 
 int run_backward(tfg_ctx* c) {
-    if (!c->fwd_done) {
-        int rc = run_forward(c, train_ptrs(c));
-        if (rc) return rc;
-    }
+    // the backward recomputes the forward from the feature tiles of this
+    // batch's forward and reads K3's gradients from io
+    if (!c->fwd_done) return fail(TFG_ERR_STATE, "field_backward: run field_forward on this batch first");
     PhaseScope ps(c, kPhFieldBwd);
     CK(cudaMemsetAsync(c->d_grads, 0, c->n_params * sizeof(float), c->st));
     FieldGradArgs g{};
@@ -1378,6 +1382,217 @@ TFG_API int tfg_batch_export(tfg_ctx* c, tfg_batch_view* out) {
         if (out->slot) out->slot[q] = uint8_t(slot);
         if (out->endpoint) out->endpoint[q] = ep[pos];
     });
+    return 0;
+}
+
+// A caller-built RaySegmentBatch (ray_batch.hpp:13-49) becomes the context's
+// current batch: the forward_batch / backward_batch drop-in (field.hpp:186-197).
+TFG_API int tfg_batch_import(tfg_ctx* c, const tfg_batch_view* in, int n_rays) {
+    if (!c || !in) return fail(TFG_ERR_INVALID, "batch_import: null argument");
+    if (c->nslots == 0) return fail(TFG_ERR_STATE, "batch_import: no loaded slots (set_window or set_slot_params)");
+    if (n_rays <= 0 || n_rays > c->max_rays) return fail(TFG_ERR_INVALID, "batch_import: n_rays outside (0, max_rays]");
+    if (!in->rays || !in->offsets || !in->t || !in->delta || !in->local || !in->slot || !in->endpoint)
+        return fail(TFG_ERR_INVALID, "batch_import: every batch array is required");
+    if (in->offsets[0] != 0) return fail(TFG_ERR_INVALID, "batch_import: offsets[0] must be 0");
+    for (int i = 0; i < n_rays; ++i)
+        if (in->offsets[i + 1] < in->offsets[i]) return fail(TFG_ERR_INVALID, "batch_import: offsets must ascend");
+    const uint64_t S = in->offsets[n_rays];
+    if (S > c->sample_cap) return fail(TFG_ERR_INVALID, "batch_import: batch exceeds the sample capacity of the context");
+    CK(cudaSetDevice(c->device));
+    // staging: rays | offsets | t | delta | local | slot | endpoint
+    const uint64_t cap = c->sample_cap, mr = uint64_t(c->max_rays);
+    const uint64_t o_off = mr * sizeof(tfg_ray_entry), o_t = o_off + ((mr + 1) * 4 + 15) / 16 * 16,
+                   o_de = o_t + cap * 4, o_lo = o_de + cap * 4, o_sl = o_lo + cap * 12, o_ep = o_sl + cap,
+                   total = o_ep + cap;
+    if (!c->d_imp && dalloc(c, &c->d_imp, total)) return TFG_ERR_CUDA;
+    uint8_t* b = c->d_imp;
+    CK(cudaMemcpyAsync(b, in->rays, size_t(n_rays) * sizeof(tfg_ray_entry), cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(b + o_off, in->offsets, size_t(n_rays + 1) * 4, cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(b + o_t, in->t, S * 4, cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(b + o_de, in->delta, S * 4, cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(b + o_lo, in->local, S * 12, cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(b + o_sl, in->slot, S, cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(b + o_ep, in->endpoint, S, cudaMemcpyHostToDevice, c->st));
+    c->h2d_bytes += n_rays * (sizeof(tfg_ray_entry) + 4) + S * 22;
+    ImportArgs a{};
+    a.rays = reinterpret_cast<const tfg_ray_entry*>(b);
+    a.offsets = reinterpret_cast<const uint32_t*>(b + o_off);
+    a.t = reinterpret_cast<const float*>(b + o_t);
+    a.delta = reinterpret_cast<const float*>(b + o_de);
+    a.local = reinterpret_cast<const float*>(b + o_lo);
+    a.slot = b + o_sl;
+    a.endpoint = b + o_ep;
+    a.n_rays = n_rays;
+    a.nslots = c->nslots;
+    {
+        PhaseScope ps(c, kPhSampler);
+        CK(cudaMemsetAsync(c->d_status, 0, sizeof(Status), c->st));
+        if (launch_import(a, c->d_rays, c->d_venc, c->d_counts, c->d_P, c->d_block_sums, c->d_tiles, c->max_tiles,
+                          c->s, c->sample_cap, c->d_status, c->st, &c->launches))
+            return fail(TFG_ERR_INVALID, "batch_import: scan capacity exceeded");
+        CK(cudaGetLastError());
+    }
+    c->cur_rays = n_rays;
+    c->have_batch = true;
+    c->fwd_done = false;
+    c->io_fwd = false;
+    c->render_mode = false;
+    return sync_status(c);
+}
+
+// Loads caller-owned parameters into a slot (FieldParamView, field.hpp:130-137)
+// or the colour net (ColorParamView, :139-144).  With no window set, slots
+// are bound detached (no tile record): forward/backward only.
+TFG_API int tfg_set_slot_params(tfg_ctx* c, int slot, const float* enc, const float* dnet) {
+    if (!c || slot < 0 || slot >= kTrainSlots) return fail(TFG_ERR_INVALID, "set_slot_params: bad slot");
+    CK(cudaSetDevice(c->device));
+    if (slot >= c->nslots) {
+        if (c->pos_r >= 0) return fail(TFG_ERR_INVALID, "set_slot_params: slot outside the window");
+        for (int k = c->nslots; k <= slot; ++k) c->slot_tile[k] = -1;
+        c->nslots = slot + 1;
+    }
+    CK(cudaStreamSynchronize(c->st));
+    const uint64_t off = uint64_t(slot) * c->stride;
+    if (enc) CK(cudaMemcpy(c->d_params + off, enc, c->enc_n * 4, cudaMemcpyHostToDevice));
+    if (dnet) CK(cudaMemcpy(c->d_params + off + c->enc_n, dnet, (c->stride - c->enc_n) * 4, cudaMemcpyHostToDevice));
+    c->fwd_done = false;
+    return 0;
+}
+
+TFG_API int tfg_set_color_params(tfg_ctx* c, const float* params) {
+    if (!c || !params) return fail(TFG_ERR_INVALID, "set_color_params: null argument");
+    CK(cudaSetDevice(c->device));
+    CK(cudaStreamSynchronize(c->st));
+    CK(cudaMemcpy(c->d_params + c->color_off, params, (c->n_params - c->color_off) * 4, cudaMemcpyHostToDevice));
+    c->fwd_done = false;
+    return 0;
+}
+
+// Writes caller-given per-sample sigma / rgb (ray order) into the batch's
+// field outputs: compositing (render + loss + render backward) then runs on
+// exactly these values.
+TFG_API int tfg_set_field_outputs(tfg_ctx* c, const float* sigma, const float* rgb) {
+    if (!c || !c->have_batch) return fail(TFG_ERR_STATE, "set_field_outputs: no batch");
+    if (!sigma || !rgb) return fail(TFG_ERR_INVALID, "set_field_outputs: null argument");
+    HostBatch hb;
+    int rc = fetch_batch_meta(c, hb);
+    if (rc) return rc;
+    std::vector<float4> io(hb.n_samples);
+    for_samples(c, hb, [&](int, uint64_t q, uint64_t pos, int) {
+        io[pos] = make_float4(sigma[q], rgb[3 * q], rgb[3 * q + 1], rgb[3 * q + 2]);
+    });
+    CK(cudaMemcpy(c->s.io, io.data(), io.size() * 16, cudaMemcpyHostToDevice));
+    c->io_fwd = true;
+    return 0;
+}
+
+// backward_batch from caller-given d_sigma / d_rgb (ray order; gradients with
+// respect to the field outputs, field.hpp:193-197): converted to the
+// pre-activation gradients K4 consumes (density_activation / sigmoid
+// derivatives, nn.hpp:270-285) against the forward's sigma / rgb, then the
+// field backward into the flat gradient buffer (zeroed first).
+TFG_API int tfg_field_backward_from(tfg_ctx* c, const float* d_sigma, const float* d_rgb) {
+    if (!c || !c->have_batch) return fail(TFG_ERR_STATE, "field_backward_from: no batch");
+    if (!d_sigma || !d_rgb) return fail(TFG_ERR_INVALID, "field_backward_from: null argument");
+    if (!c->fwd_done || !c->io_fwd)
+        return fail(TFG_ERR_STATE, "field_backward_from: run field_forward on this batch first");
+    HostBatch hb;
+    int rc = fetch_batch_meta(c, hb);
+    if (rc) return rc;
+    std::vector<float4> io(hb.n_samples);
+    CK(cudaMemcpy(io.data(), c->s.io, io.size() * 16, cudaMemcpyDeviceToHost));
+    const float dmax = c->fc.density_max;
+    for_samples(c, hb, [&](int, uint64_t q, uint64_t pos, int) {
+        const float4 f = io[pos];
+        const float dr = d_rgb[3 * q], dg = d_rgb[3 * q + 1], db = d_rgb[3 * q + 2];
+        io[pos] = make_float4(f.x >= dmax ? 0.f : d_sigma[q] * f.x, dr * f.y * (1.f - f.y), dg * f.z * (1.f - f.z),
+                              db * f.w * (1.f - f.w));
+    });
+    CK(cudaMemcpy(c->s.io, io.data(), io.size() * 16, cudaMemcpyHostToDevice));
+    c->io_fwd = false;
+    if ((rc = run_backward(c))) return rc;
+    CK(cudaStreamSynchronize(c->st));
+    return 0;
+}
+
+// adam_step (field.hpp:45-48) over caller spans (host or device memory):
+// state = (m, v, *step), schedule = (lr_base, lr_decay_rate, lr_decay_steps),
+// config = (beta1, beta2, eps).  Non-finite gradients: TFG_ERR_NONFINITE
+// naming `group`, nothing updated, step unchanged.  Synchronous.
+TFG_API int tfg_adam_step(tfg_ctx* c, float* params, const float* grads, float* m, float* v, uint64_t n,
+                          uint64_t* step, double lr_base, double lr_decay_rate, uint64_t lr_decay_steps,
+                          float beta1, float beta2, float eps, const char* group) {
+    if (!c || !params || !grads || !m || !v || !step) return fail(TFG_ERR_INVALID, "adam_step: null argument");
+    if (n == 0) {
+        ++*step;
+        return 0;
+    }
+    CK(cudaSetDevice(c->device));
+    auto on_device = [](const void* p) {
+        cudaPointerAttributes at{};
+        if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        return (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) &&
+               (reinterpret_cast<uintptr_t>(p) & 15) == 0;
+    };
+    const bool dev = on_device(params) && on_device(grads) && on_device(m) && on_device(v);
+    float *dp = params, *dm = m, *dv = v;
+    const float* dg = grads;
+    void* scratch = nullptr;
+    uint32_t* flags = nullptr;
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&flags), 32 * 4, c->st));
+    CK(cudaMemsetAsync(flags, 0, 32 * 4, c->st));
+    if (!dev) {
+        const size_t nb = (n * 4 + 255) / 256 * 256;
+        CK(cudaMallocAsync(&scratch, 4 * nb, c->st));
+        dp = static_cast<float*>(scratch);
+        float* g = reinterpret_cast<float*>(static_cast<char*>(scratch) + nb);
+        dm = reinterpret_cast<float*>(static_cast<char*>(scratch) + 2 * nb);
+        dv = reinterpret_cast<float*>(static_cast<char*>(scratch) + 3 * nb);
+        CK(cudaMemcpyAsync(dp, params, n * 4, cudaMemcpyDefault, c->st));
+        CK(cudaMemcpyAsync(g, grads, n * 4, cudaMemcpyDefault, c->st));
+        CK(cudaMemcpyAsync(dm, m, n * 4, cudaMemcpyDefault, c->st));
+        CK(cudaMemcpyAsync(dv, v, n * 4, cudaMemcpyDefault, c->st));
+        dg = g;
+    }
+    const uint64_t s = *step + 1;
+    AdamArgs a{};
+    a.params = dp;
+    a.grads = dg;
+    a.m = dm;
+    a.v = dv;
+    a.beta1 = beta1;
+    a.beta2 = beta2;
+    a.omb1 = 1.0f - beta1;
+    a.omb2 = 1.0f - beta2;
+    a.eps = eps;
+    a.group_flags = flags;
+    a.sticky = flags + 16;
+    a.seq = 1;
+    a.n_groups = 1;
+    a.g[0].offset = 0;
+    a.g[0].count = n;
+    a.g[0].lr = float(lr_decay_rate == 1.0 ? lr_base
+                                           : lr_base * std::pow(lr_decay_rate, double(s) / double(lr_decay_steps)));
+    a.g[0].bc1 = float(1.0 - std::pow(double(beta1), double(s)));
+    a.g[0].bc2 = float(1.0 - std::pow(double(beta2), double(s)));
+    launch_adam(a, n, c->st, &c->launches);
+    CK(cudaGetLastError());
+    uint32_t bad = 0;
+    CK(cudaMemcpyAsync(&bad, flags + 16, 4, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    if (!dev && bad == 0) {  // staged: the update goes back to the caller's spans
+        CK(cudaMemcpyAsync(params, dp, n * 4, cudaMemcpyDefault, c->st));
+        CK(cudaMemcpyAsync(m, dm, n * 4, cudaMemcpyDefault, c->st));
+        CK(cudaMemcpyAsync(v, dv, n * 4, cudaMemcpyDefault, c->st));
+    }
+    if (scratch) CK(cudaFreeAsync(scratch, c->st));
+    CK(cudaFreeAsync(flags, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    if (bad) return fail(TFG_ERR_NONFINITE, std::string("adam_step: non-finite gradient in group ") + (group ? group : "?"));
+    ++*step;
     return 0;
 }
 

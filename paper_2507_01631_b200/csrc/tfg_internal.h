@@ -184,6 +184,8 @@ struct tfg_ctx {
     int cur_rays = 0;
     bool have_batch = false;
     bool fwd_done = false;  // feature tiles of the current batch are resident
+    bool io_fwd = false;    // io holds the forward's (sigma, rgb) (not yet K3's gradients)
+    uint8_t* d_imp = nullptr;  // batch import staging (ray-order arrays of a caller batch)
     bool render_mode = false;
 
     // render

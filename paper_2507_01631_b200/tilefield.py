@@ -79,6 +79,13 @@ def lib() -> C.CDLL:
         "tfg_field_forward": [_vp, _vp, _vp],
         "tfg_composite": [_vp, _vp, _vp, _vp, _vp, _vp, _vp],
         "tfg_field_backward": [_vp],
+        "tfg_batch_import": [_vp, _vp, C.c_int],
+        "tfg_set_slot_params": [_vp, C.c_int, _vp, _vp],
+        "tfg_set_color_params": [_vp, _vp],
+        "tfg_set_field_outputs": [_vp, _vp, _vp],
+        "tfg_field_backward_from": [_vp, _vp, _vp],
+        "tfg_adam_step": [_vp, _vp, _vp, _vp, _vp, C.c_uint64, _vp, C.c_double, C.c_double, C.c_uint64,
+                          C.c_float, C.c_float, C.c_float, C.c_char_p],
         "tfg_get_tile_state": [_vp, C.c_int, _vp],
         "tfg_set_tile_state": [_vp, C.c_int, _vp],
         "tfg_get_color": [_vp, _vp, _vp, _vp, _vp],
@@ -279,6 +286,62 @@ class Context:
                        lc.ctypes.data, sl.ctypes.data, ep.ctypes.data, S)
         _check(lib().tfg_batch_export(self.h, C.byref(bv)))
         return dict(rays=rays, offsets=off, t=t, delta=de, local=lc.reshape(S, 3), slot=sl, endpoint=ep)
+
+    def batch_import(self, b: dict) -> int:
+        """A caller-built RaySegmentBatch (dict as batch() returns) becomes the
+        current batch (the batch argument of forward_batch / backward_batch)."""
+        rays = np.ascontiguousarray(b["rays"], RAY_DTYPE)
+        off = np.ascontiguousarray(b["offsets"], np.uint32)
+        arrs = [np.ascontiguousarray(b[k], dt) for k, dt in
+                (("t", np.float32), ("delta", np.float32), ("local", np.float32), ("slot", np.uint8),
+                 ("endpoint", np.uint8))]
+        R = rays.shape[0]
+        S = int(off[-1])
+        bv = BatchView(rays.ctypes.data, off.ctypes.data, *[a.ctypes.data for a in arrs], S)
+        _check(lib().tfg_batch_import(self.h, C.byref(bv), R))
+        self.n_rays, self.n_samples = R, S
+        return S
+
+    def set_slot_params(self, slot: int, enc=None, dnet=None) -> None:
+        """FieldParamView (field.hpp:130-137): caller parameters into a slot."""
+        e = None if enc is None else np.ascontiguousarray(enc, np.float32)
+        d = None if dnet is None else np.ascontiguousarray(dnet, np.float32)
+        _check(lib().tfg_set_slot_params(self.h, slot, ptr(e), ptr(d)))
+
+    def set_color_params(self, params) -> None:
+        """ColorParamView (field.hpp:139-144)."""
+        _check(lib().tfg_set_color_params(self.h, ptr(np.ascontiguousarray(params, np.float32))))
+
+    def set_field_outputs(self, sigma, rgb) -> None:
+        """Per-sample sigma / rgb (ray order) as the batch's field outputs."""
+        sg = np.ascontiguousarray(sigma, np.float32)
+        rg = np.ascontiguousarray(rgb, np.float32).reshape(-1)
+        if sg.size != self.n_samples or rg.size != 3 * self.n_samples:
+            raise ValueError("set_field_outputs: one sigma and three rgb per sample")
+        _check(lib().tfg_set_field_outputs(self.h, ptr(sg), ptr(rg)))
+
+    def field_backward_from(self, d_sigma, d_rgb) -> None:
+        """backward_batch from caller d_sigma / d_rgb (field.hpp:193-197)."""
+        ds = np.ascontiguousarray(d_sigma, np.float32)
+        dr = np.ascontiguousarray(d_rgb, np.float32).reshape(-1)
+        if ds.size != self.n_samples or dr.size != 3 * self.n_samples:
+            raise ValueError("field_backward_from: one d_sigma and three d_rgb per sample")
+        _check(lib().tfg_field_backward_from(self.h, ptr(ds), ptr(dr)))
+
+    def adam_step(self, params, grads, m, v, step: int, lr: float = 1e-2, decay_rate: float = 1.0,
+                  decay_steps: int = 1000, beta1: float = 0.9, beta2: float = 0.99, eps: float = 1e-15,
+                  group: str = "params") -> int:
+        """adam_step (field.hpp:45-48) in place on float32 arrays (numpy, or
+        torch CUDA tensors); returns the new step count."""
+        def addr(a):
+            if hasattr(a, "data_ptr"):
+                return C.c_void_p(a.data_ptr())
+            return ptr(a)
+        n = params.numel() if hasattr(params, "numel") else params.size
+        st = C.c_uint64(step)
+        _check(lib().tfg_adam_step(self.h, addr(params), addr(grads), addr(m), addr(v), n, C.byref(st), lr,
+                                   decay_rate, decay_steps, beta1, beta2, eps, group.encode()))
+        return st.value
 
     def field_forward(self):
         S = self.n_samples

@@ -1,0 +1,93 @@
+"""The reference-signature drop-in: a C++ caller
+(tests/cpp/field_adapter.cpp) builds nothing of its own on the GPU side — it
+hands the reference-style RaySegmentBatch (here the CPU oracle's batch),
+FieldParamViews and a ColorParamView to tilefield::gpu::forward_batch /
+backward_batch / adam_step (include/tilefield_gpu_field.hpp, the field.hpp
+signatures) and gets sigma / rgb, BatchGrads and the Adam update back; the
+results are compared with the oracle's on the same inputs."""
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+from paper_2507_01631_b200 import synth
+from paper_2507_01631_b200.abi import FieldConfig, TrainConfig
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+EXE = os.path.join(ROOT, "paper_2507_01631_b200", "bin", "field_adapter")
+
+
+def _w(d, name, a):
+    np.ascontiguousarray(a).tofile(os.path.join(d, name))
+
+
+def _r(d, name, dt):
+    return np.fromfile(os.path.join(d, name), dt)
+
+
+def test_cpp_adapter_matches_oracle(tmp_path):
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from oracle.pyoracle import Oracle, Session
+    from paper_2507_01631_b200 import build
+
+    build.build_examples()
+    scene = synth.make_scene(3, 3, tile_side=128.0, n_views=3, gsd=1.0, seed=31)
+    fc = FieldConfig.defaults()
+    tc = TrainConfig.defaults(batch_rays=1024, seed=4)
+    o = Oracle()
+    ses = Session(o, scene, fc, tc, workers=8)
+    ses.set_window(0, 1)
+    ses.build_accept()
+    rng = np.random.default_rng(5)
+    d = str(tmp_path)
+    for k in range(4):
+        st = ses.tile_state(k)
+        st["enc"] = (st["enc"] + rng.normal(0, 0.5, st["enc"].shape)).astype(np.float32)
+        ses.set_tile_state(k, st)
+        _w(d, f"enc{k}.bin", st["enc"])
+        _w(d, f"dnet{k}.bin", st["dnet"])
+    color = ses.color()[0]
+    _w(d, "color.bin", color)
+    ses.sample(2, 0, 1024, True)
+    b = ses.batch()
+    _w(d, "rays.bin", b["rays"])
+    for f in ("offsets", "t", "delta", "local", "slot", "endpoint"):
+        _w(d, f + ".bin", b[f])
+    sg, rgb = ses.forward()
+    comp = ses.composite()
+    ses.backward()
+    _w(d, "d_sigma.bin", comp["d_sigma"])
+    _w(d, "d_rgb.bin", comp["d_rgb"])
+    m0 = (rng.normal(size=color.size) * 1e-3).astype(np.float32)
+    v0 = (rng.random(color.size) * 1e-5).astype(np.float32)
+    _w(d, "adam_m.bin", m0)
+    _w(d, "adam_v.bin", v0)
+    p = subprocess.run([EXE, d], capture_output=True, text=True, timeout=300)
+    assert p.returncode == 0, p.stdout + p.stderr
+    assert "expected error: adam_step: non-finite gradient in group color" in p.stdout
+    # forward_batch: sigma / rgb (bf16 tensor-core field, stated tolerances of test_gpu_parity)
+    np.testing.assert_allclose(_r(d, "out_sigma.bin", np.float32), sg, rtol=2e-2, atol=1e-6)
+    np.testing.assert_allclose(_r(d, "out_rgb.bin", np.float32).reshape(-1, 3), rgb, atol=5e-3)
+    # backward_batch from the oracle's d_sigma / d_rgb: K4-alone tolerances
+    for k in range(4):
+        re, rd, rc = ses.grads(k)
+        for name, got, ref, tol in (("enc", _r(d, f"out_genc{k}.bin", np.float32), re, 0.05),
+                                    ("dnet", _r(d, f"out_gdnet{k}.bin", np.float32), rd, 0.03)):
+            rel = np.linalg.norm(got - ref) / max(np.linalg.norm(ref), 1e-30)
+            assert rel < tol, (k, name, rel)
+    gc = _r(d, "out_gcolor.bin", np.float32)
+    rc = ses.grads(0)[2]
+    assert np.linalg.norm(gc - rc) / np.linalg.norm(rc) < 0.01
+    # adam_step on the GPU == the reference formula on the same gradient, bit for bit
+    pr, mr, vr = color.copy(), m0.copy(), v0.copy()
+    s = o.adam_step(pr, gc, mr, vr, 7, lr=1e-3)
+    assert int(_r(d, "out_adam_step.bin", np.uint64)[0]) == s == 8
+    assert _r(d, "out_adam_p.bin", np.float32).tobytes() == pr.tobytes()
+    assert _r(d, "out_adam_m.bin", np.float32).tobytes() == mr.tobytes()
+    assert _r(d, "out_adam_v.bin", np.float32).tobytes() == vr.tobytes()
