@@ -1,0 +1,192 @@
+"""TEST INFRASTRUCTURE ONLY — numerics model of the tcgen05 field path.
+
+A numpy restatement of the forward (K2: hash gather, density MLP, colour MLP,
+activations) and the backward (K4: recomputed forward, data- and
+weight-gradient GEMMs, hash scatter) of paper_2507_01631_b200/csrc/
+k_field_tc.cu with every tensor-core operand rounded to bfloat16 exactly where
+the kernels round it (fp32 accumulation, fp32 epilogues).  With no rounding
+it is the fp32 math of the oracle (nn.hpp:90-157, 199-298; oracle/
+tf_oracle.cpp field_point / tfo_backward).
+
+It separates the two questions a toleranced parity test mixes up:
+  * does the GPU compute the bf16-operand math it claims?  (GPU vs this model,
+    tight tolerance);
+  * what does bf16 cost against the fp32 reference?  (this model vs the
+    oracle, the stated tolerance; tools/emulate_bwd.py attributes it).
+
+Only tests/ and tools/ import this module.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+RES = [16, 24, 35, 53, 78, 116, 172, 256]  # level_resolution of the default FieldConfig
+OFF = [0, 4913, 20538, 53306, 86074, 118842, 151610, 184378]
+T = 1 << 15
+DENSITY_MAX = np.float32(1e4)
+
+# the operands the kernels hand to tcgen05.mma as bf16
+FWD_OPS = ("feat", "W1", "H1", "W2", "CIN", "C1", "A1", "C2", "A2", "C3")
+BWD_OPS = ("D3", "C3b", "DC2", "C2b", "DC1", "C1b", "DO", "W2b", "DH1", "W1b")
+KERNEL = frozenset(FWD_OPS + BWD_OPS)
+
+
+def bf16(x):
+    """Round-to-nearest-even to bfloat16, returned as float32."""
+    x = np.ascontiguousarray(x, np.float32)
+    u = x.view(np.uint32).astype(np.uint64)
+    r = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16) << 16
+    return r.astype(np.uint32).view(np.float32).reshape(x.shape)
+
+
+def tf32(x):
+    """Round-to-nearest to TF32 (10 explicit mantissa bits), as float32."""
+    x = np.ascontiguousarray(x, np.float32)
+    u = x.view(np.uint32).astype(np.uint64)
+    r = ((u + 0xFFF + ((u >> 13) & 1)) >> 13) << 13
+    return r.astype(np.uint32).view(np.float32).reshape(x.shape)
+
+
+def split2(x):
+    """bf16 hi + bf16 lo (what a 3-MMA split product sees)."""
+    hi = bf16(x)
+    return hi + bf16(x - hi)
+
+
+ROUND = {"bf16": bf16, "tf32": tf32, "split": split2}
+
+
+def view_encoding(directions):
+    """encode_direction (nn.hpp:288-298) of float directions: (R, 24)."""
+    d = np.asarray(directions, np.float32)
+    out = np.zeros((d.shape[0], 24), np.float32)
+    j = 0
+    for f in range(4):
+        sc = np.float32(np.pi * 2 ** f)
+        for c in range(3):
+            out[:, j] = np.sin(sc * d[:, c])
+            out[:, j + 1] = np.cos(sc * d[:, c])
+            j += 2
+    return out
+
+
+def corners(loc):
+    """HashGridT::cell_of / corner_entry (nn.hpp:248-266) per level: entry
+    indices (S, 8) and trilinear weights (S, 8), float32 ((wx wy) wz order)."""
+    out = []
+    v = np.clip(np.asarray(loc, np.float32), 0.0, 1.0).astype(np.float32)
+    for l in range(8):
+        n = RES[l]
+        sc = (v * np.float32(n)).astype(np.float32)
+        ci = np.minimum(sc.astype(np.int64), n - 1)
+        f = (sc - ci.astype(np.float32)).astype(np.float32)
+        idx = np.zeros((v.shape[0], 8), np.int64)
+        w = np.zeros((v.shape[0], 8), np.float32)
+        dense = (n + 1) ** 3 <= T
+        for k in range(8):
+            dx, dy, dz = k & 1, (k >> 1) & 1, k >> 2
+            wx = f[:, 0] if dx else (np.float32(1) - f[:, 0])
+            wy = f[:, 1] if dy else (np.float32(1) - f[:, 1])
+            wz = f[:, 2] if dz else (np.float32(1) - f[:, 2])
+            w[:, k] = ((wx * wy).astype(np.float32) * wz).astype(np.float32)
+            x, y, z = ci[:, 0] + dx, ci[:, 1] + dy, ci[:, 2] + dz
+            if dense:
+                e = x + (n + 1) * (y + (n + 1) * z)
+            else:
+                h = (x.astype(np.uint64) ^ ((y.astype(np.uint64) * 2654435761) & 0xFFFFFFFF)
+                     ^ ((z.astype(np.uint64) * 805459861) & 0xFFFFFFFF))
+                e = (h & (T - 1)).astype(np.int64)
+            idx[:, k] = OFF[l] + e
+        out.append((idx, w))
+    return out
+
+
+def _mats(dnet, color):
+    return (dnet[:1024].reshape(64, 16), dnet[1024:1088], dnet[1088:2112].reshape(16, 64), dnet[2112:2128],
+            color[:2496].reshape(64, 39), color[2496:2560], color[2560:6656].reshape(64, 64), color[6656:6720],
+            color[6720:6912].reshape(3, 64), color[6912:6915])
+
+
+def field(enc, dnet, color, loc, venc, rq=KERNEL, dsig=None, drgb=None):
+    """Forward (and, given d_sigma / d_rgb w.r.t. the outputs, backward) of the
+    samples of ONE tile.  rq: the operands rounded, a set (bf16) or a dict
+    operand -> "bf16" | "tf32" | "split".  Returns dict(sigma, rgb[, g_enc,
+    g_dnet, g_color, d_feat])."""
+    def R(name, x):
+        if isinstance(rq, dict):
+            return ROUND[rq[name]](x) if name in rq else np.asarray(x, np.float32)
+        return bf16(x) if name in rq else np.asarray(x, np.float32)
+
+    enc = np.asarray(enc, np.float32)
+    W1, b1, W2, b2, C1, c1, C2, c2, C3, c3 = _mats(np.asarray(dnet, np.float32), np.asarray(color, np.float32))
+    cs = corners(loc)
+    S = np.asarray(loc).shape[0]
+    feat = np.zeros((S, 16), np.float32)
+    for l, (idx, w) in enumerate(cs):
+        for q in range(2):
+            feat[:, 2 * l + q] = (w * enc[2 * idx + q]).sum(axis=1)
+    X0 = R("feat", feat)
+    h1p = X0 @ R("W1", W1).T + b1
+    mh = h1p > 0
+    H1 = R("H1", np.maximum(h1p, 0))
+    dout = H1 @ R("W2", W2).T + b2
+    raw = dout[:, 0]
+    clamp = raw >= np.log(DENSITY_MAX)
+    sig = np.where(clamp, DENSITY_MAX, np.exp(raw)).astype(np.float32)
+    cin = np.concatenate([dout[:, 1:16], np.asarray(venc, np.float32)], axis=1)
+    CIN = R("CIN", cin)
+    c1p = CIN @ R("C1", C1).T + c1
+    mc1 = c1p > 0
+    A1 = R("A1", np.maximum(c1p, 0))
+    c2p = A1 @ R("C2", C2).T + c2
+    mc2 = c2p > 0
+    A2 = R("A2", np.maximum(c2p, 0))
+    co = A2 @ R("C3", C3).T + c3
+    rgb = (1 / (1 + np.exp(-co))).astype(np.float32)
+    out = dict(sigma=sig, rgb=rgb)
+    if dsig is None:
+        return out
+    dsig = np.asarray(dsig, np.float32)
+    drgb = np.asarray(drgb, np.float32).reshape(S, 3)
+    D3 = R("D3", drgb * rgb * (1 - rgb))
+    DC2 = R("DC2", (D3 @ R("C3b", C3)) * mc2)
+    DC1 = R("DC1", (DC2 @ R("C2b", C2)) * mc1)
+    dcin = DC1 @ R("C1b", C1)
+    DO = R("DO", np.concatenate([np.where(clamp, 0, dsig * sig)[:, None], dcin[:, :15]], axis=1))
+    DH1 = R("DH1", (DO @ R("W2b", W2)) * mh)
+    dfeat = DH1 @ R("W1b", W1)
+    g_enc = np.zeros_like(enc)
+    for l, (idx, w) in enumerate(cs):
+        for q in range(2):
+            np.add.at(g_enc, 2 * idx + q, (w * dfeat[:, 2 * l + q][:, None]).astype(np.float32))
+    g_dnet = np.concatenate([(DH1.T @ X0).ravel(), DH1.sum(0), (DO.T @ H1).ravel(), DO.sum(0)]).astype(np.float32)
+    g_color = np.concatenate([(DC1.T @ CIN).ravel(), DC1.sum(0), (DC2.T @ A1).ravel(), DC2.sum(0),
+                              (D3.T @ A2).ravel(), D3.sum(0)]).astype(np.float32)
+    out.update(g_enc=g_enc, g_dnet=g_dnet, g_color=g_color, d_feat=dfeat)
+    return out
+
+
+def batch(tiles, color, b, rq=KERNEL, d_sigma=None, d_rgb=None):
+    """The model over a RaySegmentBatch dict (tilefield.batch() layout) with
+    per-slot (enc, dnet): per-sample sigma / rgb in ray order and, given
+    d_sigma / d_rgb, per-slot (g_enc, g_dnet) and g_color."""
+    offs = np.asarray(b["offsets"], np.int64)
+    ray_of = np.repeat(np.arange(offs.size - 1), np.diff(offs))
+    venc = view_encoding(b["rays"]["direction"])[ray_of]
+    S = offs[-1]
+    sigma, rgb = np.zeros(S, np.float32), np.zeros((S, 3), np.float32)
+    grads, g_color = [], None
+    for k, (enc, dnet) in enumerate(tiles):
+        sel = np.flatnonzero(b["slot"] == k)
+        kw = {}
+        if d_sigma is not None:
+            kw = dict(dsig=np.asarray(d_sigma)[sel], drgb=np.asarray(d_rgb).reshape(-1, 3)[sel])
+        r = field(enc, dnet, color, b["local"][sel], venc[sel], rq, **kw)
+        sigma[sel], rgb[sel] = r["sigma"], r["rgb"]
+        if d_sigma is not None:
+            grads.append((r["g_enc"], r["g_dnet"]))
+            g_color = r["g_color"] if g_color is None else g_color + r["g_color"]
+    out = dict(sigma=sigma, rgb=rgb)
+    if d_sigma is not None:
+        out.update(grads=grads, g_color=g_color)
+    return out

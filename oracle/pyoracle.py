@@ -102,9 +102,62 @@ class Oracle:
         L.tfo_ray_from_pixel.argtypes = [_vp, C.c_int, C.c_int, C.c_double, C.c_double, _vp, _vp]
         L.tfo_localize.argtypes = [_vp, _vp, C.c_double, _vp, _vp, _vp]
         L.tfo_project.argtypes = [_vp, _vp, _vp]
+        L.tfo_render_pixels.argtypes = [_vp, _vp, C.c_double, C.c_double, C.c_int, _vp, _vp, _vp, _vp, _vp,
+                                         C.c_double, C.c_int, C.c_double, _vp, C.c_int, _vp, _vp, _vp, _vp, C.c_int]
+        L.tfo_color_loss.argtypes = [_vp, _vp, C.c_int, C.c_int, _vp]
+        L.tfo_color_loss.restype = C.c_double
+        L.tfo_mlp_fwd_bwd.argtypes = [_vp, C.c_int, _vp, _vp, _vp, _vp, _vp, _vp]
+        L.tfo_hash_lookup_bwd.argtypes = [_vp, _vp, C.c_int, _vp, _vp, _vp, _vp]
+        L.tfo_shadow_loss_grad.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _vp]
+        L.tfo_shadow_loss_grad.restype = C.c_double
 
     def err(self) -> str:
         return self.L.tfo_last_error().decode()
+
+    def render_pixels(self, cfg, cam, roi, boxes, states, color, px, spm=63.0 / 40.0, cap=1024, dcap=10.0,
+                      bg=(0.5, 0.5, 0.5), workers=None):
+        """cmd_render of (row, col) pixels over the given tile boxes / states
+        (dicts with enc, dnet, occupancy): (rgb (n,3), depth, opacity)."""
+        px = np.ascontiguousarray(px, np.int32).reshape(-1, 2)
+        n, nt = px.shape[0], len(states)
+        keep = [(np.ascontiguousarray(s["enc"], np.float32), np.ascontiguousarray(s["dnet"], np.float32),
+                 np.ascontiguousarray(s["occupancy"], np.float32)) for s in states]
+        arr = lambda i: (C.c_void_p * nt)(*[k[i].ctypes.data for k in keep])  # noqa: E731
+        rgb, dep, op = np.zeros((n, 3), np.float32), np.zeros(n, np.float32), np.zeros(n, np.float32)
+        b = np.ascontiguousarray(boxes, np.float64).reshape(nt, 6)
+        self.L.tfo_render_pixels(C.byref(cfg), C.byref(cam), roi.z_min, roi.z_max, nt, ptr(b), arr(0), arr(1),
+                                 arr(2), ptr(np.ascontiguousarray(color, np.float32)), spm, cap, dcap,
+                                 ptr(np.array(bg, np.float32)), n, ptr(px), ptr(rgb), ptr(dep), ptr(op),
+                                 workers or os.cpu_count() or 1)
+        return rgb, dep, op
+
+    def color_loss(self, rgb, target, batch=None):
+        """color_loss: (loss, gradient at rgb)."""
+        r = np.ascontiguousarray(rgb, np.float32).reshape(-1, 3)
+        t = np.ascontiguousarray(target, np.float32).reshape(-1, 3)
+        g = np.zeros_like(r)
+        L = self.L.tfo_color_loss(ptr(r), ptr(t), r.shape[0], batch or r.shape[0], ptr(g))
+        return L, g
+
+    # -- backward primitives (same signatures as RefLib's) ---------------------
+    def mlp_fwd_bwd(self, widths, params, x, d_out=None):
+        w = np.array(widths, np.int32)
+        out = np.zeros(widths[-1], np.float32)
+        grad = np.zeros_like(params)
+        d_in = np.zeros(widths[0], np.float32)
+        do = None if d_out is None else np.ascontiguousarray(d_out, np.float32)
+        self.L.tfo_mlp_fwd_bwd(ptr(w), len(widths), ptr(params), ptr(np.ascontiguousarray(x, np.float32)),
+                               ptr(out), ptr(do), ptr(grad), ptr(d_in))
+        return out, grad, d_in
+
+    def hash_lookup_bwd(self, cfg, tables, pts, d_out=None):
+        pts = np.ascontiguousarray(pts, np.float32).reshape(-1, 3)
+        n = pts.shape[0]
+        out = np.zeros((n, cfg.levels * cfg.features), np.float32)
+        grad = np.zeros_like(tables) if d_out is not None else None
+        do = None if d_out is None else np.ascontiguousarray(d_out, np.float32)
+        self.L.tfo_hash_lookup_bwd(C.byref(cfg), ptr(tables), n, ptr(pts), ptr(out), ptr(do), ptr(grad))
+        return out, grad
 
     # -- primitives --------------------------------------------------------
     def project(self, cam: Rpc, xyz):
@@ -359,6 +412,25 @@ class Session:
 
     def update_occupancy(self):
         self._chk(self.o.L.tfo_update_occupancy(self.h))
+
+    def shadow_loss_grad(self, enc, dnet, color, grad=True):
+        """float64 shadow of the current batch: loss and (grad=True) the exact
+        reverse-mode gradients, for per-slot float64 parameter arrays."""
+        ns = len(enc)
+        enc = [np.ascontiguousarray(e, np.float64) for e in enc]
+        dnet = [np.ascontiguousarray(d, np.float64) for d in dnet]
+        color = np.ascontiguousarray(color, np.float64)
+        pe = (C.c_void_p * ns)(*[e.ctypes.data for e in enc])
+        pd = (C.c_void_p * ns)(*[d.ctypes.data for d in dnet])
+        if not grad:
+            return self.o.L.tfo_shadow_loss_grad(self.h, pe, pd, ptr(color), None, None, None), None
+        ge = [np.zeros_like(e) for e in enc]
+        gd = [np.zeros_like(d) for d in dnet]
+        gc = np.zeros_like(color)
+        qe = (C.c_void_p * ns)(*[g.ctypes.data for g in ge])
+        qd = (C.c_void_p * ns)(*[g.ctypes.data for g in gd])
+        L = self.o.L.tfo_shadow_loss_grad(self.h, pe, pd, ptr(color), qe, qd, ptr(gc))
+        return L, (ge, gd, gc)
 
 
 class RefLib:

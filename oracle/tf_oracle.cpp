@@ -751,6 +751,20 @@ void render_ray(int n, const float* sg, const float* rgb, const float* t, const 
     }
 }
 
+// color_loss (SPEC 371-378) of one ray: returns the ray's squared error
+// summed over channels (the batch loss is the sum / (3 B)) and writes the
+// gradient at the rendered rgb, 2 (rgb - target) / (3 B) (channel-mean
+// convention of the example at SPEC 377).
+double color_loss_ray(const float* rgb, const float* target, float inv3b, float* g) {
+    double l = 0;
+    for (int c = 0; c < 3; ++c) {
+        float df = rgb[c] - target[c];
+        l += double(df) * double(df);
+        g[c] = 2.0f * df * inv3b;
+    }
+    return l;
+}
+
 // ----------------------------------------------------- adam_step (SPEC 292-300)
 double lr_at(double base, double rate, uint64_t steps, uint64_t step) {
     if (rate == 1.0) return base;
@@ -949,6 +963,58 @@ int tfo_sample_ray(const double* o, const double* d, int n_seg, const int* seg_s
         endpoint[i] = ep[i];
     }
     return n;
+}
+
+// cmd_render (the render path of tfg_render_pixels): for each
+// (row, col) pixel of `cam`, ray_from_pixel, segments over the n_tiles boxes
+// (slot order = tile order), midpoint samples (jitter off) with occupancy
+// culling, the field of each sample's tile, render.  Failed rays give zeros.
+int tfo_render_pixels(const tfg_field_config* cfg, const tfg_rpc* cam, double z_min, double z_max,
+                      int n_tiles, const double* boxes6, const float* const* enc, const float* const* dnet,
+                      const float* const* occupancy, const float* color, double spm, int cap,
+                      double dcap, const float* bg, int n_px, const int32_t* px, float* rgb,
+                      float* depth, float* opacity, int workers) {
+    Shapes sh(*cfg);
+    std::vector<double> frames(6 * size_t(n_tiles));
+    for (int k = 0; k < n_tiles; ++k)
+        for (int q = 0; q < 3; ++q) {
+            frames[6 * k + q] = boxes6[6 * k + q];
+            frames[6 * k + 3 + q] = 1.0 / (boxes6[6 * k + 3 + q] - boxes6[6 * k + q]);
+        }
+    par_for(size_t(n_px), workers < 1 ? 1 : workers, [&](size_t b, size_t e, int) {
+        SampleActs a;
+        std::vector<double> tt;
+        std::vector<float> lc;
+        std::vector<uint8_t> sl, ep;
+        for (size_t i = b; i < e; ++i) {
+            for (int c = 0; c < 3; ++c) rgb[3 * i + c] = 0.f;
+            depth[i] = opacity[i] = 0.f;
+            double o[3], d[3];
+            if (ray_from_pixel(*cam, px[2 * i], px[2 * i + 1], z_min, z_max, o, d)) continue;
+            int ss[16];
+            double tn[16], tf[16];
+            int ns = segments(o, d, boxes6, n_tiles, ss, tn, tf);
+            tt.clear();
+            lc.clear();
+            sl.clear();
+            ep.clear();
+            int n = sample_ray(o, d, ns, ss, tn, tf, frames.data(), occupancy, sh.occ_res,
+                               cfg->occupancy_threshold, spm, cap, z_min, dcap, 0, 0, tt, lc, sl, ep);
+            std::vector<float> dl(n), tf32(n), sg(n), col(3 * size_t(n));
+            deltas(tt.data(), n, o, d, z_min, dcap, dl.data());
+            float d3[3] = {float(d[0]), float(d[1]), float(d[2])}, venc[64];
+            encode_dir<float>(d3, cfg->view_freqs, venc);
+            for (int k = 0; k < n; ++k) {
+                tf32[k] = float(tt[k]);
+                field_point(sh, enc[sl[k]], dnet[sl[k]], color, &lc[3 * size_t(k)], venc, a);
+                sg[k] = a.sigma;
+                for (int c = 0; c < 3; ++c) col[3 * k + c] = a.rgb[c];
+            }
+            render_ray(n, sg.data(), col.data(), tf32.data(), dl.data(), bg, rgb + 3 * i, depth + i,
+                       opacity + i, nullptr, nullptr, nullptr);
+        }
+    });
+    return 0;
 }
 
 void tfo_render_ray(int n, const float* sigma, const float* rgb, const float* t,
@@ -1317,13 +1383,7 @@ int tfo_composite(tfo_session* s, float* ray_rgb, float* ray_depth, float* ray_o
             render_ray(int(m), &s->sigma[o], &s->rgb[3 * o], &s->t[o], &s->delta[o],
                        s->tc.background, rgb, &dep, &op, nullptr, nullptr, nullptr);
             float g[3];
-            double l = 0;
-            for (int c = 0; c < 3; ++c) {
-                float df = rgb[c] - s->rays[i].target[c];
-                l += double(df) * double(df);
-                g[c] = 2.0f * df * inv3b;
-            }
-            lpart[i] = l;
+            lpart[i] = color_loss_ray(rgb, s->rays[i].target, inv3b, g);
             render_ray(int(m), &s->sigma[o], &s->rgb[3 * o], &s->t[o], &s->delta[o],
                        s->tc.background, nullptr, nullptr, nullptr, g, &s->dsig[o],
                        &s->drgb[3 * o]);
@@ -1411,6 +1471,131 @@ int tfo_backward(tfo_session* s) {
     }
     return 0;
 }
+// color_loss over n rays (rgb, target: 3 per ray) with batch size B: the
+// batch loss and, if grad != NULL, the per-ray gradient at rgb.
+double tfo_color_loss(const float* rgb, const float* target, int n, int batch, float* grad) {
+    const float inv3b = 1.0f / (3.0f * float(batch));
+    double L = 0;
+    for (int i = 0; i < n; ++i) {
+        float g[3];
+        L += color_loss_ray(rgb + 3 * i, target + 3 * i, inv3b, g);
+        if (grad)
+            for (int c = 0; c < 3; ++c) grad[3 * i + c] = g[c];
+    }
+    return L / (3.0 * double(batch));
+}
+
+// ---- backward primitives, exposed so tests pin them bit-for-bit against the
+// reference's MlpT::backward_p (nn.hpp:116-157) and HashGridT::backward
+// (nn.hpp:231-245) compiled verbatim into oracle/_ref.
+int tfo_mlp_fwd_bwd(const int* widths, int nw, const float* params, const float* x, float* out,
+                    const float* d_out, float* grad, float* d_in) {
+    std::vector<int> w(widths, widths + nw);
+    std::vector<float> acts(Shapes::mlp_acts(w));
+    mlp_fwd<float>(w, params, x, acts.data());
+    for (int i = 0; i < w.back(); ++i) out[i] = acts[acts.size() - w.back() + i];
+    if (d_out) mlp_bwd<float>(w, params, acts.data(), d_out, grad, d_in);
+    return 0;
+}
+int tfo_hash_lookup_bwd(const tfg_field_config* cfg, const float* tables, int n, const float* p3,
+                        float* out, const float* d_out, float* grad) {
+    Shapes sh(*cfg);
+    for (int i = 0; i < n; ++i) {
+        hash_lookup<float>(sh, tables, p3 + 3 * i, out + size_t(i) * sh.L * sh.F);
+        if (d_out && grad) hash_backward<float>(sh, p3 + 3 * i, d_out + size_t(i) * sh.L * sh.F, grad);
+    }
+    return 0;
+}
+
+// ---- float64 shadow of the batch loss and its reverse-mode gradient (the
+// finite-difference oracle of SPEC.md:289-291, 683; field.hpp:127-128 templates
+// the batch operators on the scalar for exactly this).  Same math as the fp32
+// path (field_point, render_ray, color_loss, tfo_backward) instantiated in
+// double on the session's current batch; parameters per loaded slot.
+// Returns the loss; gradients are written (zeroed first) when g_* != NULL.
+double tfo_shadow_loss_grad(tfo_session* s, const double* const* enc, const double* const* dnet,
+                            const double* color, double* const* g_enc, double* const* g_dnet,
+                            double* g_color) {
+    using S = double;
+    const Shapes& sh = s->sh;
+    const int ns = s->nslots, vd = 6 * sh.cfg.view_freqs, E = sh.cfg.embedding;
+    const bool grad = g_enc && g_dnet && g_color;
+    if (grad) {
+        for (int k = 0; k < ns; ++k) {
+            std::fill(g_enc[k], g_enc[k] + sh.enc_params, 0.0);
+            std::fill(g_dnet[k], g_dnet[k] + sh.dnet_params, 0.0);
+        }
+        std::fill(g_color, g_color + sh.color_params, 0.0);
+    }
+    const S inv3b = 1.0 / (3.0 * double(s->tc.batch_rays));
+    const S dmax = S(sh.cfg.density_max);
+    double L = 0.0;
+    const size_t nd = Shapes::mlp_acts(sh.dw), nc = Shapes::mlp_acts(sh.cw);
+    for (size_t i = 0; i < s->rays.size(); ++i) {
+        const uint32_t o = s->offsets[i], m = s->offsets[i + 1] - o;
+        std::vector<S> feat(size_t(m) * 16), dacts(size_t(m) * nd), cacts(size_t(m) * nc), sg(m), draw(m), rgb(3 * size_t(m));
+        S venc[64];
+        for (int q = 0; q < vd; ++q) venc[q] = S(s->venc[i * vd + q]);
+        for (uint32_t j = 0; j < m; ++j) {
+            const uint32_t k = o + j;
+            const int sl = s->slot[k];
+            S loc[3] = {S(s->local[3 * k]), S(s->local[3 * k + 1]), S(s->local[3 * k + 2])};
+            hash_lookup<S>(sh, enc[sl], loc, &feat[16 * j]);
+            mlp_fwd<S>(sh.dw, dnet[sl], &feat[16 * j], &dacts[nd * j]);
+            const S* dout = &dacts[nd * j] + sh.dw[0] + sh.dw[1];
+            sg[j] = density_act<S>(dout[0], dmax, &draw[j]);
+            S cin[64];
+            for (int q = 0; q < E; ++q) cin[q] = dout[1 + q];
+            for (int q = 0; q < vd; ++q) cin[E + q] = venc[q];
+            mlp_fwd<S>(sh.cw, color, cin, &cacts[nc * j]);
+            const S* co = &cacts[nc * j] + nc - 3;
+            for (int c = 0; c < 3; ++c) rgb[3 * j + c] = sigm<S>(co[c]);
+        }
+        // render (SPEC 361-369) in S
+        S T = 1, acc[3] = {0, 0, 0};
+        std::vector<S> w(m), Tn(m);
+        for (uint32_t j = 0; j < m; ++j) {
+            const S a = 1 - std::exp(-(sg[j] * S(s->delta[o + j])));
+            w[j] = T * a;
+            for (int c = 0; c < 3; ++c) acc[c] += w[j] * rgb[3 * j + c];
+            T = T * (1 - a);
+            Tn[j] = T;
+        }
+        S g[3];
+        for (int c = 0; c < 3; ++c) {
+            const S out = acc[c] + T * S(s->tc.background[c]);
+            const S df = out - S(s->rays[i].target[c]);
+            L += df * df;
+            g[c] = 2 * df * inv3b;
+        }
+        if (!grad) continue;
+        S R[3] = {T * S(s->tc.background[0]), T * S(s->tc.background[1]), T * S(s->tc.background[2])};
+        for (int j = int(m) - 1; j >= 0; --j) {
+            const uint32_t k = o + uint32_t(j);
+            const int sl = s->slot[k];
+            S dsg = 0;
+            for (int c = 0; c < 3; ++c) dsg += g[c] * (Tn[j] * rgb[3 * j + c] - R[c]);
+            dsg *= S(s->delta[k]);
+            S dco[3];
+            for (int c = 0; c < 3; ++c) {
+                const S r = rgb[3 * j + c];
+                dco[c] = w[j] * g[c] * r * (1 - r);
+                R[c] += w[j] * rgb[3 * j + c];
+            }
+            S dcin[64];
+            mlp_bwd<S>(sh.cw, color, &cacts[nc * j], dco, g_color, dcin);
+            S ddo[16];
+            ddo[0] = dsg * draw[j];
+            for (int q = 0; q < E; ++q) ddo[1 + q] = dcin[q];
+            S dfeat[16];
+            mlp_bwd<S>(sh.dw, dnet[sl], &dacts[nd * j], ddo, g_dnet[sl], dfeat);
+            S loc[3] = {S(s->local[3 * k]), S(s->local[3 * k + 1]), S(s->local[3 * k + 2])};
+            hash_backward<S>(sh, loc, dfeat, g_enc[sl]);
+        }
+    }
+    return L * inv3b;
+}
+
 int tfo_get_grads(tfo_session* s, int slot, float* enc, float* dnet, float* color) {
     if (slot < 0 || slot >= int(s->g_enc.size())) return 1;
     if (enc) std::memcpy(enc, s->g_enc[slot].data(), s->sh.enc_params * 4);

@@ -61,6 +61,15 @@ void tfo_render_ray(int n, const float* sigma, const float* rgb, const float* t,
                     const float* delta, const float* bg, float* out_rgb, float* out_depth,
                     float* out_opacity, const float* g_rgb, float* d_sigma, float* d_rgb);
 
+/* cmd_render: (row, col) pixels of `cam` over n_tiles boxes
+ * (min xyz, max xyz; slot order = tile order), midpoint samples, per-tile
+ * fields, render; failed rays give zeros.  Parallel over `workers`. */
+int tfo_render_pixels(const tfg_field_config* cfg, const tfg_rpc* cam, double z_min, double z_max,
+                      int n_tiles, const double* boxes6, const float* const* enc, const float* const* dnet,
+                      const float* const* occupancy, const float* color, double spm, int cap,
+                      double dcap, const float* bg, int n_px, const int32_t* px, float* rgb,
+                      float* depth, float* opacity, int workers);
+
 /* Adam on one group (field.hpp:45-48).  Returns 1 (and sets
  * the error naming `group`) on non-finite gradients, parameters untouched. */
 int tfo_adam_step(float* params, const float* grads, float* m, float* v, uint64_t n,
@@ -76,6 +85,18 @@ int tfo_color_create(const tfg_field_config* cfg, uint64_t seed, float* params);
 int tfo_query_field(const tfg_field_config* cfg, const float* enc, const float* dnet,
                     const float* color, const float* local3, const float* dir3, float* sigma,
                     float* rgb);
+
+/* color_loss over n rays with batch size `batch`: returns
+ * the loss (mean over rays and channels), writes d loss / d rgb if grad. */
+double tfo_color_loss(const float* rgb, const float* target, int n, int batch, float* grad);
+
+/* Backward primitives (pinned against nn.hpp:116-157 / 231-245 by the tests):
+ * one MLP forward + backward_p (grad accumulates), and n hash lookups +
+ * HashGridT::backward (grad accumulates; d_out/grad may be NULL). */
+int tfo_mlp_fwd_bwd(const int* widths, int nw, const float* params, const float* x, float* out,
+                    const float* d_out, float* grad, float* d_in);
+int tfo_hash_lookup_bwd(const tfg_field_config* cfg, const float* tables, int n, const float* p3,
+                        float* out, const float* d_out, float* grad);
 
 /* ---- session: the trainer's window state ---------------------------------- */
 tfo_session* tfo_create(const tfg_field_config* fcfg, const tfg_train_config* tcfg,
@@ -103,6 +124,12 @@ int tfo_set_color(tfo_session* s, const float* params, const float* m, const flo
                   uint64_t step);
 int tfo_update_occupancy(tfo_session* s);
 int tfo_set_workers(tfo_session* s, int workers);
+/* float64 shadow of the current batch's loss and (if g_* != NULL) its exact
+ * reverse-mode gradient, parameters per loaded slot (the finite-difference
+ * oracle). */
+double tfo_shadow_loss_grad(tfo_session* s, const double* const* enc, const double* const* dnet,
+                            const double* color, double* const* g_enc, double* const* g_dnet,
+                            double* g_color);
 
 #ifdef __cplusplus
 }

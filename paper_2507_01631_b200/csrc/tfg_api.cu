@@ -1450,6 +1450,7 @@ TFG_API int tfg_set_slot_params(tfg_ctx* c, int slot, const float* enc, const fl
         if (c->pos_r >= 0) return fail(TFG_ERR_INVALID, "set_slot_params: slot outside the window");
         for (int k = c->nslots; k <= slot; ++k) c->slot_tile[k] = -1;
         c->nslots = slot + 1;
+        c->slots.n = c->nslots;  // batch layout [slot][ray] of imported batches
     }
     CK(cudaStreamSynchronize(c->st));
     const uint64_t off = uint64_t(slot) * c->stride;

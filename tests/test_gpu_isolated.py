@@ -22,8 +22,16 @@ N_RAYS = 2048
 # K3 in fp32 on both sides: only summation order (warp scans vs sequential)
 # and expf differ
 TOL_K3 = 1e-5
-# K4 alone: the backward's GEMMs take bf16 operands (fp32 accumulate)
-TOL_K4_GRAD_REL = {"enc": 0.05, "dnet": 0.03, "color": 0.01}
+# K4 alone vs the fp32 oracle: the field's tensor-core operands are bf16
+# (fp32 accumulate).  Measured on B200 (r02): enc 6.6%, dnet 1.6%, colour
+# 0.4% norm-relative; the CPU numerics model (oracle/bf16_model.py) predicts
+# the same 6.6%, and attributes it to ReLU masks of the bf16 forward
+# recompute flipping near zero (the backward GEMMs alone cost 0.5%;
+# tools/emulate_bwd.py).
+TOL_K4_GRAD_REL = {"enc": 0.09, "dnet": 0.03, "color": 0.01}
+# GPU vs the bf16 numerics model (same roundings): what is left is fp32
+# accumulation order inside the MMAs / atomics, FMA contraction, expf
+TOL_MODEL_GRAD_REL = {"enc": 0.02, "dnet": 0.01, "color": 0.005}
 
 
 @pytest.fixture(scope="module")
@@ -107,7 +115,13 @@ def test_composite_alone_matches_oracle(pair):
     np.testing.assert_allclose(got["depth"], ref["depth"], rtol=TOL_K3, atol=TOL_K3)
     assert abs(got["loss"] - ref["loss"]) <= TOL_K3 * abs(ref["loss"])
     np.testing.assert_allclose(got["d_rgb"], ref["d_rgb"], rtol=0, atol=TOL_K3 * np.abs(ref["d_rgb"]).max())
-    np.testing.assert_allclose(got["d_sigma"], ref["d_sigma"], rtol=0, atol=TOL_K3 * np.abs(ref["d_sigma"]).max())
+    # d_sigma_k = delta_k sum_c g_c (T_{k+1} c_k - R_k) is a difference of terms
+    # bounded by delta_k |g| (|T c|, |R| <= 1): the tolerance scales with that
+    b = ses.batch()
+    g = 2.0 * (ref["rgb"] - b["rays"]["target"]) / (3.0 * N_RAYS)
+    ray_of = np.repeat(np.arange(N_RAYS), np.diff(b["offsets"].astype(np.int64)))
+    scale = b["delta"] * np.abs(g[ray_of]).sum(axis=1) * 2.0
+    assert np.all(np.abs(got["d_sigma"] - ref["d_sigma"]) <= TOL_K3 * scale + 1e-12)
 
 
 def test_composite_weight_normalisation(pair):
@@ -147,6 +161,39 @@ def test_field_backward_alone(pair):
     print("K4-alone norm-relative gradient error:", worst)
     for name, rel in worst.items():
         assert rel < TOL_K4_GRAD_REL[name], (name, rel)
+
+
+def test_field_matches_bf16_numerics_model(pair):
+    """The GPU computes the bf16-operand math it claims: K2's sigma / rgb and
+    K4's gradients (fed the oracle's d_sigma / d_rgb) against
+    oracle/bf16_model.py with the kernels' roundings."""
+    from oracle import bf16_model as M
+
+    ctx, ses = pair
+    ses.sample(10, 0, N_RAYS, True)
+    ses.forward()
+    ref = ses.composite()
+    b = ses.batch()
+    tiles = [(ses.tile_state(k)["enc"], ses.tile_state(k)["dnet"]) for k in range(4)]
+    model = M.batch(tiles, ses.color()[0], b, M.KERNEL, ref["d_sigma"], ref["d_rgb"])
+    ctx.batch_import(b)
+    sg, rgb = ctx.field_forward()
+    rel_s = np.abs(sg - model["sigma"]) / np.maximum(model["sigma"], 1e-6)
+    d_rgb = np.abs(rgb - model["rgb"])
+    print("K2 vs model: sigma rel p99 %.2e max %.2e, rgb p99 %.2e max %.2e" %
+          (np.quantile(rel_s, 0.99), rel_s.max(), np.quantile(d_rgb, 0.99), d_rgb.max()))
+    assert np.quantile(rel_s, 0.99) < 1e-4 and np.quantile(d_rgb, 0.99) < 1e-5
+    assert rel_s.max() < 2e-2 and d_rgb.max() < 5e-3  # isolated mask flips
+    ctx.field_backward_from(ref["d_sigma"], ref["d_rgb"])
+    worst = {}
+    for k in range(4):
+        ge, gd, gc = ctx.grads(k)
+        for name, a, m in (("enc", ge, model["grads"][k][0]), ("dnet", gd, model["grads"][k][1]),
+                           ("color", gc, model["g_color"])):
+            worst[name] = max(worst.get(name, 0.0), float(np.linalg.norm(a - m) / np.linalg.norm(m)))
+    print("K4 vs bf16 model, norm-relative:", worst)
+    for name, rel in worst.items():
+        assert rel < TOL_MODEL_GRAD_REL[name], (name, rel)
 
 
 def test_field_backward_zero_in_zero_out(pair):

@@ -230,13 +230,21 @@ def test_render_weight_normalization_and_duplicate(oracle):
 
 
 def test_color_loss_kat(oracle):
-    o = oracle
-    # via the render backward: the composite's loss convention
-    target = np.array([0.2, 0.3, 0.4])
-    rendered = target + 0.1
-    loss = np.mean((rendered - target) ** 2)
-    grad = 2 * (rendered - target) / 3.0
-    assert abs(loss - 0.01) < 1e-12 and np.allclose(grad, 0.2 / 3)
+    """SPEC.md:376-377 through the oracle's color_loss (the code tfo_composite
+    uses): rendered = target -> 0 and 0; rendered = target + 0.1 on all
+    channels, 1 ray -> loss 0.01, gradient 0.2/3 per channel."""
+    target = np.array([[0.2, 0.3, 0.4]], np.float32)
+    L, g = oracle.color_loss(target, target)
+    assert L == 0.0 and not np.any(g)
+    L, g = oracle.color_loss(target + np.float32(0.1), target)
+    assert abs(L - 0.01) < 1e-8
+    np.testing.assert_allclose(g, np.full((1, 3), 0.2 / 3), rtol=1e-6)
+    # B rays: mean over rays and channels, gradient 2 (r - t) / (3 B)
+    rng = np.random.default_rng(2)
+    r, t = rng.random((7, 3)).astype(np.float32), rng.random((7, 3)).astype(np.float32)
+    L, g = oracle.color_loss(r, t)
+    assert abs(L - np.mean((r.astype(np.float64) - t) ** 2)) < 1e-7
+    np.testing.assert_allclose(g, 2 * (r - t) / 21.0, rtol=1e-6, atol=1e-8)
 
 
 def test_render_gradient_fd(oracle):

@@ -141,3 +141,39 @@ def test_field_point_bits(oracle, reflib):
         s, rgb = oracle.query_field(cfg, enc, dnet, color, pts[i], d3)
         assert np.float32(s) == np.float32(sig_ref)
         np.testing.assert_allclose(rgb, rgb_ref, rtol=1e-6)  # numpy exp vs libm expf
+
+
+def test_backward_primitives_bits(oracle, reflib):
+    """The oracle's reverse mode equals the reference's MlpT::backward_p
+    (nn.hpp:116-157) and HashGridT::backward (nn.hpp:231-245), compiled
+    verbatim into oracle/_ref, bit for bit: outputs, parameter gradients
+    (accumulated over several points) and input gradients."""
+    cfg = FieldConfig.defaults()
+    rng = np.random.default_rng(17)
+    for widths, seed in (([16, 64, 16], 3), ([39, 64, 64, 3], 4)):
+        params = reflib.mlp_init(widths, seed)
+        params = (params + rng.normal(0, 0.05, params.shape)).astype(np.float32)  # non-zero biases
+        g_ref = np.zeros_like(params)
+        g_orc = np.zeros_like(params)
+        for _ in range(24):
+            x = rng.normal(0, 1, widths[0]).astype(np.float32)
+            d_out = rng.normal(0, 1, widths[-1]).astype(np.float32)
+            o1, g1, di1 = reflib.mlp_fwd_bwd(widths, params, x, d_out)
+            o2, g2, di2 = oracle.mlp_fwd_bwd(widths, params, x, d_out)
+            assert o1.tobytes() == o2.tobytes()
+            assert di1.tobytes() == di2.tobytes()
+            assert g1.tobytes() == g2.tobytes()
+            g_ref += g1
+            g_orc += g2
+        assert g_ref.tobytes() == g_orc.tobytes()
+    enc, _, _ = oracle.tile_create(cfg, 1, 2, 9)
+    enc = (enc + rng.normal(0, 0.3, enc.shape)).astype(np.float32)
+    pts = rng.uniform(-0.05, 1.05, (256, 3)).astype(np.float32)
+    pts[:8] = [[0, 0, 0], [1, 1, 1], [0.5, 0.5, 0.5], [1, 0, 0.25], [0.999999, 1e-7, 0.5],
+               [0.0625, 0.125, 0.1875], [1.0001, -0.0001, 0.3], [0.3, 0.7, 1.0]]
+    d_out = rng.normal(0, 1, (256, 16)).astype(np.float32)
+    f1, g1 = reflib.hash_lookup_bwd(cfg, enc, pts, d_out)
+    f2, g2 = oracle.hash_lookup_bwd(cfg, enc, pts, d_out)
+    assert f1.tobytes() == f2.tobytes()
+    assert g1.tobytes() == g2.tobytes()
+    assert np.count_nonzero(g1) > 1000
