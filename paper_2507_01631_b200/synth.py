@@ -30,6 +30,8 @@ class Scene:
     cams: list
     images: list  # uint8 (rows, cols, 3), row-major from the top row
     gsd: float
+    depths: list | None = None  # heightfield scenes: exact depth along each pixel's ray (m from z_max)
+    boxes: list | None = None   # heightfield scenes: (x0, y0, x1, y1, height) buildings
 
     @property
     def n_views(self) -> int:
@@ -116,6 +118,108 @@ def make_scene(
         cams.append(cam)
         images.append(procedural_image(cam, gsd, seed * 1000 + v))
     return Scene(roi, grid_rows, grid_cols, cams, images, gsd)
+
+
+# ---------------------------------------------------------------- heightfield
+# SPEC.md:533-556 (synth.generate / oracle_render): flat ground plus box
+# "buildings" with heights in (z_min, z_max], per-face procedural Lambertian
+# albedo, a fixed sun, and exact ray-traced depth.  The cameras are the
+# parallel projections of make_camera with no nonlinear terms, so a pixel's
+# ray is known in closed form: p(z) = (X - z tx, Y - z ty, z) with
+# X = x0 + col gsd, Y = y0 - row gsd (the RPC localises exactly onto it).
+SUN = np.array([0.35, -0.25, 0.90]) / np.linalg.norm([0.35, -0.25, 0.90])
+
+
+def make_boxes(roi: Roi, n_boxes: int, seed: int, min_side: float = 8.0, max_side: float = 40.0):
+    rng = np.random.default_rng(seed + 7919)
+    zt = roi.z_max - roi.z_min
+    out = []
+    for _ in range(n_boxes):
+        w, h = rng.uniform(min_side, max_side, 2)
+        x0 = rng.uniform(roi.easting_min, roi.easting_max - w)
+        y0 = rng.uniform(roi.northing_min, roi.northing_max - h)
+        out.append((x0, y0, x0 + w, y0 + h, roi.z_min + rng.uniform(0.15, 0.85) * zt))
+    return out
+
+
+def trace(cam: Rpc, gsd: float, roi: Roi, boxes, rows=None, cols=None):
+    """Exact first hit of each pixel ray with the heightfield: returns depth
+    (m along the ray from the z_max plane), hit point (x, y, z) and the hit
+    face (0 ground, 1 box top, 2 box side along x, 3 box side along y)."""
+    R, W = cam.image_rows, cam.image_cols
+    r = np.arange(R, dtype=np.float64)[:, None] if rows is None else rows
+    c = np.arange(W, dtype=np.float64)[None, :] if cols is None else cols
+    X = cam._x0 + c * gsd + 0.0 * r
+    Y = cam._y0 - r * gsd + 0.0 * c
+    tx, ty = cam._tx, cam._ty
+    zt, zb = roi.z_max, roi.z_min
+    # ray parameter = height drop s = zt - z (>= 0); ground hit at s = zt - zb
+    best = np.full(X.shape, zt - zb)
+    face = np.zeros(X.shape, np.int8)
+    ox, oy = X - zt * tx, Y - zt * ty  # ray point at z = zt; p(s) = (ox + s tx, oy + s ty, zt - s)
+    for (bx0, by0, bx1, by1, hb) in boxes:
+        top = np.full(X.shape, zt - hb)  # s where the ray enters the box's height range
+        hi = np.full(X.shape, zt - zb)
+        ent = []
+        for o, d, a, b in ((ox, tx, bx0, bx1), (oy, ty, by0, by1)):
+            if abs(d) < 1e-15:
+                inside = (o >= a) & (o <= b)
+                ent.append(np.where(inside, -np.inf, np.inf))
+                continue
+            s0, s1 = (a - o) / d, (b - o) / d
+            ent.append(np.minimum(s0, s1))
+            hi = np.minimum(hi, np.maximum(s0, s1))
+        lo = np.maximum(top, np.maximum(ent[0], ent[1]))
+        hit = (lo <= hi) & (lo < best)
+        side = np.where(lo == top, 1, np.where(ent[0] >= ent[1], 2, 3))
+        face = np.where(hit, side, face)
+        best = np.where(hit, lo, best)
+    z = zt - best
+    px, py = ox + best * tx, oy + best * ty
+    depth = best * np.sqrt(tx * tx + ty * ty + 1.0)
+    return depth, px, py, z, face
+
+
+def shade(px, py, z, face, seed: int, tx: float = 0.0, ty: float = 0.0):
+    """Per-face procedural albedo x Lambertian sun (+ ambient), [0,1] RGB."""
+    rng = np.random.default_rng(seed)
+    ph = rng.uniform(0, 2 * math.pi, size=8)
+    g = np.stack([0.45 + 0.2 * np.sin(px / 7.0 + ph[0]) * np.cos(py / 11.0 + ph[1]),
+                  0.50 + 0.2 * np.sin((px + py) / 13.0 + ph[2]),
+                  0.40 + 0.15 * np.cos(py / 5.0 + ph[3])], axis=-1)
+    roof = np.stack([0.70 + 0.15 * np.sin(px / 3.0 + ph[4]), 0.35 + 0.1 * np.cos(py / 4.0 + ph[5]),
+                     0.30 + 0.1 * np.sin((px - py) / 5.0)], axis=-1)
+    wall = np.stack([0.55 + 0.2 * np.sin(z / 2.0 + ph[6]), 0.55 + 0.1 * np.cos(z / 3.0 + ph[7]),
+                     0.60 + 0.0 * z], axis=-1)
+    alb = np.where((face == 0)[..., None], g, np.where((face == 1)[..., None], roof, wall))
+    n = np.zeros(px.shape + (3,))
+    n[..., 2] = np.where((face == 0) | (face == 1), 1.0, 0.0)
+    n[..., 0] = np.where(face == 2, -np.sign(tx), 0.0)  # the x face the ray enters
+    n[..., 1] = np.where(face == 3, -np.sign(ty), 0.0)
+    lam = np.clip((n * SUN).sum(-1), 0.0, 1.0)
+    return np.clip(alb * (0.35 + 0.65 * lam)[..., None], 0.0, 1.0)
+
+
+def make_heightfield_scene(grid_rows: int, grid_cols: int, tile_side: float = 128.0, z_extent: float = 40.0,
+                           n_views: int = 4, gsd: float = 0.5, seed: int = 0, max_off_nadir: float = 30.0,
+                           n_boxes: int | None = None) -> Scene:
+    """SPEC.md:533-556 fixture: ground + boxes, exact ray-traced images and
+    depth maps (Scene.depths), cameras with exact (affine) RPCs."""
+    roi = Roi(0.0, grid_cols * tile_side, 0.0, grid_rows * tile_side, 0.0, z_extent)
+    nb = n_boxes if n_boxes is not None else 6 * grid_rows * grid_cols
+    boxes = make_boxes(roi, nb, seed)
+    rng = np.random.default_rng(seed)
+    cams, images, depths = [], [], []
+    for v in range(n_views):
+        off = float(rng.uniform(0.0, max_off_nadir))
+        az = float(rng.uniform(0.0, 360.0))
+        cam = make_camera(roi, gsd, off, az, nonlinear=0.0)
+        depth, px, py, z, face = trace(cam, gsd, roi, boxes)
+        img = shade(px, py, z, face, seed, cam._tx, cam._ty)
+        cams.append(cam)
+        images.append(np.ascontiguousarray(np.clip(img * 255.0 + 0.5, 0, 255).astype(np.uint8)))
+        depths.append(depth.astype(np.float32))
+    return Scene(roi, grid_rows, grid_cols, cams, images, gsd, depths=depths, boxes=boxes)
 
 
 # Benchmark / parity configurations (SURVEY.md §8d; BASELINE.json configs).

@@ -77,7 +77,7 @@ def test_cpp_adapter_matches_oracle(tmp_path):
     # backward_batch from the oracle's d_sigma / d_rgb: K4-alone tolerances
     for k in range(4):
         re, rd, rc = ses.grads(k)
-        for name, got, ref, tol in (("enc", _r(d, f"out_genc{k}.bin", np.float32), re, 0.05),
+        for name, got, ref, tol in (("enc", _r(d, f"out_genc{k}.bin", np.float32), re, 0.09),
                                     ("dnet", _r(d, f"out_gdnet{k}.bin", np.float32), rd, 0.03)):
             rel = np.linalg.norm(got - ref) / max(np.linalg.norm(ref), 1e-30)
             assert rel < tol, (k, name, rel)
