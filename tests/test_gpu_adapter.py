@@ -74,16 +74,23 @@ def test_cpp_adapter_matches_oracle(tmp_path):
     # forward_batch: sigma / rgb (bf16 tensor-core field, stated tolerances of test_gpu_parity)
     np.testing.assert_allclose(_r(d, "out_sigma.bin", np.float32), sg, rtol=2e-2, atol=1e-6)
     np.testing.assert_allclose(_r(d, "out_rgb.bin", np.float32).reshape(-1, 3), rgb, atol=5e-3)
-    # backward_batch from the oracle's d_sigma / d_rgb: K4-alone tolerances
+    # backward_batch from the oracle's d_sigma / d_rgb: against the bf16
+    # numerics model of the kernels (tight) and the fp32 oracle (the bf16
+    # cost; the hash-table error is the bf16 forward's ReLU mask flips and
+    # varies with the data, 6-10% here: tools/emulate_bwd.py)
+    from oracle import bf16_model as M
+
+    tiles = [(ses.tile_state(k)["enc"], ses.tile_state(k)["dnet"]) for k in range(4)]
+    model = M.batch(tiles, color, b, M.KERNEL, comp["d_sigma"], comp["d_rgb"])
+    rel = lambda a, r: np.linalg.norm(a - r) / max(np.linalg.norm(r), 1e-30)  # noqa: E731
     for k in range(4):
         re, rd, rc = ses.grads(k)
-        for name, got, ref, tol in (("enc", _r(d, f"out_genc{k}.bin", np.float32), re, 0.09),
-                                    ("dnet", _r(d, f"out_gdnet{k}.bin", np.float32), rd, 0.03)):
-            rel = np.linalg.norm(got - ref) / max(np.linalg.norm(ref), 1e-30)
-            assert rel < tol, (k, name, rel)
+        ge, gd = _r(d, f"out_genc{k}.bin", np.float32), _r(d, f"out_gdnet{k}.bin", np.float32)
+        assert rel(ge, model["grads"][k][0]) < 1e-3 and rel(gd, model["grads"][k][1]) < 1e-3, k
+        assert rel(ge, re) < 0.15 and rel(gd, rd) < 0.05, (k, rel(ge, re), rel(gd, rd))
     gc = _r(d, "out_gcolor.bin", np.float32)
-    rc = ses.grads(0)[2]
-    assert np.linalg.norm(gc - rc) / np.linalg.norm(rc) < 0.01
+    assert rel(gc, model["g_color"]) < 1e-3
+    assert rel(gc, ses.grads(0)[2]) < 0.01
     # adam_step on the GPU == the reference formula on the same gradient, bit for bit
     pr, mr, vr = color.copy(), m0.copy(), v0.copy()
     s = o.adam_step(pr, gc, mr, vr, 7, lr=1e-3)

@@ -31,7 +31,8 @@ TOL_K3 = 1e-5
 TOL_K4_GRAD_REL = {"enc": 0.09, "dnet": 0.03, "color": 0.01}
 # GPU vs the bf16 numerics model (same roundings): what is left is fp32
 # accumulation order inside the MMAs / atomics, FMA contraction, expf
-TOL_MODEL_GRAD_REL = {"enc": 0.02, "dnet": 0.01, "color": 0.005}
+# (measured r02: enc 5.6e-5, dnet 1.0e-5, colour 3.1e-6)
+TOL_MODEL_GRAD_REL = {"enc": 1e-3, "dnet": 1e-3, "color": 1e-4}
 
 
 @pytest.fixture(scope="module")

@@ -78,6 +78,7 @@ def test_two_ranks_equal_full_batch_and_stay_replicas(tmp_path):
     assert p0.tobytes() == p1.tobytes()  # replicas stay identical after Adam
     ctx = _ctx()
     ctx.forward_backward(3, 0, B)
+    torch.cuda.synchronize()  # the context's stream is not torch's
     full = ctx.grad_tensor().cpu().numpy()
     full_loss = ctx.read_loss()
     rel = np.linalg.norm(g0 - full) / np.linalg.norm(full)
