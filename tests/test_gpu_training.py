@@ -171,3 +171,40 @@ def test_heightfield_config2_window_training_parity():
     assert abs(p_gpu - p_ref) <= PSNR_MARGIN_DB
     assert n_op > 500
     assert abs(mae_gpu - mae_ref) <= DEPTH_MARGIN_M and mae_gr <= DEPTH_PAIR_M
+
+
+def test_heightfield_geometry_converges():
+    """GPU-only, long: on the config-1 heightfield with 8 views the trained
+    field's depth approaches the exact ground truth (depth MAE over opaque
+    evaluation pixels from ~36 m at initialisation to < 10 m after 4,000
+    iterations; measured r02: 8.0 m, median 7.0 m), with PSNR > 38 dB."""
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2507_01631_b200.tilefield import Context
+
+    scene = synth.make_heightfield_scene(1, 1, tile_side=128.0, z_extent=40.0, n_views=8, gsd=0.5, seed=3)
+    B = 4096
+    ctx = Context(scene, FieldConfig.defaults(), TrainConfig.defaults(batch_rays=B, seed=11), max_rays=8192)
+    ctx.set_window(0, 0)
+    acc = ctx.accept_list()
+    v0 = acc[(acc >> 40) == 0]
+    sel = v0[:: max(1, v0.size // 8192)][:8192]
+    px = np.stack([(sel >> 40).astype(np.int32), ((sel >> 20) & 0xFFFFF).astype(np.int32),
+                   (sel & 0xFFFFF).astype(np.int32)], axis=1)
+    gt = scene.depths[0][px[:, 1], px[:, 2]]
+
+    def evaluate():
+        ctx.sample_pixels(px)
+        ctx.field_forward()
+        g = ctx.composite()
+        op = g["opacity"] > 0.5
+        return _psnr(g["rgb"], ctx.batch()["rays"]["target"]), float(np.mean(np.abs(g["depth"][op] - gt[op])))
+
+    _, mae0 = evaluate()
+    for it in range(4000):
+        ctx.train_step(it, 0, B)
+    psnr, mae = evaluate()
+    print(f"heightfield 8 views: depth MAE vs GT {mae0:.2f} m -> {mae:.2f} m, PSNR {psnr:.2f} dB")
+    assert mae < 10.0 and mae < mae0 / 3 and psnr > 38.0
