@@ -974,30 +974,47 @@ __global__ void __launch_bounds__(32 * kS1Warps, 2) sample_kernel(RaygenArgs a, 
             if (k < nseg && valid) s_cnt[warp][sslot[k]] = kept[k];
     }
     __syncthreads();
-    // ---------------- CTA aggregate + decoupled look-back (lane s of warp 0: slot s)
-    if (warp == 0 && lane < kTrainSlots) {
-        const int s = lane;
+    // ---------------- CTA aggregate + decoupled look-back, warp s for slot s:
+    // 32 predecessors per round (lane l reads CTA b-1-l), summing aggregates
+    // down to the nearest published inclusive prefix
+    if (warp < kTrainSlots) {
+        const int s = warp;
         uint32_t agg = 0;
 #pragma unroll
         for (int w = 0; w < kS1Warps; ++w) agg += s_cnt[w][s];
         unsigned long long* my = lookback + 4ull * blockIdx.x + s;
         uint32_t excl = 0;
         if (blockIdx.x == 0) {
-            lb_publish(my, epoch, kLbPrefix, agg);
+            if (lane == 0) lb_publish(my, epoch, kLbPrefix, agg);
         } else {
-            lb_publish(my, epoch, kLbAgg, agg);
-            for (int j = int(blockIdx.x) - 1; j >= 0;) {
-                const unsigned long long x = lb_read(lookback + 4ull * j + s);
-                const uint32_t hw = uint32_t(x >> 32);
-                if ((hw >> 2) != (epoch & 0x3fffffffu) || (hw & 3u) == 0) continue;  // not published yet
-                excl += uint32_t(x);
-                if ((hw & 3u) == kLbPrefix) break;
-                --j;
+            if (lane == 0) lb_publish(my, epoch, kLbAgg, agg);
+            const uint32_t ep = epoch & 0x3fffffffu;
+            for (int base = int(blockIdx.x) - 1;;) {
+                const int j = base - lane;
+                uint32_t flag = kLbPrefix, val = 0;  // lanes before CTA 0 act as a zero prefix
+                if (j >= 0) {
+                    unsigned long long x;
+                    do {
+                        x = lb_read(lookback + 4ull * j + s);
+                    } while ((uint32_t(x >> 32) >> 2) != ep || (uint32_t(x >> 32) & 3u) == 0);
+                    flag = uint32_t(x >> 32) & 3u;
+                    val = uint32_t(x);
+                }
+                const uint32_t pm = __ballot_sync(0xffffffffu, flag == kLbPrefix);
+                const int stop = pm ? __ffs(pm) - 1 : 31;  // nearest inclusive prefix (or the whole window)
+                uint32_t part = lane <= stop ? val : 0u;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+                excl += part;
+                if (pm) break;
+                base -= 32;
             }
-            lb_publish(my, epoch, kLbPrefix, excl + agg);
+            if (lane == 0) lb_publish(my, epoch, kLbPrefix, excl + agg);
         }
-        s_off[s] = excl;
-        if (blockIdx.x == gridDim.x - 1) totals[s] = excl + agg;
+        if (lane == 0) {
+            s_off[s] = excl;
+            if (blockIdx.x == gridDim.x - 1) totals[s] = excl + agg;
+        }
     }
     __syncthreads();
     if (!valid) return;

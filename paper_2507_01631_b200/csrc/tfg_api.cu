@@ -602,6 +602,11 @@ struct HostBatch {
     std::vector<RayRec> rays;
     std::vector<uint32_t> P;
     uint64_t n_samples = 0;
+    // occupied [lo, hi) of each slot bucket in the device sample arrays (the
+    // buckets are contiguous, or fixed regions for the one-pass draw), and
+    // the extent they span
+    std::vector<std::pair<uint64_t, uint64_t>> ranges;
+    uint64_t extent = 0;
 };
 int fetch_batch_meta(tfg_ctx* c, HostBatch& hb) {
     int n = c->cur_rays;
@@ -613,6 +618,41 @@ int fetch_batch_meta(tfg_ctx* c, HostBatch& hb) {
     int st = sync_status(c);
     if (st) return st;
     hb.n_samples = c->h_status->n_samples;
+    const int ns = c->slots.n;
+    hb.ranges.assign(ns, {UINT64_MAX, 0});
+    for (int i = 0; i < n; ++i) {
+        const RayRec& R = hb.rays[i];
+        if (R.status != 0) continue;
+        for (int k = 0; k < R.nseg; ++k) {
+            const int sl = R.slot[k];
+            const uint64_t b = hb.P[uint64_t(sl) * n + i];
+            auto& r = hb.ranges[sl];
+            r.first = std::min(r.first, b);
+            r.second = std::max(r.second, b + R.cnt[k]);
+        }
+    }
+    hb.extent = 0;
+    for (auto& r : hb.ranges) {
+        if (r.first > r.second) r = {0, 0};
+        hb.extent = std::max(hb.extent, r.second);
+    }
+    return 0;
+}
+// Per-sample device array <-> host array indexed like the device (only the
+// occupied bucket ranges are copied).
+template <typename T>
+int pull_samples(const HostBatch& hb, const T* dev, std::unique_ptr<T[]>& host) {
+    host.reset(new T[std::max<uint64_t>(1, hb.extent)]);
+    for (auto& r : hb.ranges)
+        if (r.second > r.first)
+            CK(cudaMemcpy(host.get() + r.first, dev + r.first, (r.second - r.first) * sizeof(T), cudaMemcpyDeviceToHost));
+    return 0;
+}
+template <typename T>
+int push_samples(const HostBatch& hb, const T* host, T* dev) {
+    for (auto& r : hb.ranges)
+        if (r.second > r.first)
+            CK(cudaMemcpy(dev + r.first, host + r.first, (r.second - r.first) * sizeof(T), cudaMemcpyHostToDevice));
     return 0;
 }
 // Visits samples in ray order: fn(ray, sample index in ray order, bucket pos, slot).
@@ -1360,12 +1400,12 @@ TFG_API int tfg_batch_export(tfg_ctx* c, tfg_batch_view* out) {
     if (rc) return rc;
     uint64_t S = hb.n_samples;
     if (out->capacity < S) return fail(TFG_ERR_INVALID, "batch_export: capacity too small");
-    std::vector<float4> loc(S);
-    std::vector<float2> td(S);
-    std::vector<uint8_t> ep(S);
-    CK(cudaMemcpy(loc.data(), c->s.local, S * 16, cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(td.data(), c->s.td, S * 8, cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(ep.data(), c->s.endpoint, S, cudaMemcpyDeviceToHost));
+    std::unique_ptr<float4[]> loc;
+    std::unique_ptr<float2[]> td;
+    std::unique_ptr<uint8_t[]> ep;
+    if ((rc = pull_samples(hb, c->s.local, loc)) || (rc = pull_samples(hb, c->s.td, td)) ||
+        (rc = pull_samples(hb, c->s.endpoint, ep)))
+        return rc;
     int n = c->cur_rays;
     std::vector<uint32_t> cnt(n, 0);
     for (int i = 0; i < n; ++i) {
@@ -1495,11 +1535,11 @@ TFG_API int tfg_set_field_outputs(tfg_ctx* c, const float* sigma, const float* r
     HostBatch hb;
     int rc = fetch_batch_meta(c, hb);
     if (rc) return rc;
-    std::vector<float4> io(hb.n_samples);
+    std::unique_ptr<float4[]> io(new float4[std::max<uint64_t>(1, hb.extent)]);
     for_samples(c, hb, [&](int, uint64_t q, uint64_t pos, int) {
         io[pos] = make_float4(sigma[q], rgb[3 * q], rgb[3 * q + 1], rgb[3 * q + 2]);
     });
-    CK(cudaMemcpy(c->s.io, io.data(), io.size() * 16, cudaMemcpyHostToDevice));
+    if ((rc = push_samples(hb, io.get(), c->s.io))) return rc;
     c->io_fwd = true;
     return 0;
 }
@@ -1517,8 +1557,8 @@ TFG_API int tfg_field_backward_from(tfg_ctx* c, const float* d_sigma, const floa
     HostBatch hb;
     int rc = fetch_batch_meta(c, hb);
     if (rc) return rc;
-    std::vector<float4> io(hb.n_samples);
-    CK(cudaMemcpy(io.data(), c->s.io, io.size() * 16, cudaMemcpyDeviceToHost));
+    std::unique_ptr<float4[]> io;
+    if ((rc = pull_samples(hb, c->s.io, io))) return rc;
     const float dmax = c->fc.density_max;
     for_samples(c, hb, [&](int, uint64_t q, uint64_t pos, int) {
         const float4 f = io[pos];
@@ -1526,7 +1566,7 @@ TFG_API int tfg_field_backward_from(tfg_ctx* c, const float* d_sigma, const floa
         io[pos] = make_float4(f.x >= dmax ? 0.f : d_sigma[q] * f.x, dr * f.y * (1.f - f.y), dg * f.z * (1.f - f.z),
                               db * f.w * (1.f - f.w));
     });
-    CK(cudaMemcpy(c->s.io, io.data(), io.size() * 16, cudaMemcpyHostToDevice));
+    if ((rc = push_samples(hb, io.get(), c->s.io))) return rc;
     c->io_fwd = false;
     if ((rc = run_backward(c))) return rc;
     CK(cudaStreamSynchronize(c->st));
@@ -1621,8 +1661,8 @@ TFG_API int tfg_field_forward(tfg_ctx* c, float* sigma, float* rgb) {
     if (!sigma && !rgb) return 0;
     HostBatch hb;
     if ((rc = fetch_batch_meta(c, hb))) return rc;
-    std::vector<float4> io(hb.n_samples);
-    CK(cudaMemcpy(io.data(), c->s.io, hb.n_samples * 16, cudaMemcpyDeviceToHost));
+    std::unique_ptr<float4[]> io;
+    if ((rc = pull_samples(hb, c->s.io, io))) return rc;
     for_samples(c, hb, [&](int, uint64_t q, uint64_t pos, int) {
         if (sigma) sigma[q] = io[pos].x;
         if (rgb) {
@@ -1637,7 +1677,7 @@ TFG_API int tfg_field_forward(tfg_ctx* c, float* sigma, float* rgb) {
 TFG_API int tfg_composite(tfg_ctx* c, float* ray_rgb, float* ray_depth, float* ray_opacity,
                           float* d_sigma, float* d_rgb, float* loss) {
     if (!c || !c->have_batch) return fail(TFG_ERR_STATE, "composite: no batch");
-    if (!c->d_export && dalloc(c, &c->d_export, c->sample_cap)) return TFG_ERR_CUDA;
+    if (!c->d_export && dalloc(c, &c->d_export, uint64_t(kTrainSlots) * c->sample_cap)) return TFG_ERR_CUDA;
     int rc = run_composite(c, true, c->d_export);
     if (rc) return rc;
     HostBatch hb;
@@ -1652,8 +1692,8 @@ TFG_API int tfg_composite(tfg_ctx* c, float* ray_rgb, float* ray_depth, float* r
         if (ray_opacity) ray_opacity[i] = ro[4 * uint64_t(c->max_rays) + i];
     }
     if (d_sigma || d_rgb) {
-        std::vector<float4> io(hb.n_samples);
-        CK(cudaMemcpy(io.data(), c->d_export, hb.n_samples * 16, cudaMemcpyDeviceToHost));
+        std::unique_ptr<float4[]> io;
+        if ((rc = pull_samples(hb, c->d_export, io))) return rc;
         for_samples(c, hb, [&](int, uint64_t q, uint64_t pos, int) {
             if (d_sigma) d_sigma[q] = io[pos].x;
             if (d_rgb) {
