@@ -739,449 +739,6 @@ int launch_import(const ImportArgs& a, RayRec* rays, float4* venc, uint32_t* cou
     return 0;
 }
 
-// ------------------------------------------------------------------ K1 (training draw, one pass)
-// The training batch in ONE kernel: warp per ray, 8 rays per CTA.  Each warp
-// draws its pixel, reads the accept pass's memoised ray, segments it against
-// the window's 4 tile boxes (stable rank order on t_near), plans the
-// intervals and generates every candidate sample once (jitter, position,
-// occupancy test), keeping the first kStage chunks of 32 in registers.  The
-// per-slot kept counts go through a CTA scan and a decoupled look-back across
-// CTAs (one chained prefix per slot), so each warp knows where its ray's
-// samples go and writes them straight from registers.  Slot s's bucket is the
-// fixed region [s * slot_cap, (s + 1) * slot_cap) of the sample arrays (rays
-// ascending inside it); the last CTA publishes the bucket totals for the
-// tile list.  Same arithmetic, same bits as raygen + write (sample_t,
-// to_local, occupancy, delta over the concatenated kept samples).
-constexpr int kS1Warps = 8;   // rays per CTA
-constexpr int kStage = 4;     // candidate chunks of 32 kept in registers (rays have ~70 candidates)
-constexpr uint32_t kLbAgg = 1u, kLbPrefix = 2u;
-
-struct Cand {
-    double t;
-    float x, y, z;
-    int k;       // segment
-    bool keep, endp;
-};
-
-// Look-back word of (CTA, slot): epoch (30 bits) | flag (2 bits) | value (32 bits).
-__device__ __forceinline__ void lb_publish(unsigned long long* w, uint32_t epoch, uint32_t flag, uint32_t v) {
-    unsigned long long x = (static_cast<unsigned long long>((epoch << 2) | flag) << 32) | v;
-    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(w), "l"(x) : "memory");
-}
-__device__ __forceinline__ unsigned long long lb_read(const unsigned long long* w) {
-    unsigned long long x;
-    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(x) : "l"(w) : "memory");
-    return x;
-}
-
-__global__ void __launch_bounds__(32 * kS1Warps, 2) sample_kernel(RaygenArgs a, RayRec* __restrict__ rays,
-                                                                float4* __restrict__ venc, uint32_t* __restrict__ P,
-                                                                unsigned long long* __restrict__ lookback,
-                                                                uint32_t epoch, uint32_t* __restrict__ totals,
-                                                                uint64_t slot_cap, SampleArrays out,
-                                                                Status* __restrict__ status) {
-    __shared__ uint32_t s_cnt[kS1Warps][kTrainSlots];
-    __shared__ uint32_t s_off[kTrainSlots];
-    pdl_wait();
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int i = blockIdx.x * kS1Warps + warp;
-    const bool valid = i < a.n_rays;
-    const int ns = a.slots.n;
-    // ---------------- ray (warp-uniform)
-    const uint64_t g = a.ray_begin + uint64_t(valid ? i : 0);
-    const uint64_t na = *a.n_accept_dev;
-    double ro[3] = {0.0, 0.0, 0.0}, rd[3] = {0.0, 0.0, 1.0};
-    float target[3] = {0.f, 0.f, 0.f};
-    int rstatus = 1;
-    int v = 0, row = 0, col = 0;
-    if (na) {
-        Rng r(hash_combine(hash_combine(hash_combine(a.seed, kPurposePixels), a.iter), g));
-        const uint64_t e = a.accept[r.below(na)];
-        v = int(e >> 40);
-        row = int((e >> 20) & 0xFFFFF);
-        col = int(e & 0xFFFFF);
-        const int* cr = a.crop_rect + 4 * v;  // r0, c0, cols, rows: memo index = crop pixel index
-        const uint64_t pix = a.crop_offset[v] / 3 + uint64_t(row - cr[0]) * uint64_t(cr[2]) + uint64_t(col - cr[1]);
-        const double* m = a.memo_rays + 6 * pix;
-#pragma unroll
-        for (int q = 0; q < 3; ++q) {
-            ro[q] = m[q];
-            rd[q] = m[3 + q];
-        }
-        rstatus = 0;
-        const uint8_t* px = a.crop_bytes + 3 * pix;
-        const float tl = lane < 3 ? float(px[lane]) / 255.0f : 0.f;  // u8_to_unit
-#pragma unroll
-        for (int q = 0; q < 3; ++q) target[q] = __shfl_sync(0xffffffffu, tl, q);
-    } else if (valid && lane == 0) {
-        atomicOr(&status->bits, kStatusRayFail);
-    }
-    // TileBoxSet::segments: hits ordered by t_near, ties by slot (the stable
-    // insertion sort's order), as ranks over the <= 4 slots
-    double t0s[kTrainSlots], t1s[kTrainSlots];
-    bool hit[kTrainSlots];
-#pragma unroll
-    for (int s = 0; s < kTrainSlots; ++s) {
-        double box[6];
-#pragma unroll
-        for (int q = 0; q < 6; ++q) box[q] = a.slots.box[s][q];
-        hit[s] = (rstatus == 0) && s < ns && slab(ro, rd, box, &t0s[s], &t1s[s]);
-    }
-    // 4-input sorting network on (hit, t_near, slot): the order is the total
-    // order "hit first, then t_near, then slot", which is what the stable
-    // insertion sort of TileBoxSet::segments produces; all in registers
-    bool sh[kTrainSlots];
-    int sslot[kTrainSlots];
-    double stn[kTrainSlots], stf[kTrainSlots];
-    int nseg = 0;
-#pragma unroll
-    for (int s = 0; s < kTrainSlots; ++s) {
-        sh[s] = hit[s];
-        sslot[s] = s;
-        stn[s] = hit[s] ? t0s[s] : 0.0;
-        stf[s] = hit[s] ? t1s[s] : 0.0;
-        nseg += hit[s] ? 1 : 0;
-    }
-    auto cswap = [&](int x, int y) {
-        const bool less_yx = sh[y] && (!sh[x] || stn[y] < stn[x] || (stn[y] == stn[x] && sslot[y] < sslot[x]));
-        if (less_yx) {
-            const bool th = sh[x];
-            sh[x] = sh[y];
-            sh[y] = th;
-            const int ts = sslot[x];
-            sslot[x] = sslot[y];
-            sslot[y] = ts;
-            const double tn = stn[x];
-            stn[x] = stn[y];
-            stn[y] = tn;
-            const double tf = stf[x];
-            stf[x] = stf[y];
-            stf[y] = tf;
-        }
-    };
-    static_assert(kTrainSlots == 4, "the sorting network is for 4 slots");
-    cswap(0, 1);
-    cswap(2, 3);
-    cswap(0, 2);
-    cswap(1, 3);
-    cswap(1, 2);
-    // sample_segments interval counts (plan_intervals)
-    int nint[kTrainSlots];
-    {
-        long long total = 0, sumint = 0;
-#pragma unroll
-        for (int k = 0; k < kTrainSlots; ++k) {
-            nint[k] = 0;
-            if (k < nseg) {
-                long long n = (long long)ceil((stf[k] - stn[k]) * a.spm);
-                if (n < 1) n = 1;
-                nint[k] = int(n);
-                sumint += n;
-                total += n + 1;
-            }
-        }
-        if (total > a.cap) {
-            const long long budget = a.cap - nseg;
-#pragma unroll
-            for (int k = 0; k < kTrainSlots; ++k)
-                if (k < nseg) {
-                    long long n = (long long)nint[k] * budget / sumint;
-                    nint[k] = int(n < 1 ? 1 : n);
-                }
-        }
-    }
-    int cstart[kTrainSlots + 1];
-    double step[kTrainSlots];
-    cstart[0] = 0;
-#pragma unroll
-    for (int k = 0; k < kTrainSlots; ++k) {
-        cstart[k + 1] = cstart[k] + (k < nseg ? nint[k] + 1 : 0);
-        step[k] = k < nseg ? (stf[k] - stn[k]) / nint[k] : 0.0;
-    }
-    const int ncand = cstart[kTrainSlots];
-    const int nchunk = (ncand + 31) / 32;
-    const uint64_t key = hash_combine(hash_combine(hash_combine(a.seed, kPurposeJitter), a.iter), g);
-    const double o0 = ro[0], o1 = ro[1], o2 = ro[2], d0 = rd[0], d1 = rd[1], d2 = rd[2];
-    // candidate q of the ray: segment, t, local, keep (occupancy; endpoints kept)
-    // (arrays captured by value: a by-reference capture takes their address and
-    // sends them to local memory)
-    auto gen = [&a, key, o0, o1, o2, d0, d1, d2, ncand, sslot, nint, stn, stf, step, cstart](int q) {
-        Cand c;
-        c.k = 0;
-#pragma unroll
-        for (int k = 1; k < kTrainSlots; ++k)
-            if (q >= cstart[k]) c.k = k;
-        int sl = 0, n = 1, c0 = 0;
-        double tn = 0.0, tf = 0.0, st = 0.0;
-#pragma unroll
-        for (int k = 0; k < kTrainSlots; ++k)
-            if (k == c.k) {
-                sl = sslot[k];
-                n = nint[k];
-                tn = stn[k];
-                tf = stf[k];
-                st = step[k];
-                c0 = cstart[k];
-            }
-        const int j = q - c0;
-        c.keep = false;
-        c.endp = false;
-        c.t = 0.0;
-        c.x = c.y = c.z = 0.f;
-        if (q < ncand) {
-            c.t = sample_t(tn, tf, n, c.k, j, a.jitter, key, st);
-            c.x = float((o0 + c.t * d0 - a.slots.frame[sl][0]) * a.slots.frame[sl][3]);
-            c.y = float((o1 + c.t * d1 - a.slots.frame[sl][1]) * a.slots.frame[sl][4]);
-            c.z = float((o2 + c.t * d2 - a.slots.frame[sl][2]) * a.slots.frame[sl][5]);
-            c.endp = (j == 0 || j == n);
-            c.keep = c.endp || occ_test(a.occ_bits[sl], c.x, c.y, c.z);
-        }
-        return c;
-    };
-    // lanes of a chunk in segment k
-    auto seg_mask = [cstart](int c, int k) {
-        const int lo = cstart[k] - 32 * c, hi = cstart[k + 1] - 32 * c;
-        const uint32_t below_hi = hi >= 32 ? 0xffffffffu : (hi <= 0 ? 0u : ((1u << hi) - 1u));
-        const uint32_t below_lo = lo >= 32 ? 0xffffffffu : (lo <= 0 ? 0u : ((1u << lo) - 1u));
-        return below_hi & ~below_lo;
-    };
-    // ---------------- pass 1: generate, count, stage
-    Cand stg[kStage];
-    uint32_t kmask[kStage];
-    uint32_t kept[kTrainSlots] = {0, 0, 0, 0};
-#pragma unroll
-    for (int c = 0; c < kStage; ++c) {
-        kmask[c] = 0;
-        if (c < nchunk) {
-            stg[c] = gen(32 * c + lane);
-            kmask[c] = __ballot_sync(0xffffffffu, stg[c].keep);
-#pragma unroll
-            for (int k = 0; k < kTrainSlots; ++k) kept[k] += __popc(kmask[c] & seg_mask(c, k));
-        }
-    }
-    for (int c = kStage; c < nchunk; ++c) {
-        const Cand cd = gen(32 * c + lane);
-        const uint32_t m = __ballot_sync(0xffffffffu, cd.keep);
-#pragma unroll
-        for (int k = 0; k < kTrainSlots; ++k) kept[k] += __popc(m & seg_mask(c, k));
-    }
-    // per-slot kept counts of the ray
-    if (lane == 0) {
-#pragma unroll
-        for (int s = 0; s < kTrainSlots; ++s) s_cnt[warp][s] = 0;
-#pragma unroll
-        for (int k = 0; k < kTrainSlots; ++k)
-            if (k < nseg && valid) s_cnt[warp][sslot[k]] = kept[k];
-    }
-    __syncthreads();
-    // ---------------- CTA aggregate + decoupled look-back, warp s for slot s:
-    // 32 predecessors per round (lane l reads CTA b-1-l), summing aggregates
-    // down to the nearest published inclusive prefix
-    if (warp < kTrainSlots) {
-        const int s = warp;
-        uint32_t agg = 0;
-#pragma unroll
-        for (int w = 0; w < kS1Warps; ++w) agg += s_cnt[w][s];
-        unsigned long long* my = lookback + 4ull * blockIdx.x + s;
-        uint32_t excl = 0;
-        if (blockIdx.x == 0) {
-            if (lane == 0) lb_publish(my, epoch, kLbPrefix, agg);
-        } else {
-            if (lane == 0) lb_publish(my, epoch, kLbAgg, agg);
-            const uint32_t ep = epoch & 0x3fffffffu;
-            for (int base = int(blockIdx.x) - 1;;) {
-                const int j = base - lane;
-                uint32_t flag = kLbPrefix, val = 0;  // lanes before CTA 0 act as a zero prefix
-                if (j >= 0) {
-                    unsigned long long x;
-                    do {
-                        x = lb_read(lookback + 4ull * j + s);
-                    } while ((uint32_t(x >> 32) >> 2) != ep || (uint32_t(x >> 32) & 3u) == 0);
-                    flag = uint32_t(x >> 32) & 3u;
-                    val = uint32_t(x);
-                }
-                const uint32_t pm = __ballot_sync(0xffffffffu, flag == kLbPrefix);
-                const int stop = pm ? __ffs(pm) - 1 : 31;  // nearest inclusive prefix (or the whole window)
-                uint32_t part = lane <= stop ? val : 0u;
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-                excl += part;
-                if (pm) break;
-                base -= 32;
-            }
-            if (lane == 0) lb_publish(my, epoch, kLbPrefix, excl + agg);
-        }
-        if (lane == 0) {
-            s_off[s] = excl;
-            if (blockIdx.x == gridDim.x - 1) totals[s] = excl + agg;
-        }
-    }
-    __syncthreads();
-    if (!valid) return;
-    // ---------------- ray record, view encoding, bucket positions
-    uint64_t sbase[kTrainSlots];
-#pragma unroll
-    for (int s = 0; s < kTrainSlots; ++s) {
-        uint32_t pre = s_off[s];
-#pragma unroll
-        for (int w = 0; w < kS1Warps; ++w)
-            if (w < warp) pre += s_cnt[w][s];
-        sbase[s] = uint64_t(s) * slot_cap + pre;
-        if (s < ns && lane == s) P[uint64_t(s) * a.n_rays + i] = uint32_t(sbase[s]);
-        if (uint64_t(pre) + s_cnt[warp][s] > slot_cap) {
-            if (lane == 0) atomicOr(&status->bits, kStatusSampleOverflow);
-            return;
-        }
-    }
-    // segment k's bucket base (explicit selects: an indexed sbase[sslot[k]]
-    // would live in local memory)
-    uint64_t kb0, kb1, kb2, kb3;
-    {
-        auto pick = [&](int sl) {
-            return sl == 0 ? sbase[0] : (sl == 1 ? sbase[1] : (sl == 2 ? sbase[2] : sbase[3]));
-        };
-        kb0 = pick(sslot[0]);
-        kb1 = pick(sslot[1]);
-        kb2 = pick(sslot[2]);
-        kb3 = pick(sslot[3]);
-    }
-    if (lane == 0) {  // the ray record, field by field (no local-memory struct copy)
-        RayRec* O = rays + i;
-#pragma unroll
-        for (int q = 0; q < 3; ++q) {
-            O->o[q] = ro[q];
-            O->d[q] = rd[q];
-            O->target[q] = target[q];
-        }
-#pragma unroll
-        for (int k = 0; k < kMaxSeg; ++k) {
-            const bool in = k < kTrainSlots;
-            O->slot[k] = in ? uint8_t(sslot[k < kTrainSlots ? k : 0]) : 0;
-            O->tn[k] = in ? stn[k < kTrainSlots ? k : 0] : 0.0;
-            O->tf[k] = in ? stf[k < kTrainSlots ? k : 0] : 0.0;
-            O->nint[k] = in ? uint16_t(nint[k < kTrainSlots ? k : 0]) : 0;
-            O->cnt[k] = in ? uint16_t(kept[k < kTrainSlots ? k : 0]) : 0;
-        }
-        O->view = v;
-        O->row = row;
-        O->col = col;
-        O->nseg = nseg;
-        O->status = rstatus;
-    }
-    if (rstatus != 0) return;
-    if (lane < 24) {  // encode_direction (nn.hpp:288-298): element lane
-        const int f = lane / 6, cc = (lane % 6) >> 1;
-        const float scale = 3.14159265358979323846f * float(1 << f);  // pi 2^f, exactly the raygen constants
-        const float dc = cc == 0 ? float(rd[0]) : (cc == 1 ? float(rd[1]) : float(rd[2]));
-        const float x = scale * dc;
-        reinterpret_cast<float*>(venc + uint64_t(i) * 6)[lane] = (lane & 1) ? cosf(x) : sinf(x);
-    }
-    // ---------------- pass 2: write (staged chunks from registers, the rest regenerated)
-    const uint32_t lt = (1u << lane) - 1u;
-    uint32_t w0 = 0, w1 = 0, w2 = 0, w3 = 0;  // kept samples written per segment
-    long long pend_pos = -1;
-    double pend_t = 0.0;
-    // the chunk's kept samples (ballot mask) to their bucket positions; the
-    // last one's delta waits for its successor (next chunk or segment)
-#define TFG_EMIT(C, CD, MASK)                                                                                   \
-    do {                                                                                                        \
-        const uint32_t mask_ = (MASK);                                                                          \
-        if (mask_ != 0u) {                                                                                      \
-            const int first_ = __ffs(mask_) - 1, last_ = 31 - __clz(mask_);                                     \
-            const double t_first_ = __shfl_sync(0xffffffffu, (CD).t, first_);                                   \
-            if (lane == 0 && pend_pos >= 0) out.td[pend_pos] = make_float2(float(pend_t), float(t_first_ - pend_t)); \
-            const uint32_t gt_ = mask_ & ~(lt | (1u << lane));                                                   \
-            const int nxt_ = gt_ ? (__ffs(gt_) - 1) : lane;                                                     \
-            const double t_next_ = __shfl_sync(0xffffffffu, (CD).t, nxt_);                                      \
-            const uint32_t m0_ = mask_ & seg_mask((C), 0), m1_ = mask_ & seg_mask((C), 1);                      \
-            const uint32_t m2_ = mask_ & seg_mask((C), 2), m3_ = mask_ & seg_mask((C), 3);                      \
-            uint64_t pos_ = (CD).k == 0 ? kb0 + w0 + __popc(m0_ & lt)                                           \
-                          : (CD).k == 1 ? kb1 + w1 + __popc(m1_ & lt)                                           \
-                          : (CD).k == 2 ? kb2 + w2 + __popc(m2_ & lt) : kb3 + w3 + __popc(m3_ & lt);            \
-            w0 += __popc(m0_);                                                                                  \
-            w1 += __popc(m1_);                                                                                  \
-            w2 += __popc(m2_);                                                                                  \
-            w3 += __popc(m3_);                                                                                  \
-            if ((CD).keep) {                                                                                    \
-                out.local[pos_] = make_float4((CD).x, (CD).y, (CD).z, __int_as_float(i));                       \
-                if (gt_) out.td[pos_] = make_float2(float((CD).t), float(t_next_ - (CD).t));                    \
-                out.endpoint[pos_] = (CD).endp ? 1 : 0;                                                         \
-            }                                                                                                   \
-            pend_pos = __shfl_sync(0xffffffffu, (long long)pos_, last_);                                        \
-            pend_t = __shfl_sync(0xffffffffu, (CD).t, last_);                                                   \
-        }                                                                                                       \
-    } while (0)
-#pragma unroll
-    for (int c = 0; c < kStage; ++c)
-        if (c < nchunk) TFG_EMIT(c, stg[c], kmask[c]);
-    for (int c = kStage; c < nchunk; ++c) {
-        const Cand cd = gen(32 * c + lane);
-        TFG_EMIT(c, cd, __ballot_sync(0xffffffffu, cd.keep));
-    }
-#undef TFG_EMIT
-    if (lane == 0 && pend_pos >= 0) {
-        const double texit = (a.z_min - o2) / d2;
-        double r = texit - pend_t;
-        if (r < 0) r = 0;
-        if (r > a.delta_cap) r = a.delta_cap;
-        out.td[pend_pos] = make_float2(float(pend_t), float(r));
-    }
-}
-
-// Tile list of the fixed-region buckets (bucket s = [s * slot_cap, ...),
-// totals from sample_kernel's last CTA).
-__global__ void tiles_fixed_kernel(const uint32_t* __restrict__ totals, int nslots, uint64_t slot_cap,
-                                   uint64_t capacity, int max_tiles, TileDesc* __restrict__ tiles,
-                                   Status* __restrict__ status) {
-    pdl_wait();
-    __shared__ uint32_t tile_base[kTrainSlots + 1], cnt[kTrainSlots];
-    __shared__ int ok;
-    if (threadIdx.x == 0) {
-        uint32_t tb = 0;
-        uint64_t total = 0;
-        for (int s = 0; s < nslots; ++s) {
-            cnt[s] = totals[s];
-            tile_base[s] = tb;
-            tb += (cnt[s] + 127) / 128;
-            total += cnt[s];
-        }
-        tile_base[nslots] = tb;
-        ok = !(total > capacity || int(tb) > max_tiles || (status->bits & kStatusSampleOverflow));
-        if (blockIdx.x == 0) {
-            status->n_samples = total;
-            status->n_tiles = ok ? tb : 0;
-            if (!ok) atomicOr(&status->bits, kStatusSampleOverflow);
-        }
-    }
-    __syncthreads();
-    if (!ok) return;
-    const uint32_t n_tiles = tile_base[nslots];
-    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < n_tiles; t += gridDim.x * blockDim.x) {
-        int s = 0;
-        while (s + 1 < nslots && t >= tile_base[s + 1]) ++s;
-        const uint32_t k = t - tile_base[s];
-        TileDesc d;
-        d.start = uint32_t(uint64_t(s) * slot_cap) + 128 * k;
-        const uint32_t rem = cnt[s] - 128 * k;
-        d.n = uint16_t(rem < 128 ? rem : 128);
-        d.slot = uint16_t(s);
-        tiles[t] = d;
-    }
-}
-
-int launch_sample_draw(const RaygenArgs& a, RayRec* rays, float4* venc, uint32_t* P, unsigned long long* lookback,
-                       uint32_t epoch, uint32_t* totals, uint64_t slot_cap, TileDesc* tiles, int max_tiles,
-                       SampleArrays out, uint64_t capacity, Status* status, cudaStream_t st, uint64_t* launches) {
-    if (a.slots.n > kTrainSlots) return 1;
-    const int blocks = (a.n_rays + kS1Warps - 1) / kS1Warps;
-    launch_pdl(sample_kernel, dim3(blocks), dim3(32 * kS1Warps), 0, st, a, rays, venc, P, lookback, epoch, totals,
-               slot_cap, out, status);
-    launch_pdl(tiles_fixed_kernel, dim3(std::max(1, std::min(148, (max_tiles + 255) / 256))), dim3(256), 0, st,
-               static_cast<const uint32_t*>(totals), a.slots.n, slot_cap, capacity, max_tiles, tiles, status);
-    *launches += 2;
-    return 0;
-}
-
 // ------------------------------------------------------------------ host launchers
 int launch_accept(const AcceptArgs& args, uint32_t* flags, uint32_t* pos, uint32_t* block_sums,
                   uint32_t* n_out, uint64_t* out, cudaStream_t st, uint64_t* launches) {

@@ -174,12 +174,6 @@ int launch_sampler(const RaygenArgs& a, RayRec* rays, float4* venc, uint32_t* co
                    uint32_t* P, uint32_t* block_sums, TileDesc* tiles, int max_tiles,
                    SampleArrays out, uint64_t capacity, Status* status, cudaStream_t st,
                    uint64_t* launches);
-// The training draw in one kernel (memo rays, <= 4 slots): fixed-region slot
-// buckets [s * slot_cap, ...), decoupled look-back (per-launch epoch), then the
-// tile list from the bucket totals.
-int launch_sample_draw(const RaygenArgs& a, RayRec* rays, float4* venc, uint32_t* P, unsigned long long* lookback,
-                       uint32_t epoch, uint32_t* totals, uint64_t slot_cap, TileDesc* tiles, int max_tiles,
-                       SampleArrays out, uint64_t capacity, Status* status, cudaStream_t st, uint64_t* launches);
 int launch_import(const ImportArgs& a, RayRec* rays, float4* venc, uint32_t* counts, uint32_t* P,
                   uint32_t* block_sums, TileDesc* tiles, int max_tiles, SampleArrays out, uint64_t capacity,
                   Status* status, cudaStream_t st, uint64_t* launches);

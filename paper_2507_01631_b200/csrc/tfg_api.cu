@@ -511,19 +511,8 @@ int run_sampler(tfg_ctx* c, RaygenArgs& a) {
         return fail(TFG_ERR_INVALID, "sample: n_rays outside (0, max_rays]");
     PhaseScope ps(c, kPhSampler);
     CK(cudaMemsetAsync(c->d_status, 0, sizeof(Status), c->st));
-    static const bool two_pass = [] {  // A/B: the raygen + scan + write path for draws too
-        const char* e = std::getenv("TFG_TWO_PASS_SAMPLER");
-        return e && e[0] == '1';
-    }();
-    if (!a.pixels && a.memo_rays && a.slots.n <= kTrainSlots && !two_pass) {
-        c->sample_epoch = (c->sample_epoch + 1) & 0x3fffffffu;
-        if (c->sample_epoch == 0) c->sample_epoch = 1;
-        if (launch_sample_draw(a, c->d_rays, c->d_venc, c->d_P, c->d_lookback, c->sample_epoch, c->d_totals,
-                               c->sample_cap, c->d_tiles, c->max_tiles, c->s, c->sample_cap, c->d_status, c->st,
-                               &c->launches))
-            return fail(TFG_ERR_INVALID, "sample: more than 4 slots in a training draw");
-    } else if (launch_sampler(a, c->d_rays, c->d_venc, c->d_counts, c->d_P, c->d_block_sums, c->d_tiles,
-                              c->max_tiles, c->s, c->sample_cap, c->d_status, c->st, &c->launches))
+    if (launch_sampler(a, c->d_rays, c->d_venc, c->d_counts, c->d_P, c->d_block_sums, c->d_tiles,
+                       c->max_tiles, c->s, c->sample_cap, c->d_status, c->st, &c->launches))
         return fail(TFG_ERR_INVALID, "sample: scan capacity exceeded");
     CK(cudaGetLastError());
     c->cur_rays = a.n_rays;
@@ -602,8 +591,7 @@ struct HostBatch {
     std::vector<RayRec> rays;
     std::vector<uint32_t> P;
     uint64_t n_samples = 0;
-    // occupied [lo, hi) of each slot bucket in the device sample arrays (the
-    // buckets are contiguous, or fixed regions for the one-pass draw), and
+    // occupied [lo, hi) of each slot bucket in the device sample arrays and
     // the extent they span
     std::vector<std::pair<uint64_t, uint64_t>> ranges;
     uint64_t extent = 0;
@@ -806,15 +794,10 @@ TFG_API int tfg_create(const tfg_field_config* fcfg, const tfg_train_config* tcf
         rc |= dalloc(c, &c->d_counts, uint64_t(max_rays) * kMaxSlots);
         rc |= dalloc(c, &c->d_P, uint64_t(max_rays) * kMaxSlots + 1);
         rc |= dalloc(c, &c->d_tiles, c->max_tiles);
-        // per-sample arrays: kTrainSlots fixed bucket regions of sample_cap
-        // (the one-pass training draw); other batches use them contiguously
-        const uint64_t scap = uint64_t(kTrainSlots) * c->sample_cap;
-        rc |= dalloc(c, &c->s.local, scap);
-        rc |= dalloc(c, &c->s.td, scap);
-        rc |= dalloc(c, &c->s.endpoint, scap);
-        rc |= dalloc(c, &c->s.io, scap);
-        rc |= dalloc(c, &c->d_lookback, uint64_t(kTrainSlots) * ((uint64_t(max_rays) + 7) / 8));
-        rc |= dalloc(c, &c->d_totals, kTrainSlots);
+        rc |= dalloc(c, &c->s.local, c->sample_cap);
+        rc |= dalloc(c, &c->s.td, c->sample_cap);
+        rc |= dalloc(c, &c->s.endpoint, c->sample_cap);
+        rc |= dalloc(c, &c->s.io, c->sample_cap);
         rc |= dalloc(c, &c->d_ray_out, uint64_t(max_rays) * 5);
         rc |= dalloc(c, &c->d_pixels, uint64_t(max_rays) * 3);
         rc |= dalloc(c, &c->d_feat, uint64_t(c->max_tiles) * 4096);
@@ -833,7 +816,6 @@ TFG_API int tfg_create(const tfg_field_config* fcfg, const tfg_train_config* tcf
         CK(cudaMemsetAsync(c->d_v, 0, c->n_params * 4, c->st));
         CK(cudaMemsetAsync(c->d_grads, 0, c->n_params * 4, c->st));
         CK(cudaMemsetAsync(c->d_status, 0, sizeof(Status), c->st));
-        CK(cudaMemsetAsync(c->d_lookback, 0, uint64_t(kTrainSlots) * ((uint64_t(max_rays) + 7) / 8) * 8, c->st));
         // GlobalColorNet::create (field.hpp:118)
         std::vector<float> color(col);
         Rng rcn(hash_combine(c->tc.seed, kPurposeColor));
@@ -866,7 +848,7 @@ TFG_API int tfg_destroy(tfg_ctx* c) {
                    c->d_counts, c->d_P, c->d_tiles, c->s.local, c->s.td, c->s.endpoint, c->s.io,
                    c->d_ray_out, c->d_pixels, c->d_rparams, c->d_rbits, c->d_rcolor, c->d_rcam,
                    c->d_feat, c->d_tile_rays, c->d_export,
-                   c->d_stage_in, c->d_stage_out, c->d_loss_parts, c->d_imp, c->d_lookback, c->d_totals};
+                   c->d_stage_in, c->d_stage_out, c->d_loss_parts, c->d_imp};
     for (void* p : dev)
         if (p) cudaFree(p);
     stop_init_pool(c);
@@ -1677,7 +1659,7 @@ TFG_API int tfg_field_forward(tfg_ctx* c, float* sigma, float* rgb) {
 TFG_API int tfg_composite(tfg_ctx* c, float* ray_rgb, float* ray_depth, float* ray_opacity,
                           float* d_sigma, float* d_rgb, float* loss) {
     if (!c || !c->have_batch) return fail(TFG_ERR_STATE, "composite: no batch");
-    if (!c->d_export && dalloc(c, &c->d_export, uint64_t(kTrainSlots) * c->sample_cap)) return TFG_ERR_CUDA;
+    if (!c->d_export && dalloc(c, &c->d_export, c->sample_cap)) return TFG_ERR_CUDA;
     int rc = run_composite(c, true, c->d_export);
     if (rc) return rc;
     HostBatch hb;
@@ -1817,7 +1799,7 @@ TFG_API int tfg_get_memory_report(tfg_ctx* c, tfg_memory_report* o) {
     // accepted lists + the two window pixel memos + the build scratch
     o->accept_list = 2 * c->accept_cap * 8 + 2 * c->cand_cap * (4 + 48) + c->cand_cap * 8;
     o->batch_buffers = uint64_t(c->max_rays) * (sizeof(RayRec) + 96 + 8 * kMaxSlots + 20 + 12) +
-                       uint64_t(kTrainSlots) * c->sample_cap * (16 + 8 + 1 + 16);
+                       c->sample_cap * (16 + 8 + 1 + 16);
     o->color_net = (c->n_params - c->color_off) * 4;
     o->total_device = c->bytes_total;
     return 0;

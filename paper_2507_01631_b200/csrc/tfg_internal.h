@@ -186,12 +186,7 @@ struct tfg_ctx {
     bool fwd_done = false;  // feature tiles of the current batch are resident
     bool io_fwd = false;    // io holds the forward's (sigma, rgb) (not yet K3's gradients)
     uint8_t* d_imp = nullptr;  // batch import staging (ray-order arrays of a caller batch)
-    // one-pass training draw (sample_kernel): look-back words (4 per CTA),
-    // bucket totals, launch epoch; bucket s of the sample arrays is the fixed
-    // region [s * sample_cap, (s + 1) * sample_cap)
-    unsigned long long* d_lookback = nullptr;
-    uint32_t* d_totals = nullptr;
-    uint32_t sample_epoch = 0;
+
     bool render_mode = false;
 
     // render
