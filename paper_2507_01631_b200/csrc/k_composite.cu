@@ -58,7 +58,13 @@ __global__ void __launch_bounds__(1024) loss_reduce_kernel(const double* __restr
 #ifndef TFG_COMPOSITE_THREADS
 #define TFG_COMPOSITE_THREADS 256  // >= 256: d_loss_parts holds max_rays / 8 block partials
 #endif
-__global__ void __launch_bounds__(TFG_COMPOSITE_THREADS) composite_kernel(CompositeArgs a) {
+#ifndef TFG_COMPOSITE_MINB
+#define TFG_COMPOSITE_MINB 3
+#endif
+#ifndef TFG_COMPOSITE_CACHE
+#define TFG_COMPOSITE_CACHE 4
+#endif
+__global__ void __launch_bounds__(TFG_COMPOSITE_THREADS, TFG_COMPOSITE_MINB) composite_kernel(CompositeArgs a) {
     __shared__ double blk_sum;
     __shared__ unsigned blk_n;
     int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -73,33 +79,50 @@ __global__ void __launch_bounds__(TFG_COMPOSITE_THREADS) composite_kernel(Compos
         loss_arrive(&blk_sum, &blk_n, a.loss_parts, 0.0, lane);
         return;
     }
-    const RayRec& R = a.rays[i];
-    int nseg = R.status == 0 ? R.nseg : 0;
-    uint32_t base[kMaxSeg];
-    int cnt[kMaxSeg];
-    int m = 0;
-    for (int k = 0; k < nseg; ++k) {
-        base[k] = a.P[uint64_t(R.slot[k]) * a.n_rays + i];
-        cnt[k] = R.cnt[k];
-        m += cnt[k];
+    // the ray's segments from its 64 B header (one line, no dependent loads),
+    // held in registers: bucket position and kept count per segment, their
+    // prefix sums for locating a sample of the concatenated ray
+    const uint4* hq = reinterpret_cast<const uint4*>(a.hdr + i);
+    const uint4 h0 = hq[0], h1 = hq[1], h2 = hq[2], h3 = hq[3];
+    const int hseg = int(h3.w);
+    const bool ray_ok = hseg >= 0;
+    const int nseg = ray_ok ? hseg : 0;
+    const uint32_t base[kMaxSeg] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+    const uint32_t cwd[4] = {h2.x, h2.y, h2.z, h2.w};
+    const float target[3] = {__uint_as_float(h3.x), __uint_as_float(h3.y), __uint_as_float(h3.z)};
+    int pre[kMaxSeg + 1];  // pre[k]: samples of the ray before segment k
+    pre[0] = 0;
+#pragma unroll
+    for (int k = 0; k < kMaxSeg; ++k) {
+        const int c = k < nseg ? int((cwd[k >> 1] >> (16 * (k & 1))) & 0xffffu) : 0;
+        pre[k + 1] = pre[k] + c;
     }
+    const int m = pre[kMaxSeg];
     const uint32_t FULL = 0xffffffffu;
     // The first kCache chunks of 32 samples stay in registers between the
     // forward and the backward sweep (rays have ~70 samples), longer rays
     // re-read their tail.
-    constexpr int kCache = 4;
+    constexpr int kCache = TFG_COMPOSITE_CACHE;
     float4 cio[kCache];
     float2 ctd[kCache];
     uint64_t cpos[kCache];
     float cw[kCache], ct1[kCache];  // weight w_k and T_{k+1} of the cached samples
-    auto fetch = [&](int q, float4& io, float2& td, uint64_t& pos) {
+    // (base / pre captured by value: a by-reference capture would put them in local memory)
+    auto fetch = [base, pre, m, &a](int q, float4& io, float2& td, uint64_t& pos) {
         io = make_float4(0.f, 0.f, 0.f, 0.f);
         td = make_float2(0.f, 0.f);
         pos = 0;
         if (q < m) {
-            int k = 0, rem = q;
-            while (rem >= cnt[k]) { rem -= cnt[k]; ++k; }
-            pos = uint64_t(base[k]) + rem;
+            // segment of sample q: unrolled selects (no local-memory arrays)
+            uint32_t b = base[0];
+            int p0 = 0;
+#pragma unroll
+            for (int k = 1; k < kMaxSeg; ++k)
+                if (q >= pre[k]) {
+                    b = base[k];
+                    p0 = pre[k];
+                }
+            pos = uint64_t(b) + (q - p0);
             io = a.s.io[pos];
             td = a.s.td[pos];
         }
@@ -160,11 +183,11 @@ __global__ void __launch_bounds__(TFG_COMPOSITE_THREADS) composite_kernel(Compos
         if (a.ray_depth) a.ray_depth[i] = dep / fmaxf(op, 1e-10f);
         if (a.ray_opacity) a.ray_opacity[i] = op;
     }
-    if (!a.backward || R.status != 0) {
+    if (!a.backward || !ray_ok) {
         loss_arrive(&blk_sum, &blk_n, a.loss_parts, 0.0, lane);
         return;
     }
-    float er = rr - R.target[0], eg = rg - R.target[1], eb = rb - R.target[2];
+    float er = rr - target[0], eg = rg - target[1], eb = rb - target[2];
     loss_arrive(&blk_sum, &blk_n, a.loss_parts, double(er * er + eg * eg + eb * eb), lane);
     float gr = 2.f * er * a.inv3b, gg = 2.f * eg * a.inv3b, gb = 2.f * eb * a.inv3b;
     // ---------------- backward

@@ -570,16 +570,35 @@ __global__ void tiles_kernel(const uint32_t* __restrict__ P, int n_rays, int nsl
 #ifndef TFG_WRITE_THREADS
 #define TFG_WRITE_THREADS 128
 #endif
+// Lane q < 16 of the ray's warp writes word q of its composite header.
+__device__ __forceinline__ void write_hdr(RayHdr* __restrict__ hdr, const RayRec& R, const uint32_t* __restrict__ P,
+                                          int n_rays, int i, int lane) {
+    const int nseg = R.status == 0 ? R.nseg : -1;
+    uint32_t w = 0;
+    if (lane < kMaxSeg) {
+        w = lane < nseg ? P[uint64_t(R.slot[lane]) * n_rays + i] : 0u;
+    } else if (lane < kMaxSeg + kMaxSeg / 2) {
+        const int k = 2 * (lane - kMaxSeg);
+        w = (k < nseg ? uint32_t(R.cnt[k]) : 0u) | ((k + 1 < nseg ? uint32_t(R.cnt[k + 1]) : 0u) << 16);
+    } else if (lane < kMaxSeg + kMaxSeg / 2 + 3) {
+        w = __float_as_uint(R.target[lane - kMaxSeg - kMaxSeg / 2]);
+    } else if (lane == 15) {
+        w = uint32_t(nseg);
+    }
+    if (lane < 16) reinterpret_cast<uint32_t*>(hdr + i)[lane] = w;
+}
+
 __global__ void __launch_bounds__(TFG_WRITE_THREADS) write_kernel(RaygenArgs a, const RayRec* __restrict__ rays,
                                                     const uint32_t* __restrict__ P,
                                                     const Status* __restrict__ status,
-                                                    SampleArrays out) {
+                                                    SampleArrays out, RayHdr* __restrict__ hdr) {
     pdl_wait();
     int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     int lane = threadIdx.x & 31;
     if (warp >= a.n_rays) return;
     if (status->bits & kStatusSampleOverflow) return;
     const RayRec& R = rays[warp];
+    write_hdr(hdr, R, P, a.n_rays, warp, lane);
     if (R.status != 0) return;
     uint64_t g = a.ray_begin + uint64_t(warp);
     uint64_t key = hash_combine(hash_combine(hash_combine(a.seed, kPurposeJitter), a.iter), g);
@@ -703,11 +722,13 @@ __global__ void __launch_bounds__(128) import_plan_kernel(ImportArgs a, RayRec* 
 
 __global__ void __launch_bounds__(128) import_scatter_kernel(ImportArgs a, const RayRec* __restrict__ rays,
                                                              const uint32_t* __restrict__ P,
-                                                             const Status* __restrict__ status, SampleArrays out) {
+                                                             const Status* __restrict__ status, SampleArrays out,
+                                                             RayHdr* __restrict__ hdr) {
     pdl_wait();
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (warp >= a.n_rays || (status->bits & kStatusSampleOverflow)) return;
     const RayRec& R = rays[warp];
+    write_hdr(hdr, R, P, a.n_rays, warp, lane);
     if (R.status != 0) return;
     uint32_t q = a.offsets[warp];
     for (int k = 0; k < R.nseg; ++k) {
@@ -724,7 +745,7 @@ __global__ void __launch_bounds__(128) import_scatter_kernel(ImportArgs a, const
     }
 }
 
-int launch_import(const ImportArgs& a, RayRec* rays, float4* venc, uint32_t* counts, uint32_t* P,
+int launch_import(const ImportArgs& a, RayRec* rays, RayHdr* hdr, float4* venc, uint32_t* counts, uint32_t* P,
                   uint32_t* block_sums, TileDesc* tiles, int max_tiles, SampleArrays out, uint64_t capacity,
                   Status* status, cudaStream_t st, uint64_t* launches) {
     import_plan_kernel<<<(a.n_rays + 127) / 128, 128, 0, st>>>(a, rays, venc, counts, status);
@@ -734,7 +755,7 @@ int launch_import(const ImportArgs& a, RayRec* rays, float4* venc, uint32_t* cou
                a.nslots, capacity, max_tiles, tiles, status);
     launch_pdl(import_scatter_kernel, dim3((a.n_rays * 32 + 127) / 128), dim3(128), 0, st, a,
                static_cast<const RayRec*>(rays), static_cast<const uint32_t*>(P), static_cast<const Status*>(status),
-               out);
+               out, hdr);
     *launches += 3;
     return 0;
 }
@@ -761,7 +782,7 @@ int launch_accept(const AcceptArgs& args, uint32_t* flags, uint32_t* pos, uint32
     return 0;
 }
 
-int launch_sampler(const RaygenArgs& a, RayRec* rays, float4* venc, uint32_t* counts,
+int launch_sampler(const RaygenArgs& a, RayRec* rays, RayHdr* hdr, float4* venc, uint32_t* counts,
                    uint32_t* P, uint32_t* block_sums, TileDesc* tiles, int max_tiles,
                    SampleArrays out, uint64_t capacity, Status* status, cudaStream_t st,
                    uint64_t* launches) {
@@ -776,7 +797,7 @@ int launch_sampler(const RaygenArgs& a, RayRec* rays, float4* venc, uint32_t* co
     launch_pdl(tiles_kernel, dim3(std::max(1, std::min(148, (max_tiles + 255) / 256))), dim3(256), 0, st, P, a.n_rays, a.slots.n,
                capacity, max_tiles, tiles, status);
     launch_pdl(write_kernel, dim3((a.n_rays * 32 + TFG_WRITE_THREADS - 1) / TFG_WRITE_THREADS), dim3(TFG_WRITE_THREADS), 0,
-               st, a, rays, P, status, out);
+               st, a, rays, P, status, out, hdr);
     *launches += 3;
     return 0;
 }

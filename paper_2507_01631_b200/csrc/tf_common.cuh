@@ -411,6 +411,18 @@ struct RayRec {
     uint16_t cnt[kMaxSeg];      // kept samples of the segment
 };
 
+// What compositing needs of a ray, in one 64 B line (written by the sample
+// writer once the bucket positions are known): the bucket position and kept
+// count of each segment in ray order, the target colour; nseg < 0 marks a
+// failed ray (no loss, no gradient).
+struct alignas(16) RayHdr {
+    uint32_t base[kMaxSeg];
+    uint16_t cnt[kMaxSeg];
+    float target[3];
+    int32_t nseg;
+};
+static_assert(sizeof(RayHdr) == 64, "RayHdr is one 64 B line");
+
 // Tile of <= 128 consecutive samples of one slot bucket (K2/K4 work unit).
 struct TileDesc {
     uint32_t start;

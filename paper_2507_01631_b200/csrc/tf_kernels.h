@@ -113,8 +113,7 @@ struct FieldGradArgs {
 };
 
 struct CompositeArgs {
-    const RayRec* rays;
-    const uint32_t* P;   // bucket positions [slot][ray]
+    const RayHdr* hdr;   // per ray: segment positions / counts, target
     int n_rays;
     SampleArrays s;
     const Status* status_in;
@@ -170,11 +169,11 @@ int scan_exclusive(const uint32_t* in, uint64_t n, uint32_t* out, uint32_t* bloc
                    uint32_t* grand_total, cudaStream_t st, uint64_t* launches);
 int launch_accept(const AcceptArgs& a, uint32_t* flags, uint32_t* pos, uint32_t* block_sums,
                   uint32_t* n_out, uint64_t* out, cudaStream_t st, uint64_t* launches);
-int launch_sampler(const RaygenArgs& a, RayRec* rays, float4* venc, uint32_t* counts,
+int launch_sampler(const RaygenArgs& a, RayRec* rays, RayHdr* hdr, float4* venc, uint32_t* counts,
                    uint32_t* P, uint32_t* block_sums, TileDesc* tiles, int max_tiles,
                    SampleArrays out, uint64_t capacity, Status* status, cudaStream_t st,
                    uint64_t* launches);
-int launch_import(const ImportArgs& a, RayRec* rays, float4* venc, uint32_t* counts, uint32_t* P,
+int launch_import(const ImportArgs& a, RayRec* rays, RayHdr* hdr, float4* venc, uint32_t* counts, uint32_t* P,
                   uint32_t* block_sums, TileDesc* tiles, int max_tiles, SampleArrays out, uint64_t capacity,
                   Status* status, cudaStream_t st, uint64_t* launches);
 void launch_field_forward_tc(const FieldArgs& a, uint8_t* feat, int32_t* rays, int sms,

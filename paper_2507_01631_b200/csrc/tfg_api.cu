@@ -511,7 +511,7 @@ int run_sampler(tfg_ctx* c, RaygenArgs& a) {
         return fail(TFG_ERR_INVALID, "sample: n_rays outside (0, max_rays]");
     PhaseScope ps(c, kPhSampler);
     CK(cudaMemsetAsync(c->d_status, 0, sizeof(Status), c->st));
-    if (launch_sampler(a, c->d_rays, c->d_venc, c->d_counts, c->d_P, c->d_block_sums, c->d_tiles,
+    if (launch_sampler(a, c->d_rays, c->d_hdr, c->d_venc, c->d_counts, c->d_P, c->d_block_sums, c->d_tiles,
                        c->max_tiles, c->s, c->sample_cap, c->d_status, c->st, &c->launches))
         return fail(TFG_ERR_INVALID, "sample: scan capacity exceeded");
     CK(cudaGetLastError());
@@ -548,8 +548,7 @@ int run_composite(tfg_ctx* c, bool backward, float4* export_io = nullptr) {
     PhaseScope ps(c, kPhComposite);
     if (backward) c->io_fwd = false;  // io now holds the pre-activation gradients
     CompositeArgs a{};
-    a.rays = c->d_rays;
-    a.P = c->d_P;
+    a.hdr = c->d_hdr;
     a.n_rays = c->cur_rays;
     a.s = c->s;
     a.status_in = c->d_status;
@@ -790,6 +789,7 @@ TFG_API int tfg_create(const tfg_field_config* fcfg, const tfg_train_config* tcf
         rc |= dalloc(c, &c->d_sticky, 4);
         rc |= dalloc(c, &c->d_status, 1);
         rc |= dalloc(c, &c->d_rays, max_rays);
+        rc |= dalloc(c, &c->d_hdr, max_rays);
         rc |= dalloc(c, &c->d_venc, uint64_t(max_rays) * 6);
         rc |= dalloc(c, &c->d_counts, uint64_t(max_rays) * kMaxSlots);
         rc |= dalloc(c, &c->d_P, uint64_t(max_rays) * kMaxSlots + 1);
@@ -844,7 +844,7 @@ TFG_API int tfg_destroy(tfg_ctx* c) {
     void* dev[] = {c->d_params, c->d_grads, c->d_m, c->d_v, c->d_ema, c->d_bits, c->d_group_flags, c->d_sticky,
                    c->d_status, c->d_cams, c->d_east, c->d_north, c->d_flags, c->d_pos,
                    c->d_block_sums, c->d_acc_sums, c->d_todo_n, c->d_view_start, c->d_union, c->d_crop4,
-                   c->d_rays, c->d_venc,
+                   c->d_rays, c->d_hdr, c->d_venc,
                    c->d_counts, c->d_P, c->d_tiles, c->s.local, c->s.td, c->s.endpoint, c->s.io,
                    c->d_ray_out, c->d_pixels, c->d_rparams, c->d_rbits, c->d_rcolor, c->d_rcam,
                    c->d_feat, c->d_tile_rays, c->d_export,
@@ -1466,7 +1466,7 @@ TFG_API int tfg_batch_import(tfg_ctx* c, const tfg_batch_view* in, int n_rays) {
     {
         PhaseScope ps(c, kPhSampler);
         CK(cudaMemsetAsync(c->d_status, 0, sizeof(Status), c->st));
-        if (launch_import(a, c->d_rays, c->d_venc, c->d_counts, c->d_P, c->d_block_sums, c->d_tiles, c->max_tiles,
+        if (launch_import(a, c->d_rays, c->d_hdr, c->d_venc, c->d_counts, c->d_P, c->d_block_sums, c->d_tiles, c->max_tiles,
                           c->s, c->sample_cap, c->d_status, c->st, &c->launches))
             return fail(TFG_ERR_INVALID, "batch_import: scan capacity exceeded");
         CK(cudaGetLastError());
@@ -1798,7 +1798,7 @@ TFG_API int tfg_get_memory_report(tfg_ctx* c, tfg_memory_report* o) {
     o->crops = 2 * c->crop_cap;
     // accepted lists + the two window pixel memos + the build scratch
     o->accept_list = 2 * c->accept_cap * 8 + 2 * c->cand_cap * (4 + 48) + c->cand_cap * 8;
-    o->batch_buffers = uint64_t(c->max_rays) * (sizeof(RayRec) + 96 + 8 * kMaxSlots + 20 + 12) +
+    o->batch_buffers = uint64_t(c->max_rays) * (sizeof(RayRec) + sizeof(RayHdr) + 96 + 8 * kMaxSlots + 20 + 12) +
                        c->sample_cap * (16 + 8 + 1 + 16);
     o->color_net = (c->n_params - c->color_off) * 4;
     o->total_device = c->bytes_total;

@@ -166,6 +166,7 @@ struct tfg_ctx {
 
     // batch
     RayRec* d_rays = nullptr;
+    RayHdr* d_hdr = nullptr;  // per-ray composite header (written with the samples)
     float4* d_venc = nullptr;
     uint32_t *d_counts = nullptr, *d_P = nullptr;
     double* d_loss_parts = nullptr;  // per-block partial losses of K3
