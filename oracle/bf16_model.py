@@ -28,7 +28,9 @@ DENSITY_MAX = np.float32(1e4)
 # the operands the kernels hand to tcgen05.mma as bf16
 FWD_OPS = ("feat", "W1", "H1", "W2", "CIN", "C1", "A1", "C2", "A2", "C3")
 BWD_OPS = ("D3", "C3b", "DC2", "C2b", "DC1", "C1b", "DO", "W2b", "DH1", "W1b")
-KERNEL = frozenset(FWD_OPS + BWD_OPS)
+# "enc16": the forward gather reads fp16 shadows of the hash tables (as
+# instant-ngp stores them); the sums and weights stay fp32
+KERNEL = frozenset(FWD_OPS + BWD_OPS + ("enc16",))
 
 
 def bf16(x):
@@ -53,7 +55,12 @@ def split2(x):
     return hi + bf16(x - hi)
 
 
-ROUND = {"bf16": bf16, "tf32": tf32, "split": split2}
+def fp16(x):
+    """Round-to-nearest-even to IEEE half, as float32."""
+    return np.asarray(x, np.float32).astype(np.float16).astype(np.float32)
+
+
+ROUND = {"bf16": bf16, "tf32": tf32, "split": split2, "fp16": fp16}
 
 
 def view_encoding(directions):
@@ -114,17 +121,18 @@ def field(enc, dnet, color, loc, venc, rq=KERNEL, dsig=None, drgb=None):
     g_dnet, g_color, d_feat])."""
     def R(name, x):
         if isinstance(rq, dict):
-            return ROUND[rq[name]](x) if name in rq else np.asarray(x, np.float32)
+            return ROUND[rq[name]](x) if name in rq and name != "enc16" else np.asarray(x, np.float32)
         return bf16(x) if name in rq else np.asarray(x, np.float32)
 
     enc = np.asarray(enc, np.float32)
+    enc_g = fp16(enc) if ("enc16" in rq) else enc  # the tables the gather reads
     W1, b1, W2, b2, C1, c1, C2, c2, C3, c3 = _mats(np.asarray(dnet, np.float32), np.asarray(color, np.float32))
     cs = corners(loc)
     S = np.asarray(loc).shape[0]
     feat = np.zeros((S, 16), np.float32)
     for l, (idx, w) in enumerate(cs):
         for q in range(2):
-            feat[:, 2 * l + q] = (w * enc[2 * idx + q]).sum(axis=1)
+            feat[:, 2 * l + q] = (w * enc_g[2 * idx + q]).sum(axis=1)
     X0 = R("feat", feat)
     h1p = X0 @ R("W1", W1).T + b1
     mh = h1p > 0

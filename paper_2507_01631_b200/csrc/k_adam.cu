@@ -7,6 +7,7 @@
 // with lr and bias corrections of the persistent per-group step count
 // computed on the host.  A group with a non-finite gradient aborts the whole
 // step (the reference throws before updating, naming the group).
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include "tf_common.cuh"
@@ -92,6 +93,14 @@ __global__ void __launch_bounds__(256) adam_kernel(AdamArgs a, uint64_t total) {
         m4[i] = m;
         v4[i] = v;
         p4[i] = p;
+        if (G.half_slot >= 0) {  // the slot's fp16 table shadow (forward gather)
+            __half2* h = reinterpret_cast<__half2*>(a.enc16) + (uint64_t(G.half_slot) * a.enc_n + (4 * i - G.offset)) / 2;
+            uint2 q;
+            __half2 lo = __floats2half2_rn(p.x, p.y), hi = __floats2half2_rn(p.z, p.w);
+            q.x = *reinterpret_cast<uint32_t*>(&lo);
+            q.y = *reinterpret_cast<uint32_t*>(&hi);
+            *reinterpret_cast<uint2*>(h) = q;
+        }
     }
     for (uint64_t i = 4 * n4 + uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
         const AdamGroup& G = a.g[group_of(a, i)];
@@ -100,7 +109,25 @@ __global__ void __launch_bounds__(256) adam_kernel(AdamArgs a, uint64_t total) {
         a.m[i] = m;
         a.v[i] = v;
         a.params[i] = p;
+        if (G.half_slot >= 0)
+            reinterpret_cast<__half*>(a.enc16)[uint64_t(G.half_slot) * a.enc_n + (i - G.offset)] = __float2half_rn(p);
     }
+}
+
+__global__ void __launch_bounds__(256) enc_half_kernel(const float* __restrict__ params, uint64_t stride,
+                                                       uint64_t enc_n, __half2* __restrict__ out) {
+    pdl_wait();
+    const int k = blockIdx.y;
+    const float2* src = reinterpret_cast<const float2*>(params + uint64_t(k) * stride);
+    __half2* dst = out + uint64_t(k) * enc_n / 2;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < enc_n / 2; i += uint64_t(gridDim.x) * blockDim.x)
+        dst[i] = __float22half2_rn(src[i]);
+}
+
+void launch_enc_half(const float* params, uint64_t stride, int n, uint64_t enc_n, void* out, cudaStream_t st,
+                     uint64_t* launches) {
+    launch_pdl(enc_half_kernel, dim3(148, n), dim3(256), 0, st, params, stride, enc_n, static_cast<__half2*>(out));
+    *launches += 1;
 }
 
 void launch_adam(const AdamArgs& a, uint64_t total, cudaStream_t st, uint64_t* launches) {

@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(128) hash_fwd_kernel(FieldArgs a, uint8_t* __r
         if (r < td.n) {
             float4 L = a.s.local[uint64_t(td.start) + r];
             ray = __float_as_int(L.w);
-            hash_encode(a.hl, a.f.enc[td.slot], L.x, L.y, L.z, f);
+            hash_encode16(a.hl, a.f.enc16[td.slot], L.x, L.y, L.z, f);
         } else {
 #pragma unroll
             for (int i = 0; i < kFeatDim; ++i) f[i] = 0.f;

@@ -598,8 +598,10 @@ __global__ void __launch_bounds__(TFG_WRITE_THREADS) write_kernel(RaygenArgs a, 
     if (warp >= a.n_rays) return;
     if (status->bits & kStatusSampleOverflow) return;
     const RayRec& R = rays[warp];
-    write_hdr(hdr, R, P, a.n_rays, warp, lane);
-    if (R.status != 0) return;
+    if (R.status != 0) {
+        write_hdr(hdr, R, P, a.n_rays, warp, lane);
+        return;
+    }
     uint64_t g = a.ray_begin + uint64_t(warp);
     uint64_t key = hash_combine(hash_combine(hash_combine(a.seed, kPurposeJitter), a.iter), g);
     // segment fields straight from the (warp-uniform) ray record and the
@@ -663,6 +665,7 @@ __global__ void __launch_bounds__(TFG_WRITE_THREADS) write_kernel(RaygenArgs a, 
         if (r > a.delta_cap) r = a.delta_cap;
         out.td[pend_pos] = make_float2(float(pend_t), float(r));
     }
+    write_hdr(hdr, R, P, a.n_rays, warp, lane);  // last: off the samples' critical path
 }
 
 // ------------------------------------------------------------------ batch import

@@ -392,6 +392,10 @@ struct SlotTable {
 
 struct FieldPtrs {
     const float* enc[kMaxSlots];
+    // fp16 shadow of each slot's hash tables (__half2 per entry): what the
+    // forward gather reads (as instant-ngp stores its tables); kept in step
+    // with the fp32 master tables by Adam and by a conversion on reload
+    const void* enc16[kMaxSlots];
     const float* dnet[kMaxSlots];
     const uint32_t* occ_bits[kMaxSlots];
     const float* color;

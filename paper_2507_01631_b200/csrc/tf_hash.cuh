@@ -2,6 +2,7 @@
 // field kernels (HashGridT, nn.hpp:199-266).
 #pragma once
 
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include "tf_common.cuh"
@@ -107,6 +108,44 @@ __device__ __forceinline__ void hash_encode(const HashLayout& hl, const float* _
             } else {
                 e[2 * q] = __ldg(t2 + i0);
                 e[2 * q + 1] = __ldg(t2 + i1);
+            }
+        }
+        float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            a0 += c.w[k] * e[k].x;
+            a1 += c.w[k] * e[k].y;
+        }
+        feat[2 * l] = a0;
+        feat[2 * l + 1] = a1;
+    }
+}
+
+// The same gather from the fp16 shadow tables: an entry is one __half2
+// (4 bytes), an aligned x-neighbour pair one 8-byte load; the weights and
+// the sums stay fp32.  Half the bytes of hash_encode returned to registers.
+__device__ __forceinline__ void hash_encode16(const HashLayout& hl, const void* __restrict__ tab,
+                                              float x, float y, float z, float* feat) {
+    const __half2* t2 = reinterpret_cast<const __half2*>(tab);
+    const uint2* t4 = reinterpret_cast<const uint2*>(tab);
+#pragma unroll
+    for (int l = 0; l < kLevels; ++l) {
+        Corner c;
+        hash_level(hl, l, x, y, z, c);
+        float2 e[8];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            uint32_t i0 = c.idx[2 * q], i1 = c.idx[2 * q + 1];
+            if (i1 == (i0 ^ 1u)) {
+                const uint2 v = __ldg(t4 + (i0 >> 1));
+                const float2 lo = __half22float2(*reinterpret_cast<const __half2*>(&v.x));
+                const float2 hi = __half22float2(*reinterpret_cast<const __half2*>(&v.y));
+                bool odd = i0 & 1u;
+                e[2 * q] = odd ? hi : lo;
+                e[2 * q + 1] = odd ? lo : hi;
+            } else {
+                e[2 * q] = __half22float2(__ldg(t2 + i0));
+                e[2 * q + 1] = __half22float2(__ldg(t2 + i1));
             }
         }
         float a0 = 0.f, a1 = 0.f;

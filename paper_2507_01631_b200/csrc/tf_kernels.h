@@ -132,7 +132,7 @@ struct CompositeArgs {
 struct AdamGroup {
     uint64_t offset, count;
     float lr, bc1, bc2;
-    int pad;
+    int half_slot;  // >= 0: a slot's hash tables, also written to its fp16 shadow
 };
 constexpr int kMaxGroups = 2 * kTrainSlots + 1;
 struct AdamArgs {
@@ -149,6 +149,8 @@ struct AdamArgs {
     // like the reference's throw) until the host reads it
     uint32_t* sticky;
     uint32_t seq;           // host sequence number of this optimizer step
+    void* enc16;            // fp16 table shadows (slot k at k * enc_n entries of __half2)
+    uint64_t enc_n;         // floats per slot's tables
 };
 
 struct OccArgs {
@@ -182,6 +184,9 @@ void launch_field_backward_tc(const FieldArgs& a, const FieldGradArgs& g, uint8_
                               int32_t* rays, int sms, cudaStream_t st, uint64_t* launches);
 void launch_composite(const CompositeArgs& a, cudaStream_t st, uint64_t* launches);
 void launch_adam(const AdamArgs& a, uint64_t total, cudaStream_t st, uint64_t* launches);
+// fp32 hash tables of n slots (params + k * stride) -> their fp16 shadows (out + k * enc_n halves)
+void launch_enc_half(const float* params, uint64_t stride, int n, uint64_t enc_n, void* out, cudaStream_t st,
+                     uint64_t* launches);
 void launch_occupancy(const OccArgs& a, cudaStream_t st, uint64_t* launches);
 
 

@@ -276,6 +276,7 @@ FieldPtrs train_ptrs(tfg_ctx* c) {
     FieldPtrs f{};
     for (int k = 0; k < c->nslots; ++k) {
         f.enc[k] = c->d_params + uint64_t(k) * c->stride;
+        f.enc16[k] = static_cast<uint16_t*>(c->d_enc16) + uint64_t(k) * c->enc_n;
         f.dnet[k] = f.enc[k] + c->enc_n;
         f.occ_bits[k] = c->d_bits + uint64_t(k) * kOccWords;
     }
@@ -536,6 +537,10 @@ FieldArgs field_args(tfg_ctx* c, const FieldPtrs& f) {
 
 int run_forward(tfg_ctx* c, const FieldPtrs& f) {
     PhaseScope ps(c, kPhFieldFwd);
+    if (!c->render_mode && c->enc16_dirty && c->nslots > 0) {  // slot tables written outside Adam
+        launch_enc_half(c->d_params, c->stride, c->nslots, c->enc_n, c->d_enc16, c->st, &c->launches);
+        c->enc16_dirty = false;
+    }
     c->fwd_done = true;
     c->io_fwd = true;
     launch_field_forward_tc(field_args(c, f), c->d_feat, c->d_tile_rays, c->sms, c->st,
@@ -785,6 +790,7 @@ TFG_API int tfg_create(const tfg_field_config* fcfg, const tfg_train_config* tcf
         rc |= dalloc(c, &c->d_v, c->n_params);
         rc |= dalloc(c, &c->d_ema, uint64_t(kTrainSlots) * kOccVox);
         rc |= dalloc(c, &c->d_bits, uint64_t(kMaxSlots) * kOccWords);
+        rc |= dalloc(c, reinterpret_cast<uint16_t**>(&c->d_enc16), uint64_t(kTrainSlots + kMaxSlots) * c->enc_n);
         rc |= dalloc(c, &c->d_group_flags, 16);
         rc |= dalloc(c, &c->d_sticky, 4);
         rc |= dalloc(c, &c->d_status, 1);
@@ -842,6 +848,7 @@ TFG_API int tfg_destroy(tfg_ctx* c) {
     cudaDeviceSynchronize();
     comm_release(c);
     void* dev[] = {c->d_params, c->d_grads, c->d_m, c->d_v, c->d_ema, c->d_bits, c->d_group_flags, c->d_sticky,
+                   c->d_enc16,
                    c->d_status, c->d_cams, c->d_east, c->d_north, c->d_flags, c->d_pos,
                    c->d_block_sums, c->d_acc_sums, c->d_todo_n, c->d_view_start, c->d_union, c->d_crop4,
                    c->d_rays, c->d_hdr, c->d_venc,
@@ -1122,6 +1129,7 @@ TFG_API int tfg_set_window(tfg_ctx* c, int pr, int pc) {
     }
     (void)any_plain;
     for (int s = 0; s < ns; ++s) c->slot_tile[s] = next[s];
+    c->enc16_dirty = true;
     c->nslots = ns;
     c->pos_r = pr;
     c->pos_c = pc;
@@ -1298,10 +1306,13 @@ TFG_API int tfg_optimizer_step(tfg_ctx* c, uint64_t iter) {
         for (int k = 0; k < c->nslots; ++k) r.tile[k] = c->slot_tile[k];
         c->unverified.push_back(r);
     }
-    auto group = [&](AdamGroup& G, uint64_t off, uint64_t cnt, double base, uint64_t& step) {
+    a.enc16 = c->d_enc16;
+    a.enc_n = c->enc_n;
+    auto group = [&](AdamGroup& G, uint64_t off, uint64_t cnt, double base, uint64_t& step, int half_slot) {
         uint64_t s = ++step;
         G.offset = off;
         G.count = cnt;
+        G.half_slot = half_slot;
         G.lr = float(lr_at(base, s));
         G.bc1 = float(1.0 - std::pow(double(t.beta1), double(s)));
         G.bc2 = float(1.0 - std::pow(double(t.beta2), double(s)));
@@ -1309,10 +1320,10 @@ TFG_API int tfg_optimizer_step(tfg_ctx* c, uint64_t iter) {
     int ng = 0;
     for (int k = 0; k < c->nslots; ++k) {
         TileHost& th = c->tiles[c->slot_tile[k]];
-        group(a.g[ng++], uint64_t(k) * c->stride, c->enc_n, t.lr_field, th.enc_step);
-        group(a.g[ng++], uint64_t(k) * c->stride + c->enc_n, c->stride - c->enc_n, t.lr_field, th.dnet_step);
+        group(a.g[ng++], uint64_t(k) * c->stride, c->enc_n, t.lr_field, th.enc_step, k);
+        group(a.g[ng++], uint64_t(k) * c->stride + c->enc_n, c->stride - c->enc_n, t.lr_field, th.dnet_step, -1);
     }
-    group(a.g[ng++], c->color_off, c->n_params - c->color_off, t.lr_color, c->color_step);
+    group(a.g[ng++], c->color_off, c->n_params - c->color_off, t.lr_color, c->color_step, -1);
     a.n_groups = ng;
     // the colour group sits after the 4-slot region; a 1-slot window leaves a gap
     uint64_t total = c->n_params;
@@ -1321,6 +1332,7 @@ TFG_API int tfg_optimizer_step(tfg_ctx* c, uint64_t iter) {
         // gap between slot region and colour: give it a zero-lr pseudo group
         for (int g = ng; g > 2 * c->nslots; --g) a.g[g] = a.g[g - 1];
         AdamGroup gap{};
+        gap.half_slot = -1;
         gap.offset = uint64_t(c->nslots) * c->stride;
         gap.count = c->color_off - gap.offset;
         gap.lr = 0.f;
@@ -1496,6 +1508,7 @@ TFG_API int tfg_set_slot_params(tfg_ctx* c, int slot, const float* enc, const fl
     if (enc) CK(cudaMemcpy(c->d_params + off, enc, c->enc_n * 4, cudaMemcpyHostToDevice));
     if (dnet) CK(cudaMemcpy(c->d_params + off + c->enc_n, dnet, (c->stride - c->enc_n) * 4, cudaMemcpyHostToDevice));
     c->fwd_done = false;
+    c->enc16_dirty = true;
     return 0;
 }
 
@@ -1614,6 +1627,7 @@ TFG_API int tfg_adam_step(tfg_ctx* c, float* params, const float* grads, float* 
     a.n_groups = 1;
     a.g[0].offset = 0;
     a.g[0].count = n;
+    a.g[0].half_slot = -1;
     a.g[0].lr = float(lr_decay_rate == 1.0 ? lr_base
                                            : lr_base * std::pow(lr_decay_rate, double(s) / double(lr_decay_steps)));
     a.g[0].bc1 = float(1.0 - std::pow(double(beta1), double(s)));
@@ -1747,6 +1761,7 @@ TFG_API int tfg_set_tile_state(tfg_ctx* c, int slot, const tfg_tile_state* in) {
     TileHost& th = c->tiles[c->slot_tile[slot]];
     th.enc_step = in->enc_step;
     th.dnet_step = in->dnet_step;
+    c->enc16_dirty = true;
     if (rc) return rc;
     return run_occupancy(c, false, nullptr);
 }
@@ -1843,6 +1858,10 @@ TFG_API int tfg_render_setup(tfg_ctx* c, const int32_t* rows, const int32_t* col
                       cudaMemcpyHostToDevice));
     }
     CK(cudaMemcpy(c->d_rcolor, color_params, (c->n_params - c->color_off) * 4, cudaMemcpyHostToDevice));
+    // the render tiles' fp16 table shadows (after the training slots')
+    launch_enc_half(c->d_rparams, c->stride, n, c->enc_n,
+                    static_cast<uint16_t*>(c->d_enc16) + uint64_t(kTrainSlots) * c->enc_n, c->st, &c->launches);
+    CK(cudaStreamSynchronize(c->st));
     return 0;
 }
 
@@ -1856,6 +1875,7 @@ TFG_API int tfg_render_pixels(tfg_ctx* c, const tfg_rpc* cam, const int32_t* pix
     FieldPtrs f{};
     for (int k = 0; k < c->rn; ++k) {
         f.enc[k] = c->d_rparams + uint64_t(k) * c->stride;
+        f.enc16[k] = static_cast<uint16_t*>(c->d_enc16) + uint64_t(kTrainSlots + k) * c->enc_n;
         f.dnet[k] = f.enc[k] + c->enc_n;
         f.occ_bits[k] = c->d_rbits + uint64_t(k) * kOccWords;
     }

@@ -107,6 +107,11 @@ struct tfg_ctx {
     float *d_params = nullptr, *d_grads = nullptr, *d_m = nullptr, *d_v = nullptr;
     float* d_ema = nullptr;
     uint32_t* d_bits = nullptr;
+    // fp16 shadows of the hash tables for the forward gather: training slots
+    // [0, kTrainSlots), render slots after them; Adam keeps the training ones
+    // current, any other write of the slot parameters marks them dirty
+    void* d_enc16 = nullptr;
+    bool enc16_dirty = true;
     uint32_t* d_group_flags = nullptr;
     Status* d_status = nullptr;
     Status* h_status = nullptr;
