@@ -116,6 +116,18 @@ public:
         return loss;
     }
     void backward_batch() { check(tfg_field_backward(c_)); }
+    // caller-owned data (the reference operators' arguments; the field.hpp
+    // signatures themselves are in tilefield_gpu_field.hpp)
+    void import_batch(const tfg_batch_view& batch, int n_rays) { check(tfg_batch_import(c_, &batch, n_rays)); }
+    void set_slot_params(int slot, const float* enc, const float* dnet) {
+        check(tfg_set_slot_params(c_, slot, enc, dnet));
+    }
+    void set_color_params(const float* params) { check(tfg_set_color_params(c_, params)); }
+    void set_field_outputs(const float* sigma, const float* rgb) { check(tfg_set_field_outputs(c_, sigma, rgb)); }
+    void backward_batch_from(const float* d_sigma, const float* d_rgb) {
+        check(tfg_field_backward_from(c_, d_sigma, d_rgb));
+    }
+    void grads(int slot, float* enc, float* dnet, float* color) { check(tfg_get_grads(c_, slot, enc, dnet, color)); }
     void tile_state(int slot, tfg_tile_state* out) { check(tfg_get_tile_state(c_, slot, out)); }
     void set_tile_state(int slot, const tfg_tile_state& in) { check(tfg_set_tile_state(c_, slot, &in)); }
     tfg_memory_report memory_report() {
