@@ -378,14 +378,19 @@ __device__ __forceinline__ bool occ_test(const uint32_t* bits, float x, float y,
 #ifndef TFG_RAYGEN_MEMO_MINB
 #define TFG_RAYGEN_MEMO_MINB 8
 #endif
-template <bool kSolve>
+// kLanes threads per ray: 2 for explicit pixels (one Newton localisation
+// each); the memo path also runs with 8 for small batches, where the per-ray
+// interior-sample loop (split over the lanes) is the latency chain.
+template <bool kSolve, int kLanes>
 __global__ void __launch_bounds__(128, kSolve ? TFG_RAYGEN_MINB : TFG_RAYGEN_MEMO_MINB)
     raygen_kernel(RaygenArgs a, RayRec* __restrict__ rays, float4* __restrict__ venc,
                   uint32_t* __restrict__ counts, Status* __restrict__ status) {
+    static_assert(!kSolve || kLanes == 2, "the Newton path pairs two lanes per ray");
     pdl_wait();
     const int gt = blockIdx.x * blockDim.x + threadIdx.x;
-    const int i = gt >> 1, hi = gt & 1;
+    const int i = gt / kLanes, sub = gt % kLanes, hi = sub & 1;
     const uint32_t pair = 3u << ((threadIdx.x & 31) & ~1);
+    const uint32_t group = ((1u << kLanes) - 1u) << ((threadIdx.x & 31) & ~(kLanes - 1));
     const bool valid = i < a.n_rays;
     const int ii = valid ? i : 0;
     uint64_t g = a.ray_begin + uint64_t(ii);
@@ -406,7 +411,7 @@ __global__ void __launch_bounds__(128, kSolve ? TFG_RAYGEN_MINB : TFG_RAYGEN_MEM
         v = int(e >> 40);
         row = int((e >> 20) & 0xFFFFF);
         col = int(e & 0xFFFFF);
-        if (na == 0 && valid && hi == 0) atomicOr(&status->bits, kStatusRayFail);
+        if (na == 0 && valid && sub == 0) atomicOr(&status->bits, kStatusRayFail);
         if (na && a.memo_rays) {
             const int* cr = a.crop_rect + 4 * v;  // r0, c0, cols, rows: memo index = crop pixel index
             memo = a.memo_rays + 6 * (a.crop_offset[v] / 3 + uint64_t(row - cr[0]) * uint64_t(cr[2]) + uint64_t(col - cr[1]));
@@ -439,17 +444,17 @@ __global__ void __launch_bounds__(128, kSolve ? TFG_RAYGEN_MINB : TFG_RAYGEN_MEM
             R.status = rpc_ray_finish(tx, ty, bx, by, a.z_min, a.z_max, R.o, R.d);
         }
     }
-    if (valid && hi == 0)
+    if (valid && sub == 0)
         for (int s = 0; s < a.slots.n; ++s) counts[uint64_t(s) * a.n_rays + i] = 0;
     R.nseg = 0;
     if (R.status != 0) {
-        if (valid && hi == 0) {
+        if (valid && sub == 0) {
             atomicOr(&status->bits, kStatusRayFail);
             rays[i] = R;
         }
         return;
     }
-    if (a.crop_bytes && hi == 0) {
+    if (a.crop_bytes && sub == 0) {
         const int* cr = a.crop_rect + 4 * v;  // r0, c0, cols, rows
         const uint8_t* px = a.crop_bytes + a.crop_offset[v] +
                             3 * (uint64_t(row - cr[0]) * uint64_t(cr[2]) + uint64_t(col - cr[1]));
@@ -480,7 +485,7 @@ __global__ void __launch_bounds__(128, kSolve ? TFG_RAYGEN_MINB : TFG_RAYGEN_MEM
         p.tf[j] = t1;
         p.slot[j] = s;
     }
-    if (overflow && valid && hi == 0) atomicOr(&status->bits, kStatusSegOverflow);
+    if (overflow && valid && sub == 0) atomicOr(&status->bits, kStatusSegOverflow);
     plan_intervals(p, a.spm, a.cap);
     uint64_t key = hash_combine(hash_combine(hash_combine(a.seed, kPurposeJitter), a.iter), g);
     R.nseg = p.nseg;
@@ -496,28 +501,29 @@ __global__ void __launch_bounds__(128, kSolve ? TFG_RAYGEN_MINB : TFG_RAYGEN_MEM
         const double tn = p.tn[k], tf = p.tf[k];
         const double step = (tf - tn) / n;
         int cnt = 0;
-        for (int j = 1 + hi; j < n; j += 2) {
+        for (int j = 1 + sub; j < n; j += kLanes) {
             double t = sample_t(tn, tf, n, k, j, a.jitter, key, step);
             float lx = float((o0 + t * d0 - f0) * f3);
             float ly = float((o1 + t * d1 - f1) * f4);
             float lz = float((o2 + t * d2 - f2) * f5);
             cnt += occ_test(bits, lx, ly, lz);
         }
-        cnt += __shfl_xor_sync(pair, cnt, 1);
+#pragma unroll
+        for (int o = 1; o < kLanes; o <<= 1) cnt += __shfl_xor_sync(group, cnt, o);
         cnt += 2;  // endpoints are never culled
         R.slot[k] = uint8_t(p.slot[k]);
         R.tn[k] = p.tn[k];
         R.tf[k] = p.tf[k];
         R.nint[k] = uint16_t(n);
         R.cnt[k] = uint16_t(cnt);
-        if (valid && hi == 0) counts[uint64_t(p.slot[k]) * a.n_rays + i] = uint32_t(cnt);
+        if (valid && sub == 0) counts[uint64_t(p.slot[k]) * a.n_rays + i] = uint32_t(cnt);
     }
     if (!valid) return;
-    if (hi == 0) {
+    if (sub == 0) {
         rays[i] = R;
         return;
     }
-    write_view_encoding(R.d, venc + uint64_t(i) * 6);
+    if (sub == 1) write_view_encoding(R.d, venc + uint64_t(i) * 6);
 }
 
 // Slot buckets -> 128-sample single-slot tiles (one block).
@@ -792,12 +798,18 @@ int launch_sampler(const RaygenArgs& a, RayRec* rays, RayHdr* hdr, float4* venc,
                    uint32_t* P, uint32_t* block_sums, TileDesc* tiles, int max_tiles,
                    SampleArrays out, uint64_t capacity, Status* status, cudaStream_t st,
                    uint64_t* launches) {
-    if (!a.pixels && a.memo_rays)
-        launch_pdl(raygen_kernel<false>, dim3((2 * a.n_rays + 127) / 128), dim3(128), 0, st, a, rays, venc, counts,
-                   status);
+#ifndef TFG_RAYGEN_WIDE_BELOW
+#define TFG_RAYGEN_WIDE_BELOW 32768  // memo draws of fewer rays: 8 lanes per ray
+#endif
+    if (!a.pixels && a.memo_rays && a.n_rays < TFG_RAYGEN_WIDE_BELOW)
+        launch_pdl(raygen_kernel<false, 8>, dim3((8 * a.n_rays + 127) / 128), dim3(128), 0, st, a, rays, venc,
+                   counts, status);
+    else if (!a.pixels && a.memo_rays)
+        launch_pdl(raygen_kernel<false, 2>, dim3((2 * a.n_rays + 127) / 128), dim3(128), 0, st, a, rays, venc,
+                   counts, status);
     else
-        launch_pdl(raygen_kernel<true>, dim3((2 * a.n_rays + 127) / 128), dim3(128), 0, st, a, rays, venc, counts,
-                   status);
+        launch_pdl(raygen_kernel<true, 2>, dim3((2 * a.n_rays + 127) / 128), dim3(128), 0, st, a, rays, venc,
+                   counts, status);
     uint64_t n = uint64_t(a.slots.n) * a.n_rays;
     if (scan_exclusive(counts, n, P, block_sums, nullptr, st, launches)) return 1;
     launch_pdl(tiles_kernel, dim3(std::max(1, std::min(148, (max_tiles + 255) / 256))), dim3(256), 0, st, P, a.n_rays, a.slots.n,

@@ -20,6 +20,12 @@ FAMILY = {
     "raygen_kernel": "sampler",
     "raygen_kernel<0>": "sampler",
     "raygen_kernel<1>": "sampler",
+    "raygen_kernel<0, 2>": "sampler",
+    "raygen_kernel<0, 8>": "sampler",
+    "raygen_kernel<1, 2>": "sampler",
+    "enc_half_kernel": "field_fwd",
+    "import_plan_kernel": "sampler",
+    "import_scatter_kernel": "sampler",
     "loss_reduce_kernel": "composite",
     "write_kernel": "sampler",
     "tiles_kernel": "sampler",
