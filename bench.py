@@ -372,7 +372,12 @@ def run_ours(args):
         if world > 1:
             dist.all_reduce(grads)
         ctx.optimizer_step(10_000 + i)
-        ctx.read_loss()
+        # every step's loss/status reaches the host: requested now, read after
+        # the next step is enqueued (pipelined, the stream never drains)
+        ctx.request_loss()
+        if i > 0:
+            ctx.poll_loss()
+    ctx.poll_loss()
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
     h1, d1 = ctx.copy_bytes()
@@ -384,7 +389,8 @@ def run_ours(args):
            "window_move_every": args.move_every, "window_moves": (e2e_steps - 1) // args.move_every,
            "what": "public API, host images/tile records: every move stages crops + tile state "
                    "(pinned H2D/D2H) and rebuilds the accepted list (new pixels Newton-solved, the "
-                   "previous position's pixels copied from its memo); loss/status read every step"}
+                   "previous position's pixels copied from its memo); every step's loss/status copied to the "
+                   "host and read (pipelined one step behind)"}
 
     # ---- render (config 4: 4x4-tile ROI, random-init weights, occupancy all on)
     render = None

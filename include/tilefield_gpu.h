@@ -208,6 +208,15 @@ TFG_API int tfg_grad_buffer(tfg_ctx* ctx, void** dptr, uint64_t* count);
  * divided by 3*B); copies to host and synchronises. */
 TFG_API int tfg_read_loss(tfg_ctx* ctx, float* loss_out);
 
+/* Pipelined form of tfg_read_loss: tfg_loss_request enqueues an asynchronous
+ * snapshot of the loss / status of the work enqueued so far (at most 4
+ * outstanding); tfg_loss_poll waits for the oldest one and reports it exactly
+ * as tfg_read_loss does (errors, the non-finite rollback).  A training loop
+ * requests after step i and polls after enqueueing step i+1, so the host never
+ * waits for the stream to drain. */
+TFG_API int tfg_loss_request(tfg_ctx* ctx);
+TFG_API int tfg_loss_poll(tfg_ctx* ctx, float* loss_out);
+
 /* ---- multi-GPU: ray-sharded data parallelism (SURVEY.md §8b tfg_comm_init,
  * §8e).  One context per GPU; every rank holds the same window and draws rays
  * [rank * B, (rank + 1) * B) of each iteration, with batch_rays = B * nranks

@@ -101,6 +101,13 @@ public:
         check(tfg_read_loss(c_, &l));
         return l;
     }
+    // pipelined: request after step i, poll after enqueueing step i+1
+    void request_loss() { check(tfg_loss_request(c_)); }
+    float poll_loss() {
+        float l = 0.f;
+        check(tfg_loss_poll(c_, &l));
+        return l;
+    }
 
     // reference-facing operator surface (RaySegmentBatch, forward_batch, render)
     uint64_t sample_segments(uint64_t iter, uint64_t ray_begin, int n_rays, bool jitter) {

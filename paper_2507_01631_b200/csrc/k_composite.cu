@@ -6,7 +6,8 @@
 //   w_k = T_k alpha_k,  C = sum w_k c_k + T_N bg,
 //   dC/dc_k = w_k,  dC/dsigma_k = delta_k (T_{k+1} c_k - R_k),
 //   R_k = sum_{j>k} w_j c_j + T_N bg = (C - T_N bg - P_k) + T_N bg,
-// with P_k the inclusive prefix of w c.  One warp per ray; samples are read
+// with P_k the inclusive prefix of w c; the backward only needs g . R_k, so
+// it scans the scalar w (g . c) once instead of three channels.  One warp per ray; samples are read
 // segment by segment from their slot buckets (coalesced runs), transmittance
 // is a warp product scan with a carried prefix.  Memory-bound.
 #include <cuda_runtime.h>
@@ -193,9 +194,11 @@ __global__ void __launch_bounds__(TFG_COMPOSITE_THREADS, TFG_COMPOSITE_MINB) com
     loss_arrive(&blk_sum, &blk_n, a.loss_parts, double(er * er + eg * eg + eb * eb), lane);
     float gr = 2.f * er * a.inv3b, gg = 2.f * eg * a.inv3b, gb = 2.f * eb * a.inv3b;
     // ---------------- backward
-    float T2 = 1.f, pr = 0.f, pg = 0.f, pb = 0.f;
-    float Rbr = T * a.bg.x, Rbg = T * a.bg.y, Rbb = T * a.bg.z;
-    // w and T_{k+1} of a chunk: recomputed exactly as the forward sweep did
+    // g . R_k = g . Cfg - P_k + T_N (g . bg), with P_k the inclusive prefix of
+    // the scalar w_j (g . c_j): one scan instead of one per channel
+    float T2 = 1.f, ps = 0.f;
+    const float gC = (gr * cr + gg * cg) + gb * cb;
+    const float gBg = T * ((gr * a.bg.x + gg * a.bg.y) + gb * a.bg.z);    // w and T_{k+1} of a chunk: recomputed exactly as the forward sweep did
     // (same operations, same order), or taken from the forward's cache
     auto chunk_weights = [&](const float4& io, const float2& td, float& w, float& Tk1) {
         float alpha = 1.f - expf(-(io.x * td.y));
@@ -214,19 +217,15 @@ __global__ void __launch_bounds__(TFG_COMPOSITE_THREADS, TFG_COMPOSITE_MINB) com
     };
     auto bwd_chunk = [&](int q, const float4& io, const float2& td, uint64_t pos, float w, float Tk1) {
         float sg = io.x, de = td.y;
-        // inclusive prefix of w*c
-        float sr = w * io.y, sgc = w * io.z, sbc = w * io.w;
+        const float gc = (gr * io.y + gg * io.z) + gb * io.w;  // g . c_k
+        float sc = w * gc;  // inclusive prefix of w (g . c)
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            float yr = __shfl_up_sync(FULL, sr, o);
-            float yg = __shfl_up_sync(FULL, sgc, o);
-            float yb = __shfl_up_sync(FULL, sbc, o);
-            if (lane >= o) { sr += yr; sgc += yg; sbc += yb; }
+            float y = __shfl_up_sync(FULL, sc, o);
+            if (lane >= o) sc += y;
         }
-        float Rr = (cr - (pr + sr)) + Rbr;
-        float Rg = (cg - (pg + sgc)) + Rbg;
-        float Rb = (cb - (pb + sbc)) + Rbb;
-        float ds = de * (gr * (Tk1 * io.y - Rr) + gg * (Tk1 * io.z - Rg) + gb * (Tk1 * io.w - Rb));
+        const float gR = (gC - (ps + sc)) + gBg;  // g . R_k
+        float ds = de * (Tk1 * gc - gR);
         if (q < m) {
             // pre-activation gradients for K4: d raw = dsigma * exp'(raw)
             // (= sigma, or 0 where the activation is clamped, nn.hpp:270-280),
@@ -237,9 +236,7 @@ __global__ void __launch_bounds__(TFG_COMPOSITE_THREADS, TFG_COMPOSITE_MINB) com
                                       db * io.w * (1.f - io.w));
             if (a.export_io) a.export_io[pos] = make_float4(ds, dr, dg, db);
         }
-        pr += __shfl_sync(FULL, sr, 31);
-        pg += __shfl_sync(FULL, sgc, 31);
-        pb += __shfl_sync(FULL, sbc, 31);
+        ps += __shfl_sync(FULL, sc, 31);
     };
 #pragma unroll
     for (int ci = 0; ci < kCache; ++ci)

@@ -447,9 +447,8 @@ int check_status(tfg_ctx* c) {
 // step-count increments of the failed optimizer step and of every later one
 // (skipped on the device as well) are rolled back, the group is named, and
 // the record is cleared on the device.
-void consume_sticky(tfg_ctx* c) {
-    const uint32_t* k = c->h_sticky;
-    if (k[0]) {
+void consume_sticky(tfg_ctx* c, const uint32_t* k, uint32_t upto_seq) {
+    if (k[0] && k[2] != c->sticky_done_seq) {
         const uint32_t g = k[1], seq = k[2];
         char nm[96];
         std::snprintf(nm, sizeof nm, "color");
@@ -467,10 +466,19 @@ void consume_sticky(tfg_ctx* c) {
             }
         }
         c->nonfinite_pending = std::string("adam_step: non-finite gradient in group ") + nm;
+        c->sticky_done_seq = seq;
         cudaMemsetAsync(c->d_sticky, 0, 16, c->st);
+        // every step from the failing one on was skipped (and is rolled back),
+        // the earlier ones were applied
+        c->unverified.clear();
+        return;
     }
-    c->unverified.clear();
+    // no new failure up to the snapshot: the steps it covers are final
+    auto& u = c->unverified;
+    u.erase(std::remove_if(u.begin(), u.end(), [&](const tfg_ctx::StepRec& r) { return int32_t(r.seq - upto_seq) <= 0; }),
+            u.end());
 }
+void consume_sticky(tfg_ctx* c) { consume_sticky(c, c->h_sticky, c->step_seq); }
 
 // Reads the sticky record (synchronises) and settles the unverified steps.
 int settle_steps(tfg_ctx* c) {
@@ -864,6 +872,10 @@ TFG_API int tfg_destroy(tfg_ctx* c) {
         if (im) cudaFreeHost(im);
     if (c->h_status) cudaFreeHost(c->h_status);
     if (c->h_sticky) cudaFreeHost(c->h_sticky);
+    if (c->h_ring) cudaFreeHost(c->h_ring);
+    if (c->h_ring_sticky) cudaFreeHost(c->h_ring_sticky);
+    for (cudaEvent_t e : c->ev_ring)
+        if (e) cudaEventDestroy(e);
     for (void* p : {static_cast<void*>(c->h_rpix), static_cast<void*>(c->h_rout), static_cast<void*>(c->h_rstat)})
         if (p) cudaFreeHost(p);
     for (cudaEvent_t e : c->ev_rdone)
@@ -1368,6 +1380,43 @@ TFG_API int tfg_read_loss(tfg_ctx* c, float* loss) {
     int rc = sync_status(c);  // rolls back the step counts of skipped (non-finite) steps, once
     if (loss) *loss = float(c->h_status->loss / (3.0 * double(c->tc.batch_rays)));
     return rc;
+}
+
+// Pipelined status reads: request = an asynchronous snapshot of the loss /
+// status of everything enqueued so far (pinned ring, one event each); poll =
+// wait for the oldest snapshot and report it exactly as tfg_read_loss would
+// (errors, non-finite rollback).  A training loop can request after step i
+// and poll after enqueueing step i+1, so the host never drains the stream.
+TFG_API int tfg_loss_request(tfg_ctx* c) {
+    if (!c) return fail(TFG_ERR_INVALID, "loss_request: null context");
+    if (c->ring_head - c->ring_tail >= uint32_t(tfg_ctx::kRing))
+        return fail(TFG_ERR_STATE, "loss_request: 4 requests outstanding; poll first");
+    CK(cudaSetDevice(c->device));
+    if (!c->h_ring) {
+        CK(cudaHostAlloc(reinterpret_cast<void**>(&c->h_ring), tfg_ctx::kRing * sizeof(Status), cudaHostAllocDefault));
+        CK(cudaHostAlloc(reinterpret_cast<void**>(&c->h_ring_sticky), tfg_ctx::kRing * 16, cudaHostAllocDefault));
+        for (auto& e : c->ev_ring) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    const uint32_t k = c->ring_head % tfg_ctx::kRing;
+    CK(cudaMemcpyAsync(c->h_ring + k, c->d_status, sizeof(Status), cudaMemcpyDeviceToHost, c->st));
+    CK(cudaMemcpyAsync(c->h_ring_sticky + 4 * k, c->d_sticky, 16, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaEventRecord(c->ev_ring[k], c->st));
+    c->ring_seq[k] = c->step_seq;
+    c->d2h_bytes += sizeof(Status) + 16;
+    ++c->ring_head;
+    return 0;
+}
+
+TFG_API int tfg_loss_poll(tfg_ctx* c, float* loss) {
+    if (!c) return fail(TFG_ERR_INVALID, "loss_poll: null context");
+    if (c->ring_head == c->ring_tail) return fail(TFG_ERR_STATE, "loss_poll: no outstanding loss_request");
+    const uint32_t k = c->ring_tail % tfg_ctx::kRing;
+    CK(cudaEventSynchronize(c->ev_ring[k]));
+    ++c->ring_tail;
+    *c->h_status = c->h_ring[k];
+    consume_sticky(c, c->h_ring_sticky + 4 * k, c->ring_seq[k]);
+    if (loss) *loss = float(c->h_status->loss / (3.0 * double(c->tc.batch_rays)));
+    return check_status(c);
 }
 
 TFG_API int tfg_train_step(tfg_ctx* c, uint64_t iter, uint64_t ray_begin, int n_rays,

@@ -129,6 +129,15 @@ struct tfg_ctx {
     uint32_t* d_sticky = nullptr;
     uint32_t* h_sticky = nullptr;  // pinned, 4 words
     std::string nonfinite_pending;  // message of a consumed record, raised by the next status check
+    uint32_t sticky_done_seq = 0;   // failing step of the last consumed record (later snapshots repeat it)
+    // pipelined status reads (tfg_loss_request / tfg_loss_poll): pinned
+    // snapshots of the status + sticky record, one event each
+    static constexpr int kRing = 4;
+    Status* h_ring = nullptr;
+    uint32_t* h_ring_sticky = nullptr;  // kRing x 4
+    cudaEvent_t ev_ring[kRing] = {};
+    uint32_t ring_seq[kRing] = {};
+    uint32_t ring_head = 0, ring_tail = 0;
 
     // scene
     int n_views = 0;

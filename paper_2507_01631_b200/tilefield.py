@@ -73,6 +73,8 @@ def lib() -> C.CDLL:
         "tfg_train_step": [_vp, C.c_uint64, C.c_uint64, C.c_int, _vp],
         "tfg_grad_buffer": [_vp, _vp, _vp],
         "tfg_read_loss": [_vp, _vp],
+        "tfg_loss_request": [_vp],
+        "tfg_loss_poll": [_vp, _vp],
         "tfg_sample": [_vp, C.c_uint64, C.c_uint64, C.c_int, C.c_int, _vp],
         "tfg_sample_pixels": [_vp, _vp, C.c_int, _vp],
         "tfg_batch_export": [_vp, _vp],
@@ -377,6 +379,16 @@ class Context:
     def read_loss(self) -> float:
         l = C.c_float()
         _check(lib().tfg_read_loss(self.h, C.byref(l)))
+        return l.value
+
+    def request_loss(self) -> None:
+        """Asynchronous snapshot of the loss / status so far (poll_loss reads it)."""
+        _check(lib().tfg_loss_request(self.h))
+
+    def poll_loss(self) -> float:
+        """The oldest requested loss (waits for it); raises like read_loss."""
+        l = C.c_float()
+        _check(lib().tfg_loss_poll(self.h, C.byref(l)))
         return l.value
 
     def train_step(self, it: int, ray_begin: int = 0, n_rays: int | None = None) -> float:

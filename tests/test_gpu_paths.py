@@ -365,3 +365,51 @@ def test_config2_all_positions_bit_exact():
         _cmp_batch(ctx.batch(), ses.batch())
         lg, lr = ctx.train_step(it, 0, c2["batch"]), ses.train_step(it, 0, c2["batch"])
         assert abs(lg - lr) <= 1e-2 * lr, (pos, lg, lr)
+
+
+def test_pipelined_loss_reads():
+    """tfg_loss_request / tfg_loss_poll: the loss of step i read after step i+1
+    is enqueued equals the synchronous read; a non-finite step is reported
+    once, with the step counts of it and of the later (skipped) steps rolled
+    back exactly once."""
+    _need_gpu()
+    from paper_2507_01631_b200.tilefield import Context, NonFiniteGradient
+
+    scene = synth.make_scene(2, 2, n_views=2, gsd=2.0, seed=6)
+    tc = TrainConfig.defaults(batch_rays=1024, seed=3)
+    a = Context(scene, FieldConfig.defaults(), tc, max_rays=1024)
+    b = Context(scene, FieldConfig.defaults(), tc, max_rays=1024)
+    a.set_window(0, 0)
+    b.set_window(0, 0)
+    sync = [a.train_step(it, 0, 1024) for it in range(6)]
+    piped = []
+    for it in range(6):
+        b.forward_backward(it, 0, 1024)
+        b.optimizer_step(it)
+        b.request_loss()
+        if it > 0:
+            piped.append(b.poll_loss())
+    piped.append(b.poll_loss())
+    np.testing.assert_allclose(piped, sync, rtol=2e-3)
+    before = b.tile_state(0)
+    st = b.tile_state(2)
+    st["dnet"][:] = np.nan
+    b.set_tile_state(2, st)
+    raised = 0
+    for it in range(6, 9):
+        b.forward_backward(it, 0, 1024)
+        b.optimizer_step(it)
+        b.request_loss()
+        if it > 6:
+            try:
+                b.poll_loss()
+            except NonFiniteGradient:
+                raised += 1
+    try:
+        b.poll_loss()
+    except NonFiniteGradient:
+        raised += 1
+    assert raised == 1
+    after = b.tile_state(0)
+    assert after["enc_step"] == before["enc_step"]
+    np.testing.assert_array_equal(after["enc"], before["enc"])
