@@ -73,8 +73,12 @@ typedef struct tfg_roi {
     double z_min, z_max;
 } tfg_roi;
 
-/* FieldConfig, core/nn.hpp:14-37 (the GPU kernels are specialised for the
- * defaults; tfg_create rejects any other shape). */
+/* FieldConfig, core/nn.hpp:14-37.  The hash-grid geometry is free (n_min,
+ * n_max, table_size: a power of two in [2^4, 2^22]); the widths are the
+ * tensor-core kernels' tile shapes, and tfg_create rejects any value other
+ * than the default for levels (8), features (2), density_hidden (64),
+ * embedding (15), color_hidden (64), color_layers (2), view_freqs (4) and
+ * occupancy_resolution (32). */
 typedef struct tfg_field_config {
     int32_t levels, table_size, features, n_min, n_max;
     int32_t density_hidden, embedding, color_hidden, color_layers, view_freqs;

@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(256) adam_kernel(AdamArgs a, uint64_t total) {
         v4[i] = v;
         p4[i] = p;
         if (G.half_slot >= 0) {  // the slot's fp16 table shadow (forward gather)
-            __half2* h = reinterpret_cast<__half2*>(a.enc16) + (uint64_t(G.half_slot) * a.enc_n + (4 * i - G.offset)) / 2;
+            __half2* h = reinterpret_cast<__half2*>(a.enc16) + (uint64_t(G.half_slot) * a.enc16_stride + (4 * i - G.offset)) / 2;
             uint2 q;
             __half2 lo = __floats2half2_rn(p.x, p.y), hi = __floats2half2_rn(p.z, p.w);
             q.x = *reinterpret_cast<uint32_t*>(&lo);
@@ -110,23 +110,25 @@ __global__ void __launch_bounds__(256) adam_kernel(AdamArgs a, uint64_t total) {
         a.v[i] = v;
         a.params[i] = p;
         if (G.half_slot >= 0)
-            reinterpret_cast<__half*>(a.enc16)[uint64_t(G.half_slot) * a.enc_n + (i - G.offset)] = __float2half_rn(p);
+            reinterpret_cast<__half*>(a.enc16)[uint64_t(G.half_slot) * a.enc16_stride + (i - G.offset)] = __float2half_rn(p);
     }
 }
 
 __global__ void __launch_bounds__(256) enc_half_kernel(const float* __restrict__ params, uint64_t stride,
-                                                       uint64_t enc_n, __half2* __restrict__ out) {
+                                                       uint64_t enc_n, uint64_t out_stride,
+                                                       __half2* __restrict__ out) {
     pdl_wait();
     const int k = blockIdx.y;
     const float2* src = reinterpret_cast<const float2*>(params + uint64_t(k) * stride);
-    __half2* dst = out + uint64_t(k) * enc_n / 2;
+    __half2* dst = out + uint64_t(k) * out_stride / 2;
     for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < enc_n / 2; i += uint64_t(gridDim.x) * blockDim.x)
         dst[i] = __float22half2_rn(src[i]);
 }
 
-void launch_enc_half(const float* params, uint64_t stride, int n, uint64_t enc_n, void* out, cudaStream_t st,
-                     uint64_t* launches) {
-    launch_pdl(enc_half_kernel, dim3(148, n), dim3(256), 0, st, params, stride, enc_n, static_cast<__half2*>(out));
+void launch_enc_half(const float* params, uint64_t stride, int n, uint64_t enc_n, uint64_t out_stride, void* out,
+                     cudaStream_t st, uint64_t* launches) {
+    launch_pdl(enc_half_kernel, dim3(148, n), dim3(256), 0, st, params, stride, enc_n, out_stride,
+               static_cast<__half2*>(out));
     *launches += 1;
 }
 

@@ -33,7 +33,10 @@ __global__ void __launch_bounds__(256) occupancy_kernel(OccArgs a) {
         float py = (float(y) + uy) / float(kOccRes);
         float pz = (float(z) + uz) / float(kOccRes);
         float feat[kFeatDim];
-        hash_encode(a.hl, a.enc[slot], px, py, pz, feat);
+        if (a.hl.generic)
+            hash_encode<true>(a.hl, a.enc[slot], px, py, pz, feat);
+        else
+            hash_encode<false>(a.hl, a.enc[slot], px, py, pz, feat);
         float h[kDHidden];
 #pragma unroll
         for (int o = 0; o < kDHidden; ++o) {

@@ -190,6 +190,7 @@ __device__ __forceinline__ float sigm(float x) { return 1.f / (1.f + __expf(-x))
 // ------------------------------------------------------------------ K2a
 // Thread per tile row: 8-level hash gather -> 16 bf16 features in the tile's
 // chunk-major layout (the A operand of the first density layer) + ray id.
+template <bool G>
 __global__ void __launch_bounds__(128) hash_fwd_kernel(FieldArgs a, uint8_t* __restrict__ feat,
                                                        int32_t* __restrict__ rays) {
     pdl_wait();
@@ -202,7 +203,7 @@ __global__ void __launch_bounds__(128) hash_fwd_kernel(FieldArgs a, uint8_t* __r
         if (r < td.n) {
             float4 L = a.s.local[uint64_t(td.start) + r];
             ray = __float_as_int(L.w);
-            hash_encode16(a.hl, a.f.enc16[td.slot], L.x, L.y, L.z, f);
+            hash_encode16<G>(a.hl, a.f.enc16[td.slot], L.x, L.y, L.z, f);
         } else {
 #pragma unroll
             for (int i = 0; i < kFeatDim; ++i) f[i] = 0.f;
@@ -358,6 +359,19 @@ __device__ __forceinline__ void scatter_row_bfly(float* genc, float x, float y, 
     scatter_level_bfly<7>(genc, x, y, z, d[14], d[15], live);
 }
 static_assert(kLevels == 8, "scatter_row_bfly unrolls the 8 levels of the default FieldConfig");
+
+// A runtime level layout (non-default n_min / n_max / table_size): the
+// pair-vectorised scatter of every level, no butterfly (whose merge rounds
+// are chosen per default level).
+__device__ __forceinline__ void scatter_row_rt(const HashLayout& hl, float* genc, float x, float y, float z,
+                                               const float* d, bool live) {
+#pragma unroll
+    for (int l = 0; l < kLevels; ++l) {
+        Corner c;
+        hash_level_rt(hl, l, x, y, z, c);
+        if (live) scatter_pairs(genc, c, d[2 * l], d[2 * l + 1]);
+    }
+}
 
 // ------------------------------------------------------------------ K2b
 // smem: weights | X0 [128x16] (the gathered features, bulk-copied; the only
@@ -646,6 +660,7 @@ __device__ __forceinline__ void flush_color(uint32_t tmem, float* __restrict__ g
         for (int o = 0; o < 3; ++o) atomicAdd(gc + kCB3 + o, v[o]);
 }
 
+template <bool G>
 __global__ void __launch_bounds__(kBwdThreads, 2) mlp_bwd_kernel(FieldArgs a, FieldGradArgs g,
                                                       const uint8_t* __restrict__ feat,
                                                       const int32_t* __restrict__ rays) {
@@ -704,7 +719,10 @@ __global__ void __launch_bounds__(kBwdThreads, 2) mlp_bwd_kernel(FieldArgs a, Fi
             umma::fence_before_sync();
             __syncwarp();
             if ((row & 31) == 0) umma::mbar_arrive(&bar_free);  // TMEM columns free again
-            scatter_row_bfly(g.g_enc[td.slot], L.x, L.y, L.z, v, live);
+            if constexpr (G)
+                scatter_row_rt(a.hl, g.g_enc[td.slot], L.x, L.y, L.z, v, live);
+            else
+                scatter_row_bfly(g.g_enc[td.slot], L.x, L.y, L.z, v, live);
         }
         __syncthreads();  // pairs with the MLP warps' final barrier before tmem_free
         return;
@@ -1008,7 +1026,10 @@ void launch_field_forward_tc(const FieldArgs& a, uint8_t* feat, int32_t* rays, i
 #ifndef TFG_MLPF_CTAS
 #define TFG_MLPF_CTAS 4
 #endif
-    launch_pdl(hash_fwd_kernel, dim3(sms * TFG_GATHER_CTAS), dim3(128), 0, st, a, feat, rays);
+    if (a.hl.generic)
+        launch_pdl(hash_fwd_kernel<true>, dim3(sms * TFG_GATHER_CTAS), dim3(128), 0, st, a, feat, rays);
+    else
+        launch_pdl(hash_fwd_kernel<false>, dim3(sms * TFG_GATHER_CTAS), dim3(128), 0, st, a, feat, rays);
     launch_pdl(mlp_fwd_kernel, dim3(sms * TFG_MLPF_CTAS), dim3(128), kFwdSmem, st, a, feat, rays);  // 4 per SM
     *launches += 2;
 }
@@ -1017,12 +1038,16 @@ void launch_field_backward_tc(const FieldArgs& a, const FieldGradArgs& g, uint8_
                               int32_t* rays, int sms, cudaStream_t st, uint64_t* launches) {
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(mlp_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kBwdSmem));
+        cudaFuncSetAttribute(mlp_bwd_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kBwdSmem));
+        cudaFuncSetAttribute(mlp_bwd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kBwdSmem));
         attr = true;
     }
     // the feature tiles of the forward pass (same batch) are still resident;
     // the hash-table scatter is fused into the backward's last epilogue
-    launch_pdl(mlp_bwd_kernel, dim3(sms * 2), dim3(kBwdThreads), kBwdSmem, st, a, g, feat, rays);
+    if (a.hl.generic)
+        launch_pdl(mlp_bwd_kernel<true>, dim3(sms * 2), dim3(kBwdThreads), kBwdSmem, st, a, g, feat, rays);
+    else
+        launch_pdl(mlp_bwd_kernel<false>, dim3(sms * 2), dim3(kBwdThreads), kBwdSmem, st, a, g, feat, rays);
     *launches += 1;
 }
 

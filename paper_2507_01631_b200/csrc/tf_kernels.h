@@ -23,6 +23,11 @@ struct HashLayout {
     int res[kLevels];
     uint32_t off[kLevels];  // entry offset of the level
     int dense[kLevels];     // 1 when (res+1)^3 <= T (direct indexing)
+    uint32_t mask;          // T - 1
+    // 0: the default FieldConfig's layout, which the kernels fold in as
+    // constants (tf_hash.cuh); 1: another n_min / n_max / table_size, read
+    // from this struct at run time
+    int generic;
 };
 
 struct AcceptArgs {
@@ -149,8 +154,8 @@ struct AdamArgs {
     // like the reference's throw) until the host reads it
     uint32_t* sticky;
     uint32_t seq;           // host sequence number of this optimizer step
-    void* enc16;            // fp16 table shadows (slot k at k * enc_n entries of __half2)
-    uint64_t enc_n;         // floats per slot's tables
+    void* enc16;            // fp16 table shadows (slot k at k * enc16_stride halves)
+    uint64_t enc16_stride;
 };
 
 struct OccArgs {
@@ -184,8 +189,10 @@ void launch_field_backward_tc(const FieldArgs& a, const FieldGradArgs& g, uint8_
                               int32_t* rays, int sms, cudaStream_t st, uint64_t* launches);
 void launch_composite(const CompositeArgs& a, cudaStream_t st, uint64_t* launches);
 void launch_adam(const AdamArgs& a, uint64_t total, cudaStream_t st, uint64_t* launches);
-// fp32 hash tables of n slots (params + k * stride) -> their fp16 shadows (out + k * enc_n halves)
-void launch_enc_half(const float* params, uint64_t stride, int n, uint64_t enc_n, void* out, cudaStream_t st,
+// fp32 hash tables of n slots (params + k * stride, enc_n floats) -> their fp16
+// shadows (out + k * out_stride halves)
+void launch_enc_half(const float* params, uint64_t stride, int n, uint64_t enc_n, uint64_t out_stride, void* out,
+                     cudaStream_t st,
                      uint64_t* launches);
 void launch_occupancy(const OccArgs& a, cudaStream_t st, uint64_t* launches);
 

@@ -162,7 +162,9 @@ void fresh_tile(tfg_ctx* c, int ti) {
     Rng rd(hash_combine(hash_combine(hash_combine(c->tc.seed, kPurposeTileDnet), uint64_t(row)),
                         uint64_t(col)));
     const int dw[3] = {kFeatDim, kDHidden, kDOut};
-    mlp_init_host(dw, 3, rd, p + c->enc_n);
+    std::fill(p + c->enc_n, p + c->dn_off, 0.f);  // alignment padding (none by default)
+    mlp_init_host(dw, 3, rd, p + c->dn_off);
+    std::fill(p + c->dn_off + c->dn_n, p + c->stride, 0.f);
     std::memset(p + c->stride, 0, 2 * c->stride * sizeof(float));
     float* ema = p + 3 * c->stride;
     for (int i = 0; i < kOccVox; ++i) ema[i] = 1.0f;
@@ -276,8 +278,8 @@ FieldPtrs train_ptrs(tfg_ctx* c) {
     FieldPtrs f{};
     for (int k = 0; k < c->nslots; ++k) {
         f.enc[k] = c->d_params + uint64_t(k) * c->stride;
-        f.enc16[k] = static_cast<uint16_t*>(c->d_enc16) + uint64_t(k) * c->enc_n;
-        f.dnet[k] = f.enc[k] + c->enc_n;
+        f.enc16[k] = static_cast<uint16_t*>(c->d_enc16) + uint64_t(k) * c->enc16_stride;
+        f.dnet[k] = f.enc[k] + c->dn_off;
         f.occ_bits[k] = c->d_bits + uint64_t(k) * kOccWords;
     }
     f.color = c->d_params + c->color_off;
@@ -292,7 +294,7 @@ int run_occupancy(tfg_ctx* c, bool update, uint64_t* keys) {
     o.n = c->nslots;
     for (int k = 0; k < c->nslots; ++k) {
         o.enc[k] = c->d_params + uint64_t(k) * c->stride;
-        o.dnet[k] = o.enc[k] + c->enc_n;
+        o.dnet[k] = o.enc[k] + c->dn_off;
         o.ema[k] = c->d_ema + uint64_t(k) * kOccVox;
         o.bits[k] = c->d_bits + uint64_t(k) * kOccWords;
         o.base_key[k] = keys ? keys[k] : 0;
@@ -546,7 +548,8 @@ FieldArgs field_args(tfg_ctx* c, const FieldPtrs& f) {
 int run_forward(tfg_ctx* c, const FieldPtrs& f) {
     PhaseScope ps(c, kPhFieldFwd);
     if (!c->render_mode && c->enc16_dirty && c->nslots > 0) {  // slot tables written outside Adam
-        launch_enc_half(c->d_params, c->stride, c->nslots, c->enc_n, c->d_enc16, c->st, &c->launches);
+        launch_enc_half(c->d_params, c->stride, c->nslots, c->enc_n, c->enc16_stride, c->d_enc16, c->st,
+                        &c->launches);
         c->enc16_dirty = false;
     }
     c->fwd_done = true;
@@ -589,7 +592,7 @@ int run_backward(tfg_ctx* c) {
     FieldGradArgs g{};
     for (int k = 0; k < c->nslots; ++k) {
         g.g_enc[k] = c->d_grads + uint64_t(k) * c->stride;
-        g.g_dnet[k] = g.g_enc[k] + c->enc_n;
+        g.g_dnet[k] = g.g_enc[k] + c->dn_off;
     }
     g.g_color = c->d_grads + c->color_off;
     launch_field_backward_tc(field_args(c, train_ptrs(c)), g, c->d_feat, c->d_tile_rays,
@@ -727,13 +730,22 @@ TFG_API int tfg_create(const tfg_field_config* fcfg, const tfg_train_config* tcf
     if (!fcfg || !tcfg || !out || max_rays <= 0) return fail(TFG_ERR_INVALID, "create: bad arguments");
     tfg_field_config d;
     tfg_default_field_config(&d);
-    if (fcfg->levels != d.levels || fcfg->table_size != d.table_size ||
-        fcfg->features != d.features || fcfg->density_hidden != d.density_hidden ||
+    // The hash-grid geometry (n_min, n_max, table_size) is free; the feature
+    // and MLP widths are the UMMA tile shapes and TMEM column maps of the
+    // tensor-core kernels, and the occupancy grid is 32^3 bit words.
+    if (fcfg->levels != d.levels || fcfg->features != d.features || fcfg->density_hidden != d.density_hidden ||
         fcfg->embedding != d.embedding || fcfg->color_hidden != d.color_hidden ||
         fcfg->color_layers != d.color_layers || fcfg->view_freqs != d.view_freqs ||
         fcfg->occupancy_resolution != d.occupancy_resolution)
         return fail(TFG_ERR_INVALID, "create: the sm_100a kernels are specialised for the default "
-                                     "FieldConfig shapes (nn.hpp:14-37)");
+                                     "FieldConfig widths (levels 8, features 2, MLPs 16-64-16 / "
+                                     "39-64-64-3, view_freqs 4, occupancy 32^3; nn.hpp:14-37); "
+                                     "n_min, n_max and table_size are free");
+    if (fcfg->table_size < 16 || fcfg->table_size > (1 << 22) ||
+        (fcfg->table_size & (fcfg->table_size - 1)) != 0)
+        return fail(TFG_ERR_INVALID, "create: table_size must be a power of two in [2^4, 2^22]");
+    if (fcfg->n_min < 1 || fcfg->n_max < fcfg->n_min || fcfg->n_max > (1 << 16))
+        return fail(TFG_ERR_INVALID, "create: need 1 <= n_min <= n_max <= 65536");
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0 || device >= ndev)
         return fail(TFG_ERR_NO_DEVICE, "create: no CUDA device (there is no CPU fallback)");
@@ -751,28 +763,33 @@ TFG_API int tfg_create(const tfg_field_config* fcfg, const tfg_train_config* tcf
     uint64_t enc, dn, col;
     tfg_param_counts(fcfg, &enc, &dn, &col);
     c->enc_n = enc;
-    c->stride = enc + dn;
+    c->dn_n = dn;
+    c->dn_off = (enc + 3) & ~uint64_t(3);
+    c->stride = (c->dn_off + dn + 3) & ~uint64_t(3);
+    c->enc16_stride = c->dn_off;
     c->color_off = kTrainSlots * c->stride;
     c->n_params = c->color_off + col;
     uint32_t off = 0;
+    const uint64_t T = uint64_t(fcfg->table_size);
     for (int l = 0; l < kLevels; ++l) {
         int r = level_resolution(*fcfg, l);
         uint64_t dense = uint64_t(r + 1) * (r + 1) * (r + 1);
         c->hl.res[l] = r;
         c->hl.off[l] = off;
-        c->hl.dense[l] = dense <= uint64_t(kTable) ? 1 : 0;
-        off += uint32_t(std::min<uint64_t>(dense, kTable));
+        c->hl.dense[l] = dense <= T ? 1 : 0;
+        off += uint32_t(std::min<uint64_t>(dense, T));
     }
+    c->hl.mask = uint32_t(T - 1);
     {
-        // the hash kernels fold the default level layout in as constants
+        // the default layout is folded into the hash kernels as constants;
+        // any other runs their runtime-layout instantiations
+        // (TFG_GENERIC_HASH=1 forces those for the default one: a test hook)
         const int res[kLevels] = {16, 24, 35, 53, 78, 116, 172, 256};
-        const uint32_t off[kLevels] = {0, 4913, 20538, 53306, 86074, 118842, 151610, 184378};
-        for (int l = 0; l < kLevels; ++l)
-            if (c->hl.res[l] != res[l] || c->hl.off[l] != off[l]) {
-                delete c;
-                return fail(TFG_ERR_INVALID, "create: hash-grid level layout differs from the "
-                                             "default FieldConfig the kernels are built for");
-            }
+        const uint32_t off0[kLevels] = {0, 4913, 20538, 53306, 86074, 118842, 151610, 184378};
+        bool same = T == uint64_t(kTable);
+        for (int l = 0; l < kLevels; ++l) same = same && c->hl.res[l] == res[l] && c->hl.off[l] == off0[l];
+        const char* force = std::getenv("TFG_GENERIC_HASH");
+        c->hl.generic = (!same || (force && force[0] == '1')) ? 1 : 0;
     }
     c->density_lim = std::log(fcfg->density_max);
     c->sample_cap = uint64_t(max_rays) * 128;
@@ -798,7 +815,7 @@ TFG_API int tfg_create(const tfg_field_config* fcfg, const tfg_train_config* tcf
         rc |= dalloc(c, &c->d_v, c->n_params);
         rc |= dalloc(c, &c->d_ema, uint64_t(kTrainSlots) * kOccVox);
         rc |= dalloc(c, &c->d_bits, uint64_t(kMaxSlots) * kOccWords);
-        rc |= dalloc(c, reinterpret_cast<uint16_t**>(&c->d_enc16), uint64_t(kTrainSlots + kMaxSlots) * c->enc_n);
+        rc |= dalloc(c, reinterpret_cast<uint16_t**>(&c->d_enc16), uint64_t(kTrainSlots + kMaxSlots) * c->enc16_stride);
         rc |= dalloc(c, &c->d_group_flags, 16);
         rc |= dalloc(c, &c->d_sticky, 4);
         rc |= dalloc(c, &c->d_status, 1);
@@ -1319,7 +1336,7 @@ TFG_API int tfg_optimizer_step(tfg_ctx* c, uint64_t iter) {
         c->unverified.push_back(r);
     }
     a.enc16 = c->d_enc16;
-    a.enc_n = c->enc_n;
+    a.enc16_stride = c->enc16_stride;
     auto group = [&](AdamGroup& G, uint64_t off, uint64_t cnt, double base, uint64_t& step, int half_slot) {
         uint64_t s = ++step;
         G.offset = off;
@@ -1333,7 +1350,7 @@ TFG_API int tfg_optimizer_step(tfg_ctx* c, uint64_t iter) {
     for (int k = 0; k < c->nslots; ++k) {
         TileHost& th = c->tiles[c->slot_tile[k]];
         group(a.g[ng++], uint64_t(k) * c->stride, c->enc_n, t.lr_field, th.enc_step, k);
-        group(a.g[ng++], uint64_t(k) * c->stride + c->enc_n, c->stride - c->enc_n, t.lr_field, th.dnet_step, -1);
+        group(a.g[ng++], uint64_t(k) * c->stride + c->dn_off, c->dn_n, t.lr_field, th.dnet_step, -1);
     }
     group(a.g[ng++], c->color_off, c->n_params - c->color_off, t.lr_color, c->color_step, -1);
     a.n_groups = ng;
@@ -1555,7 +1572,7 @@ TFG_API int tfg_set_slot_params(tfg_ctx* c, int slot, const float* enc, const fl
     CK(cudaStreamSynchronize(c->st));
     const uint64_t off = uint64_t(slot) * c->stride;
     if (enc) CK(cudaMemcpy(c->d_params + off, enc, c->enc_n * 4, cudaMemcpyHostToDevice));
-    if (dnet) CK(cudaMemcpy(c->d_params + off + c->enc_n, dnet, (c->stride - c->enc_n) * 4, cudaMemcpyHostToDevice));
+    if (dnet) CK(cudaMemcpy(c->d_params + off + c->dn_off, dnet, (c->dn_n) * 4, cudaMemcpyHostToDevice));
     c->fwd_done = false;
     c->enc16_dirty = true;
     return 0;
@@ -1766,7 +1783,7 @@ TFG_API int tfg_get_grads(tfg_ctx* c, int slot, float* enc, float* dnet, float* 
     uint64_t off = uint64_t(slot) * c->stride;
     if (enc) CK(cudaMemcpy(enc, c->d_grads + off, c->enc_n * 4, cudaMemcpyDeviceToHost));
     if (dnet)
-        CK(cudaMemcpy(dnet, c->d_grads + off + c->enc_n, (c->stride - c->enc_n) * 4,
+        CK(cudaMemcpy(dnet, c->d_grads + off + c->dn_off, (c->dn_n) * 4,
                       cudaMemcpyDeviceToHost));
     if (color)
         CK(cudaMemcpy(color, c->d_grads + c->color_off, (c->n_params - c->color_off) * 4,
@@ -1779,14 +1796,14 @@ TFG_API int tfg_get_tile_state(tfg_ctx* c, int slot, tfg_tile_state* o) {
     if (settle_steps(c)) return TFG_ERR_CUDA;  // step counts of skipped steps rolled back
     CK(cudaStreamSynchronize(c->side));
     uint64_t off = uint64_t(slot) * c->stride;
-    uint64_t dn = c->stride - c->enc_n;
+    uint64_t dn = c->dn_n;
     auto cp = [&](float* dst, const float* src, uint64_t n) -> int {
         if (dst) CK(cudaMemcpy(dst, src, n * 4, cudaMemcpyDeviceToHost));
         return 0;
     };
-    int rc = cp(o->enc, c->d_params + off, c->enc_n) | cp(o->dnet, c->d_params + off + c->enc_n, dn) |
+    int rc = cp(o->enc, c->d_params + off, c->enc_n) | cp(o->dnet, c->d_params + off + c->dn_off, dn) |
              cp(o->enc_m, c->d_m + off, c->enc_n) | cp(o->enc_v, c->d_v + off, c->enc_n) |
-             cp(o->dnet_m, c->d_m + off + c->enc_n, dn) | cp(o->dnet_v, c->d_v + off + c->enc_n, dn) |
+             cp(o->dnet_m, c->d_m + off + c->dn_off, dn) | cp(o->dnet_v, c->d_v + off + c->dn_off, dn) |
              cp(o->occupancy, c->d_ema + uint64_t(slot) * kOccVox, kOccVox);
     const TileHost& th = c->tiles[c->slot_tile[slot]];
     o->enc_step = th.enc_step;
@@ -1798,14 +1815,14 @@ TFG_API int tfg_set_tile_state(tfg_ctx* c, int slot, const tfg_tile_state* in) {
     if (!c || slot < 0 || slot >= c->nslots) return fail(TFG_ERR_INVALID, "set_tile_state: bad slot");
     CK(cudaStreamSynchronize(c->st));
     uint64_t off = uint64_t(slot) * c->stride;
-    uint64_t dn = c->stride - c->enc_n;
+    uint64_t dn = c->dn_n;
     auto cp = [&](float* dst, const float* src, uint64_t n) -> int {
         if (src) CK(cudaMemcpy(dst, src, n * 4, cudaMemcpyHostToDevice));
         return 0;
     };
-    int rc = cp(c->d_params + off, in->enc, c->enc_n) | cp(c->d_params + off + c->enc_n, in->dnet, dn) |
+    int rc = cp(c->d_params + off, in->enc, c->enc_n) | cp(c->d_params + off + c->dn_off, in->dnet, dn) |
              cp(c->d_m + off, in->enc_m, c->enc_n) | cp(c->d_v + off, in->enc_v, c->enc_n) |
-             cp(c->d_m + off + c->enc_n, in->dnet_m, dn) | cp(c->d_v + off + c->enc_n, in->dnet_v, dn) |
+             cp(c->d_m + off + c->dn_off, in->dnet_m, dn) | cp(c->d_v + off + c->dn_off, in->dnet_v, dn) |
              cp(c->d_ema + uint64_t(slot) * kOccVox, in->occupancy, kOccVox);
     TileHost& th = c->tiles[c->slot_tile[slot]];
     th.enc_step = in->enc_step;
@@ -1894,7 +1911,7 @@ TFG_API int tfg_render_setup(tfg_ctx* c, const int32_t* rows, const int32_t* col
         }
         float* dst = c->d_rparams + uint64_t(k) * c->stride;
         CK(cudaMemcpy(dst, states[k].enc, c->enc_n * 4, cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(dst + c->enc_n, states[k].dnet, (c->stride - c->enc_n) * 4, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(dst + c->dn_off, states[k].dnet, (c->dn_n) * 4, cudaMemcpyHostToDevice));
         for (int w = 0; w < kOccWords; ++w) {
             uint32_t word = 0;
             for (int q = 0; q < 32; ++q) {
@@ -1908,8 +1925,8 @@ TFG_API int tfg_render_setup(tfg_ctx* c, const int32_t* rows, const int32_t* col
     }
     CK(cudaMemcpy(c->d_rcolor, color_params, (c->n_params - c->color_off) * 4, cudaMemcpyHostToDevice));
     // the render tiles' fp16 table shadows (after the training slots')
-    launch_enc_half(c->d_rparams, c->stride, n, c->enc_n,
-                    static_cast<uint16_t*>(c->d_enc16) + uint64_t(kTrainSlots) * c->enc_n, c->st, &c->launches);
+    launch_enc_half(c->d_rparams, c->stride, n, c->enc_n, c->enc16_stride,
+                    static_cast<uint16_t*>(c->d_enc16) + uint64_t(kTrainSlots) * c->enc16_stride, c->st, &c->launches);
     CK(cudaStreamSynchronize(c->st));
     return 0;
 }
@@ -1924,8 +1941,8 @@ TFG_API int tfg_render_pixels(tfg_ctx* c, const tfg_rpc* cam, const int32_t* pix
     FieldPtrs f{};
     for (int k = 0; k < c->rn; ++k) {
         f.enc[k] = c->d_rparams + uint64_t(k) * c->stride;
-        f.enc16[k] = static_cast<uint16_t*>(c->d_enc16) + uint64_t(kTrainSlots + k) * c->enc_n;
-        f.dnet[k] = f.enc[k] + c->enc_n;
+        f.enc16[k] = static_cast<uint16_t*>(c->d_enc16) + uint64_t(kTrainSlots + k) * c->enc16_stride;
+        f.dnet[k] = f.enc[k] + c->dn_off;
         f.occ_bits[k] = c->d_rbits + uint64_t(k) * kOccWords;
     }
     f.color = c->d_rcolor;

@@ -96,7 +96,13 @@ struct tfg_ctx {
     tfg_field_config fc{};
     tfg_train_config tc{};
     HashLayout hl{};
-    uint64_t enc_n = 0, stride = 0, n_params = 0, color_off = 0;
+    // floats per slot: hash tables (enc_n), density MLP (dn_n).  A slot's
+    // record is [tables | pad | density MLP | pad]: the MLP at dn_off =
+    // enc_n rounded up to 16 B, the next slot at stride = dn_off + dn_n
+    // rounded up to 16 B (vector loads, reds and Adam's float4 groups need
+    // aligned bases; the default FieldConfig needs no padding).
+    // enc16_stride: halves per slot of the fp16 shadows (8 B aligned).
+    uint64_t enc_n = 0, dn_n = 0, dn_off = 0, stride = 0, enc16_stride = 0, n_params = 0, color_off = 0;
     float density_lim = 0.f;
     int max_rays = 0;
     uint64_t sample_cap = 0;

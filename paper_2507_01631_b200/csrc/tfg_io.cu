@@ -169,11 +169,11 @@ TFG_API int tfg_save_run(tfg_ctx* c, const char* dir) {
         float* p = t.rec;
         tfg_tile_state st{};
         st.enc = p;
-        st.dnet = p + c->enc_n;
+        st.dnet = p + c->dn_off;
         st.enc_m = p + c->stride;
-        st.dnet_m = p + c->stride + c->enc_n;
+        st.dnet_m = p + c->stride + c->dn_off;
         st.enc_v = p + 2 * c->stride;
-        st.dnet_v = p + 2 * c->stride + c->enc_n;
+        st.dnet_v = p + 2 * c->stride + c->dn_off;
         st.occupancy = p + 3 * c->stride;
         st.enc_step = t.enc_step;
         st.dnet_step = t.dnet_step;
@@ -209,11 +209,11 @@ TFG_API int tfg_load_run(tfg_ctx* c, const char* dir) {
         float* p = t.rec;
         tfg_tile_state st{};
         st.enc = p;
-        st.dnet = p + c->enc_n;
+        st.dnet = p + c->dn_off;
         st.enc_m = p + c->stride;
-        st.dnet_m = p + c->stride + c->enc_n;
+        st.dnet_m = p + c->stride + c->dn_off;
         st.enc_v = p + 2 * c->stride;
-        st.dnet_v = p + 2 * c->stride + c->enc_n;
+        st.dnet_v = p + 2 * c->stride + c->dn_off;
         st.occupancy = p + 3 * c->stride;
         int row, col;
         int rc = tfg_load_tile_checkpoint(path.c_str(), &c->fc, &row, &col, &st);

@@ -47,6 +47,29 @@ def test_no_cpu_fallback(lib):
     assert b"no CPU fallback" in lib.tfg_last_error() or b"device" in lib.tfg_last_error()
 
 
+def test_field_config_validation(lib):
+    """tfg_create accepts any hash-grid geometry (n_min, n_max, power-of-two
+    table_size) and rejects other widths, before it looks for a device."""
+    from paper_2507_01631_b200.abi import FieldConfig, TrainConfig
+
+    def rc_of(**kw):
+        cfg = FieldConfig.defaults()
+        for k, v in kw.items():
+            setattr(cfg, k, v)
+        h = C.c_void_p()
+        rc = lib.tfg_create(C.byref(cfg), C.byref(TrainConfig.defaults()), 99, 1024, C.byref(h))
+        return rc, lib.tfg_last_error()
+
+    for bad in (dict(levels=6), dict(features=4), dict(density_hidden=32), dict(color_hidden=128),
+                dict(view_freqs=6), dict(occupancy_resolution=64), dict(table_size=3 << 12),
+                dict(table_size=1 << 23), dict(n_min=0), dict(n_min=64, n_max=32)):
+        rc, msg = rc_of(**bad)
+        assert rc == 1, (bad, rc, msg)  # TFG_ERR_INVALID
+    for ok in (dict(table_size=1 << 14), dict(table_size=1 << 19, n_max=2048), dict(n_min=8, n_max=512)):
+        rc, msg = rc_of(**ok)
+        assert rc == 4, (ok, rc, msg)  # accepted; no device 99 (here or on a GPU box)
+
+
 def test_param_counts(lib):
     from paper_2507_01631_b200.abi import FieldConfig, field_sizes
 
