@@ -142,3 +142,16 @@ def test_geometry_vs_oracle(geom):
         lg = ctx.train_step(100 + it, 0, N_RAYS)
         lr = ses.train_step(100 + it, 0, N_RAYS)
         assert abs(lg - lr) <= 1e-2 * abs(lr), (geom, it, lg, lr)
+    # the render path (its own slots and fp16 shadows) on the oracle's tiles
+    acc = ses.build_accept()
+    sel = acc[:: max(1, acc.size // 1500)][:1500]
+    px = np.stack([(sel >> 40).astype(np.int32), ((sel >> 20) & 0xFFFFF).astype(np.int32),
+                   (sel & 0xFFFFF).astype(np.int32)], axis=1)
+    v0 = px[px[:, 0] == 0]
+    ses.sample_pixels(v0)
+    ses.forward()
+    ref = ses.composite()
+    ctx.render_setup(ses.window_tiles(), [ses.tile_state(k) for k in range(4)], ses.color()[0])
+    rgb, _, op = ctx.render_pixels(ctx.scene.cams[0], v0[:, 1:])
+    np.testing.assert_allclose(rgb, ref["rgb"], atol=TOL_RAY_RGB_ATOL)
+    np.testing.assert_allclose(op, ref["opacity"], atol=TOL_RAY_RGB_ATOL)

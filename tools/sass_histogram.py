@@ -39,7 +39,10 @@ def main():
     for k in KERNELS:
         for f, c in funcs.items():
             if k in f:
-                rows.append((k + ("<1>" if "ILb1E" in f else "<0>" if "ILb0E" in f else ""), c))
+                # template arguments from the mangled name: ...kernelILb0ELi2EE... -> <0, 2>
+                m = re.search(re.escape(k) + r"I((?:L[a-z]+-?\d+E)+)E", f)
+                args = re.findall(r"L[a-z]+(-?\d+)E", m.group(1)) if m else []
+                rows.append((k + (f"<{', '.join(args)}>" if args else ""), c))
     lines = [f"# SASS instruction histogram ({tag})", "",
              f"`cuobjdump -sass {os.path.relpath(lib, ROOT)}` (sm_100a), static instruction counts per kernel "
              "(prefix match: `RED` counts every RED* form, `LDG` every LDG*).", "",

@@ -56,6 +56,11 @@ METRICS = [
 ]
 
 
+def family(k):
+    # templated kernels (raygen_kernel<0, 2>, hash_fwd_kernel<0>, ...) by base name
+    return FAMILY.get(k) or FAMILY.get(k.split("<")[0])
+
+
 def short(name):
     n = name.split("(")[0]
     n = n.split("::")[-1]
@@ -138,7 +143,7 @@ def main():
              "compare shares, not absolute times).", "",
              "| kernel | family | launches | ms/launch | share |", "|---|---|---|---|---|"]
     for k, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
-        lines.append(f"| {k} | {FAMILY.get(k, '-')} | {n} | {t / 1e6 / n:.3f} | {100 * t / tot:.1f}% |")
+        lines.append(f"| {k} | {family(k) or '-'} | {n} | {t / 1e6 / n:.3f} | {100 * t / tot:.1f}% |")
     r = collections.defaultdict(list)
     st = {}
     for rep in reps:
@@ -161,7 +166,7 @@ def main():
                      f"{g('sm__warps_active.avg.pct_of_peak_sustained_active'):.1f} | "
                      f"{g('smsp__issue_active.avg.pct_of_peak_sustained_active'):.1f} | "
                      f"{g('launch__registers_per_thread'):.0f} | {st.get(k, '')} |")
-        fam = FAMILY.get(k)
+        fam = family(k)
         if fam:
             traffic[fam] += g("dram__bytes_read.sum") + g("dram__bytes_write.sum")
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
