@@ -217,7 +217,22 @@ def red_peak():
     try:
         with open(os.path.join(ROOT, "profiles", "red_peak.json")) as f:
             r = json.load(f)
-        return {"GBps": float(r["best_GBps"]), "source": r.get("source", "profiles/red_peak.json")}
+        width = {"red.global.add.f32": 4, "red.global.add.v2.f32": 8, "red.global.add.v4.f32": 16}
+        # every width sustains the same lane-request rate (~214 G/s on B200):
+        # the scatter is bound by red requests, not bytes
+        lanes = max(v["GBps"] * 1e9 / width[v["op"]] for v in r["variants"] if v["op"] in width)
+        return {"GBps": float(r["best_GBps"]), "lanes_per_s": lanes, "source": r.get("source", "profiles/red_peak.json")}
+    except Exception:
+        return None
+
+
+def red_lanes():
+    """Dynamic red requests per sample of the backward's scatter, counted by
+    ncu on a profiled launch (tools/summarize_profiles.py ->
+    profiles/red_lanes.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "red_lanes.json")) as f:
+            return json.load(f)
     except Exception:
         return None
 
@@ -344,6 +359,18 @@ def run_ours(args):
             "resource": "global fp32 reds of the hash-table gradients (random indices into the 7 MB window tables)",
             "red_bytes_per_sample": SCATTER_BYTES, "achieved": ach, "unit": "GB/s of red payload",
             "peak": red["GBps"], "frac": ach / red["GBps"], "peak_source": red["source"]}
+        rl = red_lanes()
+        if rl:
+            # the same bound in the unit the hardware limits: red requests
+            # (one per lane per red instruction, any width); the count per
+            # sample is ncu's dynamic count on a profiled launch (the
+            # butterfly merges and v4 pairing make it data dependent)
+            lps = rl["lane_reds_per_sample"] * n_samples / (bwd_ms / 1e3)
+            roofline["limiter"].update({
+                "red_requests_per_sample": rl["lane_reds_per_sample"],
+                "achieved_requests_per_s": lps, "peak_requests_per_s": red["lanes_per_s"],
+                "frac_requests": lps / red["lanes_per_s"],
+                "requests_source": rl["source"]})
 
     # ---- end to end through the public API with host buffers: window slides
     # (pinned host <-> HBM tile state + crops), accepted-list rebuilds, loss

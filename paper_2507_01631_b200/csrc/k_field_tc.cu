@@ -413,10 +413,13 @@ __global__ void __launch_bounds__(128, 4) mlp_fwd_kernel(FieldArgs a, const uint
     const uint32_t id16 = umma::idesc_bf16(128, 16, 0, 0);
     // the next tile's descriptor and ray ids are loaded one tile ahead (their
     // latency was the largest single stall of the chain)
-    TileDesc td_next{};
+    // (the descriptor is carried packed and unpacked only when its tile
+    // becomes current: unpacked at load time, its field extraction stalled on
+    // the load right away)
+    uint2 td_next = make_uint2(0u, 0u);
     int ray_next = -1;
     if (blockIdx.x < n_tiles) {
-        td_next = a.tiles[blockIdx.x];
+        td_next = __ldg(reinterpret_cast<const uint2*>(a.tiles) + blockIdx.x);
         ray_next = rays[uint64_t(blockIdx.x) * kT + r];
         if (r == 0) {
             umma::mbar_expect_tx(&bar_ld[0], kFeatTile);
@@ -425,12 +428,13 @@ __global__ void __launch_bounds__(128, 4) mlp_fwd_kernel(FieldArgs a, const uint
     }
     uint32_t it = 0;
     for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
-        const TileDesc td = td_next;
+        asm volatile("" : "+r"(td_next.x), "+r"(td_next.y));
+        const TileDesc td{td_next.x, uint16_t(td_next.y & 0xffffu), uint16_t(td_next.y >> 16)};
         const int ray = ray_next;
         const uint32_t b = it & 1u;
         uint8_t* X0 = b ? X0b1 : X0b0;
         if (t + gridDim.x < n_tiles) {
-            td_next = a.tiles[t + gridDim.x];
+            td_next = __ldg(reinterpret_cast<const uint2*>(a.tiles) + (t + gridDim.x));
             ray_next = rays[uint64_t(t + gridDim.x) * kT + r];
             // the other buffer's last reader (the previous tile's layer-1
             // MMA) has completed

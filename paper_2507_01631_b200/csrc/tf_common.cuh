@@ -428,11 +428,12 @@ struct alignas(16) RayHdr {
 static_assert(sizeof(RayHdr) == 64, "RayHdr is one 64 B line");
 
 // Tile of <= 128 consecutive samples of one slot bucket (K2/K4 work unit).
-struct TileDesc {
+struct TileDesc {  // 8 B: mlp_fwd_kernel loads it as one uint2
     uint32_t start;
     uint16_t n;
     uint16_t slot;
 };
+static_assert(sizeof(TileDesc) == 8, "TileDesc is loaded as one uint2");
 
 // Status word bits (read back with the loss).
 enum : uint32_t {

@@ -1,7 +1,7 @@
 #!/bin/bash
 # Round-end evidence on one GPU: build, GPU tests, the default bench line, the
 # reference arm, and the ncu profile round.  usage: tools/gpu_final.sh <tag>
-TAG=${1:-r02b}
+TAG=${1:-r02x}
 python -c "import sys; sys.path.insert(0,'.'); from paper_2507_01631_b200 import build as b; b.build(); b.build_examples()" > gpurun_out/${TAG}_build.log 2>&1
 timeout 1800 python -m pytest tests -m gpu -q -rA > gpurun_out/${TAG}_gputest.log 2>&1
 timeout 900 python bench.py > gpurun_out/${TAG}_bench.log 2>&1

@@ -51,6 +51,13 @@ def main():
             ra = rb / sec / 1e9
             out.append(f"| field_bwd (scatter) | {k['ms_per_step']:.4f} | {bench.SCATTER_BYTES} B red payload x {S} "
                        f"samples = {rb / 1e6:.0f} MB | {ra:.1f} GB/s | {red['GBps']} | {ra / red['GBps']:.3f} |")
+            rl_ = bench.red_lanes()
+            if rl_:
+                n = rl_["lane_reds_per_sample"] * S
+                out.append(f"| field_bwd (scatter requests) | {k['ms_per_step']:.4f} | {rl_['lane_reds_per_sample']:.2f} "
+                           f"red requests x {S} samples = {n / 1e6:.0f} M (ncu, profiles/red_lanes.json) | "
+                           f"{n / sec / 1e9:.1f} G/s | {red['lanes_per_s'] / 1e9:.1f} G/s | "
+                           f"{n / sec / red['lanes_per_s']:.3f} |")
     rl = line["roofline"]
     out += ["", f"Headline `roofline` of the line: kernel {rl['kernel']}, achieved {rl['achieved']:.2f} "
                 f"{rl['unit']}, peak {rl['peak']}, frac {rl['frac']:.4f}; traffic (ncu DRAM bytes per launch, "
@@ -58,6 +65,11 @@ def main():
     if "limiter" in rl:
         lm = rl["limiter"]
         out.append(f"Limiter: {lm['resource']}: {lm['achieved']:.1f} {lm['unit']} of {lm['peak']} = {lm['frac']:.3f}.")
+        if "frac_requests" in lm:
+            out.append(f"In red requests (the unit every red width shares: f32, v2 and v4 all sustain "
+                       f"{lm['peak_requests_per_s'] / 1e9:.1f} G lane-requests/s in profiles/red_peak.json): "
+                       f"{lm['red_requests_per_sample']:.2f} per sample, {lm['achieved_requests_per_s'] / 1e9:.1f} G/s "
+                       f"= {lm['frac_requests']:.3f} of the peak.")
     if launches and os.path.exists(launches):
         rows = list(csv.reader(io.StringIO("".join(l for l in open(launches) if l.startswith('"')))))
         hdr = rows[0]

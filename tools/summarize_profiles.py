@@ -3,6 +3,11 @@ metrics, and profiles/traffic.json = measured DRAM bytes per launch of each
 bench kernel family, read by bench.py's roofline 'traffic' field).
 
 usage: python tools/summarize_profiles.py <launches.csv> <tag> <prof.ncu-rep> [more.ncu-rep ...]
+
+With the backward's source page (<tag>_mlp_bwd_kernel_source.csv) and the
+plain bench line (<tag>_plain.log) beside its capture, also writes
+profiles/red_lanes.json: the scatter's dynamic red count per sample (bench.py's
+limiter reads it).
 """
 import collections
 import csv
@@ -134,6 +139,35 @@ def stalls(rep, top=3):
     return ", ".join(f"{k} {100 * v / n:.0f}%" for k, v in tot.most_common(top))
 
 
+RED_WIDTH = {"F32x4": 16, "F32x2": 8, "F32": 4}
+
+
+def red_lanes(src_csv, plain_log):
+    """Dynamic global-red counts of the captured backward launch by width
+    (predicated-on thread instructions of REDG.E.ADD.F32[x2|x4] on its ncu
+    source page) per sample of the bench step it was taken from."""
+    rows = list(csv.reader(open(src_csv)))
+    hi = [i for i, r in enumerate(rows) if "Address" in r and "Source" in r][0]
+    h = rows[hi]
+    ci = h.index("Predicated-On Thread Instructions Executed")
+    by = collections.Counter()
+    for r in rows[hi + 1:]:
+        if len(r) <= ci:
+            continue
+        op = r[1].strip().split(" ")[0]
+        if op.startswith("REDG.E.ADD.F32"):
+            w = op.split(".")[3]
+            by[w] += int(float(r[ci] or 0))
+    line = [l for l in open(plain_log) if l.startswith("{")][-1]
+    samples = json.loads(line)["config"]["samples_per_step_per_gpu"]
+    lanes = sum(by.values())
+    return {"lane_reds_per_launch": lanes, "by_width": dict(by),
+            "red_bytes_per_launch": sum(n * RED_WIDTH[w] for w, n in by.items()),
+            "samples_per_launch": samples, "lane_reds_per_sample": lanes / samples,
+            "source": f"ncu source page of one mlp_bwd_kernel launch ({os.path.basename(src_csv)}), "
+                      f"samples from the same command's plain bench line"}
+
+
 def main():
     lpath, tag, reps = sys.argv[1], sys.argv[2], sys.argv[3:]
     agg = launches(lpath)
@@ -174,6 +208,14 @@ def main():
         f.write("\n".join(lines) + "\n")
     with open(os.path.join(ROOT, "profiles", "traffic.json"), "w") as f:
         json.dump({k: v for k, v in traffic.items()}, f, indent=1)
+    for rep in reps:
+        src = rep.replace(".ncu-rep", "_source.csv")
+        plain = os.path.join(os.path.dirname(rep), f"{tag}_plain.log")
+        if "mlp_bwd_kernel" in rep and os.path.exists(src) and os.path.exists(plain):
+            rl = red_lanes(src, plain)
+            with open(os.path.join(ROOT, "profiles", "red_lanes.json"), "w") as f:
+                json.dump(rl, f, indent=1)
+            print("red lanes:", rl)
     print("\n".join(lines))
 
 
