@@ -796,8 +796,20 @@ __global__ void __launch_bounds__(kBwdThreads, 2) mlp_bwd_kernel(FieldArgs a, Fi
     const uint32_t idw48 = umma::idesc_bf16(128, 48, 1, 1);
     const uint32_t idw32 = umma::idesc_bf16(128, 32, 1, 1);
     const uint32_t idw16 = umma::idesc_bf16(128, 16, 1, 1);
+    // the next tile's descriptor (packed) and ray ids one tile ahead, as in
+    // mlp_fwd_kernel: this tile's sample and view-encoding loads then issue
+    // without a dependent load in front of them
+    const uint2* tiles2 = reinterpret_cast<const uint2*>(a.tiles);
+    uint2 td_next = blockIdx.x < n_tiles ? __ldg(tiles2 + blockIdx.x) : make_uint2(0u, 0u);
+    int ray_next = blockIdx.x < n_tiles ? rays[uint64_t(blockIdx.x) * kT + r] : -1;
     for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-        TileDesc td = a.tiles[t];
+        asm volatile("" : "+r"(td_next.x), "+r"(td_next.y));
+        const TileDesc td{td_next.x, uint16_t(td_next.y & 0xffffu), uint16_t(td_next.y >> 16)};
+        const int ray = ray_next;
+        if (t + gridDim.x < n_tiles) {
+            td_next = __ldg(tiles2 + t + gridDim.x);
+            ray_next = rays[uint64_t(t + gridDim.x) * kT + r];
+        }
         if (td.slot != cur) {
             if (cur >= 0) flush_density(tmem, g.g_dnet[cur], reinterpret_cast<float*>(C1));
             stage_density<false>(W, a.f.dnet[td.slot]);
@@ -809,7 +821,6 @@ __global__ void __launch_bounds__(kBwdThreads, 2) mlp_bwd_kernel(FieldArgs a, Fi
             umma::bulk_g2s(X0, feat + uint64_t(t) * kFeatTile, kFeatTile, &bar_ld);
         }
         bool live = r < td.n;
-        int ray = rays[uint64_t(t) * kT + r];
         float4 dio = live ? a.s.io[uint64_t(td.start) + r] : make_float4(0.f, 0.f, 0.f, 0.f);
         float ve[kViewDim];
         {
