@@ -934,10 +934,11 @@ __global__ void __launch_bounds__(kBwdThreads, 2) mlp_bwd_kernel(FieldArgs a, Fi
 #pragma unroll
             for (int c = 0; c < 8; ++c) st_chunk(C2, r, c, v + 8 * c);
         }
-        sync_mlp();
         {
             // K3 already applied the sigmoid derivative: io = (d raw sigma,
-            // d pre-sigmoid r, g, b), so the colour output layer is not recomputed
+            // d pre-sigmoid r, g, b), so the colour output layer is not
+            // recomputed.  (D3 = DO: the previous tile's readers of DO have
+            // completed; one barrier covers C2 and D3.)
             float d3[16];
             d3[0] = dio.y;
             d3[1] = dio.z;
