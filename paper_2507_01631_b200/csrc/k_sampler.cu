@@ -804,9 +804,12 @@ int launch_sampler(const RaygenArgs& a, RayRec* rays, RayHdr* hdr, float4* venc,
     if (!a.pixels && a.memo_rays && a.n_rays < TFG_RAYGEN_WIDE_BELOW)
         launch_pdl(raygen_kernel<false, 8>, dim3((8 * a.n_rays + 127) / 128), dim3(128), 0, st, a, rays, venc,
                    counts, status);
+#ifndef TFG_RAYGEN_LANES
+#define TFG_RAYGEN_LANES 2  // memo draws of TFG_RAYGEN_WIDE_BELOW rays or more
+#endif
     else if (!a.pixels && a.memo_rays)
-        launch_pdl(raygen_kernel<false, 2>, dim3((2 * a.n_rays + 127) / 128), dim3(128), 0, st, a, rays, venc,
-                   counts, status);
+        launch_pdl(raygen_kernel<false, TFG_RAYGEN_LANES>, dim3((TFG_RAYGEN_LANES * a.n_rays + 127) / 128), dim3(128),
+                   0, st, a, rays, venc, counts, status);
     else
         launch_pdl(raygen_kernel<true, 2>, dim3((2 * a.n_rays + 127) / 128), dim3(128), 0, st, a, rays, venc,
                    counts, status);
