@@ -136,7 +136,12 @@ def test_color_checkpoint_round_trip(tmp_path):
 
 
 @pytest.mark.gpu
-def test_run_save_resume(tmp_path):
+@pytest.mark.parametrize("geometry", [{}, {"table_size": 1 << 17, "n_min": 16, "n_max": 1024}],
+                         ids=["default", "T2^17_padded"])
+def test_run_save_resume(tmp_path, geometry):
+    """Save a run mid-snake and resume it bit-exactly; also for a hash-grid
+    geometry whose table count is not a multiple of 4 floats (the slot
+    records carry alignment padding, the files do not)."""
     import torch
 
     if not torch.cuda.is_available():
@@ -145,6 +150,8 @@ def test_run_save_resume(tmp_path):
 
     scene = synth.make_scene(3, 3, tile_side=96.0, n_views=2, gsd=1.5, seed=4)
     fc, tc = FieldConfig.defaults(), TrainConfig.defaults(batch_rays=2048, seed=2)
+    for k, v in geometry.items():
+        setattr(fc, k, v)
     a = Context(scene, fc, tc, max_rays=2048)
     path = snake_path(3, 3)
     it = 0
@@ -157,6 +164,10 @@ def test_run_save_resume(tmp_path):
     a.save_run(run)
     assert sorted(os.listdir(os.path.join(run, "tiles")))[:2] == ["r0_c0.ckpt", "r0_c1.ckpt"]
     assert len(os.listdir(os.path.join(run, "tiles"))) == 9
+    enc_n, dnet_n, _, _ = field_sizes(fc)
+    # the file holds the reference's arrays, no alignment padding
+    h = _parse(os.path.join(run, "tiles", "r0_c0.ckpt"), fc)
+    assert h["n_params"] == enc_n + dnet_n and h["body"].size == 3 * (enc_n + dnet_n) + 32 ** 3
     b = Context(scene, fc, tc, max_rays=2048)
     b.load_run(run)
     b.set_window(*path[2])
