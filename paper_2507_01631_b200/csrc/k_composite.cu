@@ -268,17 +268,11 @@ __global__ void __launch_bounds__(TFG_COMPOSITE_THREADS, TFG_COMPOSITE_MINB) com
 }
 
 void launch_composite(const CompositeArgs& a, cudaStream_t st, uint64_t* launches) {
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
 #ifndef TFG_COMPOSITE_WAVES
 #define TFG_COMPOSITE_WAVES 1  // resident blocks per SM x this = the persistent grid
 #endif
     const int need = (a.n_rays * 32 + TFG_COMPOSITE_THREADS - 1) / TFG_COMPOSITE_THREADS;
-    const int blocks = std::max(1, std::min(need, sms * TFG_COMPOSITE_MINB * TFG_COMPOSITE_WAVES));
+    const int blocks = std::max(1, std::min(need, a.sms * TFG_COMPOSITE_MINB * TFG_COMPOSITE_WAVES));
     launch_pdl(composite_kernel, dim3(blocks), dim3(TFG_COMPOSITE_THREADS), 0, st, a);
     *launches += 1;
     if (a.backward) {

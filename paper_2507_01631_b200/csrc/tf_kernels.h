@@ -120,6 +120,7 @@ struct FieldGradArgs {
 struct CompositeArgs {
     const RayHdr* hdr;   // per ray: segment positions / counts, target
     int n_rays;
+    int sms;             // the persistent grid is sized from it
     SampleArrays s;
     const Status* status_in;
     Status* status;

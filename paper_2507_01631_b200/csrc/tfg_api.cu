@@ -566,6 +566,7 @@ int run_composite(tfg_ctx* c, bool backward, float4* export_io = nullptr) {
     CompositeArgs a{};
     a.hdr = c->d_hdr;
     a.n_rays = c->cur_rays;
+    a.sms = c->sms;
     a.s = c->s;
     a.status_in = c->d_status;
     a.status = c->d_status;
