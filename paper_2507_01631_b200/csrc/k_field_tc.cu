@@ -24,6 +24,8 @@
 // A tile is <= 128 samples of one slot bucket (K1), so the density weights of
 // a tile are one tile's.  Precision: bf16 operands, fp32 accumulation (tests
 // state the tolerance against the fp32 oracle).
+#include <mutex>
+
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -1082,13 +1084,26 @@ __global__ void __launch_bounds__(kBwdThreads, 2) mlp_bwd_kernel(FieldArgs a, Fi
 }
 
 // ------------------------------------------------------------------ launchers
+// Function attributes belong to the current device's context: set them once
+// per device (not once per process), under a lock so that no launch on that
+// device overtakes the setting.
+static void set_smem_attributes_once() {
+    static std::mutex mu;
+    static uint64_t done = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t bit = uint64_t(1) << (dev & 63);
+    std::lock_guard<std::mutex> lock(mu);
+    if (done & bit) return;
+    cudaFuncSetAttribute(mlp_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kFwdSmem));
+    cudaFuncSetAttribute(mlp_bwd_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kBwdSmem));
+    cudaFuncSetAttribute(mlp_bwd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kBwdSmem));
+    done |= bit;
+}
+
 void launch_field_forward_tc(const FieldArgs& a, uint8_t* feat, int32_t* rays, int sms,
                              cudaStream_t st, uint64_t* launches) {
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(mlp_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kFwdSmem));
-        attr = true;
-    }
+    set_smem_attributes_once();
 #ifndef TFG_GATHER_CTAS
 #define TFG_GATHER_CTAS 5
 #endif
@@ -1105,12 +1120,7 @@ void launch_field_forward_tc(const FieldArgs& a, uint8_t* feat, int32_t* rays, i
 
 void launch_field_backward_tc(const FieldArgs& a, const FieldGradArgs& g, uint8_t* feat,
                               int32_t* rays, int sms, cudaStream_t st, uint64_t* launches) {
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(mlp_bwd_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kBwdSmem));
-        cudaFuncSetAttribute(mlp_bwd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kBwdSmem));
-        attr = true;
-    }
+    set_smem_attributes_once();
     // the feature tiles of the forward pass (same batch) are still resident;
     // the hash-table scatter is fused into the backward's last epilogue
     if (a.hl.generic)
