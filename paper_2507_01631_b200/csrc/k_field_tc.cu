@@ -173,11 +173,21 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
     __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
     return *reinterpret_cast<uint32_t*>(&h);
 }
+// ReLU folded into the bf16 pack (one F2FP.RELU per pair): relu then round
+// equals round then relu, bit for bit.  Used by the forward's epilogues (the
+// backward keeps fmaxf + pack: there the folded form measured slower, 1.25 ->
+// 1.28-1.29 ms, as every change to its instruction mix so far).
+__device__ __forceinline__ uint32_t pack2_relu(float a, float b) {
+    uint32_t d;
+    asm("cvt.rn.relu.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(b), "f"(a));
+    return d;
+}
 // Writes 8 consecutive columns [8c, 8c+8) of row r of a 128-row tile.
 __device__ __forceinline__ void st_chunk(uint8_t* buf, int r, int c, const float* v) {
     uint4 q = make_uint4(pack2(v[0], v[1]), pack2(v[2], v[3]), pack2(v[4], v[5]), pack2(v[6], v[7]));
     *reinterpret_cast<uint4*>(buf + c * kChunk + (r >> 3) * 128 + (r & 7) * 16) = q;
 }
+
 
 // Descriptors for the chunk-major tiles (see umma.cuh).
 __device__ __forceinline__ uint64_t kmaj(const uint8_t* base, uint32_t rows, int kstep) {
@@ -226,6 +236,17 @@ __device__ __forceinline__ void tst_bf16(uint32_t tmem, int col, const float* v)
         uint32_t q[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) q[j] = pack2(v[16 * c + 2 * j], v[16 * c + 2 * j + 1]);
+        umma::st8(tmem + ((32u * w) << 16) + uint32_t(col + 8 * c), q);
+    }
+}
+template <int N>
+__device__ __forceinline__ void tst_bf16_relu(uint32_t tmem, int col, const float* v) {
+    const uint32_t w = threadIdx.x >> 5;
+#pragma unroll
+    for (int c = 0; c < N / 16; ++c) {
+        uint32_t q[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) q[j] = pack2_relu(v[16 * c + 2 * j], v[16 * c + 2 * j + 1]);
         umma::st8(tmem + ((32u * w) << 16) + uint32_t(col + 8 * c), q);
     }
 }
@@ -531,8 +552,8 @@ __global__ void __launch_bounds__(128, 4) mlp_fwd_kernel(FieldArgs a, const uint
             tld16(tmem, 48, v + 48);
             umma::ld_wait();
 #pragma unroll
-            for (int i = 0; i < 64; ++i) v[i] = fmaxf(v[i] + W.b1d[i], 0.f);
-            tst_bf16<64>(tmem, kColA, v);
+            for (int i = 0; i < 64; ++i) v[i] += W.b1d[i];
+            tst_bf16_relu<64>(tmem, kColA, v);
         }
         sync_for_mma_tmem();
         // ---- density layer 2: [128x64] x W2d^T -> 16 (raw sigma | embedding)
@@ -577,8 +598,8 @@ __global__ void __launch_bounds__(128, 4) mlp_fwd_kernel(FieldArgs a, const uint
             tld16(tmem, 48, v + 48);
             umma::ld_wait();
 #pragma unroll
-            for (int i = 0; i < 64; ++i) v[i] = fmaxf(v[i] + W.bc1[i], 0.f);
-            tst_bf16<64>(tmem, kColA, v);
+            for (int i = 0; i < 64; ++i) v[i] += W.bc1[i];
+            tst_bf16_relu<64>(tmem, kColA, v);
         }
         sync_for_mma_tmem();
         // ---- colour layer 2: [128x64] x Wc2^T -> 64
@@ -597,8 +618,8 @@ __global__ void __launch_bounds__(128, 4) mlp_fwd_kernel(FieldArgs a, const uint
             tld16(tmem, 48, v + 48);
             umma::ld_wait();
 #pragma unroll
-            for (int i = 0; i < 64; ++i) v[i] = fmaxf(v[i] + W.bc2[i], 0.f);
-            tst_bf16<64>(tmem, kColA, v);
+            for (int i = 0; i < 64; ++i) v[i] += W.bc2[i];
+            tst_bf16_relu<64>(tmem, kColA, v);
         }
         sync_for_mma_tmem();
         // ---- colour layer 3: [128x64] x Wc3^T -> 16 (3 real) -> sigmoid
