@@ -169,6 +169,35 @@ __device__ __forceinline__ void stage_color(const Weights& w, const float* __res
     for (int i = threadIdx.x; i < 16; i += kT) w.bc3[i] = i < 3 ? p[kCB3 + i] : 0.f;
 }
 
+// Forward only: each layer's bias as an MMA operand, so the accumulator
+// starts at the bias and the epilogues carry no bias add.  B tile [N x 16]
+// (chunk-major, rows = out features): column 0 = bf16(b), column 1 =
+// bf16(b - bf16(b)), the rest 0; multiplied by the constant A tile whose
+// columns 0 and 1 are 1, it contributes b to 16 mantissa bits (the bias
+// enters first, then the layer's products).
+constexpr uint32_t kBiasTile64 = 64 * 16 * 2, kBiasTile16 = 16 * 16 * 2;
+struct BiasTiles {
+    uint8_t* ones;  // [128 x 16]: columns 0, 1 = 1
+    uint8_t* l1;    // [64 x 16]
+    uint8_t* l2;    // [16 x 16]
+    uint8_t* c1;
+    uint8_t* c2;
+    uint8_t* c3;    // [16 x 16] (3 real rows)
+};
+template <int N>
+__device__ __forceinline__ void stage_bias_tile(uint8_t* dst, const float* __restrict__ b, int n_real) {
+    for (int o = threadIdx.x; o < N; o += kT) {
+        const float x = o < n_real ? b[o] : 0.f;
+        const __nv_bfloat16 hi = __float2bfloat16_rn(x);
+        const __nv_bfloat16 lo = __float2bfloat16_rn(x - __bfloat162float(hi));
+        uint4 q = make_uint4(uint32_t(*reinterpret_cast<const uint16_t*>(&hi)) |
+                                 (uint32_t(*reinterpret_cast<const uint16_t*>(&lo)) << 16),
+                             0u, 0u, 0u);
+        *reinterpret_cast<uint4*>(dst + umma::off(N, o, 0)) = q;
+        *reinterpret_cast<uint4*>(dst + umma::off(N, o, 8)) = make_uint4(0u, 0u, 0u, 0u);
+    }
+}
+
 __device__ __forceinline__ uint32_t pack2(float a, float b) {
     __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
     return *reinterpret_cast<uint32_t*>(&h);
@@ -452,7 +481,7 @@ __device__ __forceinline__ void scatter_row_rt(const HashLayout& hl, float* genc
 // ------------------------------------------------------------------ K2b
 // smem: weights | X0 [128x16] (the gathered features, bulk-copied; the only
 // activation tile in smem).  4 resident CTAs per SM (TMEM and registers).
-constexpr uint32_t kFwdSmem = kWeightsBytes + 2 * kFeatTile + 128;
+constexpr uint32_t kFwdSmem = kWeightsBytes + 3 * kFeatTile + 3 * kBiasTile64 + 2 * kBiasTile16 + 128;
 // TMEM: accumulator [0, 64); layers 2-5 take their A operand (the previous
 // layer's activations, bf16 pairs) from columns [64, 96), so activations never
 // touch smem (measured: the MLP's smem pipe was its contended resource).
@@ -470,6 +499,13 @@ __global__ void __launch_bounds__(128, 4) mlp_fwd_kernel(FieldArgs a, const uint
     // flight while tile i runs
     uint8_t* const X0b0 = carve(p, kFeatTile);
     uint8_t* const X0b1 = carve(p, kFeatTile);
+    BiasTiles BT;
+    BT.ones = carve(p, kFeatTile);
+    BT.l1 = carve(p, kBiasTile64);
+    BT.l2 = carve(p, kBiasTile16);
+    BT.c1 = carve(p, kBiasTile64);
+    BT.c2 = carve(p, kBiasTile64);
+    BT.c3 = carve(p, kBiasTile16);
     const int r = threadIdx.x;
     if (r == 0) {
         umma::mbar_init(&bar_mma, 1);
@@ -479,6 +515,14 @@ __global__ void __launch_bounds__(128, 4) mlp_fwd_kernel(FieldArgs a, const uint
     }
     if (r < 32) umma::tmem_alloc<kFwdTmemCols>(&tmem_slot);
     stage_color(W, a.f.color);
+    {
+        const float o2[8] = {1.f, 1.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        st_chunk(BT.ones, r, 0, o2);
+        st_chunk(BT.ones, r, 1, z);
+        stage_bias_tile<64>(BT.c1, a.f.color + kCB1, kCHidden);
+        stage_bias_tile<64>(BT.c2, a.f.color + kCB2, kCHidden);
+        stage_bias_tile<16>(BT.c3, a.f.color + kCB3, 3);
+    }
     uint32_t ph_mma = 0, ph_ld = 0;  // bit b: phase of bar_ld[b]
     int cur = -1;
     pdl_wait();  // hash_fwd's feature tiles and ray ids
@@ -521,6 +565,8 @@ __global__ void __launch_bounds__(128, 4) mlp_fwd_kernel(FieldArgs a, const uint
         }
         if (td.slot != cur) {
             stage_density<true>(W, a.f.dnet[td.slot]);
+            stage_bias_tile<64>(BT.l1, a.f.dnet[td.slot] + kDB1, kDHidden);
+            stage_bias_tile<16>(BT.l2, a.f.dnet[td.slot] + kDB2, kDOut);
             cur = td.slot;
         }
         float ve[kViewDim];
@@ -540,7 +586,8 @@ __global__ void __launch_bounds__(128, 4) mlp_fwd_kernel(FieldArgs a, const uint
         ph_ld ^= 1u << b;
         // ---- density layer 1: [128x16] x W1d^T -> 64
         if (r == 0) {
-            umma::mma(tmem, kmaj(X0, kT, 0), kmaj(W.w1d, kW1dRows, 0), id64, 0);
+            umma::mma(tmem, kmaj(BT.ones, kT, 0), kmaj(BT.l1, 64, 0), id64, 0);  // bias
+            umma::mma(tmem, kmaj(X0, kT, 0), kmaj(W.w1d, kW1dRows, 0), id64, 1);
             umma::commit(&bar_mma);
         }
         wait_mma(&bar_mma, ph_mma);
@@ -552,15 +599,15 @@ __global__ void __launch_bounds__(128, 4) mlp_fwd_kernel(FieldArgs a, const uint
             tld16(tmem, 48, v + 48);
             umma::ld_wait();
 #pragma unroll
-            for (int i = 0; i < 64; ++i) v[i] += W.b1d[i];
             tst_bf16_relu<64>(tmem, kColA, v);
         }
         sync_for_mma_tmem();
         // ---- density layer 2: [128x64] x W2d^T -> 16 (raw sigma | embedding)
         if (r == 0) {
+            umma::mma(tmem, kmaj(BT.ones, kT, 0), kmaj(BT.l2, 16, 0), id16, 0);
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-                umma::mma_ts(tmem, tmem + kColA + 8 * k, kmaj(W.w2d, kW2dRows, k), id16, k > 0);
+                umma::mma_ts(tmem, tmem + kColA + 8 * k, kmaj(W.w2d, kW2dRows, k), id16, 1);
             umma::commit(&bar_mma);
         }
         wait_mma(&bar_mma, ph_mma);
@@ -569,11 +616,11 @@ __global__ void __launch_bounds__(128, 4) mlp_fwd_kernel(FieldArgs a, const uint
             float v[16];
             tld16(tmem, 0, v);
             umma::ld_wait();
-            float raw = v[0] + W.b2d[0];
+            float raw = v[0];
             sigma = raw >= a.density_lim ? a.density_max : __expf(raw);
             float cin[48];
 #pragma unroll
-            for (int i = 0; i < kEmb; ++i) cin[i] = v[1 + i] + W.b2d[1 + i];
+            for (int i = 0; i < kEmb; ++i) cin[i] = v[1 + i];
 #pragma unroll
             for (int i = 0; i < kViewDim; ++i) cin[kEmb + i] = ve[i];
             cin[kCIn] = 1.f;  // ones column (bias gradient of colour layer 1 in K4)
@@ -584,9 +631,10 @@ __global__ void __launch_bounds__(128, 4) mlp_fwd_kernel(FieldArgs a, const uint
         sync_for_mma_tmem();
         // ---- colour layer 1: [128x48] x Wc1^T -> 64
         if (r == 0) {
+            umma::mma(tmem, kmaj(BT.ones, kT, 0), kmaj(BT.c1, 64, 0), id64, 0);
 #pragma unroll
             for (int k = 0; k < 3; ++k)
-                umma::mma_ts(tmem, tmem + kColA + 8 * k, kmaj(W.wc1, kWc1Rows, k), id64, k > 0);
+                umma::mma_ts(tmem, tmem + kColA + 8 * k, kmaj(W.wc1, kWc1Rows, k), id64, 1);
             umma::commit(&bar_mma);
         }
         wait_mma(&bar_mma, ph_mma);
@@ -598,15 +646,15 @@ __global__ void __launch_bounds__(128, 4) mlp_fwd_kernel(FieldArgs a, const uint
             tld16(tmem, 48, v + 48);
             umma::ld_wait();
 #pragma unroll
-            for (int i = 0; i < 64; ++i) v[i] += W.bc1[i];
             tst_bf16_relu<64>(tmem, kColA, v);
         }
         sync_for_mma_tmem();
         // ---- colour layer 2: [128x64] x Wc2^T -> 64
         if (r == 0) {
+            umma::mma(tmem, kmaj(BT.ones, kT, 0), kmaj(BT.c2, 64, 0), id64, 0);
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-                umma::mma_ts(tmem, tmem + kColA + 8 * k, kmaj(W.wc2, kWc2Rows, k), id64, k > 0);
+                umma::mma_ts(tmem, tmem + kColA + 8 * k, kmaj(W.wc2, kWc2Rows, k), id64, 1);
             umma::commit(&bar_mma);
         }
         wait_mma(&bar_mma, ph_mma);
@@ -618,15 +666,15 @@ __global__ void __launch_bounds__(128, 4) mlp_fwd_kernel(FieldArgs a, const uint
             tld16(tmem, 48, v + 48);
             umma::ld_wait();
 #pragma unroll
-            for (int i = 0; i < 64; ++i) v[i] += W.bc2[i];
             tst_bf16_relu<64>(tmem, kColA, v);
         }
         sync_for_mma_tmem();
         // ---- colour layer 3: [128x64] x Wc3^T -> 16 (3 real) -> sigmoid
         if (r == 0) {
+            umma::mma(tmem, kmaj(BT.ones, kT, 0), kmaj(BT.c3, 16, 0), id16, 0);
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-                umma::mma_ts(tmem, tmem + kColA + 8 * k, kmaj(W.wc3, kWc3Rows, k), id16, k > 0);
+                umma::mma_ts(tmem, tmem + kColA + 8 * k, kmaj(W.wc3, kWc3Rows, k), id16, 1);
             umma::commit(&bar_mma);
         }
         wait_mma(&bar_mma, ph_mma);
@@ -636,7 +684,7 @@ __global__ void __launch_bounds__(128, 4) mlp_fwd_kernel(FieldArgs a, const uint
             umma::ld_wait();
             if (r < td.n)
                 a.s.io[uint64_t(td.start) + r] =
-                    make_float4(sigma, sigm(v[0] + W.bc3[0]), sigm(v[1] + W.bc3[1]), sigm(v[2] + W.bc3[2]));
+                    make_float4(sigma, sigm(v[0]), sigm(v[1]), sigm(v[2]));
         }
     }
     umma::fence_before_sync();
