@@ -598,7 +598,6 @@ __global__ void __launch_bounds__(128, 4) mlp_fwd_kernel(FieldArgs a, const uint
             tld16(tmem, 32, v + 32);
             tld16(tmem, 48, v + 48);
             umma::ld_wait();
-#pragma unroll
             tst_bf16_relu<64>(tmem, kColA, v);
         }
         sync_for_mma_tmem();
@@ -645,7 +644,6 @@ __global__ void __launch_bounds__(128, 4) mlp_fwd_kernel(FieldArgs a, const uint
             tld16(tmem, 32, v + 32);
             tld16(tmem, 48, v + 48);
             umma::ld_wait();
-#pragma unroll
             tst_bf16_relu<64>(tmem, kColA, v);
         }
         sync_for_mma_tmem();
@@ -665,7 +663,6 @@ __global__ void __launch_bounds__(128, 4) mlp_fwd_kernel(FieldArgs a, const uint
             tld16(tmem, 32, v + 32);
             tld16(tmem, 48, v + 48);
             umma::ld_wait();
-#pragma unroll
             tst_bf16_relu<64>(tmem, kColA, v);
         }
         sync_for_mma_tmem();
