@@ -700,7 +700,8 @@ __global__ void __launch_bounds__(128, 4) mlp_fwd_kernel(FieldArgs a, const uint
 // accumulators persistent across the CTA's tiles:
 //   dWc2^T [64,128)  dWc1 [128,176)  dW1d [176,208)  dWc3^T [208,224)  dW2d^T [224,240)
 constexpr uint32_t kBufA = 9 * kChunk;  // 18432
-constexpr uint32_t kBwdSmem = 3 * kBufA + 4 * kChunk + 6 * kChunk + 2 * kChunk + kWeightsBytes + 128;
+constexpr uint32_t kBwdSmem = 3 * kBufA + 4 * kChunk + 6 * kChunk + 2 * kChunk + kWeightsBytes + 3 * kBiasTile64 +
+                               kBiasTile16 + 128;
 constexpr uint32_t kBwdTmemCols = 256;
 constexpr int kColWc2 = 64, kColWc1 = 128, kColW1d = 176, kColWc3 = 208, kColW2d = 224;
 constexpr int kColDX = 240;  // d(features) of the last tile, read by the scatter warps
@@ -801,6 +802,14 @@ __global__ void __launch_bounds__(kBwdThreads, 2) mlp_bwd_kernel(FieldArgs a, Fi
     uint8_t* D3 = carve(p, 2 * kChunk);
     uint8_t* DO = D3;  // D3 is dead once (A)'s MMAs have completed; DO is written in (C)
     Weights W = carve_weights(p);
+    // bias tiles of the recomputed forward layers (as mlp_fwd_kernel: the
+    // accumulators start at the bias, so both kernels compute the same
+    // pre-activations bit for bit); the A side is X0's K step 1, whose
+    // columns 16 and 17 are 1
+    uint8_t* const bt_l1 = carve(p, kBiasTile64);
+    uint8_t* const bt_l2 = carve(p, kBiasTile16);
+    uint8_t* const bt_c1 = carve(p, kBiasTile64);
+    uint8_t* const bt_c2 = carve(p, kBiasTile64);
     const int r = threadIdx.x;
     if (r == 0) {
         umma::mbar_init(&bar_mma, 1);
@@ -817,9 +826,12 @@ __global__ void __launch_bounds__(kBwdThreads, 2) mlp_bwd_kernel(FieldArgs a, Fi
         set_ones_chunk(H1, 8, r);
         set_ones_chunk(C1, 8, r);
         set_ones_chunk(C2, 8, r);
-        set_ones_chunk(X0, 2, r);
+        const float o2[8] = {1.f, 1.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        st_chunk(X0, r, 2, o2);  // col 16: dW1d's bias column; 16-17: the bias MMAs' A
         float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         st_chunk(X0, r, 3, z);
+        stage_bias_tile<64>(bt_c1, a.f.color + kCB1, kCHidden);
+        stage_bias_tile<64>(bt_c2, a.f.color + kCB2, kCHidden);
     }
     pdl_wait();  // the composite's gradients
     uint32_t n_tiles = a.status->n_tiles;
@@ -881,6 +893,8 @@ __global__ void __launch_bounds__(kBwdThreads, 2) mlp_bwd_kernel(FieldArgs a, Fi
         if (td.slot != cur) {
             if (cur >= 0) flush_density(tmem, g.g_dnet[cur], reinterpret_cast<float*>(C1));
             stage_density<false>(W, a.f.dnet[td.slot]);
+            stage_bias_tile<64>(bt_l1, a.f.dnet[td.slot] + kDB1, kDHidden);
+            stage_bias_tile<16>(bt_l2, a.f.dnet[td.slot] + kDB2, kDOut);
             cur = td.slot;
             first_d = true;
         }
@@ -908,7 +922,8 @@ __global__ void __launch_bounds__(kBwdThreads, 2) mlp_bwd_kernel(FieldArgs a, Fi
         uint32_t mh[2], mc1[2], mc2[2];  // ReLU masks of H1, C1, C2
         // ================= forward recompute
         if (r == 0) {
-            umma::mma(tmem, kmaj(X0, kT, 0), kmaj(W.w1d, kW1dRows, 0), id64, 0);
+            umma::mma(tmem, kmaj(X0, kT, 1), kmaj(bt_l1, 64, 0), id64, 0);  // bias
+            umma::mma(tmem, kmaj(X0, kT, 0), kmaj(W.w1d, kW1dRows, 0), id64, 1);
             umma::commit(&bar_mma);
         }
         wait_mma(&bar_mma, ph_mma);
@@ -922,7 +937,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2) mlp_bwd_kernel(FieldArgs a, Fi
             mh[0] = mh[1] = 0;
 #pragma unroll
             for (int i = 0; i < 64; ++i) {
-                float x = v[i] + W.b1d[i];
+                float x = v[i];
                 if (x > 0.f) mh[i >> 5] |= 1u << (i & 31);
                 v[i] = fmaxf(x, 0.f);
             }
@@ -931,9 +946,10 @@ __global__ void __launch_bounds__(kBwdThreads, 2) mlp_bwd_kernel(FieldArgs a, Fi
         }
         sync_mlp();
         if (r == 0) {
+            umma::mma(tmem, kmaj(X0, kT, 1), kmaj(bt_l2, 16, 0), id16, 0);
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-                umma::mma(tmem, kmaj(H1, kT, k), kmaj(W.w2d, kW2dRows, k), id16, k > 0);
+                umma::mma(tmem, kmaj(H1, kT, k), kmaj(W.w2d, kW2dRows, k), id16, 1);
             umma::commit(&bar_mma);
         }
         wait_mma(&bar_mma, ph_mma);
@@ -943,7 +959,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2) mlp_bwd_kernel(FieldArgs a, Fi
             umma::ld_wait();
             float cin[48];
 #pragma unroll
-            for (int i = 0; i < kEmb; ++i) cin[i] = v[1 + i] + W.b2d[1 + i];
+            for (int i = 0; i < kEmb; ++i) cin[i] = v[1 + i];
 #pragma unroll
             for (int i = 0; i < kViewDim; ++i) cin[kEmb + i] = ve[i];
             cin[kCIn] = 1.f;
@@ -954,9 +970,10 @@ __global__ void __launch_bounds__(kBwdThreads, 2) mlp_bwd_kernel(FieldArgs a, Fi
         }
         sync_mlp();
         if (r == 0) {
+            umma::mma(tmem, kmaj(X0, kT, 1), kmaj(bt_c1, 64, 0), id64, 0);
 #pragma unroll
             for (int k = 0; k < 3; ++k)
-                umma::mma(tmem, kmaj(CIN, kT, k), kmaj(W.wc1, kWc1Rows, k), id64, k > 0);
+                umma::mma(tmem, kmaj(CIN, kT, k), kmaj(W.wc1, kWc1Rows, k), id64, 1);
             umma::commit(&bar_mma);
         }
         wait_mma(&bar_mma, ph_mma);
@@ -970,7 +987,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2) mlp_bwd_kernel(FieldArgs a, Fi
             mc1[0] = mc1[1] = 0;
 #pragma unroll
             for (int i = 0; i < 64; ++i) {
-                float x = v[i] + W.bc1[i];
+                float x = v[i];
                 if (x > 0.f) mc1[i >> 5] |= 1u << (i & 31);
                 v[i] = fmaxf(x, 0.f);
             }
@@ -979,9 +996,10 @@ __global__ void __launch_bounds__(kBwdThreads, 2) mlp_bwd_kernel(FieldArgs a, Fi
         }
         sync_mlp();
         if (r == 0) {
+            umma::mma(tmem, kmaj(X0, kT, 1), kmaj(bt_c2, 64, 0), id64, 0);
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-                umma::mma(tmem, kmaj(C1, kT, k), kmaj(W.wc2, kWc2Rows, k), id64, k > 0);
+                umma::mma(tmem, kmaj(C1, kT, k), kmaj(W.wc2, kWc2Rows, k), id64, 1);
             umma::commit(&bar_mma);
         }
         wait_mma(&bar_mma, ph_mma);
@@ -995,7 +1013,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2) mlp_bwd_kernel(FieldArgs a, Fi
             mc2[0] = mc2[1] = 0;
 #pragma unroll
             for (int i = 0; i < 64; ++i) {
-                float x = v[i] + W.bc2[i];
+                float x = v[i];
                 if (x > 0.f) mc2[i >> 5] |= 1u << (i & 31);
                 v[i] = fmaxf(x, 0.f);
             }
