@@ -203,9 +203,7 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
     return *reinterpret_cast<uint32_t*>(&h);
 }
 // ReLU folded into the bf16 pack (one F2FP.RELU per pair): relu then round
-// equals round then relu, bit for bit.  Used by the forward's epilogues (the
-// backward keeps fmaxf + pack: there the folded form measured slower, 1.25 ->
-// 1.28-1.29 ms, as every change to its instruction mix so far).
+// equals round then relu, bit for bit.
 __device__ __forceinline__ uint32_t pack2_relu(float a, float b) {
     uint32_t d;
     asm("cvt.rn.relu.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(b), "f"(a));
@@ -214,6 +212,11 @@ __device__ __forceinline__ uint32_t pack2_relu(float a, float b) {
 // Writes 8 consecutive columns [8c, 8c+8) of row r of a 128-row tile.
 __device__ __forceinline__ void st_chunk(uint8_t* buf, int r, int c, const float* v) {
     uint4 q = make_uint4(pack2(v[0], v[1]), pack2(v[2], v[3]), pack2(v[4], v[5]), pack2(v[6], v[7]));
+    *reinterpret_cast<uint4*>(buf + c * kChunk + (r >> 3) * 128 + (r & 7) * 16) = q;
+}
+__device__ __forceinline__ void st_chunk_relu(uint8_t* buf, int r, int c, const float* v) {
+    uint4 q = make_uint4(pack2_relu(v[0], v[1]), pack2_relu(v[2], v[3]), pack2_relu(v[4], v[5]),
+                         pack2_relu(v[6], v[7]));
     *reinterpret_cast<uint4*>(buf + c * kChunk + (r >> 3) * 128 + (r & 7) * 16) = q;
 }
 
@@ -939,10 +942,9 @@ __global__ void __launch_bounds__(kBwdThreads, 2) mlp_bwd_kernel(FieldArgs a, Fi
             for (int i = 0; i < 64; ++i) {
                 float x = v[i];
                 if (x > 0.f) mh[i >> 5] |= 1u << (i & 31);
-                v[i] = fmaxf(x, 0.f);
             }
 #pragma unroll
-            for (int c = 0; c < 8; ++c) st_chunk(H1, r, c, v + 8 * c);
+            for (int c = 0; c < 8; ++c) st_chunk_relu(H1, r, c, v + 8 * c);
         }
         sync_mlp();
         if (r == 0) {
@@ -989,10 +991,9 @@ __global__ void __launch_bounds__(kBwdThreads, 2) mlp_bwd_kernel(FieldArgs a, Fi
             for (int i = 0; i < 64; ++i) {
                 float x = v[i];
                 if (x > 0.f) mc1[i >> 5] |= 1u << (i & 31);
-                v[i] = fmaxf(x, 0.f);
             }
 #pragma unroll
-            for (int c = 0; c < 8; ++c) st_chunk(C1, r, c, v + 8 * c);
+            for (int c = 0; c < 8; ++c) st_chunk_relu(C1, r, c, v + 8 * c);
         }
         sync_mlp();
         if (r == 0) {
@@ -1015,10 +1016,9 @@ __global__ void __launch_bounds__(kBwdThreads, 2) mlp_bwd_kernel(FieldArgs a, Fi
             for (int i = 0; i < 64; ++i) {
                 float x = v[i];
                 if (x > 0.f) mc2[i >> 5] |= 1u << (i & 31);
-                v[i] = fmaxf(x, 0.f);
             }
 #pragma unroll
-            for (int c = 0; c < 8; ++c) st_chunk(C2, r, c, v + 8 * c);
+            for (int c = 0; c < 8; ++c) st_chunk_relu(C2, r, c, v + 8 * c);
         }
         {
             // K3 already applied the sigmoid derivative: io = (d raw sigma,
