@@ -214,6 +214,18 @@ __device__ __forceinline__ void st_chunk(uint8_t* buf, int r, int c, const float
     uint4 q = make_uint4(pack2(v[0], v[1]), pack2(v[2], v[3]), pack2(v[4], v[5]), pack2(v[6], v[7]));
     *reinterpret_cast<uint4*>(buf + c * kChunk + (r >> 3) * 128 + (r & 7) * 16) = q;
 }
+// Overwrites the 8 ReLU'd activations of row r, chunk c with 8 gradients
+// masked by the ReLU: kept where the activation is positive, 0 elsewhere
+// (one HSET2 mask + one AND per pair; the masks need no registers between
+// the forward recompute and the backward).
+__device__ __forceinline__ void st_chunk_masked(uint8_t* buf, int r, int c, const float* v) {
+    uint4* const p = reinterpret_cast<uint4*>(buf + c * kChunk + (r >> 3) * 128 + (r & 7) * 16);
+    const uint4 act = *p;
+    const __nv_bfloat162 zero = __float2bfloat162_rn(0.f);
+    auto gt0 = [&](uint32_t w) { return __hgt2_mask(*reinterpret_cast<const __nv_bfloat162*>(&w), zero); };
+    *p = make_uint4(pack2(v[0], v[1]) & gt0(act.x), pack2(v[2], v[3]) & gt0(act.y), pack2(v[4], v[5]) & gt0(act.z),
+                    pack2(v[6], v[7]) & gt0(act.w));
+}
 __device__ __forceinline__ void st_chunk_relu(uint8_t* buf, int r, int c, const float* v) {
     uint4 q = make_uint4(pack2_relu(v[0], v[1]), pack2_relu(v[2], v[3]), pack2_relu(v[4], v[5]),
                          pack2_relu(v[6], v[7]));
@@ -922,7 +934,6 @@ __global__ void __launch_bounds__(kBwdThreads, 2) mlp_bwd_kernel(FieldArgs a, Fi
         sync_mlp();
         umma::mbar_wait(&bar_ld, ph_ld);
         ph_ld ^= 1u;
-        uint32_t mh[2], mc1[2], mc2[2];  // ReLU masks of H1, C1, C2
         // ================= forward recompute
         if (r == 0) {
             umma::mma(tmem, kmaj(X0, kT, 1), kmaj(bt_l1, 64, 0), id64, 0);  // bias
@@ -937,12 +948,6 @@ __global__ void __launch_bounds__(kBwdThreads, 2) mlp_bwd_kernel(FieldArgs a, Fi
             tld16(tmem, 32, v + 32);
             tld16(tmem, 48, v + 48);
             umma::ld_wait();
-            mh[0] = mh[1] = 0;
-#pragma unroll
-            for (int i = 0; i < 64; ++i) {
-                float x = v[i];
-                if (x > 0.f) mh[i >> 5] |= 1u << (i & 31);
-            }
 #pragma unroll
             for (int c = 0; c < 8; ++c) st_chunk_relu(H1, r, c, v + 8 * c);
         }
@@ -986,12 +991,6 @@ __global__ void __launch_bounds__(kBwdThreads, 2) mlp_bwd_kernel(FieldArgs a, Fi
             tld16(tmem, 32, v + 32);
             tld16(tmem, 48, v + 48);
             umma::ld_wait();
-            mc1[0] = mc1[1] = 0;
-#pragma unroll
-            for (int i = 0; i < 64; ++i) {
-                float x = v[i];
-                if (x > 0.f) mc1[i >> 5] |= 1u << (i & 31);
-            }
 #pragma unroll
             for (int c = 0; c < 8; ++c) st_chunk_relu(C1, r, c, v + 8 * c);
         }
@@ -1011,12 +1010,6 @@ __global__ void __launch_bounds__(kBwdThreads, 2) mlp_bwd_kernel(FieldArgs a, Fi
             tld16(tmem, 32, v + 32);
             tld16(tmem, 48, v + 48);
             umma::ld_wait();
-            mc2[0] = mc2[1] = 0;
-#pragma unroll
-            for (int i = 0; i < 64; ++i) {
-                float x = v[i];
-                if (x > 0.f) mc2[i >> 5] |= 1u << (i & 31);
-            }
 #pragma unroll
             for (int c = 0; c < 8; ++c) st_chunk_relu(C2, r, c, v + 8 * c);
         }
@@ -1053,11 +1046,9 @@ __global__ void __launch_bounds__(kBwdThreads, 2) mlp_bwd_kernel(FieldArgs a, Fi
             tld16(tmem, 32, v + 32);
             tld16(tmem, 48, v + 48);
             umma::ld_wait();
-#pragma unroll
-            for (int i = 0; i < 64; ++i) v[i] = ((mc2[i >> 5] >> (i & 31)) & 1u) ? v[i] : 0.f;
             wait_mma(&bar_w, ph_w);  // dWc3^T has read C2
 #pragma unroll
-            for (int c = 0; c < 8; ++c) st_chunk(C2, r, c, v + 8 * c);  // DC2 over C2
+            for (int c = 0; c < 8; ++c) st_chunk_masked(C2, r, c, v + 8 * c);  // DC2 over C2
         }
         sync_mlp();
         // (B) dC1pre = DC2 . Wc2 ; dWc2^T += [C1|1]^T . DC2
@@ -1079,11 +1070,9 @@ __global__ void __launch_bounds__(kBwdThreads, 2) mlp_bwd_kernel(FieldArgs a, Fi
             tld16(tmem, 32, v + 32);
             tld16(tmem, 48, v + 48);
             umma::ld_wait();
-#pragma unroll
-            for (int i = 0; i < 64; ++i) v[i] = ((mc1[i >> 5] >> (i & 31)) & 1u) ? v[i] : 0.f;
             wait_mma(&bar_w, ph_w);  // dWc2^T has read C1
 #pragma unroll
-            for (int c = 0; c < 8; ++c) st_chunk(C1, r, c, v + 8 * c);  // DC1 over C1
+            for (int c = 0; c < 8; ++c) st_chunk_masked(C1, r, c, v + 8 * c);  // DC1 over C1
         }
         sync_mlp();
         // (C) dCIN[0:16] = DC1 . Wc1[:, 0:16] ; dWc1 += DC1^T . CIN
@@ -1129,11 +1118,9 @@ __global__ void __launch_bounds__(kBwdThreads, 2) mlp_bwd_kernel(FieldArgs a, Fi
             tld16(tmem, 32, v + 32);
             tld16(tmem, 48, v + 48);
             umma::ld_wait();
-#pragma unroll
-            for (int i = 0; i < 64; ++i) v[i] = ((mh[i >> 5] >> (i & 31)) & 1u) ? v[i] : 0.f;
             wait_mma(&bar_w, ph_w);  // dW2d^T has read H1
 #pragma unroll
-            for (int c = 0; c < 8; ++c) st_chunk(H1, r, c, v + 8 * c);  // DH1 over H1
+            for (int c = 0; c < 8; ++c) st_chunk_masked(H1, r, c, v + 8 * c);  // DH1 over H1
         }
         sync_mlp();
         // (E) dX0 = DH1 . W1d into the scatter warps' columns (once they have
