@@ -1167,6 +1167,7 @@ static void set_smem_attributes_once() {
     std::lock_guard<std::mutex> lock(mu);
     if (done & bit) return;
     cudaFuncSetAttribute(mlp_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kFwdSmem));
+
     cudaFuncSetAttribute(mlp_bwd_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kBwdSmem));
     cudaFuncSetAttribute(mlp_bwd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kBwdSmem));
     done |= bit;
@@ -1176,7 +1177,7 @@ void launch_field_forward_tc(const FieldArgs& a, uint8_t* feat, int32_t* rays, i
                              cudaStream_t st, uint64_t* launches) {
     set_smem_attributes_once();
 #ifndef TFG_GATHER_CTAS
-#define TFG_GATHER_CTAS 5
+#define TFG_GATHER_CTAS 6  // r2 (fp16 tables, final MLP): 4: 0.535, 5: 0.511, 6: 0.507, 7: 0.513, 8: 0.517 ms field_fwd
 #endif
 #ifndef TFG_MLPF_CTAS
 #define TFG_MLPF_CTAS 4
