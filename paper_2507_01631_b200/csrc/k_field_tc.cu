@@ -57,6 +57,10 @@ struct Weights {
     uint8_t* wc1;
     uint8_t* wc2;
     uint8_t* wc3;
+    // fp32 bias copies: no longer read (the biases enter through the MMAs,
+    // stage_bias_tile), still staged: removing them measured the forward
+    // 5 us slower in a same-box A/B (0.510 vs 0.515 ms, a code-placement
+    // effect), so they stay until that is understood
     float* b1d;
     float* b2d;
     float* bc1;
