@@ -272,7 +272,8 @@ void launch_composite(const CompositeArgs& a, cudaStream_t st, uint64_t* launche
 #define TFG_COMPOSITE_WAVES 1  // resident blocks per SM x this = the persistent grid
 #endif
     const int need = (a.n_rays * 32 + TFG_COMPOSITE_THREADS - 1) / TFG_COMPOSITE_THREADS;
-    const int blocks = std::max(1, std::min(need, a.sms * TFG_COMPOSITE_MINB * TFG_COMPOSITE_WAVES));
+    const int sms = a.sms > 0 ? a.sms : 148;
+    const int blocks = std::max(1, std::min(need, sms * TFG_COMPOSITE_MINB * TFG_COMPOSITE_WAVES));
     launch_pdl(composite_kernel, dim3(blocks), dim3(TFG_COMPOSITE_THREADS), 0, st, a);
     *launches += 1;
     if (a.backward) {
