@@ -8,10 +8,10 @@ the kernels round it (fp32 accumulation, fp32 epilogues).  With no rounding
 it is the fp32 math of the oracle (nn.hpp:90-157, 199-298; oracle/
 tf_oracle.cpp field_point / tfo_backward).
 
-The forward kernel starts each accumulator at the layer's bias through an
-extra MMA with the bias split into two bf16 halves (16 mantissa bits, added
-before the products); the model adds the fp32 bias after them, a difference
-far below the GPU-vs-model tolerances.
+The forward kernel and the backward's recompute start each accumulator at
+the layer's bias through an extra MMA with the bias split into two bf16
+halves (16 mantissa bits, added before the products); the model adds the
+fp32 bias after them, a difference far below the GPU-vs-model tolerances.
 
 It separates the two questions a toleranced parity test mixes up:
   * does the GPU compute the bf16-operand math it claims?  (GPU vs this model,
