@@ -214,7 +214,8 @@ __global__ void __launch_bounds__(128, TFG_ACCEPT_MINB) accept_solve_kernel(Acce
         candidate_pixel(a, idx, &v, &row, &col);
         uint32_t ok = 0;
         double gx = 0.0, gy = 0.0;
-        int st = rpc_localize(a.cams[v], double(row), double(col), hi ? a.z_min : a.z_max, &gx, &gy);
+        int st = rpc_localize(a.cams[v], double(row), double(col), hi ? a.z_min : a.z_max, &gx, &gy,
+                              a.loc ? a.loc + 2 * v + hi : nullptr);
         double ox = __shfl_xor_sync(pair, gx, 1), oy = __shfl_xor_sync(pair, gy, 1);
         int ost = __shfl_xor_sync(pair, st, 1);
         double o[3], d[3];
@@ -433,7 +434,8 @@ __global__ void __launch_bounds__(128, kSolve ? TFG_RAYGEN_MINB : TFG_RAYGEN_MEM
         R.status = 1;  // empty accepted list (flagged above)
     } else {
         double gx = 0.0, gy = 0.0;
-        int st = rpc_localize(a.cams[v], double(row), double(col), hi ? a.z_min : a.z_max, &gx, &gy);
+        int st = rpc_localize(a.cams[v], double(row), double(col), hi ? a.z_min : a.z_max, &gx, &gy,
+                              a.loc ? a.loc + 2 * v + hi : nullptr);
         double ox = __shfl_xor_sync(pair, gx, 1), oy = __shfl_xor_sync(pair, gy, 1);
         int ost = __shfl_xor_sync(pair, st, 1);
         // status of the top (z_max) localisation first, as ray_from_pixel throws
@@ -792,6 +794,16 @@ int launch_accept(const AcceptArgs& args, uint32_t* flags, uint32_t* pos, uint32
     accept_scatter_kernel<<<nb, 128, 0, st>>>(a, flags, pos, out);
     *launches += 3;
     return 0;
+}
+
+__global__ void loc_start_kernel(const tfg_rpc* __restrict__ cams, int n, double z_min, double z_max,
+                                 LocStart* __restrict__ out) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < 2 * n) rpc_loc_start(cams[t >> 1], (t & 1) ? z_min : z_max, out + t);
+}
+
+void launch_loc_start(const tfg_rpc* cams, int n, double z_min, double z_max, LocStart* out, cudaStream_t st) {
+    if (n > 0) loc_start_kernel<<<(2 * n + 63) / 64, 64, 0, st>>>(cams, n, z_min, z_max, out);
 }
 
 int launch_sampler(const RaygenArgs& a, RayRec* rays, RayHdr* hdr, float4* venc, uint32_t* counts,

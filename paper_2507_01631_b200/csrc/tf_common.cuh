@@ -262,21 +262,59 @@ TF_HD void lu2_solve(double a00, double a01, double a10, double a11, double b0, 
 
 TF_HD double hyp2(double a, double b) { return sqrt(a * a + b * b); }
 
+// The pixel-independent head of localize at one height: every solve starts
+// at the RPC centre, so the first projection and the first iteration's four
+// Jacobian projections are the same for all pixels of a camera.  Computed
+// once per (camera, height) with the same code, they are the same bits.
+struct LocStart {
+    int st;                  // 0; 1: the centre projection threw; 2: the first Jacobian's did
+    double r, q;             // projection of the centre
+    double pr4[4], pc4[4];   // the four central-difference points around it
+};
+TF_HD void rpc_loc_start(const tfg_rpc& c, double h, LocStart* s) {
+    const double x = c.long_off, y = c.lat_off;
+    const double hx = 1e-6 * c.long_scale;
+    const double hy = 1e-6 * c.lat_scale;
+    s->st = 0;
+    if (!rpc_project(c, x, y, h, &s->r, &s->q)) {
+        s->st = 1;
+        return;
+    }
+    const double px[4] = {x + hx, x - hx, x + 0.0, x - 0.0};
+    const double py[4] = {y + 0.0, y - 0.0, y + hy, y - hy};
+    if (!rpc_project4(c, px, py, h, s->pr4, s->pc4)) s->st = 2;
+}
+
 // localize (camera.cpp:66-103): damped Newton at fixed height, central FD
 // Jacobian (step 1e-6 * scale), <= 6 step halvings, tol 1e-4 px, <= 50 its.
-// 0 ok, 1 project() threw, 2 no convergence.
-TF_HD int rpc_localize(const tfg_rpc& c, double pr, double pc, double h, double* gx, double* gy) {
+// 0 ok, 1 project() threw, 2 no convergence.  `start` (optional): this
+// camera's and height's rpc_loc_start, which replaces the first projection
+// and the first iteration's Jacobian projections (same results, bit for bit).
+TF_HD int rpc_localize(const tfg_rpc& c, double pr, double pc, double h, double* gx, double* gy,
+                       const LocStart* start = nullptr) {
     double x = c.long_off, y = c.lat_off;
     const double hx = 1e-6 * c.long_scale;
     const double hy = 1e-6 * c.lat_scale;
     double r, q;
-    if (!rpc_project(c, x, y, h, &r, &q)) return 1;
+    if (start) {
+        if (start->st == 1) return 1;
+        r = start->r;
+        q = start->q;
+    } else if (!rpc_project(c, x, y, h, &r, &q)) {
+        return 1;
+    }
     double f0 = r - pr, f1 = q - pc;
     for (int it = 1; it <= 50; ++it) {
         double fn = hyp2(f0, f1);
         if (fn < 1e-4) { *gx = x; *gy = y; return 0; }
         double a0, a1, b0, b1, c0, c1, d0, d1;
-        {
+        if (start && it == 1) {
+            if (start->st == 2) return 1;
+            a0 = start->pr4[0]; a1 = start->pc4[0];
+            b0 = start->pr4[1]; b1 = start->pc4[1];
+            c0 = start->pr4[2]; c1 = start->pc4[2];
+            d0 = start->pr4[3]; d1 = start->pc4[3];
+        } else {
             const double px[4] = {x + hx, x - hx, x + 0.0, x - 0.0};
             const double py[4] = {y + 0.0, y - 0.0, y + hy, y - hy};
             double pr4[4], pc4[4];

@@ -32,6 +32,7 @@ struct HashLayout {
 
 struct AcceptArgs {
     const tfg_rpc* cams;
+    const LocStart* loc;         // per view: rpc_loc_start at z_max, then at z_min (or null)
     int n_views;
     const uint64_t* view_start;  // candidate offset of each view (n_views)
     const int* union_rect;       // r0, r1, c0, c1 per view
@@ -68,6 +69,7 @@ constexpr uint32_t kMemoDone = 1u << 31, kMemoHit = 1u << 30;
 
 struct RaygenArgs {
     const tfg_rpc* cams;
+    const LocStart* loc;     // per view: rpc_loc_start at z_max, then at z_min (or null)
     const uint64_t* accept;  // draw mode: accepted list
     const uint32_t* n_accept_dev;  // its length, read on device (no host sync per move)
     const double* memo_rays;  // draw mode: the window's pixel-ray memo (accept pass), indexed like the crop pixels
@@ -196,6 +198,8 @@ void launch_enc_half(const float* params, uint64_t stride, int n, uint64_t enc_n
                      cudaStream_t st,
                      uint64_t* launches);
 void launch_occupancy(const OccArgs& a, cudaStream_t st, uint64_t* launches);
+// rpc_loc_start of n cameras at z_max and z_min -> out[2 v], out[2 v + 1]
+void launch_loc_start(const tfg_rpc* cams, int n, double z_min, double z_max, LocStart* out, cudaStream_t st);
 
 
 // Launch with programmatic stream serialization (the kernel calls

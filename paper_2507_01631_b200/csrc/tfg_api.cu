@@ -365,6 +365,7 @@ int stage_window(tfg_ctx* c, WinBuf& w, int pr, int pc, cudaStream_t st) {
     CK(cudaMemcpyAsync(c->d_crop4, crect.data(), crect.size() * 4, cudaMemcpyHostToDevice, st));
     AcceptArgs a{};
     a.cams = c->d_cams;
+    a.loc = c->d_loc;
     a.n_views = c->n_views;
     a.view_start = c->d_view_start;
     a.union_rect = c->d_union;
@@ -502,6 +503,7 @@ int sync_status(tfg_ctx* c) {
 RaygenArgs base_raygen(tfg_ctx* c) {
     RaygenArgs a{};
     a.cams = c->d_cams;
+    a.loc = c->d_loc;
     a.seed = c->tc.seed;
     a.z_min = c->roi.z_min;
     a.z_max = c->roi.z_max;
@@ -839,6 +841,7 @@ TFG_API int tfg_create(const tfg_field_config* fcfg, const tfg_train_config* tcf
         rc |= dalloc(c, &c->d_acc_sums, 4096 + 64);
         rc |= dalloc(c, &c->d_todo_n, 1);
         rc |= dalloc(c, &c->d_rcam, 1);
+        rc |= dalloc(c, &c->d_rloc, 2);
         if (rc) return TFG_ERR_CUDA;
         CK(cudaHostAlloc(reinterpret_cast<void**>(&c->h_status), sizeof(Status), cudaHostAllocDefault));
         CK(cudaHostAlloc(reinterpret_cast<void**>(&c->h_sticky), 16, cudaHostAllocDefault));
@@ -879,7 +882,7 @@ TFG_API int tfg_destroy(tfg_ctx* c) {
                    c->d_block_sums, c->d_acc_sums, c->d_todo_n, c->d_view_start, c->d_union, c->d_crop4,
                    c->d_rays, c->d_hdr, c->d_venc,
                    c->d_counts, c->d_P, c->d_tiles, c->s.local, c->s.td, c->s.endpoint, c->s.io,
-                   c->d_ray_out, c->d_pixels, c->d_rparams, c->d_rbits, c->d_rcolor, c->d_rcam,
+                   c->d_ray_out, c->d_pixels, c->d_rparams, c->d_rbits, c->d_rcolor, c->d_rcam, c->d_rloc, c->d_loc,
                    c->d_feat, c->d_tile_rays, c->d_export,
                    c->d_stage_in, c->d_stage_out, c->d_loss_parts, c->d_imp};
     for (void* p : dev)
@@ -995,6 +998,7 @@ TFG_API int tfg_set_scene(tfg_ctx* c, const tfg_rpc* cams, int n_views,
     c->crop_cap = cropb;
     int rc = 0;
     dfree(c, c->d_cams);
+    dfree(c, c->d_loc);
     dfree(c, c->d_east);
     dfree(c, c->d_north);
     dfree(c, c->d_flags);
@@ -1003,6 +1007,7 @@ TFG_API int tfg_set_scene(tfg_ctx* c, const tfg_rpc* cams, int n_views,
     dfree(c, c->d_union);
     dfree(c, c->d_crop4);
     rc |= dalloc(c, &c->d_cams, n_views);
+    rc |= dalloc(c, &c->d_loc, 2 * uint64_t(n_views));
     rc |= dalloc(c, &c->d_east, grid_cols + 1);
     rc |= dalloc(c, &c->d_north, grid_rows + 1);
     // per window buffer: crops, accepted list and the pixel memo of the crop
@@ -1038,6 +1043,7 @@ TFG_API int tfg_set_scene(tfg_ctx* c, const tfg_rpc* cams, int n_views,
         c->memo_reuse = grid_rows <= 128 && grid_cols <= 128 && !(off_env && off_env[0] == '1');
     }
     CK(cudaMemcpyAsync(c->d_cams, c->cams.data(), n_views * sizeof(tfg_rpc), cudaMemcpyHostToDevice, c->st));
+    launch_loc_start(c->d_cams, n_views, c->roi.z_min, c->roi.z_max, c->d_loc, c->st);
     CK(cudaMemcpyAsync(c->d_east, c->east.data(), (grid_cols + 1) * 8, cudaMemcpyHostToDevice, c->st));
     CK(cudaMemcpyAsync(c->d_north, c->north.data(), (grid_rows + 1) * 8, cudaMemcpyHostToDevice, c->st));
     CK(cudaStreamSynchronize(c->st));
@@ -1939,6 +1945,7 @@ TFG_API int tfg_render_pixels(tfg_ctx* c, const tfg_rpc* cam, const int32_t* pix
     if (!c || c->rn == 0) return fail(TFG_ERR_STATE, "render_pixels: call render_setup first");
     CK(cudaSetDevice(c->device));
     CK(cudaMemcpyAsync(c->d_rcam, cam, sizeof(tfg_rpc), cudaMemcpyHostToDevice, c->st));
+    launch_loc_start(c->d_rcam, 1, c->roi.z_min, c->roi.z_max, c->d_rloc, c->st);
     FieldPtrs f{};
     for (int k = 0; k < c->rn; ++k) {
         f.enc[k] = c->d_rparams + uint64_t(k) * c->stride;
@@ -1987,6 +1994,7 @@ TFG_API int tfg_render_pixels(tfg_ctx* c, const tfg_rpc* cam, const int32_t* pix
         CK(cudaMemcpyAsync(c->d_pixels, c->h_rpix + b * 2 * M, size_t(nb) * 8, cudaMemcpyHostToDevice, c->st));
         RaygenArgs a{};
         a.cams = c->d_rcam;
+        a.loc = c->d_rloc;
         a.pixels = c->d_pixels;
         a.pixel_pairs = 1;
         a.n_rays = nb;

@@ -188,6 +188,9 @@ struct tfg_ctx {
     RayRec* d_rays = nullptr;
     RayHdr* d_hdr = nullptr;  // per-ray composite header (written with the samples)
     float4* d_venc = nullptr;
+    // rpc_loc_start per scene view (z_max, z_min) and for the render camera
+    LocStart* d_loc = nullptr;
+    LocStart* d_rloc = nullptr;
     uint32_t *d_counts = nullptr, *d_P = nullptr;
     double* d_loss_parts = nullptr;  // per-block partial losses of K3
     TileDesc* d_tiles = nullptr;
