@@ -7,13 +7,18 @@
 //                         (4 KB/tile), reused by K4b
 //   K2b mlp_fwd_kernel    density MLP 16->64->16 + colour MLP 39->64->64->3 as
 //                         tcgen05.mma (bf16 x bf16 -> fp32 in TMEM), weights
-//                         and features staged by the bulk-copy engine,
-//                         epilogues (bias, ReLU, exp/sigmoid) from tcgen05.ld;
-//                         each epilogue's bf16 output goes back to TMEM with
-//                         tcgen05.st as the next layer's A operand
-//   K4b mlp_bwd_kernel    recomputed forward + data-gradient GEMMs + weight-
-//                         gradient GEMMs (K = 128 samples, MN-major operands
-//                         read from the same smem tiles) accumulated in TMEM
+//                         and features staged by the bulk-copy engine; each
+//                         accumulator starts at the layer's bias (one extra
+//                         K=16 MMA), epilogues (ReLU folded into the bf16
+//                         pack, exp/sigmoid) from tcgen05.ld; each epilogue's
+//                         bf16 output goes back to TMEM with tcgen05.st as the
+//                         next layer's A operand
+//   K4b mlp_bwd_kernel    recomputed forward (biases through the MMA as in
+//                         K2b, so the pre-activations are the forward's bits)
+//                         + data-gradient GEMMs (ReLU masks read from the
+//                         stored bf16 activations) + weight-gradient GEMMs
+//                         (K = 128 samples, MN-major operands read from the
+//                         same smem tiles) accumulated in TMEM
 //                         across all tiles of a persistent CTA, flushed with
 //                         one fp32 atomic per weight per CTA
 //   (K4a)                 hash-table scatter-add on K4b's own scatter warps
