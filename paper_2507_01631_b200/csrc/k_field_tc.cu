@@ -142,27 +142,10 @@ __device__ __forceinline__ void stage_matrix(uint8_t* dst, const float* __restri
                            pack2(v[q][6], v[q][7]));
     }
 }
-// Element-wise form, kept for the backward: there the staging overlaps the
-// scatter warps' reds, and the batched form measured 12 us slower per step
-// (1.302 vs 1.290 ms) against 25 us faster in the forward.
-__device__ __forceinline__ void stage_matrix_elem(uint8_t* dst, const float* __restrict__ W, int rows_src,
-                                                  int cols_src, int rows, int cols) {
-    for (int i = threadIdx.x; i < rows * cols; i += kT) {
-        int r = i / cols, c = i - r * cols;
-        float v = (r < rows_src && c < cols_src) ? W[r * cols_src + c] : 0.f;
-        *reinterpret_cast<__nv_bfloat16*>(dst + umma::off(rows, r, c)) = __float2bfloat16_rn(v);
-    }
-}
-template <bool kBatched>
 __device__ __forceinline__ void stage_density(const Weights& w, const float* __restrict__ p) {
     static_assert(kDW1 % 4 == 0 && kDW2 % 4 == 0, "density weight rows are float4 aligned");
-    if constexpr (kBatched) {
-        stage_matrix<kDHidden, kFeatDim, 64, 16>(w.w1d, p + kDW1);
-        stage_matrix<kDOut, kDHidden, 16, 64>(w.w2d, p + kDW2);
-    } else {
-        stage_matrix_elem(w.w1d, p + kDW1, kDHidden, kFeatDim, 64, 16);
-        stage_matrix_elem(w.w2d, p + kDW2, kDOut, kDHidden, 16, 64);
-    }
+    stage_matrix<kDHidden, kFeatDim, 64, 16>(w.w1d, p + kDW1);
+    stage_matrix<kDOut, kDHidden, 16, 64>(w.w2d, p + kDW2);
     for (int i = threadIdx.x; i < 64; i += kT) w.b1d[i] = p[kDB1 + i];
     for (int i = threadIdx.x; i < 16; i += kT) w.b2d[i] = p[kDB2 + i];
 }
@@ -588,7 +571,7 @@ __global__ void __launch_bounds__(128, 4) mlp_fwd_kernel(FieldArgs a, const uint
             }
         }
         if (td.slot != cur) {
-            stage_density<true>(W, a.f.dnet[td.slot]);
+            stage_density(W, a.f.dnet[td.slot]);
             stage_bias_tile<64>(BT.l1, a.f.dnet[td.slot] + kDB1, kDHidden);
             stage_bias_tile<16>(BT.l2, a.f.dnet[td.slot] + kDB2, kDOut);
             cur = td.slot;
@@ -916,7 +899,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2) mlp_bwd_kernel(FieldArgs a, Fi
         }
         if (td.slot != cur) {
             if (cur >= 0) flush_density(tmem, g.g_dnet[cur], reinterpret_cast<float*>(C1));
-            stage_density<false>(W, a.f.dnet[td.slot]);
+            stage_density(W, a.f.dnet[td.slot]);
             stage_bias_tile<64>(bt_l1, a.f.dnet[td.slot] + kDB1, kDHidden);
             stage_bias_tile<16>(bt_l2, a.f.dnet[td.slot] + kDB2, kDOut);
             cur = td.slot;
