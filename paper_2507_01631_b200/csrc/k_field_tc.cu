@@ -161,8 +161,9 @@ __device__ __forceinline__ void stage_color(const Weights& w, const float* __res
     for (int i = threadIdx.x; i < 16; i += kT) w.bc3[i] = i < 3 ? p[kCB3 + i] : 0.f;
 }
 
-// Forward only: each layer's bias as an MMA operand, so the accumulator
-// starts at the bias and the epilogues carry no bias add.  B tile [N x 16]
+// Each layer's bias as an MMA operand (the forward and the backward's
+// recompute), so the accumulator starts at the bias and the epilogues carry
+// no bias add.  B tile [N x 16]
 // (chunk-major, rows = out features): column 0 = bf16(b), column 1 =
 // bf16(b - bf16(b)), the rest 0; multiplied by the constant A tile whose
 // columns 0 and 1 are 1, it contributes b to 16 mantissa bits (the bias
