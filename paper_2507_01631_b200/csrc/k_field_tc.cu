@@ -152,6 +152,16 @@ __device__ __forceinline__ void stage_density(const Weights& w, const float* __r
 __device__ __forceinline__ void stage_color(const Weights& w, const float* __restrict__ p) {
     static_assert(kCW2 % 4 == 0 && kCW3 % 4 == 0, "colour weight rows are float4 aligned");
     stage_matrix<kCHidden, kCIn, 64, 48>(w.wc1, p + kCW1);
+    // colour layer 1's bias rides in its own K range: input column kCIn (the
+    // ones column the backward's dWc1 bias gradient uses) and kCIn + 1 are 1,
+    // the weight tile holds bf16(bc1) and bf16(bc1 - bf16(bc1)) there
+    for (int o = threadIdx.x; o < kCHidden; o += kT) {
+        const float x = p[kCB1 + o];
+        const __nv_bfloat16 hi = __float2bfloat16_rn(x);
+        const __nv_bfloat16 lo = __float2bfloat16_rn(x - __bfloat162float(hi));
+        *reinterpret_cast<__nv_bfloat16*>(w.wc1 + umma::off(kWc1Rows, o, kCIn)) = hi;
+        *reinterpret_cast<__nv_bfloat16*>(w.wc1 + umma::off(kWc1Rows, o, kCIn + 1)) = lo;
+    }
     stage_matrix<kCHidden, kCHidden, 64, 64>(w.wc2, p + kCW2);
     stage_matrix<3, kCHidden, 16, 64>(w.wc3, p + kCW3);
     for (int i = threadIdx.x; i < 64; i += kT) {
@@ -173,8 +183,7 @@ struct BiasTiles {
     uint8_t* ones;  // [128 x 16]: columns 0, 1 = 1
     uint8_t* l1;    // [64 x 16]
     uint8_t* l2;    // [16 x 16]
-    uint8_t* c1;
-    uint8_t* c2;
+    uint8_t* c2;  // (colour layer 1's bias rides in its weight tile: stage_color)
     uint8_t* c3;    // [16 x 16] (3 real rows)
 };
 template <int N>
@@ -489,7 +498,7 @@ __device__ __forceinline__ void scatter_row_rt(const HashLayout& hl, float* genc
 // ------------------------------------------------------------------ K2b
 // smem: weights | X0 [128x16] (the gathered features, bulk-copied; the only
 // activation tile in smem).  4 resident CTAs per SM (TMEM and registers).
-constexpr uint32_t kFwdSmem = kWeightsBytes + 3 * kFeatTile + 3 * kBiasTile64 + 2 * kBiasTile16 + 128;
+constexpr uint32_t kFwdSmem = kWeightsBytes + 3 * kFeatTile + 2 * kBiasTile64 + 2 * kBiasTile16 + 128;
 // TMEM: accumulator [0, 64); layers 2-5 take their A operand (the previous
 // layer's activations, bf16 pairs) from columns [64, 96), so activations never
 // touch smem (measured: the MLP's smem pipe was its contended resource).
@@ -511,7 +520,6 @@ __global__ void __launch_bounds__(128, 4) mlp_fwd_kernel(FieldArgs a, const uint
     BT.ones = carve(p, kFeatTile);
     BT.l1 = carve(p, kBiasTile64);
     BT.l2 = carve(p, kBiasTile16);
-    BT.c1 = carve(p, kBiasTile64);
     BT.c2 = carve(p, kBiasTile64);
     BT.c3 = carve(p, kBiasTile16);
     const int r = threadIdx.x;
@@ -527,7 +535,6 @@ __global__ void __launch_bounds__(128, 4) mlp_fwd_kernel(FieldArgs a, const uint
         const float o2[8] = {1.f, 1.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         st_chunk(BT.ones, r, 0, o2);
         st_chunk(BT.ones, r, 1, z);
-        stage_bias_tile<64>(BT.c1, a.f.color + kCB1, kCHidden);
         stage_bias_tile<64>(BT.c2, a.f.color + kCB2, kCHidden);
         stage_bias_tile<16>(BT.c3, a.f.color + kCB3, 3);
     }
@@ -630,18 +637,17 @@ __global__ void __launch_bounds__(128, 4) mlp_fwd_kernel(FieldArgs a, const uint
             for (int i = 0; i < kEmb; ++i) cin[i] = v[1 + i];
 #pragma unroll
             for (int i = 0; i < kViewDim; ++i) cin[kEmb + i] = ve[i];
-            cin[kCIn] = 1.f;  // ones column (bias gradient of colour layer 1 in K4)
+            cin[kCIn] = cin[kCIn + 1] = 1.f;  // the bias columns (and K4's bias-gradient column)
 #pragma unroll
-            for (int i = kCIn + 1; i < 48; ++i) cin[i] = 0.f;
+            for (int i = kCIn + 2; i < 48; ++i) cin[i] = 0.f;
             tst_bf16<48>(tmem, kColA, cin);
         }
         sync_for_mma_tmem();
         // ---- colour layer 1: [128x48] x Wc1^T -> 64
         if (r == 0) {
-            umma::mma(tmem, kmaj(BT.ones, kT, 0), kmaj(BT.c1, 64, 0), id64, 0);
 #pragma unroll
             for (int k = 0; k < 3; ++k)
-                umma::mma_ts(tmem, tmem + kColA + 8 * k, kmaj(W.wc1, kWc1Rows, k), id64, 1);
+                umma::mma_ts(tmem, tmem + kColA + 8 * k, kmaj(W.wc1, kWc1Rows, k), id64, k > 0);
             umma::commit(&bar_mma);
         }
         wait_mma(&bar_mma, ph_mma);
@@ -708,7 +714,7 @@ __global__ void __launch_bounds__(128, 4) mlp_fwd_kernel(FieldArgs a, const uint
 // accumulators persistent across the CTA's tiles:
 //   dWc2^T [64,128)  dWc1 [128,176)  dW1d [176,208)  dWc3^T [208,224)  dW2d^T [224,240)
 constexpr uint32_t kBufA = 9 * kChunk;  // 18432
-constexpr uint32_t kBwdSmem = 3 * kBufA + 4 * kChunk + 6 * kChunk + 2 * kChunk + kWeightsBytes + 3 * kBiasTile64 +
+constexpr uint32_t kBwdSmem = 3 * kBufA + 4 * kChunk + 6 * kChunk + 2 * kChunk + kWeightsBytes + 2 * kBiasTile64 +
                                kBiasTile16 + 128;
 constexpr uint32_t kBwdTmemCols = 256;
 constexpr int kColWc2 = 64, kColWc1 = 128, kColW1d = 176, kColWc3 = 208, kColW2d = 224;
@@ -816,7 +822,6 @@ __global__ void __launch_bounds__(kBwdThreads, 2) mlp_bwd_kernel(FieldArgs a, Fi
     // columns 16 and 17 are 1
     uint8_t* const bt_l1 = carve(p, kBiasTile64);
     uint8_t* const bt_l2 = carve(p, kBiasTile16);
-    uint8_t* const bt_c1 = carve(p, kBiasTile64);
     uint8_t* const bt_c2 = carve(p, kBiasTile64);
     const int r = threadIdx.x;
     if (r == 0) {
@@ -838,7 +843,6 @@ __global__ void __launch_bounds__(kBwdThreads, 2) mlp_bwd_kernel(FieldArgs a, Fi
         st_chunk(X0, r, 2, o2);  // col 16: dW1d's bias column; 16-17: the bias MMAs' A
         float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         st_chunk(X0, r, 3, z);
-        stage_bias_tile<64>(bt_c1, a.f.color + kCB1, kCHidden);
         stage_bias_tile<64>(bt_c2, a.f.color + kCB2, kCHidden);
     }
     pdl_wait();  // the composite's gradients
@@ -962,18 +966,17 @@ __global__ void __launch_bounds__(kBwdThreads, 2) mlp_bwd_kernel(FieldArgs a, Fi
             for (int i = 0; i < kEmb; ++i) cin[i] = v[1 + i];
 #pragma unroll
             for (int i = 0; i < kViewDim; ++i) cin[kEmb + i] = ve[i];
-            cin[kCIn] = 1.f;
+            cin[kCIn] = cin[kCIn + 1] = 1.f;  // bias columns (see stage_color)
 #pragma unroll
-            for (int i = kCIn + 1; i < 48; ++i) cin[i] = 0.f;
+            for (int i = kCIn + 2; i < 48; ++i) cin[i] = 0.f;
 #pragma unroll
             for (int c = 0; c < 6; ++c) st_chunk(CIN, r, c, cin + 8 * c);
         }
         sync_mlp();
         if (r == 0) {
-            umma::mma(tmem, kmaj(X0, kT, 1), kmaj(bt_c1, 64, 0), id64, 0);
 #pragma unroll
             for (int k = 0; k < 3; ++k)
-                umma::mma(tmem, kmaj(CIN, kT, k), kmaj(W.wc1, kWc1Rows, k), id64, 1);
+                umma::mma(tmem, kmaj(CIN, kT, k), kmaj(W.wc1, kWc1Rows, k), id64, k > 0);
             umma::commit(&bar_mma);
         }
         wait_mma(&bar_mma, ph_mma);
