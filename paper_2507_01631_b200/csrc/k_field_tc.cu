@@ -149,19 +149,29 @@ __device__ __forceinline__ void stage_density(const Weights& w, const float* __r
     for (int i = threadIdx.x; i < 64; i += kT) w.b1d[i] = p[kDB1 + i];
     for (int i = threadIdx.x; i < 16; i += kT) w.b2d[i] = p[kDB2 + i];
 }
+// Colour layer 1's weights [64 x 48] with its bias riding in its own K range:
+// input column kCIn (the ones column the backward's dWc1 bias gradient uses)
+// and kCIn + 1 are 1, so the tile holds bf16(bc1) and bf16(bc1 - bf16(bc1))
+// there.  Written by the thread that writes the chunk (one writer per byte).
+__device__ __forceinline__ void stage_wc1(uint8_t* dst, const float* __restrict__ p) {
+    static_assert(kCIn == 39, "the bias columns 39 / 40 straddle chunks 4 and 5");
+    constexpr int kCh = 6, kItems = 64 * kCh;
+    for (int it = threadIdx.x; it < kItems; it += kT) {
+        const int r = it / kCh, c = it % kCh, c0 = 8 * c;
+        float v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = c0 + j < kCIn ? __ldg(p + kCW1 + r * kCIn + c0 + j) : 0.f;
+        const float b = p[kCB1 + r];
+        const float hi = __bfloat162float(__float2bfloat16_rn(b));
+        if (c == 4) v[7] = b;         // col 39: rounds to hi
+        if (c == 5) v[0] = b - hi;    // col 40: rounds to bf16(b - hi)
+        *reinterpret_cast<uint4*>(dst + umma::off(64, r, c0)) =
+            make_uint4(pack2(v[0], v[1]), pack2(v[2], v[3]), pack2(v[4], v[5]), pack2(v[6], v[7]));
+    }
+}
 __device__ __forceinline__ void stage_color(const Weights& w, const float* __restrict__ p) {
     static_assert(kCW2 % 4 == 0 && kCW3 % 4 == 0, "colour weight rows are float4 aligned");
-    stage_matrix<kCHidden, kCIn, 64, 48>(w.wc1, p + kCW1);
-    // colour layer 1's bias rides in its own K range: input column kCIn (the
-    // ones column the backward's dWc1 bias gradient uses) and kCIn + 1 are 1,
-    // the weight tile holds bf16(bc1) and bf16(bc1 - bf16(bc1)) there
-    for (int o = threadIdx.x; o < kCHidden; o += kT) {
-        const float x = p[kCB1 + o];
-        const __nv_bfloat16 hi = __float2bfloat16_rn(x);
-        const __nv_bfloat16 lo = __float2bfloat16_rn(x - __bfloat162float(hi));
-        *reinterpret_cast<__nv_bfloat16*>(w.wc1 + umma::off(kWc1Rows, o, kCIn)) = hi;
-        *reinterpret_cast<__nv_bfloat16*>(w.wc1 + umma::off(kWc1Rows, o, kCIn + 1)) = lo;
-    }
+    stage_wc1(w.wc1, p);
     stage_matrix<kCHidden, kCHidden, 64, 64>(w.wc2, p + kCW2);
     stage_matrix<3, kCHidden, 16, 64>(w.wc3, p + kCW3);
     for (int i = threadIdx.x; i < 64; i += kT) {
