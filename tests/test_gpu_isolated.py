@@ -197,6 +197,37 @@ def test_field_matches_bf16_numerics_model(pair):
         assert rel < TOL_MODEL_GRAD_REL[name], (name, rel)
 
 
+def test_field_forward_deterministic(pair):
+    """The forward is a pure function of the batch and the parameters: the
+    same batch repeated in one context and once in a fresh context give the
+    same bits.  (Races that need drifting warps can slip past this; the
+    run save/resume test, two contexts training in step, is the stricter
+    check: it caught a staging race of colour layer 1's bias columns.)"""
+    from paper_2507_01631_b200.tilefield import Context
+
+    ctx, ses = pair
+    ses.sample(12, 0, N_RAYS, True)
+    b = ses.batch()
+    ctx.batch_import(b)
+    s1, r1 = ctx.field_forward()
+    for _ in range(16):  # a race shows only when warps drift apart: repeat
+        ctx.batch_import(b)
+        s2, r2 = ctx.field_forward()
+        np.testing.assert_array_equal(s1, s2)
+        np.testing.assert_array_equal(r1, r2)
+    other = Context(ctx.scene, FieldConfig.defaults(), TrainConfig.defaults(batch_rays=N_RAYS, seed=5),
+                    max_rays=N_RAYS)
+    other.set_window(1, 1)
+    for k in range(4):
+        other.set_tile_state(k, ctx.tile_state(k))
+    p, m, v, st = ctx.color()
+    other.set_color(p, m, v, st)
+    other.batch_import(b)
+    s3, r3 = other.field_forward()
+    np.testing.assert_array_equal(s1, s3)
+    np.testing.assert_array_equal(r1, r3)
+
+
 def test_field_backward_zero_in_zero_out(pair):
     """zero loss gradient in -> zero gradients out."""
     ctx, ses = pair
