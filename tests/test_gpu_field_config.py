@@ -155,3 +155,46 @@ def test_geometry_vs_oracle(geom):
     rgb, _, op = ctx.render_pixels(ctx.scene.cams[0], v0[:, 1:])
     np.testing.assert_allclose(rgb, ref["rgb"], atol=TOL_RAY_RGB_ATOL)
     np.testing.assert_allclose(op, ref["opacity"], atol=TOL_RAY_RGB_ATOL)
+
+
+def test_geometry_operator_path():
+    """The operator-level entry points (forward_batch / backward_batch over a
+    caller-built batch: tfg_batch_import, tfg_field_backward_from) on a padded
+    geometry: the oracle's own batch imports bit for bit, and the field
+    backward fed the oracle's d_sigma / d_rgb matches the oracle's gradients
+    within the default tolerances."""
+    from oracle.pyoracle import Oracle, Session
+
+    fc = FieldConfig.defaults()
+    for k, v in GEOMETRIES["T2^17_n16-1024"].items():
+        setattr(fc, k, v)
+    scene = _scene()
+    tc = TrainConfig.defaults(batch_rays=N_RAYS, seed=5)
+    ctx = _context(scene, fc, tc)
+    ses = Session(Oracle(), scene, fc, tc, workers=8)
+    ctx.set_window(0, 1)
+    ses.set_window(0, 1)
+    ses.build_accept()
+    rng = np.random.default_rng(3)
+    for k in range(4):
+        st = _perturbed(ses.tile_state(k), rng)
+        ses.set_tile_state(k, st)
+        ctx.set_tile_state(k, st)
+    p, m, v, s = ses.color()
+    ctx.set_color(p, m, v, s)
+    ses.sample(7, 0, N_RAYS, True)
+    b = ses.batch()
+    assert ctx.batch_import(b) == b["offsets"][-1]
+    got = ctx.batch()
+    for f in ("offsets", "t", "delta", "local", "slot", "endpoint"):
+        np.testing.assert_array_equal(got[f], b[f], err_msg=f)
+    sr, rr = ses.forward()
+    ref = ses.composite()
+    sg, rgb = ctx.field_forward()
+    np.testing.assert_allclose(sg, sr, rtol=TOL_SIGMA_RTOL, atol=1e-6)
+    np.testing.assert_allclose(rgb, rr, atol=TOL_RGB_ATOL)
+    ses.backward()
+    ctx.field_backward_from(ref["d_sigma"], ref["d_rgb"])
+    for k in range(4):
+        for name, x, y in zip(("enc", "dnet", "color"), ctx.grads(k), ses.grads(k)):
+            assert _rel(x, y) < TOL_GRAD_REL[name], (k, name, _rel(x, y))
